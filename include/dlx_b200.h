@@ -1,0 +1,185 @@
+/*
+ * dlx_b200.h — C-ABI of the B200-native DiLoCoX outer-synchronisation path.
+ *
+ * Drop-in boundary for the reference's compressor / worker-sync / outer-optimiser API
+ * (reference /root/reference/proj/core; citations are include/dilocox/NAME.hpp and src/NAME.cpp
+ * file:line). Every entry point is extern "C", takes plain pointers and sizes, never a
+ * torch type. Device pointers are caller-owned CUDA global memory; the library owns
+ * per-context workspaces. All compute calls are asynchronous on the given cudaStream_t
+ * (passed as void*); one host thread per context; not re-entrant per context.
+ *
+ * Data layout (device):
+ *   - A ParamSet (reference params.hpp:12-33) is ONE fp32 "slab"; tensor i starts at
+ *     element dlx_layout_offsets()[i] (256-byte aligned), row-major, in table order.
+ *   - Factor buffers (warm Q, and P/Q scratch) are column-major per 2-D tensor, column
+ *     stride ld = round_up(rows, 32); offsets via dlx_factor_offsets().
+ *   - A compressed payload is one byte buffer of dlx_payload_bytes(): per tensor, in
+ *     table order, 16-byte aligned segments  [P codes][Q codes][P scales][Q scales]
+ *     (2-D) or [codes][scale] (1-D). Codes are q-bit two's complement, LSB-first,
+ *     column-major — byte-identical to the code sections of the reference wire format
+ *     (compress.cpp:352-367, 395-426). Scales are fp32. D payloads back to back form
+ *     the all-gather buffer that dlx_outer_update consumes.
+ *
+ * Status codes mirror the reference exception taxonomy (errors.hpp:8-34).
+ */
+#ifndef DLX_B200_H
+#define DLX_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dlx_status {
+  DLX_OK = 0,
+  DLX_ERR_VALIDATION = 1, /* dilocox::ValidationError */
+  DLX_ERR_SHAPE = 2,      /* dilocox::ShapeError */
+  DLX_ERR_FORMAT = 3,     /* dilocox::FormatError */
+  DLX_ERR_NUMERIC = 4,    /* dilocox::NumericError */
+  DLX_ERR_IO = 5,         /* dilocox::IoError */
+  DLX_ERR_CUDA = 6,
+  DLX_ERR_NCCL = 7
+} dlx_status;
+
+enum { DLX_ROUND_STOCHASTIC = 0, DLX_ROUND_NEAREST = 1 }; /* compress.hpp:13 Rounding */
+enum { DLX_MODE_OVERLAPPED = 0, DLX_MODE_SYNC = 1 };      /* engine.cpp:423-509 */
+
+typedef struct dlx_ctx dlx_ctx;
+typedef struct dlx_layout dlx_layout;
+
+/* Round statistics written by dlx_outer_update (device doubles; see RoundRecord
+ * engine.hpp:74-95). */
+typedef struct dlx_round_stats {
+  double err_num;        /* sum (dec(payload_self) - delta_pending)^2   (measure_error) */
+  double err_den;        /* sum delta_pending^2                                           */
+  double delta_norm_sq;  /* ||delta_new||^2        (stage_deltas max_delta_norm)          */
+  double err_norm_sq;    /* ||e||^2                (RoundRecord.err_buf_norm)             */
+  double nonfinite;      /* count of non-finite anchor values produced (NumericError)     */
+  double pad[3];
+} dlx_round_stats;
+
+/* ---- context / errors --------------------------------------------------------------- */
+const char* dlx_version(void);
+const char* dlx_last_error(void); /* thread-local message of the last failing call */
+dlx_status dlx_ctx_create(int device, dlx_ctx** out);
+dlx_status dlx_ctx_destroy(dlx_ctx* ctx);
+
+/* ---- tensor table (ParamSet layout) ---------------------------------------------------
+ * ndim[i] in {1,2}; dims[2i], dims[2i+1] = (rows, cols) or (n, 1). Mirrors
+ * ParamSet::add / same_layout (params.hpp:12-33). */
+dlx_status dlx_layout_create(dlx_ctx* ctx, int nt, const int* ndim, const int64_t* dims,
+                             dlx_layout** out);
+dlx_status dlx_layout_destroy(dlx_layout* layout);
+int64_t dlx_layout_slab_elems(const dlx_layout* layout);
+dlx_status dlx_layout_offsets(const dlx_layout* layout, int64_t* offsets /* nt */);
+/* Per-2-D-tensor column-major factor offsets (elements) for the given rank (b side for
+ * Q / warm Q when side = 1, a side for P when side = 0); entries for 1-D tensors are -1.
+ * Returns the total element count of the factor buffer. */
+int64_t dlx_factor_offsets(const dlx_layout* layout, int rank, int side, int64_t* offsets);
+
+/* ---- payload geometry (compress.cpp:92-114, 395-426) --------------------------------- */
+int64_t dlx_payload_bytes(const dlx_layout* layout, int rank, int qbits);
+/* seg[4*i + {0,1,2,3}] = byte offsets of P codes, Q codes, P scales, Q scales
+ * (1-D: codes, -1, scale, -1). */
+dlx_status dlx_payload_segments(const dlx_layout* layout, int rank, int qbits, int64_t* seg);
+uint64_t dlx_payload_bits(const dlx_layout* layout, int rank, int qbits);
+
+/* ---- synthetic inputs -----------------------------------------------------------------
+ * out[t] = (base ? base[t] : 0) + scale * g, g = Tensor::gaussian (tensor.cpp:49-53) drawn
+ * from RngStream(seed, stream_key({tag, worker, t})) per tensor t, bit-identical to the
+ * reference generator; two separate fp32 roundings (mul, add). */
+dlx_status dlx_fill_gaussian(dlx_ctx* ctx, const dlx_layout* layout, float* d_out,
+                             const float* d_base, float scale, uint64_t seed, uint64_t tag,
+                             uint64_t worker, void* stream);
+
+/* ---- compressor (compress.hpp:94-95 compress) -------------------------------------------
+ * Low-rank (warm-started power iteration, power_iters >= 1) + per-column q-bit
+ * quantisation of every 2-D tensor, quantisation of every 1-D tensor, in table order,
+ * consuming the shared splitmix stream whose state is rng_state (RngStream after
+ * construction, rng.hpp:13-16). d_warm_q (nullable) is the previous round's Q factors
+ * for warm_rank; used iff warm_rank == rank (compress.cpp:161). Writes the payload and
+ * the float Q factors (next warm start, compress.hpp:86-90). *d_draws (nullable, device
+ * uint64) receives the number of draws consumed (the reference advances its RngStream&
+ * by exactly that). */
+dlx_status dlx_compress(dlx_ctx* ctx, const dlx_layout* layout, const float* d_delta, int rank,
+                        int qbits, int rounding, int power_iters, uint64_t rng_state,
+                        const float* d_warm_q, int warm_rank, uint8_t* d_payload,
+                        float* d_q_out, uint64_t* d_draws, void* stream);
+
+/* Quantise given float factors exactly as compress does after lowrank_approx
+ * (quantize_columns compress.cpp:119-131 per 2-D tensor P then Q, quantize :24-49 per
+ * 1-D tensor taken from d_delta). cold != 0 inserts the b*r cold-start draws before each
+ * 2-D tensor (compress.cpp:64-69). d_p / d_q use dlx_factor_offsets layouts. */
+dlx_status dlx_quantize_factors(dlx_ctx* ctx, const dlx_layout* layout, const float* d_p,
+                                const float* d_q, const float* d_delta, int rank, int qbits,
+                                int rounding, uint64_t rng_state, int cold,
+                                uint8_t* d_payload, uint64_t* d_draws, void* stream);
+
+/* decompress (compress.cpp:201-238) of one payload into a dense slab. */
+dlx_status dlx_decompress(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
+                          const uint8_t* d_payload, float* d_out, void* stream);
+
+/* allreduce_avg (collective.cpp:17-46): mean of the D payloads' reconstructions, given the
+ * all-gather buffer (D payloads back to back). Dense fp32 output. */
+dlx_status dlx_allreduce_avg(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
+                             int D, const uint8_t* d_gathered, float* d_out, void* stream);
+
+/* ---- fused outer update (engine.cpp:254-276 + optim.cpp:56-78) ---------------------------
+ * Given the all-gather buffer, reconstructs Delta = (1/D) sum_w P_w Q_w^T per tensor in
+ * the tile, never materialising it, and in the same pass:
+ *   overlapped: e = pending - Delta; pending <- (anchor - local) + e  (pre-update anchor)
+ *   sync:       pending <- pending - Delta                           (pending becomes e)
+ *   both:       v <- beta v + Delta; anchor <- anchor - gamma (Delta + beta v)
+ *               (classical: anchor <- anchor - gamma v)
+ * self_index >= 0 also accumulates measure_error (compress.cpp:246-262) for that worker's
+ * payload. d_stats (device dlx_round_stats, nullable) receives the reductions. */
+dlx_status dlx_outer_update(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits, int D,
+                            const uint8_t* d_gathered, int self_index, int mode,
+                            float* d_pending, float* d_anchor, const float* d_local,
+                            float* d_velocity, float gamma, float beta, int classical,
+                            dlx_round_stats* d_stats, void* stream);
+
+/* stage_deltas (engine.cpp:266-276): pending <- (anchor - local) + (d_err ? d_err : 0).
+ * d_err may alias d_pending. d_norm_sq (nullable device double) gets ||pending||^2. */
+dlx_status dlx_stage_deltas(dlx_ctx* ctx, const dlx_layout* layout, const float* d_anchor,
+                            const float* d_local, const float* d_err, float* d_pending,
+                            double* d_norm_sq, void* stream);
+
+/* nesterov_outer_step (optim.cpp:56-78) on a dense averaged delta. */
+dlx_status dlx_nesterov(dlx_ctx* ctx, int64_t n, float gamma, float beta, int classical,
+                        float* d_anchor, float* d_velocity, const float* d_delta, void* stream);
+
+/* ---- adaptive rank (compress.cpp:306-344, engine.cpp:294-308) ----------------------------
+ * effective_rank of the averaged delta, computed in factor space from the all-gather
+ * buffer: the nonzero singular values of (1/D) [P_1..P_D][Q_1..Q_D]^T are those of the
+ * (D r) x (D r) matrix L^T (P^T P) L with L L^T = Q^T Q, so no dense SVD is needed.
+ * d_per_tensor (device int, one per 2-D tensor) and d_energy (device double, per 2-D
+ * tensor) are written; dlx_effective_rank_reduce aggregates on the host exactly as the
+ * reference (size-weighted mean, ceil, clamp to [1, r_max]). */
+dlx_status dlx_effective_rank(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
+                              int D, const uint8_t* d_gathered, double tau, int* d_per_tensor,
+                              double* d_energy, void* stream);
+dlx_status dlx_effective_rank_reduce(const dlx_layout* layout, const int* per_tensor,
+                                     const double* energy, int r_max, int* aggregate,
+                                     int* all_zero);
+dlx_status dlx_adapt_compression(const int* window, int len, int r1, int H1, int c, int h_min,
+                                 int* r_out, int* h_out);
+double dlx_omega_bound(int r, int d, int q);
+
+/* ---- wire format (compress.cpp:395-482) -------------------------------------------------
+ * Host-side conversion between a device payload (copied to host) and DLXC v1 bytes.
+ * Tensor names are caller-provided (names[i]); rank is CompressedDelta::rank. */
+int64_t dlx_serialize(const dlx_layout* layout, int rank, int qbits, const char* const* names,
+                      const uint8_t* h_payload, uint8_t* out, int64_t cap);
+dlx_status dlx_parse(const dlx_layout* layout, int rank, int qbits, const uint8_t* bytes,
+                     int64_t size, uint8_t* h_payload);
+
+/* Number of kernels this library launched on the calling thread since the last call
+ * (launch accounting for benchmarks). */
+uint64_t dlx_take_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DLX_B200_H */

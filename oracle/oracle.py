@@ -202,7 +202,7 @@ class Oracle:
         scales = np.empty(self.lib.orc_scales_count(table.nt, _p(ndim, C.c_int),
                                                     _p(dims, C.c_int64), _p(ranks, C.c_int)),
                           np.float32)
-        qf = np.empty(max(1, self.lib.orc_qfactor_count(table.nt, _p(ndim, C.c_int),
+        qf = np.zeros(max(1, self.lib.orc_qfactor_count(table.nt, _p(ndim, C.c_int),
                                                         _p(dims, C.c_int64), _p(ranks, C.c_int))),
                       np.float32)
         st = C.c_uint64(state)

@@ -490,7 +490,6 @@ int orc_outer_round(int D, int nt, const int* ndim, const int64_t* dims, uint64_
     h.momentum = beta;
     h.classical = classical != 0;
     NesterovState outer = make_nesterov_state(anc, h);
-    unmake_ps(outer.velocity, velocity);  // keep layout; overwrite below
     outer.velocity = make_ps(nt, ndim, dims, velocity);
     WarmStart warm = make_warm(nt, ndim, dims, *warm_rank, warm_q);
     std::vector<ParamSet> pend, loc;

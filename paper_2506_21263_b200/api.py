@@ -1,0 +1,376 @@
+"""Host-side mirror of the reference compressor / worker-sync / outer-optimiser API
+(reference proj/core: compress.hpp, collective.hpp, optim.hpp, engine.hpp) over
+device-resident ParamSets. Every compute call goes through the C-ABI (include/dlx_b200.h);
+torch is used only for device memory, streams and torch.distributed plumbing.
+
+A ParamSet lives in one fp32 "slab" (a 1-D torch CUDA tensor) laid out by a Layout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+STOCHASTIC, NEAREST = 0, 1
+OVERLAPPED, SYNC = 0, 1
+GOLDEN = 0x9E3779B97F4A7C15
+M64 = (1 << 64) - 1
+
+
+# ----------------------------------------------------------------------------- RNG (rng.hpp)
+def _fmix(z: int) -> int:
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def _mix(z: int) -> int:
+    return _fmix((z + GOLDEN) & M64)
+
+
+def stream_key(*parts: int) -> int:
+    """stream_key (rng.hpp:63-66)."""
+    h = 0x100000001B3
+    for p in parts:
+        h = _mix(h ^ _mix(p & M64))
+    return h
+
+
+def rng_stream(seed: int, stream_id: int) -> int:
+    """State of RngStream(seed, stream_id) after construction (rng.hpp:13-16)."""
+    s = _mix((seed ^ GOLDEN) & M64)
+    return _mix(s ^ _mix((stream_id + 0xBF58476D1CE4E5B9) & M64))
+
+
+def _stream(s) -> C.c_void_p:
+    if s is None:
+        s = torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+# ----------------------------------------------------------------------------- context/layout
+class Context:
+    """One device context (dlx_ctx): workspaces and plan caches live here."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        check(lib().dlx_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().dlx_ctx_destroy(self.h)
+            self.h = None
+
+
+@dataclass
+class QuantSpec:
+    """compress.hpp:21-27."""
+    qbits: int = 4
+    rounding: int = STOCHASTIC
+
+    def levels(self) -> int:
+        return (1 << (self.qbits - 1)) - 1
+
+
+class Layout:
+    """ParamSet tensor table (params.hpp:12-33) mapped onto one device slab."""
+
+    def __init__(self, ctx: Context, table):
+        self.ctx = ctx
+        self.names = [n for n, _ in table]
+        self.shapes = [tuple(int(d) for d in s) for _, s in table]
+        if len(set(self.names)) != len(self.names):
+            raise _lib.ValidationError("duplicate parameter name")
+        nt = len(self.shapes)
+        self.ndim = np.array([len(s) for s in self.shapes], np.int32)
+        self.dims = np.zeros(2 * max(nt, 1), np.int64)
+        for i, s in enumerate(self.shapes):
+            self.dims[2 * i] = s[0]
+            self.dims[2 * i + 1] = s[1] if len(s) == 2 else 1
+        h = C.c_void_p()
+        check(lib().dlx_layout_create(ctx.h, nt, self.ndim.ctypes.data_as(C.POINTER(C.c_int)),
+                                      self.dims.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(h)))
+        self.h = h
+        self.nt = nt
+        self.slab_elems = lib().dlx_layout_slab_elems(h)
+        self.offsets = np.zeros(max(nt, 1), np.int64)
+        check(lib().dlx_layout_offsets(h, self.offsets.ctypes.data_as(C.POINTER(C.c_int64))))
+        self.numels = [int(np.prod(s)) for s in self.shapes]
+        self.total_params = int(sum(self.numels))
+
+    # -- slabs
+    def empty(self, device=None) -> torch.Tensor:
+        return torch.zeros(self.slab_elems, dtype=torch.float32,
+                           device=device or f"cuda:{self.ctx.device}")
+
+    def to_slab(self, arrays, device=None) -> torch.Tensor:
+        host = np.zeros(self.slab_elems, np.float32)
+        for i, a in enumerate(arrays):
+            a = np.asarray(a, np.float32).reshape(-1)
+            host[self.offsets[i]:self.offsets[i] + self.numels[i]] = a
+        return torch.from_numpy(host).to(device or f"cuda:{self.ctx.device}")
+
+    def from_slab(self, slab: torch.Tensor):
+        host = slab.detach().cpu().numpy()
+        return [host[self.offsets[i]:self.offsets[i] + self.numels[i]].reshape(self.shapes[i])
+                for i in range(self.nt)]
+
+    def pack(self, flat: np.ndarray, device=None) -> torch.Tensor:
+        """Reference-order concatenation (no padding) -> padded slab."""
+        out, o = [], 0
+        for n in self.numels:
+            out.append(flat[o:o + n])
+            o += n
+        return self.to_slab(out, device)
+
+    def unpack(self, slab: torch.Tensor) -> np.ndarray:
+        return np.concatenate([a.reshape(-1) for a in self.from_slab(slab)]) if self.nt else \
+            np.zeros(0, np.float32)
+
+    # -- geometry
+    def payload_bytes(self, rank: int, qbits: int) -> int:
+        n = lib().dlx_payload_bytes(self.h, rank, qbits)
+        if n < 0:
+            check(int(-n))
+        return int(n)
+
+    def payload_bits(self, rank: int, qbits: int) -> int:
+        """payload_bits_formula (compress.cpp:92-114)."""
+        return int(lib().dlx_payload_bits(self.h, rank, qbits))
+
+    def segments(self, rank: int, qbits: int) -> np.ndarray:
+        seg = np.zeros(4 * max(self.nt, 1), np.int64)
+        check(lib().dlx_payload_segments(self.h, rank, qbits,
+                                         seg.ctypes.data_as(C.POINTER(C.c_int64))))
+        return seg.reshape(-1, 4)
+
+    def factor_offsets(self, rank: int, side: int):
+        off = np.zeros(max(self.nt, 1), np.int64)
+        total = lib().dlx_factor_offsets(self.h, rank, side,
+                                         off.ctypes.data_as(C.POINTER(C.c_int64)))
+        if total < 0:
+            check(int(-total))
+        return off, int(total)
+
+    def ranks(self, rank: int):
+        return [min(rank, s[0], s[1]) if len(s) == 2 else 0 for s in self.shapes]
+
+    def q_factor_elems(self, rank: int) -> int:
+        return self.factor_offsets(rank, 1)[1]
+
+    def factors_to_device(self, mats, rank: int, side: int, device=None) -> torch.Tensor:
+        """List (per 2-D tensor, table order) of n x r row-major factors -> device buffer."""
+        off, total = self.factor_offsets(rank, side)
+        host = np.zeros(total, np.float32)
+        k = 0
+        for i, s in enumerate(self.shapes):
+            if len(s) != 2:
+                continue
+            m = np.asarray(mats[k], np.float32)
+            n, r = m.shape
+            ld = (n + 31) // 32 * 32
+            for j in range(r):
+                host[off[i] + j * ld: off[i] + j * ld + n] = m[:, j]
+            k += 1
+        return torch.from_numpy(host).to(device or f"cuda:{self.ctx.device}")
+
+    def factors_from_device(self, buf: torch.Tensor, rank: int, side: int):
+        off, _ = self.factor_offsets(rank, side)
+        host = buf.detach().cpu().numpy()
+        out = []
+        for i, s in enumerate(self.shapes):
+            if len(s) != 2:
+                continue
+            n = s[side]
+            r = min(rank, s[0], s[1])
+            ld = (n + 31) // 32 * 32
+            out.append(np.stack([host[off[i] + j * ld: off[i] + j * ld + n] for j in range(r)], 1))
+        return out
+
+    # -- wire format (compress.cpp:395-482)
+    def serialize(self, payload: torch.Tensor, rank: int, qbits: int, names=None) -> bytes:
+        host = payload.detach().cpu().numpy().astype(np.uint8, copy=False)
+        nm = names if names is not None else self.names
+        arr = (C.c_char_p * self.nt)(*[n.encode() for n in nm])
+        args = [self.h, rank, qbits, arr, host.ctypes.data_as(C.c_void_p)]
+        n = lib().dlx_serialize(*args, None, 0)
+        if n < 0:
+            check(int(-n))
+        buf = np.zeros(n, np.uint8)
+        lib().dlx_serialize(*args, buf.ctypes.data_as(C.c_void_p), n)
+        return buf.tobytes()
+
+    def parse(self, data: bytes, rank: int, qbits: int, device=None) -> torch.Tensor:
+        src = np.frombuffer(data, np.uint8).copy()
+        out = np.zeros(self.payload_bytes(rank, qbits), np.uint8)
+        check(lib().dlx_parse(self.h, rank, qbits, src.ctypes.data_as(C.c_void_p), len(src),
+                              out.ctypes.data_as(C.c_void_p)))
+        return torch.from_numpy(out).to(device or f"cuda:{self.ctx.device}")
+
+    def close(self):
+        if self.h:
+            lib().dlx_layout_destroy(self.h)
+            self.h = None
+
+
+# ----------------------------------------------------------------------------- compressor
+@dataclass
+class CompressResult:
+    """compress.hpp:86-90 (payload + the float Q factors for the next warm start)."""
+    payload: torch.Tensor
+    q_factors: torch.Tensor
+    draws: torch.Tensor  # device uint64: RNG draws consumed
+    rank: int
+    qbits: int
+
+
+def fill_gaussian(layout: Layout, out: torch.Tensor, scale: float, seed: int, tag: int,
+                  worker: int, base: torch.Tensor | None = None, stream=None):
+    """out = base + scale * Tensor::gaussian, per-tensor streams
+    RngStream(seed, stream_key({tag, worker, t})) — bit-identical to the reference."""
+    check(lib().dlx_fill_gaussian(layout.ctx.h, layout.h, _ptr(out), _ptr(base), scale, seed,
+                                  tag, worker, _stream(stream)))
+    return out
+
+
+def compress(layout: Layout, delta: torch.Tensor, rank: int, spec: QuantSpec,
+             warm_q: torch.Tensor | None, warm_rank: int, power_iters: int, rng_state: int,
+             payload: torch.Tensor | None = None, q_out: torch.Tensor | None = None,
+             stream=None) -> CompressResult:
+    """compress (compress.cpp:146-183). q_out may alias warm_q (in-place warm refresh)."""
+    dev = delta.device
+    if payload is None:
+        payload = torch.empty(layout.payload_bytes(rank, spec.qbits), dtype=torch.uint8, device=dev)
+    if q_out is None:
+        q_out = torch.zeros(max(layout.q_factor_elems(rank), 1), dtype=torch.float32, device=dev)
+    draws = torch.zeros(1, dtype=torch.int64, device=dev)
+    check(lib().dlx_compress(layout.ctx.h, layout.h, _ptr(delta), rank, spec.qbits, spec.rounding,
+                             power_iters, rng_state & M64, _ptr(warm_q), warm_rank, _ptr(payload),
+                             _ptr(q_out), _ptr(draws), _stream(stream)))
+    return CompressResult(payload, q_out, draws, rank, spec.qbits)
+
+
+def quantize_factors(layout: Layout, p: torch.Tensor, q: torch.Tensor, delta: torch.Tensor,
+                     rank: int, spec: QuantSpec, rng_state: int, cold: bool, stream=None):
+    dev = delta.device
+    payload = torch.zeros(layout.payload_bytes(rank, spec.qbits), dtype=torch.uint8, device=dev)
+    draws = torch.zeros(1, dtype=torch.int64, device=dev)
+    check(lib().dlx_quantize_factors(layout.ctx.h, layout.h, _ptr(p), _ptr(q), _ptr(delta), rank,
+                                     spec.qbits, spec.rounding, rng_state & M64, int(cold),
+                                     _ptr(payload), _ptr(draws), _stream(stream)))
+    return payload, draws
+
+
+def decompress(layout: Layout, payload: torch.Tensor, rank: int, qbits: int, stream=None):
+    """decompress (compress.cpp:201-238) — reference-exact fp64 accumulation."""
+    out = layout.empty(payload.device)
+    check(lib().dlx_decompress(layout.ctx.h, layout.h, rank, qbits, _ptr(payload), _ptr(out),
+                               _stream(stream)))
+    return out
+
+
+def allreduce_avg(layout: Layout, gathered: torch.Tensor, D: int, rank: int, qbits: int,
+                  stream=None):
+    """allreduce_avg (collective.cpp:17-46) given the all-gather buffer of D payloads."""
+    out = layout.empty(gathered.device)
+    check(lib().dlx_allreduce_avg(layout.ctx.h, layout.h, rank, qbits, D, _ptr(gathered),
+                                  _ptr(out), _stream(stream)))
+    return out
+
+
+def outer_update(layout: Layout, gathered: torch.Tensor, D: int, rank: int, qbits: int,
+                 pending: torch.Tensor, anchor: torch.Tensor, local: torch.Tensor | None,
+                 velocity: torch.Tensor, gamma: float, beta: float, classical: bool = False,
+                 mode: int = OVERLAPPED, self_index: int = -1, stats: torch.Tensor | None = None,
+                 stream=None):
+    """Fused reconstruct + error feedback + stage + Nesterov (engine.cpp:254-276,
+    optim.cpp:56-78). stats: device float64[8] (dlx_round_stats) or None."""
+    check(lib().dlx_outer_update(layout.ctx.h, layout.h, rank, qbits, D, _ptr(gathered),
+                                 self_index, mode, _ptr(pending), _ptr(anchor), _ptr(local),
+                                 _ptr(velocity), gamma, beta, int(classical), _ptr(stats),
+                                 _stream(stream)))
+
+
+def stage_deltas(layout: Layout, anchor, local, err, pending, norm_sq=None, stream=None):
+    """stage_deltas (engine.cpp:266-276): pending = (anchor - local) + err."""
+    check(lib().dlx_stage_deltas(layout.ctx.h, layout.h, _ptr(anchor), _ptr(local), _ptr(err),
+                                 _ptr(pending), _ptr(norm_sq), _stream(stream)))
+
+
+def nesterov_outer_step(ctx: Context, anchor: torch.Tensor, velocity: torch.Tensor,
+                        delta: torch.Tensor, gamma: float = 0.7, beta: float = 0.9,
+                        classical: bool = False, stream=None):
+    """nesterov_outer_step (optim.cpp:56-78), in place on anchor / velocity."""
+    check(lib().dlx_nesterov(ctx.h, anchor.numel(), gamma, beta, int(classical), _ptr(anchor),
+                             _ptr(velocity), _ptr(delta), _stream(stream)))
+
+
+@dataclass
+class EffectiveRank:
+    """compress.hpp:121-125."""
+    aggregate: int = 1
+    per_tensor: list = field(default_factory=list)
+    all_zero: bool = False
+
+
+def effective_rank_device(layout: Layout, gathered: torch.Tensor, D: int, rank: int,
+                          qbits: int, tau: float, stream=None):
+    """Launch the factor-space effective rank; returns device (per_tensor, energy)."""
+    n2 = sum(1 for s in layout.shapes if len(s) == 2)
+    per = torch.zeros(max(n2, 1), dtype=torch.int32, device=gathered.device)
+    energy = torch.zeros(max(n2, 1), dtype=torch.float64, device=gathered.device)
+    check(lib().dlx_effective_rank(layout.ctx.h, layout.h, rank, qbits, D, _ptr(gathered), tau,
+                                   _ptr(per), _ptr(energy), _stream(stream)))
+    return per, energy
+
+
+def effective_rank_reduce(layout: Layout, per: np.ndarray, energy: np.ndarray,
+                          r_max: int) -> EffectiveRank:
+    per = np.ascontiguousarray(per, np.int32)
+    energy = np.ascontiguousarray(energy, np.float64)
+    agg, z = C.c_int(0), C.c_int(0)
+    check(lib().dlx_effective_rank_reduce(layout.h, per.ctypes.data_as(C.POINTER(C.c_int)),
+                                          energy.ctypes.data_as(C.POINTER(C.c_double)), r_max,
+                                          C.byref(agg), C.byref(z)))
+    names2 = [n for n, s in zip(layout.names, layout.shapes) if len(s) == 2]
+    return EffectiveRank(agg.value, list(zip(names2, per.tolist())), bool(z.value))
+
+
+def effective_rank(layout: Layout, gathered: torch.Tensor, D: int, rank: int, qbits: int,
+                   tau: float, r_max: int, stream=None) -> EffectiveRank:
+    """effective_rank (compress.cpp:306-344) of allreduce_avg(gathered), in factor space."""
+    per, energy = effective_rank_device(layout, gathered, D, rank, qbits, tau, stream)
+    n2 = sum(1 for s in layout.shapes if len(s) == 2)
+    return effective_rank_reduce(layout, per.cpu().numpy()[:n2], energy.cpu().numpy()[:n2], r_max)
+
+
+def adapt_compression(window, r1: int, H1: int, c: int, h_min: int):
+    """adapt_compression (engine.cpp:294-308)."""
+    w = np.ascontiguousarray(window if len(window) else [0], np.int32)
+    r, h = C.c_int(0), C.c_int(0)
+    check(lib().dlx_adapt_compression(w.ctypes.data_as(C.POINTER(C.c_int)), len(window), r1, H1,
+                                      c, h_min, C.byref(r), C.byref(h)))
+    return r.value, h.value
+
+
+def omega_bound(r: int, d: int, q: int) -> float:
+    """omega_bound (compress.cpp:240-244)."""
+    v = lib().dlx_omega_bound(r, d, q)
+    if v < 0:
+        raise _lib.ValidationError("omega_bound: need 1 <= r <= d")
+    return v
+
+
+def take_launch_count() -> int:
+    return int(lib().dlx_take_launch_count())

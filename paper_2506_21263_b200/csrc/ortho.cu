@@ -1,0 +1,430 @@
+// ortho.cu — batched orthonormalisation of the power-iteration factors
+// (orthonormalize tensor.cpp:174-227) and the batched fp64 Gram used by the effective rank.
+//
+// B200 design: all factors of one side (every P, or every Q) are orthonormalised in one
+// pass of four launches instead of a column-serial MGS per tensor:
+//   Gram (fp64, row-split, deterministic) -> Cholesky + R^-1 (one CTA per factor)
+//   -> apply Y R^-1 (fp64 accumulate)  — twice (CholQR2, equal to MGS2 up to rounding).
+// A factor whose Cholesky pivot falls within 10x of the reference's dependence tolerance
+// (1e-7 * max(1, largest column norm)) is left untouched by CholQR2 and re-done by an exact
+// MGS2 kernel with the reference's seeded column replacement (RngStream(0x5eedc01,
+// stream_key({n, r, j, attempt}))). That path only triggers on (near) rank-deficient
+// inputs such as all-zero tensors.
+#include "dlx_internal.cuh"
+
+namespace dlx {
+
+// ------------------------------------------------------------------ job tables
+struct GramJob {
+  std::vector<DevMat> mats;
+  DevMat* d_mats = nullptr;
+  std::vector<int4> splits;  // (entry, row0, row1, part index)
+  int4* d_splits = nullptr;
+  std::vector<int4> apply;   // (entry, row0, col block, -)
+  int4* d_apply = nullptr;
+  std::vector<int> part0;    // per entry: first part index
+  int* d_part0 = nullptr;
+  std::vector<int> nparts;   // per entry
+  int* d_nparts = nullptr;
+  int rmax = 0;
+  int total_parts = 0;
+};
+
+static GramJob* make_job(const std::vector<DevMat>& mats) {
+  auto* J = new GramJob();
+  J->mats = mats;
+  for (size_t e = 0; e < mats.size(); ++e) {
+    const DevMat& m = mats[e];
+    J->rmax = std::max(J->rmax, m.r);
+    const int64_t ns = std::max<int64_t>(1, ceil_div(m.n, 1024));
+    const int64_t rows = round_up(ceil_div(m.n, ns), 32);
+    J->part0.push_back(J->total_parts);
+    int cnt = 0;
+    for (int64_t r0 = 0; r0 < m.n; r0 += rows, ++cnt)
+      J->splits.push_back(make_int4(static_cast<int>(e), static_cast<int>(r0),
+                                    static_cast<int>(std::min(m.n, r0 + rows)),
+                                    J->total_parts + cnt));
+    J->nparts.push_back(cnt);
+    J->total_parts += cnt;
+    for (int64_t r0 = 0; r0 < m.n; r0 += 128)
+      for (int cb = 0; cb < m.r; cb += 32)
+        J->apply.push_back(make_int4(static_cast<int>(e), static_cast<int>(r0), cb / 32, 0));
+  }
+  auto up = [](auto& v) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    T* d = nullptr;
+    if (v.empty()) return d;
+    DLX_CUDA(cudaMalloc(&d, sizeof(T) * v.size()));
+    DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    return d;
+  };
+  J->d_mats = up(J->mats);
+  J->d_splits = up(J->splits);
+  J->d_apply = up(J->apply);
+  J->d_part0 = up(J->part0);
+  J->d_nparts = up(J->nparts);
+  return J;
+}
+
+static GramJob& job_for(const Plan& P, const std::string& key,
+                        const std::vector<DevMat>& mats) {
+  static thread_local std::map<std::pair<const Plan*, std::string>, std::unique_ptr<GramJob>> cache;
+  auto& slot = cache[{&P, key}];
+  if (!slot) slot.reset(make_job(mats));
+  return *slot;
+}
+
+// ------------------------------------------------------------------ deterministic reduce
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32, nw = blockDim.x / 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];  // fixed order
+  return s;
+}
+
+// ------------------------------------------------------------------ Gram (fp64)
+// partial[p][j*rr + k] = sum over rows of the split of Y[row, j] * Y[row, k] for the
+// 4x4 block of (j, k) owned by a thread (upper block triangle only).
+constexpr int kGramRows = 32;
+
+__global__ void __launch_bounds__(256) k_gram(const DevMat* __restrict__ mats,
+                                              const int4* __restrict__ splits,
+                                              const float* __restrict__ buf, int rr,
+                                              double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int4 sp = splits[blockIdx.x];
+  const DevMat m = mats[sp.x];
+  const int nb = (m.r + 3) / 4, nblk = nb * (nb + 1) / 2;
+  float* Ys = reinterpret_cast<float*>(smem_raw);  // [rpad][kGramRows]
+  const int rpad = nb * 4;
+  // thread -> (block, group); block index across grid.y passes when nblk > 256
+  const int groups = nblk >= 256 ? 1 : 256 / nblk;
+  const int blk = nblk >= 256 ? threadIdx.x + 256 * blockIdx.y : threadIdx.x % nblk;
+  const int grp = nblk >= 256 ? 0 : threadIdx.x / nblk;
+  const bool active = blk < nblk && grp < groups;
+  if (nblk < 256 && blockIdx.y > 0) return;  // uniform per CTA
+  int jb = 0, kb = 0;
+  if (active) {  // unrank blk -> (jb <= kb), row-major over the upper block triangle
+    int rem = blk;
+    jb = 0;
+    while (rem >= nb - jb) {
+      rem -= nb - jb;
+      ++jb;
+    }
+    kb = jb + rem;
+  }
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  const float* Y = buf + m.off;
+  for (int r0 = sp.y; r0 < sp.z; r0 += kGramRows) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < rpad * kGramRows; e += 256) {
+      const int c = e / kGramRows, rr0 = e % kGramRows;
+      const int row = r0 + rr0;
+      Ys[e] = (c < m.r && row < sp.z) ? Y[(int64_t)c * m.ld + row] : 0.f;
+    }
+    __syncthreads();
+    if (active) {
+      for (int rr0 = grp; rr0 < kGramRows; rr0 += groups) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          a[i] = (double)Ys[(jb * 4 + i) * kGramRows + rr0];
+          b[i] = (double)Ys[(kb * 4 + i) * kGramRows + rr0];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      }
+    }
+  }
+  // reduce groups in fixed order through shared memory
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(smem_raw);
+  if (groups > 1) {
+    if (active)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) red[(grp * nblk + blk) * 16 + i] = acc[i / 4][i % 4];
+    __syncthreads();
+    if (active && grp == 0) {
+      for (int g = 1; g < groups; ++g)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i / 4][i % 4] += red[(g * nblk + blk) * 16 + i];
+    }
+  }
+  if (active && grp == 0) {
+    double* out = partial + (int64_t)sp.w * rr * rr;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int gj = jb * 4 + i, gk = kb * 4 + j;
+        if (gj < m.r && gk < m.r) out[gj * rr + gk] = acc[i][j];
+      }
+  }
+}
+
+static size_t gram_smem(int rmax) {
+  const int rpad = (rmax + 3) / 4 * 4;
+  return std::max<size_t>(sizeof(float) * rpad * kGramRows, sizeof(double) * 16 * 256);
+}
+
+static void launch_gram(const GramJob& J, const float* buf, double* partial, cudaStream_t s) {
+  const int nb = (J.rmax + 3) / 4, nblk = nb * (nb + 1) / 2;
+  const int gy = nblk >= 256 ? (nblk + 255) / 256 : 1;
+  const size_t sm = gram_smem(J.rmax);
+  static bool attr = false;
+  if (!attr) {
+    DLX_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    attr = true;
+  }
+  k_gram<<<dim3(J.splits.size(), gy), 256, sm, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial);
+  DLX_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ Cholesky + R^-1
+// G = sum_p partial[p] (fixed order); upper Cholesky G = R^T R in place; flag the entry if
+// a pivot is within 10x of the reference dependence tolerance; Rinv = R^-1 (upper).
+__global__ void __launch_bounds__(256) k_chol(const DevMat* __restrict__ mats,
+                                              const int* __restrict__ part0,
+                                              const int* __restrict__ nparts, int rr,
+                                              const double* __restrict__ partial,
+                                              double* __restrict__ work,
+                                              double* __restrict__ rinv,
+                                              int* __restrict__ flags) {
+  __shared__ int s_flag;
+  __shared__ double s_thr;
+  const int e = blockIdx.x;
+  const DevMat m = mats[e];
+  const int r = m.r;
+  double* W = work + (int64_t)e * rr * rr;
+  double* X = rinv + (int64_t)e * rr * rr;
+  const double* src = partial + (int64_t)part0[e] * rr * rr;
+  const int np = nparts[e];
+  for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
+    const int j = idx / r, k = idx % r;
+    if (k < j) continue;
+    double g = 0.0;
+    for (int p = 0; p < np; ++p) g += src[(int64_t)p * rr * rr + j * rr + k];
+    W[j * rr + k] = g;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int j = 0; j < r; ++j) mx = fmax(mx, W[j * rr + j]);
+    const double big = sqrt(mx);
+    const double tol = 1e-7 * fmax(1.0, big);
+    s_thr = (10.0 * tol) * (10.0 * tol);
+    s_flag = 0;
+  }
+  __syncthreads();
+  for (int j = 0; j < r; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = W[j * rr + j];
+      if (!(d > s_thr)) s_flag = 1;
+    }
+    __syncthreads();
+    if (s_flag) break;
+    const double rjj = sqrt(W[j * rr + j]);
+    const double inv = 1.0 / rjj;
+    __syncthreads();
+    for (int k = j + 1 + threadIdx.x; k < r; k += blockDim.x) W[j * rr + k] *= inv;
+    if (threadIdx.x == 0) W[j * rr + j] = rjj;
+    __syncthreads();
+    const int rem = r - j - 1;
+    for (int idx = threadIdx.x; idx < rem * rem; idx += blockDim.x) {
+      const int i = j + 1 + idx / rem, k = j + 1 + idx % rem;
+      if (k < i) continue;
+      W[i * rr + k] -= W[j * rr + i] * W[j * rr + k];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) flags[e] = s_flag;
+  if (s_flag) return;
+  // upper-triangular inverse, one column per thread (back substitution)
+  for (int c = threadIdx.x; c < r; c += blockDim.x) {
+    X[c * rr + c] = 1.0 / W[c * rr + c];
+    for (int i = c - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int k = i + 1; k <= c; ++k) s += W[i * rr + k] * X[k * rr + c];
+      X[i * rr + c] = -s / W[i * rr + i];
+    }
+    for (int i = c + 1; i < r; ++i) X[i * rr + c] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------------ apply: out = Y R^-1
+__global__ void __launch_bounds__(128) k_apply(const DevMat* __restrict__ mats,
+                                               const int4* __restrict__ jobs, int rr,
+                                               const double* __restrict__ rinv,
+                                               const int* __restrict__ flags,
+                                               const float* __restrict__ in,
+                                               float* __restrict__ out) {
+  __shared__ double Rs[32][33];
+  const int4 jb = jobs[blockIdx.x];
+  const DevMat m = mats[jb.x];
+  if (flags[jb.x]) return;
+  const int cb = jb.z;
+  const int64_t row = jb.y + threadIdx.x;
+  const bool live = row < m.n;
+  const double* X = rinv + (int64_t)jb.x * rr * rr;
+  const float* Y = in + m.off;
+  double acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+  for (int kb = 0; kb <= cb; ++kb) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 32 * 32; idx += 128) {
+      const int k = kb * 32 + idx / 32, j = cb * 32 + idx % 32;
+      Rs[idx / 32][idx % 32] = (k < m.r && j < m.r) ? X[k * rr + j] : 0.0;
+    }
+    __syncthreads();
+    const int kmax = min(32, m.r - kb * 32);
+    for (int k = 0; k < kmax; ++k) {
+      const double y = live ? (double)Y[(int64_t)(kb * 32 + k) * m.ld + row] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = fma(y, Rs[k][j], acc[j]);
+    }
+  }
+  if (!live) return;
+  float* O = out + m.off;
+  const int jmax = min(32, m.r - cb * 32);
+  for (int j = 0; j < jmax; ++j) O[(int64_t)(cb * 32 + j) * m.ld + row] = (float)acc[j];
+}
+
+// ------------------------------------------------------------------ exact MGS2 fallback
+__global__ void __launch_bounds__(1024) k_mgs_fallback(const DevMat* __restrict__ mats,
+                                                       const int* __restrict__ flags,
+                                                       float* __restrict__ buf,
+                                                       double* __restrict__ scratch) {
+  __shared__ double red[32];
+  const int e = blockIdx.x;
+  if (!flags[e]) return;
+  const DevMat m = mats[e];
+  const int64_t n = m.n;
+  const int r = m.r;
+  float* Yf = buf + m.off;
+  double* Yd = scratch + m.off;  // same indexing as the float buffer
+  double big = 0.0;
+  for (int j = 0; j < r; ++j) {
+    double ss = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const double v = (double)Yf[j * m.ld + i];
+      Yd[j * m.ld + i] = v;
+      ss += v * v;
+    }
+    big = fmax(big, sqrt(block_sum(ss, red)));
+  }
+  const double tol = 1e-7 * fmax(1.0, big);
+  for (int j = 0; j < r; ++j) {
+    double* cj = Yd + (int64_t)j * m.ld;
+    for (int attempt = 0; attempt < 1000; ++attempt) {
+      for (int pass = 0; pass < 2; ++pass)
+        for (int p = 0; p < j; ++p) {
+          const double* cp = Yd + (int64_t)p * m.ld;
+          double d = 0.0;
+          for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d += cj[i] * cp[i];
+          const double dot = block_sum(d, red);
+          for (int64_t i = threadIdx.x; i < n; i += blockDim.x) cj[i] -= dot * cp[i];
+          __syncthreads();
+        }
+      double ss = 0.0;
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) ss += cj[i] * cj[i];
+      const double nrm = sqrt(block_sum(ss, red));
+      if (nrm > tol) {
+        const double inv = 1.0 / nrm;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) cj[i] *= inv;
+        __syncthreads();
+        break;
+      }
+      const uint64_t st = stream_init(0x5eedc01ull, stream_key4((uint64_t)n, (uint64_t)r,
+                                                                 (uint64_t)j, (uint64_t)attempt));
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        cj[i] = (double)__fadd_rn(-1.0f, __fmul_rn(2.0f, unit_f(draw_at(st, i + 1))));
+      __syncthreads();
+    }
+  }
+  for (int j = 0; j < r; ++j)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) Yf[j * m.ld + i] = (float)Yd[j * m.ld + i];
+}
+
+// ------------------------------------------------------------------ driver
+static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* tmp, const std::string& tag,
+                    int64_t buf_elems, cudaStream_t s) {
+  const int rr = J.rmax;
+  const size_t ne = J.mats.size();
+  auto* partial = static_cast<double*>(ctx->scratch("gram_part", sizeof(double) * J.total_parts * rr * rr));
+  auto* work = static_cast<double*>(ctx->scratch("chol_work", sizeof(double) * ne * rr * rr));
+  auto* rinv = static_cast<double*>(ctx->scratch("chol_rinv", sizeof(double) * ne * rr * rr));
+  auto* flags1 = static_cast<int*>(ctx->scratch("ortho_flags1" + tag, sizeof(int) * ne));
+  auto* flags2 = static_cast<int*>(ctx->scratch("ortho_flags2" + tag, sizeof(int) * ne));
+  // pass 1: buf -> tmp
+  launch_gram(J, buf, partial, s);
+  k_chol<<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags1);
+  DLX_LAUNCHED();
+  k_apply<<<J.apply.size(), 128, 0, s>>>(J.d_mats, J.d_apply, rr, rinv, flags1, buf, tmp);
+  DLX_LAUNCHED();
+  // pass 2: tmp -> buf (entries flagged in pass 1 are skipped by both applies)
+  launch_gram(J, tmp, partial, s);
+  k_chol<<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags2);
+  DLX_LAUNCHED();
+  k_apply<<<J.apply.size(), 128, 0, s>>>(J.d_mats, J.d_apply, rr, rinv, flags1, tmp, buf);
+  DLX_LAUNCHED();
+  // exact MGS2 for flagged entries (pass-1 flags: buf still holds their input)
+  auto* dscr = static_cast<double*>(ctx->scratch("mgs_scratch", sizeof(double) * buf_elems));
+  k_mgs_fallback<<<ne, 1024, 0, s>>>(J.d_mats, flags1, buf, dscr);
+  DLX_LAUNCHED();
+}
+
+void orthonormalize_batched(dlx_ctx* ctx, const Plan& P, int side, float* buf, float* tmp,
+                            cudaStream_t s) {
+  if (P.mats[side].empty()) return;
+  GramJob& J = job_for(P, side == 0 ? "P" : "Q", P.mats[side]);
+  cholqr2(ctx, J, buf, tmp, side == 0 ? "P" : "Q", side == 0 ? P.pelems : P.qelems, s);
+}
+
+__global__ void k_gram_fold(const DevMat* __restrict__ mats, const int* __restrict__ part0,
+                            const int* __restrict__ nparts, int rr,
+                            const double* __restrict__ partial, double* __restrict__ out) {
+  const int e = blockIdx.x;
+  const int r = mats[e].r;
+  const double* src = partial + (int64_t)part0[e] * rr * rr;
+  double* dst = out + (int64_t)e * rr * rr;
+  for (int idx = threadIdx.x; idx < rr * rr; idx += blockDim.x) {
+    const int j = idx / rr, k = idx % rr;
+    double g = 0.0;
+    if (j < r && k < r) {
+      const int a = min(j, k), b = max(j, k);
+      for (int p = 0; p < nparts[e]; ++p) g += src[(int64_t)p * rr * rr + a * rr + b];
+    }
+    dst[idx] = g;  // full symmetric
+  }
+}
+
+// Batched fp64 Gram of arbitrary column-major matrices: out[e] = M_e^T M_e (rr x rr full,
+// rr = max columns). Used by the factor-space effective rank.
+void gram_batched(dlx_ctx* ctx, const Plan& P, const std::string& key,
+                  const std::vector<DevMat>& mats, const float* buf, double* out,
+                  cudaStream_t s) {
+  GramJob& J = job_for(P, key, mats);
+  const int rr = J.rmax;
+  auto* partial = static_cast<double*>(ctx->scratch("gram_part_er", sizeof(double) * J.total_parts * rr * rr));
+  launch_gram(J, buf, partial, s);
+  k_gram_fold<<<J.mats.size(), 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, out);
+  DLX_LAUNCHED();
+}
+
+int gram_rr(const Plan& P, const std::string& key, const std::vector<DevMat>& mats) {
+  return job_for(P, key, mats).rmax;
+}
+
+}  // namespace dlx

@@ -1,0 +1,393 @@
+// outer.cu — the fused outer update (K5): reconstruction of the averaged pseudo-gradient
+// from the all-gathered factors + error feedback + delta staging + Nesterov, in one pass
+// over the outer state, plus the reference-API dense helpers (decompress / allreduce_avg /
+// stage_deltas / nesterov_outer_step).
+//
+// Reference semantics (bit-exact op order, -ffp-contract=off):
+//   allreduce_avg        collective.cpp:17-46   Delta = float(sum_w double(dec_w) * (1/D))
+//   error feedback       engine.cpp:254-257     e = delta_pending - Delta
+//   stage_deltas         engine.cpp:266-276     delta = (anchor - local) + e   (pre-update anchor)
+//   nesterov_outer_step  optim.cpp:56-78        v = beta v + Delta; anchor -= gamma (Delta + beta v)
+// HBM traffic per element of a 2-D tensor: read pending, anchor, local, v; write pending,
+// anchor, v = 28 B; Delta itself never touches HBM.
+#include "dlx_internal.cuh"
+
+namespace dlx {
+
+struct EpiOut {
+  float pend, anchor, v, e;
+};
+
+// One element of the fused epilogue given Delta (all roundings explicit).
+__device__ __forceinline__ EpiOut epilogue(float delta, float pend, float anchor, float local,
+                                           float v, int mode, float gamma, float beta,
+                                           int classical) {
+  EpiOut o;
+  if (mode == DLX_MODE_OVERLAPPED) {
+    o.e = __fsub_rn(pend, delta);
+    o.pend = __fadd_rn(__fsub_rn(anchor, local), o.e);
+  } else {
+    o.e = __fsub_rn(pend, delta);
+    o.pend = o.e;
+  }
+  o.v = __fadd_rn(__fmul_rn(beta, v), delta);
+  if (classical) {
+    o.anchor = __fsub_rn(anchor, __fmul_rn(gamma, o.v));
+  } else {
+    o.anchor = __fsub_rn(anchor, __fmul_rn(gamma, __fadd_rn(delta, __fmul_rn(beta, o.v))));
+  }
+  return o;
+}
+
+__device__ __forceinline__ void stats_add(dlx_round_stats* st, double num, double den,
+                                          double dn, double en, double nf, double* red) {
+  // warp reduce then one atomic per warp (stats are diagnostics, not state)
+  double v[5] = {num, den, dn, en, nf};
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  if ((threadIdx.x & 31) == 0 && st) {
+    if (v[0] != 0.0) atomicAdd(&st->err_num, v[0]);
+    if (v[1] != 0.0) atomicAdd(&st->err_den, v[1]);
+    if (v[2] != 0.0) atomicAdd(&st->delta_norm_sq, v[2]);
+    if (v[3] != 0.0) atomicAdd(&st->err_norm_sq, v[3]);
+    if (v[4] != 0.0) atomicAdd(&st->nonfinite, v[4]);
+  }
+  (void)red;
+}
+
+// ------------------------------------------------------------------ K5, 2-D tensors
+// Tile 32 rows x 128 cols of delta; 256 threads, each 4 rows x 4 consecutive cols.
+// Delta_tile = (1/D) * Phat[rows, :] Qhat[cols, :]^T with K = D*r (fp32 accumulate).
+__global__ void __launch_bounds__(256) k5_outer(const DevT2* __restrict__ T,
+                                                const int4* __restrict__ tiles,
+                                                const float* __restrict__ phat,
+                                                const float* __restrict__ qhat, int D,
+                                                int self_index, int mode, float* pending,
+                                                float* anchor, const float* __restrict__ local,
+                                                float* velocity, float gamma, float beta,
+                                                int classical, dlx_round_stats* stats) {
+  __shared__ __align__(16) float Ps[32][36];
+  __shared__ __align__(16) float Qs[32][132];
+  const int4 tile = tiles[blockIdx.x];
+  const DevT2 t = T[tile.x];
+  const int64_t m0 = tile.y, n0 = tile.z;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int K = D * t.r;
+  const float* Ph = phat + D * t.poff;
+  const float* Qh = qhat + D * t.qoff;
+  const int s_lo = self_index >= 0 ? self_index * t.r : K, s_hi = s_lo + t.r;
+  float acc[4][4], sacc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = sacc[i][j] = 0.f;
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    {  // Phat 32(k) x 32(rows): one float4 per thread
+      const int kk = tid / 8, c4 = (tid % 8) * 4;
+      const int k = k0 + kk;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < K) {
+        const float* src = Ph + (int64_t)k * t.lda + m0 + c4;  // lda % 32 == 0 -> aligned
+        v = *reinterpret_cast<const float4*>(src);            // rows >= a are zero padding
+      }
+      *reinterpret_cast<float4*>(&Ps[kk][c4]) = v;
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {  // Qhat 32(k) x 128(cols)
+      const int e = tid + 256 * l, kk = e / 32, c4 = (e % 32) * 4;
+      const int k = k0 + kk;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < K && n0 + c4 < t.ldb) v = *reinterpret_cast<const float4*>(Qh + (int64_t)k * t.ldb + n0 + c4);
+      *reinterpret_cast<float4*>(&Qs[kk][c4]) = v;
+    }
+    __syncthreads();
+    const int kmax = min(32, K - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+      const float4 a4 = *reinterpret_cast<const float4*>(&Ps[kk][ty * 4]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Qs[kk][tx * 4]);
+      const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      const int k = k0 + kk;
+      if (k >= s_lo && k < s_hi) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sacc[i][j] = fmaf(av[i], bv[j], sacc[i][j]);
+      }
+    }
+    __syncthreads();
+  }
+  const float invD = __fdiv_rn(1.0f, (float)D);
+  double num = 0.0, den = 0.0, dn = 0.0, en = 0.0, nf = 0.0;
+  const bool vec = (t.b % 4) == 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = m0 + ty * 4 + i;
+    if (row >= t.a) continue;
+    const int64_t col = n0 + tx * 4;
+    if (col >= t.b) continue;
+    const int64_t base = t.off + row * t.b + col;
+    float pd[4], an[4], lo[4], ve[4];
+    const int nv = (int)(t.b - col < 4 ? t.b - col : 4);
+    if (vec && nv == 4) {
+      const float4 a = *reinterpret_cast<const float4*>(pending + base);
+      const float4 b = *reinterpret_cast<const float4*>(anchor + base);
+      const float4 c = mode == DLX_MODE_OVERLAPPED ? __ldg(reinterpret_cast<const float4*>(local + base)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 d = *reinterpret_cast<const float4*>(velocity + base);
+      pd[0] = a.x; pd[1] = a.y; pd[2] = a.z; pd[3] = a.w;
+      an[0] = b.x; an[1] = b.y; an[2] = b.z; an[3] = b.w;
+      lo[0] = c.x; lo[1] = c.y; lo[2] = c.z; lo[3] = c.w;
+      ve[0] = d.x; ve[1] = d.y; ve[2] = d.z; ve[3] = d.w;
+    } else {
+      for (int j = 0; j < 4; ++j) {
+        pd[j] = j < nv ? pending[base + j] : 0.f;
+        an[j] = j < nv ? anchor[base + j] : 0.f;
+        lo[j] = (j < nv && mode == DLX_MODE_OVERLAPPED) ? local[base + j] : 0.f;
+        ve[j] = j < nv ? velocity[base + j] : 0.f;
+      }
+    }
+    float op[4], oa[4], ov[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float delta = __fmul_rn(acc[i][j], invD);
+      const EpiOut o = epilogue(delta, pd[j], an[j], lo[j], ve[j], mode, gamma, beta, classical);
+      op[j] = o.pend;
+      oa[j] = o.anchor;
+      ov[j] = o.v;
+      if (j < nv) {
+        if (self_index >= 0) {
+          const double df = (double)sacc[i][j] - (double)pd[j];
+          num += df * df;
+          den += (double)pd[j] * (double)pd[j];
+        }
+        en += (double)o.e * (double)o.e;
+        if (mode == DLX_MODE_OVERLAPPED) dn += (double)o.pend * (double)o.pend;
+        if (!isfinite(o.anchor)) nf += 1.0;
+      }
+    }
+    if (vec && nv == 4) {
+      *reinterpret_cast<float4*>(pending + base) = make_float4(op[0], op[1], op[2], op[3]);
+      *reinterpret_cast<float4*>(anchor + base) = make_float4(oa[0], oa[1], oa[2], oa[3]);
+      *reinterpret_cast<float4*>(velocity + base) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+    } else {
+      for (int j = 0; j < nv; ++j) {
+        pending[base + j] = op[j];
+        anchor[base + j] = oa[j];
+        velocity[base + j] = ov[j];
+      }
+    }
+  }
+  stats_add(stats, num, den, dn, en, nf, nullptr);
+}
+
+void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
+                     int self_index, int mode, float* pending, float* anchor,
+                     const float* local, float* velocity, float gamma, float beta,
+                     int classical, dlx_round_stats* stats, cudaStream_t s) {
+  if (P.t2.empty()) return;
+  float* phat = static_cast<float*>(ctx->scratch("phat", sizeof(float) * P.pelems * D));
+  float* qhat = static_cast<float*>(ctx->scratch("qhat", sizeof(float) * P.qelems * D));
+  dequant_factors(P, D, gathered, P.payload_bytes, phat, qhat, 0, s);
+  k5_outer<<<P.k5_tiles.size(), 256, 0, s>>>(P.d_t2, P.d_k5_tiles, phat, qhat, D, self_index,
+                                            mode, pending, anchor, local, velocity, gamma, beta,
+                                            classical, stats);
+  DLX_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ 1-D tensors
+__device__ __forceinline__ int code_at(const uint8_t* seg, int64_t k, int qbits) {
+  const int64_t bit = k * qbits;
+  const uint32_t w = static_cast<uint32_t>(seg[bit >> 3]) |
+                     (static_cast<uint32_t>(seg[(bit >> 3) + 1]) << 8);
+  const int u = static_cast<int>((w >> (bit & 7)) & ((1u << qbits) - 1u));
+  return (u & (1 << (qbits - 1))) ? u - (1 << qbits) : u;
+}
+
+// Delta of a 1-D tensor exactly as allreduce_avg: dequantise (fp32 product), sum in
+// double over workers in order, multiply by 1/D in double, round once.
+__device__ __forceinline__ float avg_1d(const uint8_t* gathered, int64_t pay_bytes,
+                                        const DevT1& t, int64_t k, int D, int qbits) {
+  double acc = 0.0;
+  for (int w = 0; w < D; ++w) {
+    const uint8_t* pay = gathered + w * pay_bytes;
+    const float sc = *reinterpret_cast<const float*>(pay + t.seg_s);
+    acc = __dadd_rn(acc, (double)__fmul_rn((float)code_at(pay + t.seg_c, k, qbits), sc));
+  }
+  return (float)__dmul_rn(acc, 1.0 / (double)D);
+}
+
+__global__ void __launch_bounds__(256) k_outer_1d(const DevT1* __restrict__ T,
+                                                  const uint8_t* __restrict__ gathered,
+                                                  int64_t pay_bytes, int qbits, int D,
+                                                  int self_index, int mode, float* pending,
+                                                  float* anchor, const float* local,
+                                                  float* velocity, float gamma, float beta,
+                                                  int classical, dlx_round_stats* stats) {
+  const DevT1 t = T[blockIdx.y];
+  double num = 0.0, den = 0.0, dn = 0.0, en = 0.0, nf = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < t.n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const float delta = avg_1d(gathered, pay_bytes, t, k, D, qbits);
+    const int64_t i = t.off + k;
+    const float pd = pending[i];
+    const EpiOut o = epilogue(delta, pd, anchor[i], mode == DLX_MODE_OVERLAPPED ? local[i] : 0.f,
+                              velocity[i], mode, gamma, beta, classical);
+    if (self_index >= 0) {
+      const uint8_t* pay = gathered + self_index * pay_bytes;
+      const float rec = __fmul_rn((float)code_at(pay + t.seg_c, k, qbits),
+                                  *reinterpret_cast<const float*>(pay + t.seg_s));
+      const double df = (double)rec - (double)pd;
+      num += df * df;
+      den += (double)pd * (double)pd;
+    }
+    en += (double)o.e * (double)o.e;
+    if (mode == DLX_MODE_OVERLAPPED) dn += (double)o.pend * (double)o.pend;
+    if (!isfinite(o.anchor)) nf += 1.0;
+    pending[i] = o.pend;
+    anchor[i] = o.anchor;
+    velocity[i] = o.v;
+  }
+  stats_add(stats, num, den, dn, en, nf, nullptr);
+}
+
+void launch_outer_1d(const Plan& P, int D, const uint8_t* gathered, int self_index, int mode,
+                     float* pending, float* anchor, const float* local, float* velocity,
+                     float gamma, float beta, int classical, dlx_round_stats* stats,
+                     cudaStream_t s) {
+  if (P.t1.empty()) return;
+  int64_t mx = 1;
+  for (const DevT1& t : P.t1) mx = std::max(mx, t.n);
+  const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 64));
+  k_outer_1d<<<dim3(gx, P.t1.size()), 256, 0, s>>>(P.d_t1, gathered, P.payload_bytes, P.qbits,
+                                                   D, self_index, mode, pending, anchor, local,
+                                                   velocity, gamma, beta, classical, stats);
+  DLX_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ dense reconstruction
+// Reference-exact decompress / allreduce_avg (fp64 accumulation over ascending k per
+// worker, float per worker, double sum over workers, * 1/D, float): bit-identical output.
+__global__ void __launch_bounds__(256) k_recon_2d(const DevT2* __restrict__ T, int nt2,
+                                                  const float* __restrict__ phat,
+                                                  const float* __restrict__ qhat, int D,
+                                                  float* __restrict__ out) {
+  const DevT2 t = T[blockIdx.z];
+  const int64_t j = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int64_t i = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (i >= t.a || j >= t.b) return;
+  const float* Ph = phat + D * t.poff;
+  const float* Qh = qhat + D * t.qoff;
+  double total = 0.0;
+  for (int w = 0; w < D; ++w) {
+    double acc = 0.0;
+    for (int k = 0; k < t.r; ++k) {
+      const int c = w * t.r + k;
+      acc = fma((double)Ph[(int64_t)c * t.lda + i], (double)Qh[(int64_t)c * t.ldb + j], acc);
+    }
+    total = __dadd_rn(total, (double)(float)acc);
+  }
+  out[t.off + i * t.b + j] = (float)__dmul_rn(total, 1.0 / (double)D);
+}
+
+__global__ void k_recon_1d(const DevT1* __restrict__ T, const uint8_t* __restrict__ gathered,
+                           int64_t pay_bytes, int qbits, int D, float* __restrict__ out) {
+  const DevT1 t = T[blockIdx.y];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < t.n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[t.off + k] = avg_1d(gathered, pay_bytes, t, k, D, qbits);
+}
+
+void launch_reconstruct_dense(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
+                              float* out, cudaStream_t s) {
+  if (!P.t2.empty()) {
+    float* phat = static_cast<float*>(ctx->scratch("phat", sizeof(float) * P.pelems * D));
+    float* qhat = static_cast<float*>(ctx->scratch("qhat", sizeof(float) * P.qelems * D));
+    dequant_factors(P, D, gathered, P.payload_bytes, phat, qhat, 0, s);
+    int64_t ma = 1, mb = 1;
+    for (const DevT2& t : P.t2) {
+      ma = std::max(ma, t.a);
+      mb = std::max(mb, t.b);
+    }
+    k_recon_2d<<<dim3(ceil_div(mb, 32), ceil_div(ma, 8), P.t2.size()), 256, 0, s>>>(
+        P.d_t2, (int)P.t2.size(), phat, qhat, D, out);
+    DLX_LAUNCHED();
+  }
+  if (!P.t1.empty()) {
+    int64_t mx = 1;
+    for (const DevT1& t : P.t1) mx = std::max(mx, t.n);
+    k_recon_1d<<<dim3(std::min<int64_t>(ceil_div(mx, 256), 64), P.t1.size()), 256, 0, s>>>(
+        P.d_t1, gathered, P.payload_bytes, P.qbits, D, out);
+    DLX_LAUNCHED();
+  }
+}
+
+// ------------------------------------------------------------------ stage / nesterov
+struct Span {
+  int64_t off, n;
+};
+
+__global__ void __launch_bounds__(256) k_stage(const Span* __restrict__ spans,
+                                               const float* __restrict__ anchor,
+                                               const float* __restrict__ local, const float* err,
+                                               float* pending, double* norm_sq) {
+  const Span sp = spans[blockIdx.y];
+  double ss = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < sp.n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = sp.off + k;
+    const float e = err ? err[i] : 0.0f;
+    const float d = __fadd_rn(__fsub_rn(anchor[i], local[i]), e);  // ps_sub then ps_add
+    pending[i] = d;
+    ss += (double)d * (double)d;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0 && norm_sq && ss != 0.0) atomicAdd(norm_sq, ss);
+}
+
+void launch_stage(const dlx_layout& L, const float* anchor, const float* local,
+                  const float* err, float* pending, double* norm_sq, cudaStream_t s) {
+  if (L.nt == 0) return;
+  std::vector<Span> spans(L.nt);
+  int64_t mx = 1;
+  for (int i = 0; i < L.nt; ++i) {
+    spans[i] = {L.offsets[i], L.numel(i)};
+    mx = std::max(mx, spans[i].n);
+  }
+  static thread_local std::map<const dlx_layout*, Span*> cache;
+  Span*& d = cache[&L];
+  if (!d) {
+    DLX_CUDA(cudaMalloc(&d, sizeof(Span) * L.nt));
+    DLX_CUDA(cudaMemcpy(d, spans.data(), sizeof(Span) * L.nt, cudaMemcpyHostToDevice));
+  }
+  const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 1024));
+  k_stage<<<dim3(gx, L.nt), 256, 0, s>>>(d, anchor, local, err, pending, norm_sq);
+  DLX_LAUNCHED();
+}
+
+__global__ void __launch_bounds__(256) k_nesterov(int64_t n, float gamma, float beta,
+                                                  int classical, float* anchor, float* v,
+                                                  const float* __restrict__ delta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const EpiOut o = epilogue(delta[i], 0.f, anchor[i], 0.f, v[i], DLX_MODE_SYNC, gamma, beta,
+                              classical);
+    anchor[i] = o.anchor;
+    v[i] = o.v;
+  }
+}
+
+void launch_nesterov(int64_t n, float gamma, float beta, int classical, float* anchor,
+                     float* v, const float* delta, cudaStream_t s) {
+  if (n <= 0) return;
+  const int g = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 148 * 16));
+  k_nesterov<<<g, 256, 0, s>>>(n, gamma, beta, classical, anchor, v, delta);
+  DLX_LAUNCHED();
+}
+
+}  // namespace dlx

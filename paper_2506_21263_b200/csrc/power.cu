@@ -1,0 +1,338 @@
+// power.cu — synthetic inputs, cold-start init, and the power-iteration GEMMs
+// (lowrank_approx compress.cpp:56-78):  Y = delta Q  (K1)   and   Z = delta^T P  (K2).
+//
+// delta is a x b row-major fp32 (slab); P (a x r) and Q (b x r) are column-major with
+// padded column strides. Both sweeps are HBM-bound for r <~ 80 (2r flops per 4 B of
+// delta); each delta element is read exactly once per sweep. Accumulation is fp32 with a
+// fixed per-thread order (deterministic; the reference accumulates in fp64, tolerance).
+#include "dlx_internal.cuh"
+
+namespace dlx {
+
+// --------------------------------------------------------------- synthetic gaussian fill
+struct TensorSpan {
+  int64_t off, n;
+};
+
+__global__ void k_fill_gaussian(const TensorSpan* spans, float* out, const float* base,
+                                float scale, uint64_t seed, uint64_t tag, uint64_t worker) {
+  const int t = blockIdx.y;
+  const TensorSpan sp = spans[t];
+  // RngStream(seed, stream_key({tag, worker, t})) (rng.hpp:13-16, 63-66)
+  uint64_t h = 0x100000001b3ull;
+  h = mix64(h ^ mix64(tag));
+  h = mix64(h ^ mix64(worker));
+  h = mix64(h ^ mix64(static_cast<uint64_t>(t)));
+  const uint64_t s0 = stream_init(seed, h);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < sp.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    // element i consumes draws 12i+1 .. 12i+12 (Tensor::gaussian, rng.hpp:52-56)
+    double s = 0.0;
+#pragma unroll
+    for (int k = 1; k <= 12; ++k) s = __dadd_rn(s, unit_d(draw_at(s0, 12ull * i + k)));
+    const float g = (float)__dadd_rn(s, -6.0);
+    const float v = __fmul_rn(scale, g);
+    out[sp.off + i] = base ? __fadd_rn(base[sp.off + i], v) : v;
+  }
+}
+
+void launch_fill_gaussian(const dlx_layout& L, float* out, const float* base, float scale,
+                          uint64_t seed, uint64_t tag, uint64_t worker, cudaStream_t s) {
+  if (L.nt == 0) return;
+  std::vector<TensorSpan> spans(L.nt);
+  int64_t maxn = 1;
+  for (int i = 0; i < L.nt; ++i) {
+    spans[i] = {L.offsets[i], L.numel(i)};
+    maxn = std::max(maxn, spans[i].n);
+  }
+  auto* d = static_cast<TensorSpan*>(L.ctx->scratch("fill_spans", sizeof(TensorSpan) * L.nt));
+  DLX_CUDA(cudaMemcpyAsync(d, spans.data(), sizeof(TensorSpan) * L.nt, cudaMemcpyHostToDevice, s));
+  const int gx = static_cast<int>(std::min<int64_t>(ceil_div(maxn, 256), 1024));
+  k_fill_gaussian<<<dim3(gx, L.nt), 256, 0, s>>>(d, out, base, scale, seed, tag, worker);
+  DLX_LAUNCHED();
+  // the spans upload is pageable; keep it alive until the copy has been consumed
+  DLX_CUDA(cudaStreamSynchronize(s));
+}
+
+// --------------------------------------------------------------- cold start (compress.cpp:64-69)
+// Q0 = uniform(-1, 1)^{b x r} row-major from the shared stream at the tensor's draw base,
+// stored column-major. Value = lo + (hi - lo) * u with separate roundings (rng.hpp:39).
+__global__ void k_cold_init(const DevT2* T, int nt2, float* q, const int64_t* bases, uint64_t s0) {
+  const int k = blockIdx.y;
+  const DevT2 t = T[k];
+  const int64_t total = t.b * t.r;
+  const uint64_t base = static_cast<uint64_t>(bases[k]);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / t.r, j = e % t.r;
+    const float u = unit_f(draw_at(s0, base + e + 1));
+    q[t.qoff + j * t.ldb + i] = __fadd_rn(-1.0f, __fmul_rn(2.0f, u));
+  }
+}
+
+void launch_cold_init(const Plan& P, float* q, const int64_t* d_bases, uint64_t s0,
+                      cudaStream_t s) {
+  if (P.t2.empty()) return;
+  int64_t mx = 1;
+  for (const DevT2& t : P.t2) mx = std::max(mx, t.b * t.r);
+  const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 512));
+  k_cold_init<<<dim3(gx, P.t2.size()), 256, 0, s>>>(P.d_t2, (int)P.t2.size(), q, d_bases, s0);
+  DLX_LAUNCHED();
+}
+
+// --------------------------------------------------------------- K1: Y = delta * Q
+constexpr int kBK = 32;
+
+template <int BM, int BN>
+__global__ void __launch_bounds__(256) k1_gemm(const DevT2* __restrict__ T,
+                                               const int4* __restrict__ tiles,
+                                               const float* __restrict__ slab,
+                                               const float* __restrict__ qbuf,
+                                               float* __restrict__ ybuf) {
+  constexpr int TX = BN / 4, TY = 256 / TX, TM = BM / TY;
+  static_assert(TM == 4, "4x4 register tile");
+  __shared__ __align__(16) float As[kBK][BM + 4];
+  __shared__ __align__(16) float Bs[kBK][BN + 4];
+  const int4 tile = tiles[blockIdx.x];
+  const DevT2 t = T[tile.x];
+  const int64_t m0 = tile.y;
+  const int n0 = tile.z;
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const float* A = slab + t.off;
+  const float* Q = qbuf + t.qoff;
+  const bool vec = (t.b % 4) == 0;
+  float acc[TM][4];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (int64_t k0 = 0; k0 < t.b; k0 += kBK) {
+    // delta tile BM x 32 -> As[k][m]
+#pragma unroll
+    for (int l = 0; l < BM * 8 / 256; ++l) {
+      const int e = tid + 256 * l, row = e / 8, c4 = (e % 8) * 4;
+      const int64_t gm = m0 + row, gk = k0 + c4;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (gm < t.a) {
+        const float* src = A + gm * t.b + gk;
+        if (vec && gk + 3 < t.b) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = (gk + q < t.b) ? __ldg(src + q) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) As[c4 + q][row] = v[q];
+    }
+    // Q tile 32 x BN -> Bs[k][n]
+#pragma unroll
+    for (int l = 0; l < BN * 8 / 256; ++l) {
+      const int e = tid + 256 * l, col = e / 8, c4 = (e % 8) * 4;
+      const int gn = n0 + col;
+      const int64_t gk = k0 + c4;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (gn < t.r) {
+        const float* src = Q + gn * t.ldb + gk;
+        if (gk + 3 < t.b) {
+          const float4 x = *reinterpret_cast<const float4*>(src);
+          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = (gk + q < t.b) ? src[q] : 0.f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Bs[c4 + q][col] = v[q];
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kBK; ++kk) {
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * TM]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* Y = ybuf + t.poff;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int gn = n0 + tx * 4 + j;
+    if (gn >= t.r) continue;
+    const int64_t gm = m0 + ty * TM;
+    float* dst = Y + gn * t.lda + gm;
+    if (gm + 3 < t.a) {
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[0][j], acc[1][j], acc[2][j], acc[3][j]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+        if (gm + i < t.a) dst[i] = acc[i][j];
+    }
+  }
+}
+
+void launch_k1(const Plan& P, const float* slab, const float* q, float* y, cudaStream_t s) {
+  if (P.k1_tiles.empty()) return;
+  const int n = static_cast<int>(P.k1_tiles.size());
+  if (P.rmax <= 32)
+    k1_gemm<128, 32><<<n, 256, 0, s>>>(P.d_t2, P.d_k1_tiles, slab, q, y);
+  else
+    k1_gemm<64, 64><<<n, 256, 0, s>>>(P.d_t2, P.d_k1_tiles, slab, q, y);
+  DLX_LAUNCHED();
+}
+
+// --------------------------------------------------------------- K2: Z = delta^T * P
+// Tile: 64 columns of delta (rows of Z) x BC factor columns, over one 2048-row k split.
+template <int BC>
+__global__ void __launch_bounds__(256) k2_gemm(const DevT2* __restrict__ T,
+                                               const int4* __restrict__ tiles,
+                                               const int* __restrict__ splits,
+                                               const int64_t* __restrict__ part_off,
+                                               const float* __restrict__ slab,
+                                               const float* __restrict__ pbuf,
+                                               float* __restrict__ zbuf,
+                                               float* __restrict__ part) {
+  constexpr int TX = BC / 4, TY = 256 / TX, TM = 64 / TY;
+  constexpr int64_t KC = 2048;
+  __shared__ __align__(16) float As[kBK][64 + 4];
+  __shared__ __align__(16) float Bs[kBK][BC + 4];
+  const int4 tile = tiles[blockIdx.x];
+  const DevT2 t = T[tile.x];
+  const int64_t j0 = tile.y;
+  const int c0 = tile.z, sp = tile.w;
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const float* A = slab + t.off;
+  const float* Pf = pbuf + t.poff;
+  const bool vec = (t.b % 4) == 0;
+  const int64_t i_begin = sp * KC, i_end = min(t.a, i_begin + KC);
+  float acc[TM][4];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (int64_t i0 = i_begin; i0 < i_end; i0 += kBK) {
+    // delta rows i0..i0+31, cols j0..j0+63 -> As[k][j]
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      const int e = tid + 256 * l, kk = e / 16, c4 = (e % 16) * 4;
+      const int64_t gi = i0 + kk, gj = j0 + c4;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (gi < i_end) {
+        const float* src = A + gi * t.b + gj;
+        if (vec && gj + 3 < t.b) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = (gj + q < t.b) ? __ldg(src + q) : 0.f;
+        }
+      }
+      *reinterpret_cast<float4*>(&As[kk][c4]) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    // P rows i0..i0+31, cols c0..c0+BC-1 -> Bs[k][c]
+#pragma unroll
+    for (int l = 0; l < BC * 8 / 256; ++l) {
+      const int e = tid + 256 * l, col = e / 8, c4 = (e % 8) * 4;
+      const int gc = c0 + col;
+      const int64_t gi = i0 + c4;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (gc < t.r) {
+        const float* src = Pf + gc * t.lda + gi;
+        if (gi + 3 < i_end) {
+          const float4 x = *reinterpret_cast<const float4*>(src);
+          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = (gi + q < i_end) ? src[q] : 0.f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Bs[c4 + q][col] = v[q];
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kBK; ++kk) {
+      float av[TM];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) av[i] = As[kk][ty * TM + i];
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const int ns = splits[tile.x];
+  float* Z = ns > 1 ? part + part_off[tile.x] + sp * (t.ldb * t.r) : zbuf + t.qoff;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int gc = c0 + tx * 4 + j;
+    if (gc >= t.r) continue;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int64_t gj = j0 + ty * TM + i;
+      if (gj < t.b) Z[gc * t.ldb + gj] = acc[i][j];
+    }
+  }
+}
+
+// Deterministic split-K reduction: Z = sum_s part[s] in split order.
+__global__ void k2_reduce(const DevT2* __restrict__ T, const int* __restrict__ slots,
+                          const int* __restrict__ splits, const int64_t* __restrict__ part_off,
+                          const float* __restrict__ part, float* __restrict__ zbuf) {
+  const int k = slots[blockIdx.y];
+  const DevT2 t = T[k];
+  const int ns = splits[k];
+  const int64_t total = t.ldb * t.r;
+  const float* src = part + part_off[k];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e % t.ldb >= t.b) continue;
+    float s = 0.f;
+    for (int q = 0; q < ns; ++q) s += src[q * total + e];
+    zbuf[t.qoff + e] = s;
+  }
+}
+
+void launch_k2(const Plan& P, const float* slab, const float* p, float* z, float* part,
+               cudaStream_t s) {
+  if (P.k2_tiles.empty()) return;
+  const int n = static_cast<int>(P.k2_tiles.size());
+  if (P.rmax <= 32)
+    k2_gemm<32><<<n, 256, 0, s>>>(P.d_t2, P.d_k2_tiles, P.d_k2_splits, P.d_k2_part_off, slab,
+                                  p, z, part);
+  else
+    k2_gemm<64><<<n, 256, 0, s>>>(P.d_t2, P.d_k2_tiles, P.d_k2_splits, P.d_k2_part_off, slab,
+                                  p, z, part);
+  DLX_LAUNCHED();
+  // split slots (static per plan): cache the list in a device arena keyed by the plan
+  std::vector<int> slots;
+  int64_t mx = 1;
+  for (size_t k = 0; k < P.t2.size(); ++k)
+    if (P.k2_splits[k] > 1) {
+      slots.push_back(static_cast<int>(k));
+      mx = std::max(mx, P.t2[k].ldb * P.t2[k].r);
+    }
+  if (slots.empty()) return;
+  static thread_local std::map<const Plan*, int*> cache;
+  int*& d = cache[&P];
+  if (!d) {
+    DLX_CUDA(cudaMalloc(&d, sizeof(int) * slots.size()));
+    DLX_CUDA(cudaMemcpy(d, slots.data(), sizeof(int) * slots.size(), cudaMemcpyHostToDevice));
+  }
+  const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 1024));
+  k2_reduce<<<dim3(gx, slots.size()), 256, 0, s>>>(P.d_t2, d, P.d_k2_splits, P.d_k2_part_off,
+                                                  part, z);
+  DLX_LAUNCHED();
+}
+
+}  // namespace dlx

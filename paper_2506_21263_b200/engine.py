@@ -1,0 +1,228 @@
+"""Device-resident outer-synchronisation engine: one process = one DiLoCoX worker = one GPU.
+
+Mirrors the hot-path part of the reference engine (engine.cpp): RoundState (engine.hpp:114-132)
+restricted to the outer state, collective_average (:215-263), stage_deltas (:266-276),
+push_rank_window / adapt_compression (:278-308) and the round orderings
+run_round_overlapped (:458-509) / run_round_sync (:423-456). Inner training is out of
+scope: the caller hands in each round's local parameters (a device slab).
+
+Exchange: the reference's "all-reduce" is a mean of per-worker reconstructions
+(collective.cpp:17-46), so workers all-gather their compressed payloads (NCCL over NVLink
+via torch.distributed) and every rank reconstructs the same Delta with K = D*r; worker 0's
+float Q factors are broadcast as the next warm start (engine.cpp:498-501). The exchange and
+the effective-rank measurement run on a side stream.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import api
+from .api import NEAREST, OVERLAPPED, STOCHASTIC, SYNC, QuantSpec
+
+
+@dataclass
+class OuterConfig:
+    """The config keys the path accepts (config.cpp:209-235); defaults engine.hpp:21-36,
+    compress.hpp:21-27, optim.hpp:30-34."""
+    rank1: int = 64
+    qbits: int = 4
+    rounding: int = STOCHASTIC
+    power_iters: int = 2
+    H1: int = 125
+    adaptive: bool = True
+    window_c: int = 5
+    tau: float = 0.5
+    H_min: int = 0
+    outer_lr: float = 0.7
+    outer_momentum: float = 0.9
+    outer_classical: bool = False
+    seed: int = 1
+    overlap: bool = True      # dilocox (overlapped) vs dilocox-no-overlap (sync)
+    measure_error: bool = True
+
+    def resolved_H_min(self) -> int:
+        return self.H_min if self.H_min > 0 else (self.H1 + 9) // 10
+
+
+@dataclass
+class RoundRecord:
+    """Hot-path fields of RoundRecord (engine.hpp:74-95)."""
+    round: int = 0
+    r_t: int = 0
+    H_t: int = 0
+    r_prime: int = 0
+    payload_bytes: float = 0.0
+    comp_error: float = 0.0
+    omega_sq: float = 0.0
+    bound_violated: bool = False
+    err_buf_norm: float = 0.0
+    max_delta_norm: float = 0.0
+    averaged: bool = False
+    nonfinite: int = 0
+
+
+class OuterSync:
+    def __init__(self, layout: api.Layout, cfg: OuterConfig, anchor: torch.Tensor,
+                 world: int = 1, rank: int = 0, group=None, side_stream: bool = True):
+        self.L = layout
+        self.cfg = cfg
+        self.world, self.rank, self.group = world, rank, group
+        dev = anchor.device
+        self.anchor = anchor
+        self.velocity = torch.zeros_like(anchor)
+        self.pending = torch.zeros_like(anchor)
+        self.r_t = cfg.rank1
+        self.H_t = cfg.H1
+        self.round = 0
+        self.has_pending = False
+        self.window: list[int] = []
+        self.warm_rank = 0
+        qel = max(layout.q_factor_elems(cfg.rank1), 1)
+        self.warm_q = torch.zeros(qel, dtype=torch.float32, device=dev)
+        pb = layout.payload_bytes(cfg.rank1, cfg.qbits)
+        self.payload = torch.zeros(pb, dtype=torch.uint8, device=dev)
+        self.gathered = torch.zeros(world * pb, dtype=torch.uint8, device=dev)
+        self.stats = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.side = torch.cuda.Stream(device=dev) if side_stream else None
+        self.stats_host = torch.zeros(8, dtype=torch.float64, pin_memory=True)
+        n2 = sum(1 for s in layout.shapes if len(s) == 2)
+        self._n2 = n2
+        self.per_host = torch.zeros(max(n2, 1), dtype=torch.int32, pin_memory=True)
+        self.energy_host = torch.zeros(max(n2, 1), dtype=torch.float64, pin_memory=True)
+        self.last = RoundRecord()
+
+    # -- pieces -------------------------------------------------------------------------
+    def _omega_sq(self, r: int) -> float:
+        # size-weighted per-tensor bound with d = min(a, b) (engine.cpp:242-253)
+        w = s = 0.0
+        for sh in self.L.shapes:
+            if len(sh) != 2:
+                continue
+            a, b = sh
+            re = min(r, a, b)
+            sz = a * b
+            s += sz * (1.0 - (re / min(a, b)) * 2.0 ** (-self.cfg.qbits))
+            w += sz
+        return s / w if w > 0 else 0.0
+
+    def _exchange(self, pb: int, qel: int):
+        """All-gather payloads; broadcast worker-0 Q (warm start) — NCCL over NVLink."""
+        if self.world == 1:
+            return self.payload[:pb]
+        import torch.distributed as dist
+        g = self.gathered[:self.world * pb]
+        dist.all_gather_into_tensor(g, self.payload[:pb], group=self.group)
+        if qel > 0:
+            dist.broadcast(self.warm_q[:qel], src=0, group=self.group)
+        return g
+
+    def collective_average(self, local: torch.Tensor | None, mode: int) -> RoundRecord:
+        """Compress (shared stream per round), exchange, measure, fused outer update."""
+        cfg, L = self.cfg, self.L
+        r, q = self.r_t, cfg.qbits
+        pb = L.payload_bytes(r, q)
+        qel = L.q_factor_elems(r)
+        s0 = api.rng_stream(cfg.seed, api.stream_key(0xC09C, self.round))  # engine.cpp:226
+        # compress in place over the warm buffer: each rank overwrites it with its own Q,
+        # then rank 0's copy is broadcast (engine.cpp:498-501)
+        api.compress(L, self.pending, r, QuantSpec(q, cfg.rounding),
+                     self.warm_q if self.warm_rank == r else None, self.warm_rank,
+                     cfg.power_iters, s0, payload=self.payload[:pb], q_out=self.warm_q[:max(qel, 1)])
+        gathered = self._exchange(pb, qel)
+        cur = torch.cuda.current_stream()
+        if cfg.adaptive and self._n2:
+            # factor-space effective rank on the side stream, overlapping the outer update
+            side = self.side or cur
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                per, energy = api.effective_rank_device(L, gathered, self.world, r, q, cfg.tau,
+                                                        stream=side)
+                self.per_host.copy_(per, non_blocking=True)
+                self.energy_host.copy_(energy, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(side)
+        api.outer_update(L, gathered, self.world, r, q, self.pending, self.anchor, local,
+                         self.velocity, cfg.outer_lr, cfg.outer_momentum, cfg.outer_classical,
+                         mode=mode, self_index=self.rank if cfg.measure_error else -1,
+                         stats=self.stats, stream=cur)
+        self.stats_host.copy_(self.stats, non_blocking=True)
+        rec = RoundRecord(round=self.round, r_t=r, H_t=self.H_t, averaged=True,
+                          payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
+        if cfg.adaptive and self._n2:
+            ev.synchronize()
+            er = api.effective_rank_reduce(L, self.per_host.numpy()[:self._n2],
+                                           self.energy_host.numpy()[:self._n2], cfg.rank1)
+            rec.r_prime = er.aggregate
+            cur.wait_stream(self.side or cur)
+        self.warm_rank = r
+        return rec
+
+    def _finish(self, rec: RoundRecord, mode: int) -> RoundRecord:
+        torch.cuda.current_stream().synchronize()
+        st = self.stats_host.numpy()
+        if rec.averaged:
+            rec.comp_error = float(st[0] / st[1]) if st[1] > 0 else 0.0
+            rec.bound_violated = rec.omega_sq > 0 and rec.comp_error > rec.omega_sq
+            rec.err_buf_norm = math.sqrt(st[3])
+            rec.nonfinite = int(st[4])
+            if mode == OVERLAPPED:
+                rec.max_delta_norm = math.sqrt(st[2])
+        if rec.nonfinite:
+            from ._lib import NumericError
+            raise NumericError(f"outer update produced {rec.nonfinite} non-finite parameters")
+        self.last = rec
+        return rec
+
+    def _adapt(self):
+        cfg = self.cfg
+        if not cfg.adaptive:
+            return self.r_t, self.H_t
+        return api.adapt_compression(self.window, cfg.rank1, cfg.H1, cfg.window_c,
+                                     cfg.resolved_H_min())
+
+    def _push_window(self, r_prime: int):
+        self.window.append(r_prime)
+        if len(self.window) > self.cfg.window_c:
+            del self.window[:len(self.window) - self.cfg.window_c]
+
+    # -- rounds -------------------------------------------------------------------------
+    def round_overlapped(self, local: torch.Tensor) -> RoundRecord:
+        """run_round_overlapped (engine.cpp:458-509) minus inner training: the sync of the
+        previous round's delta, then staging of this round's delta against the pre-update
+        anchor, then the one-step-delayed Nesterov step — all fused in one device pass."""
+        self.round += 1
+        if self.has_pending:
+            rec = self.collective_average(local, OVERLAPPED)
+            if self.cfg.adaptive:
+                self._push_window(rec.r_prime)
+        else:
+            rec = RoundRecord(round=self.round, r_t=self.r_t, H_t=self.H_t)
+            api.stage_deltas(self.L, self.anchor, local, None, self.pending, None)
+        r_next, h_next = self._adapt()
+        self.has_pending = True
+        rec = self._finish(rec, OVERLAPPED)
+        self.r_t, self.H_t = r_next, h_next
+        return rec
+
+    def round_sync(self, local: torch.Tensor) -> RoundRecord:
+        """run_round_sync (engine.cpp:423-456): stage with the carried error, average the
+        fresh delta, then Nesterov (pending carries e between rounds)."""
+        self.round += 1
+        api.stage_deltas(self.L, self.anchor, local, self.pending if self.has_pending else None,
+                         self.pending, None)
+        self.has_pending = True
+        rec = self.collective_average(None, SYNC)
+        r_next, h_next = self.r_t, self.H_t
+        if self.cfg.adaptive:
+            self._push_window(rec.r_prime)
+            r_next, h_next = self._adapt()
+        rec = self._finish(rec, SYNC)
+        self.r_t, self.H_t = r_next, h_next
+        return rec
+
+    def step(self, local: torch.Tensor) -> RoundRecord:
+        return self.round_overlapped(local) if self.cfg.overlap else self.round_sync(local)

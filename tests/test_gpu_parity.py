@@ -1,0 +1,311 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle and the reference's
+golden vectors. Bars (BASELINE.json north_star):
+  * integer / byte work bit-exact: RNG draws, codes, scales, packed payload bytes, draw counts;
+  * reference-exact fp64 helpers (decompress, allreduce_avg) bit-exact;
+  * elementwise epilogue (staging, error feedback, Nesterov) bit-exact given Delta;
+  * fused fp32-accumulate reconstruction: per tensor ||Delta_gpu - Delta_ref||_F <= 1e-5 ||Delta_ref||_F
+    and max|Delta_gpu - Delta_ref| <= 1e-5 max|Delta_ref| (TOL_RECON);
+  * power iteration (fp32 GEMMs vs fp64): |Q_gpu - Q_ref| <= 1e-4, >= 99.9% identical codes,
+    decompressed payload rel. Frobenius difference <= 1e-3 (TOL_COMPRESS).
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import Table
+from tests._util import decode_payload, draws_between, rel_fro, split_dense, split_q
+
+pytestmark = pytest.mark.gpu
+
+TOL_RECON = 1e-5
+TOL_Q = 1e-4
+TOL_COMPRESS = 1e-3
+
+TABLES = {
+    "mixed": [(24, 18), (18,), (18, 6), (6,), (10, 8)],
+    "zero2d": [(16, 12), (12,)],
+    "clamp": [(6, 4), (7,), (40, 33)],
+}
+
+
+def mk(ctx, shapes):
+    from paper_2506_21263_b200 import api
+    return api.Layout(ctx, [(f"t{i}", s) for i, s in enumerate(shapes)])
+
+
+def test_fill_gaussian_bitexact(ctx, oracle):
+    from paper_2506_21263_b200 import api
+    shapes = [(24, 18), (18,), (300, 7)]
+    L = mk(ctx, shapes)
+    out = L.empty()
+    api.fill_gaussian(L, out, 0.02, seed=7, tag=0xA7C4, worker=3)
+    base = out.clone()
+    api.fill_gaussian(L, out, -1e-3, seed=1, tag=0xDA7A, worker=1, base=base)
+    got0 = L.from_slab(base)
+    got1 = L.from_slab(out)
+    for t, s in enumerate(shapes):
+        n = int(np.prod(s))
+        g, _ = oracle.gaussian(oracle.stream(7, oracle.stream_key(0xA7C4, 3, t)), n)
+        want0 = (np.float32(0.02) * g).astype(np.float32)
+        assert np.array_equal(got0[t].reshape(-1), want0)
+        g1, _ = oracle.gaussian(oracle.stream(1, oracle.stream_key(0xDA7A, 1, t)), n)
+        want1 = (want0 + (np.float32(-1e-3) * g1).astype(np.float32)).astype(np.float32)
+        assert np.array_equal(got1[t].reshape(-1), want1)
+
+
+@pytest.mark.parametrize("tname", list(TABLES))
+@pytest.mark.parametrize("q", [2, 4, 5, 8])
+@pytest.mark.parametrize("rnd", [0, 1])
+@pytest.mark.parametrize("rank", [3, 6])
+def test_quantize_factors_bitexact(ctx, oracle, golden, tname, q, rnd, rank):
+    """North-star bar: codes + scales bit-exact when fed the reference's fp32 factors."""
+    from paper_2506_21263_b200 import api
+    shapes = TABLES[tname]
+    L = mk(ctx, shapes)
+    key = f"c_{tname}_q{q}_r{rnd}_k{rank}"
+    data = golden[f"c_{tname}_data"]
+    delta = L.pack(data)
+    dense = split_dense(shapes, data)
+    st0 = int(golden[key + "_state0"][0])
+    for variant in ("", "_warm"):
+        qs = split_q(shapes, rank, golden[f"{key}{variant}_q"])
+        ps = [oracle.matmul(d, qm) for d, qm in zip([d for d, s in zip(dense, shapes) if len(s) == 2], qs)]
+        P = L.factors_to_device(ps, rank, 0)
+        Q = L.factors_to_device(qs, rank, 1)
+        payload, draws = api.quantize_factors(L, P, Q, delta, rank, api.QuantSpec(q, rnd), st0,
+                                              cold=(variant == ""))
+        codes, scales = decode_payload(L, payload, rank, q)
+        gc = golden[f"{key}{variant}_codes"] if variant else golden[key + "_codes"]
+        gs = golden[f"{key}{variant}_scales"] if variant else golden[key + "_scales"]
+        assert np.array_equal(codes, gc), variant
+        assert np.array_equal(scales.view(np.uint32), gs.view(np.uint32)), variant
+        s1 = int(golden[f"{key}{variant}_state1"][0])
+        assert int(draws.item()) == draws_between(st0, s1), variant
+        if variant == "":
+            wire = L.serialize(payload, rank, q, names=[f"t{i}" for i in range(len(shapes))])
+            assert np.array_equal(np.frombuffer(wire, np.uint8), golden[key + "_wire"])
+            back = L.parse(wire, rank, q)
+            assert np.array_equal(back.cpu().numpy(), payload.cpu().numpy())
+
+
+def test_parse_rejects_corruption(ctx, golden):
+    from paper_2506_21263_b200 import FormatError
+    L = mk(ctx, TABLES["mixed"])
+    wire = golden["c_mixed_q4_r0_k3_wire"].tobytes()
+    with pytest.raises(FormatError):
+        L.parse(wire[: len(wire) // 2], 3, 4)
+    bad = bytearray(wire)
+    bad[0] ^= 0xFF
+    with pytest.raises(FormatError):
+        L.parse(bytes(bad), 3, 4)
+    with pytest.raises(FormatError):
+        L.parse(wire + b"\x00", 3, 4)
+
+
+def _payload_from_oracle(L, oracle, table, ranks, rank, q, codes, scales):
+    wire = oracle.serialize(table, ranks, rank, q, codes, scales)
+    return L.parse(wire, rank, q)
+
+
+def test_allreduce_decompress_bitexact(ctx, oracle, golden):
+    from paper_2506_21263_b200 import api
+    import torch
+    shapes = [(16, 12), (12,)]
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    ranks = golden["ar_ranks"]
+    pays = [_payload_from_oracle(L, oracle, t, ranks, 4, 4, golden[f"ar_codes_{i}"],
+                                 golden[f"ar_scales_{i}"]) for i in range(3)]
+    gathered = torch.cat(pays)
+    avg = api.allreduce_avg(L, gathered, 3, 4, 4)
+    assert np.array_equal(L.unpack(avg), golden["ar_avg"])
+    dec = api.decompress(L, pays[1], 4, 4)
+    want = oracle.decompress(t, ranks, golden["ar_codes_1"], golden["ar_scales_1"])
+    assert np.array_equal(L.unpack(dec), want)
+
+
+def _rand_state(oracle, L, seed):
+    n = L.total_params
+    anchor = (np.float32(0.02) * oracle.gaussian(oracle.stream(seed, 1), n)[0]).astype(np.float32)
+    local = (anchor - np.float32(1e-3) * oracle.gaussian(oracle.stream(seed, 2), n)[0]).astype(np.float32)
+    vel = (np.float32(1e-4) * oracle.gaussian(oracle.stream(seed, 3), n)[0]).astype(np.float32)
+    pend = (np.float32(1e-3) * oracle.gaussian(oracle.stream(seed, 4), n)[0]).astype(np.float32)
+    return anchor, local, vel, pend
+
+
+@pytest.mark.parametrize("D", [1, 2, 3])
+@pytest.mark.parametrize("classical", [False, True])
+def test_outer_update_against_oracle(ctx, oracle, D, classical):
+    """Fused K5: Delta within TOL_RECON of allreduce_avg; epilogue bit-exact given Delta."""
+    from paper_2506_21263_b200 import api
+    import torch
+    shapes = [(40, 36), (36,), (64, 130), (130,), (7, 5), (9,)]
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    rank, q = 6, 4
+    ranks = t.ranks(rank)
+    codes, scales, pays = [], [], []
+    for w in range(D):
+        d = oracle.gaussian(oracle.stream(w, 6), t.numel())[0]
+        c = oracle.compress(t, d, rank, q, 0, 2, oracle.stream(7, 7))
+        codes.append(c["codes"]); scales.append(c["scales"])
+        pays.append(_payload_from_oracle(L, oracle, t, ranks, rank, q, c["codes"], c["scales"]))
+    gathered = torch.cat(pays)
+    ref = oracle.allreduce_avg(t, ranks, codes, scales)
+    # Delta_gpu via sync mode on a zero pending buffer: pending' = 0 - Delta
+    z = L.empty(); a0 = L.empty(); v0 = L.empty()
+    api.outer_update(L, gathered, D, rank, q, z, a0, None, v0, 0.7, 0.9, classical, mode=api.SYNC)
+    dg = -L.unpack(z)
+    for i, (x, y) in enumerate(zip(split_dense(shapes, dg), split_dense(shapes, ref))):
+        if len(shapes[i]) == 1:
+            assert np.array_equal(x, y), i  # 1-D: reference-exact fp64 average
+        else:
+            assert rel_fro(x, y) <= TOL_RECON, i
+            assert np.abs(x - y).max() <= TOL_RECON * np.abs(y).max(), i
+    # overlapped epilogue, bit-exact given Delta_gpu (op order of engine.cpp / optim.cpp)
+    anchor, local, vel, pend = _rand_state(oracle, L, 11)
+    dA, dL, dV, dP = L.pack(anchor), L.pack(local), L.pack(vel), L.pack(pend)
+    stats = torch.zeros(8, dtype=torch.float64, device="cuda")
+    api.outer_update(L, gathered, D, rank, q, dP, dA, dL, dV, 0.7, 0.9, classical,
+                     mode=api.OVERLAPPED, self_index=0, stats=stats)
+    f = np.float32
+    dgf = dg.astype(np.float32)
+    e = (pend - dgf).astype(f)
+    want_p = ((anchor - local).astype(f) + e).astype(f)
+    want_v = ((f(0.9) * vel).astype(f) + dgf).astype(f)
+    if classical:
+        want_a = (anchor - (f(0.7) * want_v).astype(f)).astype(f)
+    else:
+        want_a = (anchor - (f(0.7) * (dgf + (f(0.9) * want_v).astype(f)).astype(f)).astype(f)).astype(f)
+    assert np.array_equal(L.unpack(dP), want_p)
+    assert np.array_equal(L.unpack(dV), want_v)
+    assert np.array_equal(L.unpack(dA), want_a)
+    st = stats.cpu().numpy()
+    # measure_error of worker 0 (compress.cpp:246-262)
+    ce = oracle.measure_error(t, pend, ranks, codes[0], scales[0])
+    assert abs(st[0] / st[1] - ce) <= 1e-4 * max(ce, 1e-12)
+    assert abs(st[3] - float(np.sum(e.astype(np.float64) ** 2))) <= 1e-6 * st[3]
+
+
+def test_stage_and_nesterov_bitexact(ctx, oracle, golden):
+    from paper_2506_21263_b200 import api
+    import torch
+    a = torch.from_numpy(golden["nest_in_a"]).cuda()
+    for cl in (0, 1):
+        aa, vv = a.clone(), torch.from_numpy(golden["nest_in_v"]).cuda()
+        api.nesterov_outer_step(ctx, aa, vv, torch.from_numpy(golden["nest_in_d"]).cuda(), 0.7, 0.9,
+                                bool(cl))
+        assert np.array_equal(aa.cpu().numpy(), golden[f"nest_out_a_{cl}"])
+        assert np.array_equal(vv.cpu().numpy(), golden[f"nest_out_v_{cl}"])
+    shapes = [(5, 7), (3,)]
+    L = mk(ctx, shapes)
+    anchor, local, vel, pend = _rand_state(oracle, L, 3)
+    dP = L.empty()
+    api.stage_deltas(L, L.pack(anchor), L.pack(local), L.pack(pend), dP)
+    assert np.array_equal(L.unpack(dP), ((anchor - local).astype(np.float32) + pend).astype(np.float32))
+    api.stage_deltas(L, L.pack(anchor), L.pack(local), None, dP)
+    assert np.array_equal(L.unpack(dP), ((anchor - local).astype(np.float32) + np.float32(0)))
+
+
+@pytest.mark.parametrize("tname", list(TABLES))
+@pytest.mark.parametrize("q,rnd", [(4, 0), (8, 1), (2, 0), (5, 0)])
+def test_compress_against_oracle(ctx, oracle, golden, tname, q, rnd):
+    """End-to-end compress (power iteration on device) vs the reference, cold then warm."""
+    from paper_2506_21263_b200 import api
+    shapes = TABLES[tname]
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    rank = 6
+    data = golden[f"c_{tname}_data"]
+    delta = L.pack(data)
+    st0 = oracle.stream(12, q * 10 + rnd)
+    ref = oracle.compress(t, data, rank, q, rnd, 2, st0)
+    res = api.compress(L, delta, rank, api.QuantSpec(q, rnd), None, 0, 2, st0)
+    _check_compress(L, t, oracle, ref, res, rank, q, st0)
+    ref_w = oracle.compress(t, data, rank, q, rnd, 1, st0, warm_rank=rank, warm_q=ref["q"])
+    warm = L.factors_to_device(split_q(shapes, rank, ref["q"]), rank, 1)
+    res_w = api.compress(L, delta, rank, api.QuantSpec(q, rnd), warm, rank, 1, st0)
+    _check_compress(L, t, oracle, ref_w, res_w, rank, q, st0)
+
+
+def _check_compress(L, t, oracle, ref, res, rank, q, st0):
+    codes, scales = decode_payload(L, res.payload, rank, q)
+    assert int(res.draws.item()) == draws_between(st0, ref["state"])
+    assert (codes == ref["codes"]).mean() >= 0.999
+    qs = L.factors_from_device(res.q_factors, rank, 1)
+    for got, want in zip(qs, split_q(t.shapes, rank, ref["q"])):
+        assert np.abs(got - want).max() <= TOL_Q
+    d_gpu = oracle.decompress(t, ref["ranks"], codes, scales)
+    d_ref = oracle.decompress(t, ref["ranks"], ref["codes"], ref["scales"])
+    assert rel_fro(d_gpu, d_ref) <= TOL_COMPRESS
+    assert np.allclose(scales, ref["scales"], rtol=1e-5, atol=0)
+
+
+def test_compress_larger_shapes(ctx, oracle):
+    """Multi-tile GEMM paths (k-split of K2 above 2048 rows, r > 32 tile variant)."""
+    from paper_2506_21263_b200 import api
+    for shapes, rank in (([(2600, 96), (96,), (128, 300)], 8), ([(300, 260), (260,)], 40)):
+        t = Table(shapes)
+        L = mk(ctx, shapes)
+        st = oracle.stream(5, 5)
+        # low-rank + noise spectrum (tools/dilocox.cpp:183-192) so the subspace is well defined
+        data = []
+        for i, s in enumerate(shapes):
+            if len(s) == 2:
+                a, b = s
+                u = oracle.gaussian(oracle.stream(i, 1), a * rank)[0].reshape(a, rank)
+                v = oracle.gaussian(oracle.stream(i, 2), b * rank)[0].reshape(b, rank)
+                m = oracle.matmul_nt(u, v)
+                n = oracle.gaussian(oracle.stream(i, 3), a * b)[0].reshape(a, b)
+                data.append((m + np.float32(0.05) * n).reshape(-1))
+            else:
+                data.append(oracle.gaussian(oracle.stream(i, 4), s[0])[0])
+        flat = np.concatenate(data).astype(np.float32)
+        ref = oracle.compress(t, flat, rank, 8, 0, 2, st)
+        res = api.compress(L, L.pack(flat), rank, api.QuantSpec(8, 0), None, 0, 2, st)
+        _check_compress(L, t, oracle, ref, res, rank, 8, st)
+
+
+def test_effective_rank_factor_space(ctx, oracle):
+    from paper_2506_21263_b200 import api
+    import torch
+    shapes = [(48, 40), (40,), (30, 64), (20, 20)]
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    rank, q, D = 6, 8, 3
+    ranks = t.ranks(rank)
+    codes, scales, pays = [], [], []
+    for w in range(D):
+        d = oracle.gaussian(oracle.stream(w, 9), t.numel())[0]
+        c = oracle.compress(t, d, rank, q, 0, 2, oracle.stream(3, 3))
+        codes.append(c["codes"]); scales.append(c["scales"])
+        pays.append(_payload_from_oracle(L, oracle, t, ranks, rank, q, c["codes"], c["scales"]))
+    avg = oracle.allreduce_avg(t, ranks, codes, scales)
+    for tau in (0.3, 0.5, 0.9):
+        per, agg, allz = oracle.effective_rank(t, avg, tau, rank)
+        er = api.effective_rank(L, torch.cat(pays), D, rank, q, tau, rank)
+        assert [k for _, k in er.per_tensor] == per.tolist()
+        assert er.aggregate == agg and er.all_zero == allz
+
+
+def test_errors_are_typed(ctx):
+    from paper_2506_21263_b200 import ShapeError, ValidationError, api
+    L = mk(ctx, [(8, 8)])
+    d = L.empty()
+    with pytest.raises(ValidationError):
+        api.compress(L, d, 0, api.QuantSpec(4, 0), None, 0, 2, 1)
+    with pytest.raises(ValidationError):
+        api.compress(L, d, 4, api.QuantSpec(9, 0), None, 0, 2, 1)
+    with pytest.raises(ValidationError):
+        api.compress(L, d, 4, api.QuantSpec(4, 0), None, 0, 0, 1)
+    with pytest.raises(ShapeError):
+        api.Layout(ctx, [("x", (2, 2, 2))])
+
+
+def test_opt_1_3b_geometry(ctx, oracle):
+    from paper_2506_21263_b200 import api, layouts
+    tbl = layouts.opt_1_3b()
+    L = api.Layout(ctx, tbl)
+    assert L.total_params == 1_315_758_080
+    t = Table([s for _, s in tbl])
+    assert L.payload_bits(32, 4) == oracle.payload_bits(t, t.ranks(32), 4)
+    assert abs(L.payload_bits(32, 4) / 8 / 1e6 - 15.418) < 0.001
