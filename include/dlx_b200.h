@@ -175,6 +175,10 @@ int64_t dlx_serialize(const dlx_layout* layout, int rank, int qbits, const char*
 dlx_status dlx_parse(const dlx_layout* layout, int rank, int qbits, const uint8_t* bytes,
                      int64_t size, uint8_t* h_payload);
 
+/* Runtime options. "tensor_cores" (default 1): 0 routes the power-iteration sweeps through
+ * the SIMT kernels instead of the tcgen05 ones (A/B testing; also env DLX_TENSOR_CORES=0). */
+dlx_status dlx_set_option(const char* key, int value);
+
 /* Number of kernels this library launched on the calling thread since the last call
  * (launch accounting for benchmarks). */
 uint64_t dlx_take_launch_count(void);

@@ -83,6 +83,7 @@ PROTOS = {
     "dlx_serialize": (_i64, [_vp, _i32, _i32, C.POINTER(C.c_char_p), _vp, _vp, _i64]),
     "dlx_parse": (_i32, [_vp, _i32, _i32, _vp, _i64, _vp]),
     "dlx_take_launch_count": (_u64, []),
+    "dlx_set_option": (_i32, [C.c_char_p, _i32]),
 }
 
 _lib = None

@@ -374,3 +374,9 @@ def omega_bound(r: int, d: int, q: int) -> float:
 
 def take_launch_count() -> int:
     return int(lib().dlx_take_launch_count())
+
+
+def set_option(key: str, value: int) -> None:
+    """dlx_set_option: e.g. set_option("tensor_cores", 0) routes the power-iteration sweeps
+    through the SIMT kernels (A/B testing)."""
+    check(lib().dlx_set_option(key.encode(), int(value)))

@@ -45,7 +45,7 @@ static T* upload(const std::vector<T>& v) {
 Plan::~Plan() {
   void* ptrs[] = {d_t2, d_t1, d_chunks, d_streams, d_mats[0], d_mats[1], d_k1_tiles,
                   d_k2_tiles, d_k2_part_off, d_k2_splits, d_k5_tiles, d_cold_base_spec[0],
-                  d_cold_base_spec[1]};
+                  d_cold_base_spec[1], d_k1_rest, d_k2_rest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -195,17 +195,22 @@ static std::unique_ptr<Plan> build_plan(const dlx_layout& L, int rank, int qbits
   int64_t part = 0;
   for (size_t k = 0; k < P->t2.size(); ++k) {
     const DevT2& t = P->t2[k];
+    const bool tc = tc_eligible(t);
     for (int64_t m0 = 0; m0 < t.a; m0 += bm1)
-      for (int n0 = 0; n0 < t.r; n0 += bn1)
+      for (int n0 = 0; n0 < t.r; n0 += bn1) {
         P->k1_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0), n0, 0));
+        if (!tc) P->k1_rest.push_back(P->k1_tiles.back());
+      }
     const int splits = static_cast<int>(ceil_div(t.a, kc));
     P->k2_splits.push_back(splits);
     P->k2_part_off.push_back(part);
     if (splits > 1) part += static_cast<int64_t>(splits) * t.ldb * t.r;
     for (int s = 0; s < splits; ++s)
       for (int64_t j0 = 0; j0 < t.b; j0 += 64)
-        for (int c0 = 0; c0 < t.r; c0 += bc2)
+        for (int c0 = 0; c0 < t.r; c0 += bc2) {
           P->k2_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(j0), c0, s));
+          if (!tc) P->k2_rest.push_back(P->k2_tiles.back());
+        }
     for (int64_t m0 = 0; m0 < t.a; m0 += 32)
       for (int64_t n0 = 0; n0 < t.b; n0 += 128)
         P->k5_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0),
@@ -224,6 +229,8 @@ static std::unique_ptr<Plan> build_plan(const dlx_layout& L, int rank, int qbits
   P->d_k2_part_off = upload(P->k2_part_off);
   P->d_k2_splits = upload(P->k2_splits);
   P->d_k5_tiles = upload(P->k5_tiles);
+  P->d_k1_rest = upload(P->k1_rest);
+  P->d_k2_rest = upload(P->k2_rest);
   P->d_cold_base_spec[0] = upload(P->cold_base_spec[0]);
   P->d_cold_base_spec[1] = upload(P->cold_base_spec[1]);
   return P;
@@ -275,6 +282,17 @@ extern "C" {
 
 const char* dlx_version(void) { return "dlx_b200 0.1 (sm_100a)"; }
 const char* dlx_last_error(void) { return g_last_error.c_str(); }
+dlx_status dlx_set_option(const char* key, int value) {
+  return guard([&] {
+    const std::string k = key ? key : "";
+    if (k == "tensor_cores") {
+      option_tensor_cores() = value != 0;
+    } else {
+      raise(DLX_ERR_VALIDATION, "unknown option: " + k);
+    }
+  });
+}
+
 uint64_t dlx_take_launch_count(void) {
   const uint64_t n = g_launches;
   g_launches = 0;

@@ -164,6 +164,9 @@ struct Plan {
   int4* d_k2_tiles = nullptr;
   int64_t* d_k2_part_off = nullptr;
   int* d_k2_splits = nullptr;
+  std::vector<int4> k1_rest, k2_rest;  // SIMT tiles of tensors outside the tcgen05 path
+  int4* d_k1_rest = nullptr;
+  int4* d_k2_rest = nullptr;
   std::vector<int4> k5_tiles;  // (t2 slot, m0, n0, -)
   int4* d_k5_tiles = nullptr;
   // speculative cold-start draw bases per 2-D slot, [0] stochastic (assumes no all-zero
@@ -179,6 +182,12 @@ void launch_fill_gaussian(const dlx_layout& L, float* out, const float* base, fl
 void launch_cold_init(const Plan& P, float* q, const int64_t* d_cold_base, uint64_t s0,
                       cudaStream_t s);
 void launch_k1(const Plan& P, const float* slab, const float* q, float* y, cudaStream_t s);
+bool tc_supported(const Plan& P);
+bool tc_eligible(const DevT2& t);
+void launch_k1_tc(const Plan& P, const float* slab, const float* q, float* y, cudaStream_t s);
+void launch_k2_tc(const Plan& P, const float* slab, const float* p, float* z, float* part,
+                  cudaStream_t s);
+bool& option_tensor_cores();
 void launch_k2(const Plan& P, const float* slab, const float* p, float* z, float* part,
                cudaStream_t s);
 void orthonormalize_batched(dlx_ctx* ctx, const Plan& P, int side, float* buf, float* tmp,

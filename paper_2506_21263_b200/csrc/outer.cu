@@ -60,14 +60,39 @@ __device__ __forceinline__ void stats_add(dlx_round_stats* st, double num, doubl
 // ------------------------------------------------------------------ K5, 2-D tensors
 // Tile 32 rows x 128 cols of delta; 256 threads, each 4 rows x 4 consecutive cols.
 // Delta_tile = (1/D) * Phat[rows, :] Qhat[cols, :]^T with K = D*r (fp32 accumulate).
-__global__ void __launch_bounds__(256) k5_outer(const DevT2* __restrict__ T,
-                                                const int4* __restrict__ tiles,
-                                                const float* __restrict__ phat,
-                                                const float* __restrict__ qhat, int D,
-                                                int self_index, int mode, float* pending,
-                                                float* anchor, const float* __restrict__ local,
-                                                float* velocity, float gamma, float beta,
-                                                int classical, dlx_round_stats* stats) {
+// The four streamed operands of the tile are loaded (evict-first) before the small
+// factor GEMM so their HBM latency overlaps it: 256 B in flight per thread.
+__device__ __forceinline__ void load4(const float* p, bool full, int nv, float (&v)[4]) {
+  if (full) {
+    const float4 x = __ldcs(reinterpret_cast<const float4*>(p));
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = j < nv ? p[j] : 0.f;
+  }
+}
+
+__device__ __forceinline__ void store4(float* p, bool full, int nv, const float (&v)[4]) {
+  if (full) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < nv) p[j] = v[j];
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) k5_outer(const DevT2* __restrict__ T,
+                                                   const int4* __restrict__ tiles,
+                                                   const float* __restrict__ phat,
+                                                   const float* __restrict__ qhat, int D,
+                                                   int self_index, int mode,
+                                                   float* __restrict__ pending,
+                                                   float* __restrict__ anchor,
+                                                   const float* __restrict__ local,
+                                                   float* __restrict__ velocity, float gamma,
+                                                   float beta, int classical,
+                                                   dlx_round_stats* stats) {
   __shared__ __align__(16) float Ps[32][36];
   __shared__ __align__(16) float Qs[32][132];
   const int4 tile = tiles[blockIdx.x];
@@ -78,6 +103,32 @@ __global__ void __launch_bounds__(256) k5_outer(const DevT2* __restrict__ T,
   const float* Ph = phat + D * t.poff;
   const float* Qh = qhat + D * t.qoff;
   const int s_lo = self_index >= 0 ? self_index * t.r : K, s_hi = s_lo + t.r;
+  const bool vec = (t.b % 4) == 0;
+  const bool ovl = mode == DLX_MODE_OVERLAPPED;
+  const int64_t col = n0 + tx * 4;
+  const int nv = col < t.b ? (int)(t.b - col < 4 ? t.b - col : 4) : 0;
+
+  // 1. streamed operands of this thread's 4 rows
+  float pd[4][4], an[4][4], lo[4][4], ve[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = m0 + ty * 4 + i;
+    const bool live = row < t.a && nv > 0;
+    const int n = live ? nv : 0;
+    const bool full = live && vec && nv == 4;
+    const int64_t base = t.off + (live ? row * t.b + col : 0);
+    load4(pending + base, full, n, pd[i]);
+    load4(anchor + base, full, n, an[i]);
+    if (ovl) {
+      load4(local + base, full, n, lo[i]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) lo[i][j] = 0.f;
+    }
+    load4(velocity + base, full, n, ve[i]);
+  }
+
+  // 2. factor GEMM
   float acc[4][4], sacc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -88,10 +139,7 @@ __global__ void __launch_bounds__(256) k5_outer(const DevT2* __restrict__ T,
       const int kk = tid / 8, c4 = (tid % 8) * 4;
       const int k = k0 + kk;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (k < K) {
-        const float* src = Ph + (int64_t)k * t.lda + m0 + c4;  // lda % 32 == 0 -> aligned
-        v = *reinterpret_cast<const float4*>(src);            // rows >= a are zero padding
-      }
+      if (k < K) v = *reinterpret_cast<const float4*>(Ph + (int64_t)k * t.lda + m0 + c4);
       *reinterpret_cast<float4*>(&Ps[kk][c4]) = v;
     }
 #pragma unroll
@@ -122,65 +170,39 @@ __global__ void __launch_bounds__(256) k5_outer(const DevT2* __restrict__ T,
     }
     __syncthreads();
   }
+
+  // 3. fused epilogue
   const float invD = __fdiv_rn(1.0f, (float)D);
   double num = 0.0, den = 0.0, dn = 0.0, en = 0.0, nf = 0.0;
-  const bool vec = (t.b % 4) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t row = m0 + ty * 4 + i;
-    if (row >= t.a) continue;
-    const int64_t col = n0 + tx * 4;
-    if (col >= t.b) continue;
+    if (row >= t.a || nv == 0) continue;
     const int64_t base = t.off + row * t.b + col;
-    float pd[4], an[4], lo[4], ve[4];
-    const int nv = (int)(t.b - col < 4 ? t.b - col : 4);
-    if (vec && nv == 4) {
-      const float4 a = *reinterpret_cast<const float4*>(pending + base);
-      const float4 b = *reinterpret_cast<const float4*>(anchor + base);
-      const float4 c = mode == DLX_MODE_OVERLAPPED ? __ldg(reinterpret_cast<const float4*>(local + base)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 d = *reinterpret_cast<const float4*>(velocity + base);
-      pd[0] = a.x; pd[1] = a.y; pd[2] = a.z; pd[3] = a.w;
-      an[0] = b.x; an[1] = b.y; an[2] = b.z; an[3] = b.w;
-      lo[0] = c.x; lo[1] = c.y; lo[2] = c.z; lo[3] = c.w;
-      ve[0] = d.x; ve[1] = d.y; ve[2] = d.z; ve[3] = d.w;
-    } else {
-      for (int j = 0; j < 4; ++j) {
-        pd[j] = j < nv ? pending[base + j] : 0.f;
-        an[j] = j < nv ? anchor[base + j] : 0.f;
-        lo[j] = (j < nv && mode == DLX_MODE_OVERLAPPED) ? local[base + j] : 0.f;
-        ve[j] = j < nv ? velocity[base + j] : 0.f;
-      }
-    }
     float op[4], oa[4], ov[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float delta = __fmul_rn(acc[i][j], invD);
-      const EpiOut o = epilogue(delta, pd[j], an[j], lo[j], ve[j], mode, gamma, beta, classical);
+      const EpiOut o = epilogue(delta, pd[i][j], an[i][j], lo[i][j], ve[i][j], mode, gamma, beta,
+                                classical);
       op[j] = o.pend;
       oa[j] = o.anchor;
       ov[j] = o.v;
       if (j < nv) {
         if (self_index >= 0) {
-          const double df = (double)sacc[i][j] - (double)pd[j];
+          const double df = (double)sacc[i][j] - (double)pd[i][j];
           num += df * df;
-          den += (double)pd[j] * (double)pd[j];
+          den += (double)pd[i][j] * (double)pd[i][j];
         }
         en += (double)o.e * (double)o.e;
-        if (mode == DLX_MODE_OVERLAPPED) dn += (double)o.pend * (double)o.pend;
+        if (ovl) dn += (double)o.pend * (double)o.pend;
         if (!isfinite(o.anchor)) nf += 1.0;
       }
     }
-    if (vec && nv == 4) {
-      *reinterpret_cast<float4*>(pending + base) = make_float4(op[0], op[1], op[2], op[3]);
-      *reinterpret_cast<float4*>(anchor + base) = make_float4(oa[0], oa[1], oa[2], oa[3]);
-      *reinterpret_cast<float4*>(velocity + base) = make_float4(ov[0], ov[1], ov[2], ov[3]);
-    } else {
-      for (int j = 0; j < nv; ++j) {
-        pending[base + j] = op[j];
-        anchor[base + j] = oa[j];
-        velocity[base + j] = ov[j];
-      }
-    }
+    const bool full = vec && nv == 4;
+    store4(pending + base, full, nv, op);
+    store4(anchor + base, full, nv, oa);
+    store4(velocity + base, full, nv, ov);
   }
   stats_add(stats, num, den, dn, en, nf, nullptr);
 }

@@ -5,6 +5,8 @@
 // padded column strides. Both sweeps are HBM-bound for r <~ 80 (2r flops per 4 B of
 // delta); each delta element is read exactly once per sweep. Accumulation is fp32 with a
 // fixed per-thread order (deterministic; the reference accumulates in fp64, tolerance).
+#include <cstdlib>
+
 #include "dlx_internal.cuh"
 
 namespace dlx {
@@ -177,13 +179,27 @@ __global__ void __launch_bounds__(256) k1_gemm(const DevT2* __restrict__ T,
   }
 }
 
+bool& option_tensor_cores() {
+  static bool on = [] {
+    const char* e = getenv("DLX_TENSOR_CORES");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static bool use_tc(const Plan& P) { return option_tensor_cores() && tc_supported(P); }
+
 void launch_k1(const Plan& P, const float* slab, const float* q, float* y, cudaStream_t s) {
-  if (P.k1_tiles.empty()) return;
-  const int n = static_cast<int>(P.k1_tiles.size());
+  const bool tc = use_tc(P);
+  if (tc) launch_k1_tc(P, slab, q, y, s);
+  const std::vector<int4>& tiles = tc ? P.k1_rest : P.k1_tiles;
+  const int4* d_tiles = tc ? P.d_k1_rest : P.d_k1_tiles;
+  if (tiles.empty()) return;
+  const int n = static_cast<int>(tiles.size());
   if (P.rmax <= 32)
-    k1_gemm<128, 32><<<n, 256, 0, s>>>(P.d_t2, P.d_k1_tiles, slab, q, y);
+    k1_gemm<128, 32><<<n, 256, 0, s>>>(P.d_t2, d_tiles, slab, q, y);
   else
-    k1_gemm<64, 64><<<n, 256, 0, s>>>(P.d_t2, P.d_k1_tiles, slab, q, y);
+    k1_gemm<64, 64><<<n, 256, 0, s>>>(P.d_t2, d_tiles, slab, q, y);
   DLX_LAUNCHED();
 }
 
@@ -306,14 +322,20 @@ __global__ void k2_reduce(const DevT2* __restrict__ T, const int* __restrict__ s
 void launch_k2(const Plan& P, const float* slab, const float* p, float* z, float* part,
                cudaStream_t s) {
   if (P.k2_tiles.empty()) return;
-  const int n = static_cast<int>(P.k2_tiles.size());
-  if (P.rmax <= 32)
-    k2_gemm<32><<<n, 256, 0, s>>>(P.d_t2, P.d_k2_tiles, P.d_k2_splits, P.d_k2_part_off, slab,
-                                  p, z, part);
-  else
-    k2_gemm<64><<<n, 256, 0, s>>>(P.d_t2, P.d_k2_tiles, P.d_k2_splits, P.d_k2_part_off, slab,
-                                  p, z, part);
-  DLX_LAUNCHED();
+  const bool tc = use_tc(P);
+  if (tc) launch_k2_tc(P, slab, p, z, part, s);
+  const std::vector<int4>& tiles = tc ? P.k2_rest : P.k2_tiles;
+  const int4* d_tiles = tc ? P.d_k2_rest : P.d_k2_tiles;
+  const int n = static_cast<int>(tiles.size());
+  if (n > 0) {
+    if (P.rmax <= 32)
+      k2_gemm<32><<<n, 256, 0, s>>>(P.d_t2, d_tiles, P.d_k2_splits, P.d_k2_part_off, slab, p, z,
+                                    part);
+    else
+      k2_gemm<64><<<n, 256, 0, s>>>(P.d_t2, d_tiles, P.d_k2_splits, P.d_k2_part_off, slab, p, z,
+                                    part);
+    DLX_LAUNCHED();
+  }
   // split slots (static per plan): cache the list in a device arena keyed by the plan
   std::vector<int> slots;
   int64_t mx = 1;

@@ -1,0 +1,490 @@
+// tc_gemm.cu — tcgen05 / TMEM / TMA power-iteration sweeps (lowrank_approx
+// compress.cpp:70-77):  K1  Y = delta Q  (A = delta, K-major)   and
+//                       K2  Z = delta^T P (A = delta^T, MN-major), deterministic split-K.
+//
+// Both sweeps stream every element of delta from HBM exactly once; the factor operand
+// (Q or P, <= 256 columns) is the MMA N dimension. Precision: 3xTF32 — each fp32 operand
+// tile is split in shared memory into hi (tf32-exact, low 13 mantissa bits cleared) and
+// lo = x - hi, and the accumulator (fp32, TMEM) receives hi*hi + hi*lo + lo*hi, i.e.
+// ~fp32-grade products (the reference accumulates in fp64; tolerance-tested).
+//
+// Per CTA (persistent, one per SM): warp 0 = TMA producer (one elected lane), warp 1 =
+// tcgen05.mma issuer (one lane; also owns the TMEM allocation), warps 2-5 = 128 threads
+// that split each landed stage into hi/lo and, at the end of a tile, drain the TMEM
+// accumulator (tcgen05.ld) to the column-major factor buffer.
+// Pipeline (mbarriers per stage): full (TMA bytes) -> split (128 arrivals) -> empty
+// (tcgen05.commit); per tile: tmem_full (commit) -> tmem_empty (128 arrivals).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
+#include "dlx_internal.cuh"
+
+namespace dlx {
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Bounded wait: a pipeline bug traps (launch error) instead of hanging the device.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t n = 0;
+  while (!mbar_try(b, parity)) {
+    if (++n > (1u << 24)) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B (tcgen05 "version 1" layout).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;  // descriptor version (sm_100)
+  d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, M = 128.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn ? 1u << 15 : 0u) | (b_mn ? 1u << 16 : 0u) |
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+}
+
+// ------------------------------------------------------------------ kernel
+struct TcMaps {
+  CUtensorMap a;  // delta: K1 box {32, 128} (K-major); K2 box {32, 32} (MN-major)
+  CUtensorMap b;  // factor (Q for K1, P for K2): box {32, N}
+};
+
+constexpr int kTcThreads = 192;
+constexpr uint32_t kAStage = 128 * 32 * 4;  // 16 KB
+
+// A_MN: false = K1 (A = delta rows, K-major), true = K2 (A = delta^T, MN-major).
+template <bool A_MN>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_tc_sweep(const DevT2* __restrict__ T, const TcMaps* __restrict__ maps,
+               const int4* __restrict__ tiles, int ntiles, int N, int stages,
+               const int* __restrict__ splits, const int64_t* __restrict__ part_off,
+               float* __restrict__ out, float* __restrict__ part) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t b_bytes = static_cast<uint32_t>(N) * 128;
+  const uint32_t stage_bytes = 2 * kAStage + 2 * b_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* split = bars + stages;
+  uint64_t* empty = bars + 2 * stages;
+  uint64_t* tfull = bars + 3 * stages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t tmem_cols = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr int64_t KC = 2048;
+
+  // k-loop extent of a tile
+  auto tile_k = [&](const int4& tl, const DevT2& t, int64_t& k0, int64_t& k1) {
+    if (!A_MN) {
+      k0 = 0;
+      k1 = t.b;
+    } else {
+      k0 = tl.w * KC;
+      k1 = min(t.a, k0 + KC);
+    }
+  };
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const int4 tl = tiles[ti];
+        const DevT2 t = T[tl.x];
+        const TcMaps* mp = maps + tl.x;
+        prefetch_map(&mp->a);
+        prefetch_map(&mp->b);
+        int64_t k0, k1;
+        tile_k(tl, t, k0, k1);
+        for (int64_t k = k0; k < k1; k += 32, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (it / stages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * stage_bytes;
+          mbar_expect_tx(&full[s], kAStage + b_bytes);
+          if (!A_MN) {
+            tma_load_2d(st, &mp->a, &full[s], static_cast<int>(k), tl.y);  // {k, m0}
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)  // 4 MN blocks of 32 columns, 32 rows each
+              tma_load_2d(st + q * 4096, &mp->a, &full[s], tl.y + 32 * q, static_cast<int>(k));
+          }
+          tma_load_2d(st + 2 * kAStage, &mp->b, &full[s], static_cast<int>(k), 0);  // {k, n}
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(N, A_MN, false);
+      uint32_t it = 0, tphase = 0;
+      for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const int4 tl = tiles[ti];
+        const DevT2 t = T[tl.x];
+        int64_t k0, k1;
+        tile_k(tl, t, k0, k1);
+        mbar_wait(tempty, tphase ^ 1);
+        tc_fence_after();
+        bool first = true;
+        for (int64_t k = k0; k < k1; k += 32, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (it / stages) & 1;
+          mbar_wait(&split[s], ph);
+          tc_fence_after();
+          const uint32_t a_hi = su32(smem + s * stage_bytes);
+          const uint32_t a_lo = a_hi + kAStage;
+          const uint32_t b_hi = a_hi + 2 * kAStage;
+          const uint32_t b_lo = b_hi + b_bytes;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            // K-major A: +32 B per 8-element k step inside the 128-B swizzle atom;
+            // MN-major A: one 8-row (1024-B) atom per k step, MN blocks 4096 B apart.
+            const uint32_t aoff = A_MN ? kk * 1024u : kk * 32u;
+            const uint32_t lbo = A_MN ? 4096u : 16u;
+            const uint64_t ah = sdesc(a_hi + aoff, lbo, 1024u);
+            const uint64_t al = sdesc(a_lo + aoff, lbo, 1024u);
+            const uint64_t bh = sdesc(b_hi + kk * 32u, 16u, 1024u);
+            const uint64_t bl = sdesc(b_lo + kk * 32u, 16u, 1024u);
+            mma_tf32(tmem, ah, bh, idesc, first ? 0u : 1u);
+            mma_tf32(tmem, ah, bl, idesc, 1u);
+            mma_tf32(tmem, al, bh, idesc, 1u);
+            first = false;
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(tfull);
+        tphase ^= 1;
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- split + epilogue
+    const int et = threadIdx.x - 64;     // 0..127
+    const int quarter = warp % 4;        // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane; // accumulator row (M index) of this thread
+    uint32_t it = 0, tphase = 0;
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+      const int4 tl = tiles[ti];
+      const DevT2 t = T[tl.x];
+      int64_t k0, k1;
+      tile_k(tl, t, k0, k1);
+      for (int64_t k = k0; k < k1; k += 32, ++it) {
+        const int s = it % stages;
+        const uint32_t ph = (it / stages) & 1;
+        mbar_wait(&full[s], ph);
+        uint8_t* st = smem + s * stage_bytes;
+        // hi = tf32-exact truncation (written back), lo = x - hi
+        float4* ah = reinterpret_cast<float4*>(st);
+        float4* al = reinterpret_cast<float4*>(st + kAStage);
+#pragma unroll 4
+        for (int i = et; i < static_cast<int>(kAStage / 16); i += 128) {
+          float4 x = ah[i], h, l;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u); l.x = x.x - h.x;
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u); l.y = x.y - h.y;
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u); l.z = x.z - h.z;
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u); l.w = x.w - h.w;
+          ah[i] = h;
+          al[i] = l;
+        }
+        float4* bh = reinterpret_cast<float4*>(st + 2 * kAStage);
+        float4* bl = reinterpret_cast<float4*>(st + 2 * kAStage + b_bytes);
+        for (int i = et; i < static_cast<int>(b_bytes / 16); i += 128) {
+          float4 x = bh[i], h, l;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u); l.x = x.x - h.x;
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u); l.y = x.y - h.y;
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u); l.z = x.z - h.z;
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u); l.w = x.w - h.w;
+          bh[i] = h;
+          bl[i] = l;
+        }
+        fence_async_smem();
+        mbar_arrive(&split[s]);
+      }
+      // epilogue: TMEM -> column-major factor (or split-K partial)
+      mbar_wait(tfull, tphase);
+      tc_fence_after();
+      const int64_t m = tl.y + row;
+      const int64_t mlim = A_MN ? t.b : t.a;
+      const int64_t ld = A_MN ? t.ldb : t.lda;
+      float* dst;
+      if (!A_MN) {
+        dst = out + t.poff;
+      } else {
+        dst = splits[tl.x] > 1 ? part + part_off[tl.x] + tl.w * (t.ldb * t.r) : out + t.qoff;
+      }
+      for (int c = 0; c < N; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
+        if (m < mlim) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c + j < t.r) dst[(c + j) * ld + m] = v[j];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+      tphase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(tmem_cols));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    DLX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static void encode(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t stride1_bytes,
+                   uint32_t b0, uint32_t b1) {
+  const cuuint64_t dims[2] = {d0, d1};
+  const cuuint64_t strides[1] = {stride1_bytes};
+  const cuuint32_t box[2] = {b0, b1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
+bool tc_eligible(const DevT2& t) { return (t.b % 4) == 0 && t.r >= 1; }
+
+int tc_n(const Plan& P) { return static_cast<int>(std::max<int64_t>(16, round_up(P.rmax, 16))); }
+
+struct TcState {
+  std::vector<int4> k1, k2;
+  int4* d_k1 = nullptr;
+  int4* d_k2 = nullptr;
+  TcMaps* d_maps[2] = {nullptr, nullptr};
+  const void* key[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  std::vector<TcMaps> host[2];
+};
+
+static TcState& tc_state(const Plan& P) {
+  static thread_local std::map<const Plan*, std::unique_ptr<TcState>> cache;
+  auto& s = cache[&P];
+  if (!s) {
+    s.reset(new TcState());
+    constexpr int64_t KC = 2048;
+    for (size_t k = 0; k < P.t2.size(); ++k) {
+      const DevT2& t = P.t2[k];
+      if (!tc_eligible(t)) continue;
+      for (int64_t m0 = 0; m0 < t.a; m0 += 128) s->k1.push_back(make_int4((int)k, (int)m0, 0, 0));
+      const int sp = static_cast<int>(ceil_div(t.a, KC));
+      for (int q = 0; q < sp; ++q)
+        for (int64_t j0 = 0; j0 < t.b; j0 += 128) s->k2.push_back(make_int4((int)k, (int)j0, 0, q));
+    }
+    auto up = [](const std::vector<int4>& v) {
+      int4* d = nullptr;
+      if (v.empty()) return d;
+      DLX_CUDA(cudaMalloc(&d, sizeof(int4) * v.size()));
+      DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(int4) * v.size(), cudaMemcpyHostToDevice));
+      return d;
+    };
+    s->d_k1 = up(s->k1);
+    s->d_k2 = up(s->k2);
+    for (int w = 0; w < 2; ++w) {
+      DLX_CUDA(cudaMalloc(&s->d_maps[w], sizeof(TcMaps) * std::max<size_t>(P.t2.size(), 1)));
+      s->host[w].resize(P.t2.size());
+    }
+  }
+  return *s;
+}
+
+// which = 0: K1 maps (delta box {32,128}, Q); which = 1: K2 maps (delta box {32,32}, P)
+static const TcMaps* tc_maps(const Plan& P, int which, const float* slab, const float* fac,
+                             cudaStream_t s) {
+  TcState& S = tc_state(P);
+  if (S.key[which][0] == slab && S.key[which][1] == fac) return S.d_maps[which];
+  const int N = tc_n(P);
+  for (size_t k = 0; k < P.t2.size(); ++k) {
+    const DevT2& t = P.t2[k];
+    TcMaps& m = S.host[which][k];
+    std::memset(&m, 0, sizeof(m));
+    if (!tc_eligible(t)) continue;
+    const float* A = slab + t.off;
+    if (which == 0) {
+      encode(&m.a, A, t.b, t.a, t.b * 4, 32, 128);
+      encode(&m.b, fac + t.qoff, t.b, t.r, t.ldb * 4, 32, N);
+    } else {
+      encode(&m.a, A, t.b, t.a, t.b * 4, 32, 32);
+      encode(&m.b, fac + t.poff, t.a, t.r, t.lda * 4, 32, N);
+    }
+  }
+  DLX_CUDA(cudaMemcpyAsync(S.d_maps[which], S.host[which].data(), sizeof(TcMaps) * P.t2.size(),
+                           cudaMemcpyHostToDevice, s));
+  DLX_CUDA(cudaStreamSynchronize(s));  // host staging buffer reused on the next re-encode
+  S.key[which][0] = slab;
+  S.key[which][1] = fac;
+  return S.d_maps[which];
+}
+
+static int tc_stages(int N) {
+  const int stage = 2 * 16384 + 2 * N * 128;
+  return std::max(2, std::min(6, (200 * 1024) / stage));
+}
+
+static size_t tc_smem(int N, int stages) {
+  return 1024 + static_cast<size_t>(stages) * (2 * 16384 + 2 * N * 128) + 8 * (3 * stages + 2) + 16;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    DLX_CUDA(cudaGetDevice(&dev));
+    DLX_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+template <bool A_MN>
+static void launch_sweep(const Plan& P, const TcMaps* maps, const std::vector<int4>& tiles,
+                         const int4* d_tiles, float* out, float* part, cudaStream_t s) {
+  if (tiles.empty()) return;
+  const int N = tc_n(P);
+  const int stages = tc_stages(N);
+  const size_t sm = tc_smem(N, stages);
+  static bool attr = false;
+  if (!attr) {
+    DLX_CUDA(cudaFuncSetAttribute(k_tc_sweep<A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    attr = true;
+  }
+  const int grid = static_cast<int>(std::min<size_t>(tiles.size(), num_sms()));
+  k_tc_sweep<A_MN><<<grid, kTcThreads, sm, s>>>(P.d_t2, maps, d_tiles, (int)tiles.size(), N,
+                                                stages, P.d_k2_splits, P.d_k2_part_off, out, part);
+  DLX_LAUNCHED();
+}
+
+// Tensor-core sweeps for the eligible tensors; returns false if the plan is outside the
+// tcgen05 path (then the SIMT kernels handle every tensor).
+bool tc_supported(const Plan& P) { return P.rmax >= 1 && P.rmax <= 256; }
+
+void launch_k1_tc(const Plan& P, const float* slab, const float* q, float* y, cudaStream_t s) {
+  TcState& S = tc_state(P);
+  const TcMaps* maps = tc_maps(P, 0, slab, q, s);
+  launch_sweep<false>(P, maps, S.k1, S.d_k1, y, nullptr, s);
+}
+
+void launch_k2_tc(const Plan& P, const float* slab, const float* p, float* z, float* part,
+                  cudaStream_t s) {
+  TcState& S = tc_state(P);
+  const TcMaps* maps = tc_maps(P, 1, slab, p, s);
+  launch_sweep<true>(P, maps, S.k2, S.d_k2, z, part, s);
+}
+
+}  // namespace dlx

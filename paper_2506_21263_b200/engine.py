@@ -43,6 +43,9 @@ class OuterConfig:
     seed: int = 1
     overlap: bool = True      # dilocox (overlapped) vs dilocox-no-overlap (sync)
     measure_error: bool = True
+    # benchmarking aid: run the adaptive measurement + controller every round but keep
+    # operating at rank1 (the controller's choice is recorded in RoundRecord.r_next)
+    hold_rank: bool = False
 
     def resolved_H_min(self) -> int:
         return self.H_min if self.H_min > 0 else (self.H1 + 9) // 10
@@ -63,6 +66,8 @@ class RoundRecord:
     max_delta_norm: float = 0.0
     averaged: bool = False
     nonfinite: int = 0
+    r_next: int = 0
+    H_next: int = 0
 
 
 class OuterSync:
@@ -94,6 +99,16 @@ class OuterSync:
         self.per_host = torch.zeros(max(n2, 1), dtype=torch.int32, pin_memory=True)
         self.energy_host = torch.zeros(max(n2, 1), dtype=torch.float64, pin_memory=True)
         self.last = RoundRecord()
+        self.phase_events = None  # optional: list collecting (name, event) on the main stream
+        self.side_events: list = []  # (start, end) of the effective rank on the side stream
+
+    def _ev(self, name: str):
+        if self.phase_events is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream())
+        self.phase_events.append((name, e))
+        return e
 
     # -- pieces -------------------------------------------------------------------------
     def _omega_sq(self, r: int) -> float:
@@ -127,20 +142,30 @@ class OuterSync:
         pb = L.payload_bytes(r, q)
         qel = L.q_factor_elems(r)
         s0 = api.rng_stream(cfg.seed, api.stream_key(0xC09C, self.round))  # engine.cpp:226
+        self._ev("compress")
         # compress in place over the warm buffer: each rank overwrites it with its own Q,
         # then rank 0's copy is broadcast (engine.cpp:498-501)
         api.compress(L, self.pending, r, QuantSpec(q, cfg.rounding),
                      self.warm_q if self.warm_rank == r else None, self.warm_rank,
                      cfg.power_iters, s0, payload=self.payload[:pb], q_out=self.warm_q[:max(qel, 1)])
+        self._ev("exchange")
         gathered = self._exchange(pb, qel)
         cur = torch.cuda.current_stream()
+        self._ev("outer_update")
         if cfg.adaptive and self._n2:
             # factor-space effective rank on the side stream, overlapping the outer update
             side = self.side or cur
             side.wait_stream(cur)
             with torch.cuda.stream(side):
+                if self.phase_events is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(side)
                 per, energy = api.effective_rank_device(L, gathered, self.world, r, q, cfg.tau,
                                                         stream=side)
+                if self.phase_events is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(side)
+                    self.side_events.append((e0, e1))
                 self.per_host.copy_(per, non_blocking=True)
                 self.energy_host.copy_(energy, non_blocking=True)
                 ev = torch.cuda.Event()
@@ -149,6 +174,7 @@ class OuterSync:
                          self.velocity, cfg.outer_lr, cfg.outer_momentum, cfg.outer_classical,
                          mode=mode, self_index=self.rank if cfg.measure_error else -1,
                          stats=self.stats, stream=cur)
+        self._ev("end")
         self.stats_host.copy_(self.stats, non_blocking=True)
         rec = RoundRecord(round=self.round, r_t=r, H_t=self.H_t, averaged=True,
                           payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
@@ -184,6 +210,11 @@ class OuterSync:
         return api.adapt_compression(self.window, cfg.rank1, cfg.H1, cfg.window_c,
                                      cfg.resolved_H_min())
 
+    def _apply_next(self, rec: RoundRecord, r_next: int, h_next: int):
+        rec.r_next, rec.H_next = r_next, h_next
+        if not self.cfg.hold_rank:
+            self.r_t, self.H_t = r_next, h_next
+
     def _push_window(self, r_prime: int):
         self.window.append(r_prime)
         if len(self.window) > self.cfg.window_c:
@@ -205,7 +236,7 @@ class OuterSync:
         r_next, h_next = self._adapt()
         self.has_pending = True
         rec = self._finish(rec, OVERLAPPED)
-        self.r_t, self.H_t = r_next, h_next
+        self._apply_next(rec, r_next, h_next)
         return rec
 
     def round_sync(self, local: torch.Tensor) -> RoundRecord:
@@ -221,7 +252,7 @@ class OuterSync:
             self._push_window(rec.r_prime)
             r_next, h_next = self._adapt()
         rec = self._finish(rec, SYNC)
-        self.r_t, self.H_t = r_next, h_next
+        self._apply_next(rec, r_next, h_next)
         return rec
 
     def step(self, local: torch.Tensor) -> RoundRecord:
