@@ -179,6 +179,13 @@ dlx_status dlx_parse(const dlx_layout* layout, int rank, int qbits, const uint8_
  * the SIMT kernels instead of the tcgen05 ones (A/B testing; also env DLX_TENSOR_CORES=0). */
 dlx_status dlx_set_option(const char* key, int value);
 
+/* Test hook: one power-iteration sweep — which = 0: out = delta * in (K1, in = Q factors),
+ * which = 1: out = delta^T * in (K2, in = P factors) — on the tcgen05 (use_tc = 1) or SIMT
+ * path. Factor buffers use the dlx_factor_offsets layouts. */
+dlx_status dlx_debug_sweep(dlx_ctx* ctx, const dlx_layout* layout, int rank, int which,
+                           const float* d_slab, const float* d_in, float* d_out, int use_tc,
+                           void* stream);
+
 /* Number of kernels this library launched on the calling thread since the last call
  * (launch accounting for benchmarks). */
 uint64_t dlx_take_launch_count(void);

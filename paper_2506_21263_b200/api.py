@@ -380,3 +380,14 @@ def set_option(key: str, value: int) -> None:
     """dlx_set_option: e.g. set_option("tensor_cores", 0) routes the power-iteration sweeps
     through the SIMT kernels (A/B testing)."""
     check(lib().dlx_set_option(key.encode(), int(value)))
+
+
+def debug_sweep(layout: Layout, rank: int, which: int, slab: torch.Tensor, fac_in: torch.Tensor,
+                use_tc: bool, stream=None) -> torch.Tensor:
+    """Test hook: one K1 (which=0, out = delta Q) or K2 (which=1, out = delta^T P) sweep."""
+    side_out = 0 if which == 0 else 1
+    out = torch.zeros(max(layout.factor_offsets(rank, side_out)[1], 1), dtype=torch.float32,
+                      device=slab.device)
+    check(lib().dlx_debug_sweep(layout.ctx.h, layout.h, rank, which, _ptr(slab), _ptr(fac_in),
+                                _ptr(out), int(use_tc), _stream(stream)))
+    return out

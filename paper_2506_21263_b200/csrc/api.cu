@@ -45,7 +45,7 @@ static T* upload(const std::vector<T>& v) {
 Plan::~Plan() {
   void* ptrs[] = {d_t2, d_t1, d_chunks, d_streams, d_mats[0], d_mats[1], d_k1_tiles,
                   d_k2_tiles, d_k2_part_off, d_k2_splits, d_k5_tiles, d_cold_base_spec[0],
-                  d_cold_base_spec[1], d_k1_rest, d_k2_rest};
+                  d_cold_base_spec[1], d_k1_rest, d_k2_rest, d_k5s_tiles};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -211,10 +211,17 @@ static std::unique_ptr<Plan> build_plan(const dlx_layout& L, int rank, int qbits
           P->k2_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(j0), c0, s));
           if (!tc) P->k2_rest.push_back(P->k2_tiles.back());
         }
-    for (int64_t m0 = 0; m0 < t.a; m0 += 32)
+    if (t.b % 4 == 0) {
       for (int64_t n0 = 0; n0 < t.b; n0 += 128)
-        P->k5_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0),
-                                        static_cast<int>(n0), 0));
+        for (int64_t m0 = 0; m0 < t.a; m0 += 16)
+          P->k5s_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0),
+                                           static_cast<int>(n0), 0));
+    } else {
+      for (int64_t m0 = 0; m0 < t.a; m0 += 16)
+        for (int64_t n0 = 0; n0 < t.b; n0 += 128)
+          P->k5_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0),
+                                          static_cast<int>(n0), 0));
+    }
   }
   P->k2_part_elems = std::max<int64_t>(part, 32);
 
@@ -229,6 +236,7 @@ static std::unique_ptr<Plan> build_plan(const dlx_layout& L, int rank, int qbits
   P->d_k2_part_off = upload(P->k2_part_off);
   P->d_k2_splits = upload(P->k2_splits);
   P->d_k5_tiles = upload(P->k5_tiles);
+  P->d_k5s_tiles = upload(P->k5s_tiles);
   P->d_k1_rest = upload(P->k1_rest);
   P->d_k2_rest = upload(P->k2_rest);
   P->d_cold_base_spec[0] = upload(P->cold_base_spec[0]);
@@ -290,6 +298,25 @@ dlx_status dlx_set_option(const char* key, int value) {
     } else {
       raise(DLX_ERR_VALIDATION, "unknown option: " + k);
     }
+  });
+}
+
+dlx_status dlx_debug_sweep(dlx_ctx* ctx, const dlx_layout* layout, int rank, int which,
+                           const float* d_slab, const float* d_in, float* d_out, int use_tc,
+                           void* stream) {
+  return guard([&] {
+    set_device(ctx);
+    Plan& P = const_cast<dlx_layout*>(layout)->plan(rank, 8);
+    const bool saved = option_tensor_cores();
+    option_tensor_cores() = use_tc != 0;
+    cudaStream_t s = as_stream(stream);
+    if (which == 0) {
+      launch_k1(P, d_slab, d_in, d_out, s);
+    } else {
+      float* part = static_cast<float*>(ctx->scratch("k2part", sizeof(float) * P.k2_part_elems));
+      launch_k2(P, d_slab, d_in, d_out, part, s);
+    }
+    option_tensor_cores() = saved;
   });
 }
 

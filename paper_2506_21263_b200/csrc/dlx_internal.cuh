@@ -167,8 +167,10 @@ struct Plan {
   std::vector<int4> k1_rest, k2_rest;  // SIMT tiles of tensors outside the tcgen05 path
   int4* d_k1_rest = nullptr;
   int4* d_k2_rest = nullptr;
-  std::vector<int4> k5_tiles;  // (t2 slot, m0, n0, -)
+  std::vector<int4> k5_tiles;   // (t2 slot, m0, n0, -): register kernel (b % 4 != 0)
   int4* d_k5_tiles = nullptr;
+  std::vector<int4> k5s_tiles;  // streamed persistent kernel, column-block-major order
+  int4* d_k5s_tiles = nullptr;
   // speculative cold-start draw bases per 2-D slot, [0] stochastic (assumes no all-zero
   // chunk), [1] nearest (exact: quantisation draws nothing)
   std::vector<int64_t> cold_base_spec[2];

@@ -11,6 +11,7 @@
 // HBM traffic per element of a 2-D tensor: read pending, anchor, local, v; write pending,
 // anchor, v = 28 B; Delta itself never touches HBM.
 #include "dlx_internal.cuh"
+#include "ptx.cuh"
 
 namespace dlx {
 
@@ -58,7 +59,7 @@ __device__ __forceinline__ void stats_add(dlx_round_stats* st, double num, doubl
 }
 
 // ------------------------------------------------------------------ K5, 2-D tensors
-// Tile 32 rows x 128 cols of delta; 256 threads, each 4 rows x 4 consecutive cols.
+// Tile 16 rows x 128 cols of delta; 256 threads, each 2 rows x 4 consecutive cols.
 // Delta_tile = (1/D) * Phat[rows, :] Qhat[cols, :]^T with K = D*r (fp32 accumulate).
 // The four streamed operands of the tile are loaded (evict-first) before the small
 // factor GEMM so their HBM latency overlaps it: 256 B in flight per thread.
@@ -82,7 +83,8 @@ __device__ __forceinline__ void store4(float* p, bool full, int nv, const float 
   }
 }
 
-__global__ void __launch_bounds__(256, 1) k5_outer(const DevT2* __restrict__ T,
+template <bool SELF>
+__global__ void __launch_bounds__(256, 3) k5_outer(const DevT2* __restrict__ T,
                                                    const int4* __restrict__ tiles,
                                                    const float* __restrict__ phat,
                                                    const float* __restrict__ qhat, int D,
@@ -93,7 +95,8 @@ __global__ void __launch_bounds__(256, 1) k5_outer(const DevT2* __restrict__ T,
                                                    float* __restrict__ velocity, float gamma,
                                                    float beta, int classical,
                                                    dlx_round_stats* stats) {
-  __shared__ __align__(16) float Ps[32][36];
+  // tile: 16 rows x 128 cols; thread (ty, tx) owns rows 2ty, 2ty+1 and cols 4tx..4tx+3
+  __shared__ __align__(16) float Ps[32][20];
   __shared__ __align__(16) float Qs[32][132];
   const int4 tile = tiles[blockIdx.x];
   const DevT2 t = T[tile.x];
@@ -102,17 +105,17 @@ __global__ void __launch_bounds__(256, 1) k5_outer(const DevT2* __restrict__ T,
   const int K = D * t.r;
   const float* Ph = phat + D * t.poff;
   const float* Qh = qhat + D * t.qoff;
-  const int s_lo = self_index >= 0 ? self_index * t.r : K, s_hi = s_lo + t.r;
+  const int s_lo = SELF ? self_index * t.r : K, s_hi = s_lo + t.r;
   const bool vec = (t.b % 4) == 0;
   const bool ovl = mode == DLX_MODE_OVERLAPPED;
   const int64_t col = n0 + tx * 4;
   const int nv = col < t.b ? (int)(t.b - col < 4 ? t.b - col : 4) : 0;
 
-  // 1. streamed operands of this thread's 4 rows
-  float pd[4][4], an[4][4], lo[4][4], ve[4][4];
+  // 1. streamed operands of this thread's 2 rows (issued before the factor GEMM)
+  float pd[2][4], an[2][4], lo[2][4], ve[2][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t row = m0 + ty * 4 + i;
+  for (int i = 0; i < 2; ++i) {
+    const int64_t row = m0 + ty * 2 + i;
     const bool live = row < t.a && nv > 0;
     const int n = live ? nv : 0;
     const bool full = live && vec && nv == 4;
@@ -128,15 +131,15 @@ __global__ void __launch_bounds__(256, 1) k5_outer(const DevT2* __restrict__ T,
     load4(velocity + base, full, n, ve[i]);
   }
 
-  // 2. factor GEMM
-  float acc[4][4], sacc[4][4];
+  // 2. factor GEMM: acc = Phat[rows, :] Qhat[cols, :]^T
+  float acc[2][4], sacc[2][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = sacc[i][j] = 0.f;
   for (int k0 = 0; k0 < K; k0 += 32) {
-    {  // Phat 32(k) x 32(rows): one float4 per thread
-      const int kk = tid / 8, c4 = (tid % 8) * 4;
+    if (tid < 128) {  // Phat 32(k) x 16(rows)
+      const int kk = tid / 4, c4 = (tid % 4) * 4;
       const int k = k0 + kk;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (k < K) v = *reinterpret_cast<const float4*>(Ph + (int64_t)k * t.lda + m0 + c4);
@@ -153,19 +156,21 @@ __global__ void __launch_bounds__(256, 1) k5_outer(const DevT2* __restrict__ T,
     __syncthreads();
     const int kmax = min(32, K - k0);
     for (int kk = 0; kk < kmax; ++kk) {
-      const float4 a4 = *reinterpret_cast<const float4*>(&Ps[kk][ty * 4]);
+      const float2 a2 = *reinterpret_cast<const float2*>(&Ps[kk][ty * 2]);
       const float4 b4 = *reinterpret_cast<const float4*>(&Qs[kk][tx * 4]);
-      const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+      const float av[2] = {a2.x, a2.y}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-      const int k = k0 + kk;
-      if (k >= s_lo && k < s_hi) {
+      if (SELF) {
+        const int k = k0 + kk;
+        if (k >= s_lo && k < s_hi) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) sacc[i][j] = fmaf(av[i], bv[j], sacc[i][j]);
+            for (int j = 0; j < 4; ++j) sacc[i][j] = fmaf(av[i], bv[j], sacc[i][j]);
+        }
       }
     }
     __syncthreads();
@@ -175,8 +180,8 @@ __global__ void __launch_bounds__(256, 1) k5_outer(const DevT2* __restrict__ T,
   const float invD = __fdiv_rn(1.0f, (float)D);
   double num = 0.0, den = 0.0, dn = 0.0, en = 0.0, nf = 0.0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t row = m0 + ty * 4 + i;
+  for (int i = 0; i < 2; ++i) {
+    const int64_t row = m0 + ty * 2 + i;
     if (row >= t.a || nv == 0) continue;
     const int64_t base = t.off + row * t.b + col;
     float op[4], oa[4], ov[4];
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(256, 1) k5_outer(const DevT2* __restrict__ T,
       oa[j] = o.anchor;
       ov[j] = o.v;
       if (j < nv) {
-        if (self_index >= 0) {
+        if (SELF) {
           const double df = (double)sacc[i][j] - (double)pd[i][j];
           num += df * df;
           den += (double)pd[i][j] * (double)pd[i][j];
@@ -207,6 +212,197 @@ __global__ void __launch_bounds__(256, 1) k5_outer(const DevT2* __restrict__ T,
   stats_add(stats, num, den, dn, en, nf, nullptr);
 }
 
+// ------------------------------------------------------------------ K5s: persistent, streamed
+// One CTA per SM loops over 16 x 128 tiles (ordered column-block-major so the Qhat tile is
+// reused across consecutive tiles). Warp 8 streams the tile's four operand row segments
+// (pending, anchor, local, velocity; 512 B each) into a 4-stage shared-memory ring with
+// cp.async.bulk (the Blackwell bulk-copy engine, mbarrier complete_tx); warps 0-7 compute
+// the factor GEMM for the tile while the copies land, then run the fused epilogue from
+// shared memory and store the three outputs (evict-first). Up to 4 x 32 KB of operand
+// traffic is in flight per SM.
+constexpr int kK5Stages = 4;
+constexpr int kK5StageBytes = 4 * 16 * 128 * 4;  // 4 streams x 16 rows x 128 floats
+
+template <bool SELF>
+__global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
+                                                    const int4* __restrict__ tiles, int ntiles,
+                                                    const float* __restrict__ phat,
+                                                    const float* __restrict__ qhat, int D,
+                                                    int self_index, int mode,
+                                                    float* __restrict__ pending,
+                                                    float* __restrict__ anchor,
+                                                    const float* __restrict__ local,
+                                                    float* __restrict__ velocity, float gamma,
+                                                    float beta, int classical,
+                                                    dlx_round_stats* stats) {
+  extern __shared__ __align__(128) uint8_t k5smem[];
+  float* ring = reinterpret_cast<float*>(k5smem);                         // [stage][stream][16][128]
+  float* Qs = reinterpret_cast<float*>(k5smem + kK5Stages * kK5StageBytes);  // [32][132]
+  float* Ps = Qs + 32 * 132;                                                // [32][20]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Ps + 32 * 20);
+  uint64_t* empty = full + kK5Stages;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const bool ovl = mode == DLX_MODE_OVERLAPPED;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kK5Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);  // one arrival per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer (bulk copies)
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+        const int4 tl = tiles[ti];
+        const DevT2 t = T[tl.x];
+        const int s = it % kK5Stages;
+        mbar_wait(&empty[s], ((it / kK5Stages) & 1) ^ 1);
+        const int rows = static_cast<int>(t.a - tl.y < 16 ? t.a - tl.y : 16);
+        const int cols = static_cast<int>(t.b - tl.z < 128 ? t.b - tl.z : 128);
+        const uint32_t seg = static_cast<uint32_t>(cols) * 4;
+        const int nstreams = ovl ? 4 : 3;
+        mbar_expect_tx(&full[s], seg * rows * nstreams);
+        float* st = ring + s * (kK5StageBytes / 4);
+        const float* srcs[4] = {pending, anchor, velocity, local};
+        for (int q = 0; q < nstreams; ++q)
+          for (int r = 0; r < rows; ++r)
+            bulk_g2s(st + (q * 16 + r) * 128, srcs[q] + t.off + (tl.y + r) * t.b + tl.z, seg,
+                     &full[s]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers (8 warps)
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  double num = 0.0, den = 0.0, dn = 0.0, en = 0.0, nf = 0.0;
+  const float invD = __fdiv_rn(1.0f, (float)D);
+  int cached_slot = -1, cached_n0 = -1;
+  uint32_t it = 0;
+  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+    const int4 tl = tiles[ti];
+    const DevT2 t = T[tl.x];
+    const int64_t m0 = tl.y, n0 = tl.z;
+    const int K = D * t.r;
+    const float* Ph = phat + D * t.poff;
+    const float* Qh = qhat + D * t.qoff;
+    const int s_lo = SELF ? self_index * t.r : K, s_hi = s_lo + t.r;
+    float acc[2][4], sacc[2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = sacc[i][j] = 0.f;
+    const bool reuse_q = (tl.x == cached_slot && n0 == cached_n0 && K <= 32);
+    for (int k0 = 0; k0 < K; k0 += 32) {
+      named_bar(1, 256);  // previous users of Ps / Qs are done
+      if (tid < 128) {
+        const int kk = tid / 4, c4 = (tid % 4) * 4;
+        const int k = k0 + kk;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < K) v = *reinterpret_cast<const float4*>(Ph + (int64_t)k * t.lda + m0 + c4);
+        *reinterpret_cast<float4*>(&Ps[kk * 20 + c4]) = v;
+      }
+      if (!reuse_q) {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          const int e = tid + 256 * l, kk = e / 32, c4 = (e % 32) * 4;
+          const int k = k0 + kk;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (k < K && n0 + c4 < t.ldb)
+            v = *reinterpret_cast<const float4*>(Qh + (int64_t)k * t.ldb + n0 + c4);
+          *reinterpret_cast<float4*>(&Qs[kk * 132 + c4]) = v;
+        }
+      }
+      named_bar(1, 256);
+      const int kmax = min(32, K - k0);
+      for (int kk = 0; kk < kmax; ++kk) {
+        const float2 a2 = *reinterpret_cast<const float2*>(&Ps[kk * 20 + ty * 2]);
+        const float4 b4 = *reinterpret_cast<const float4*>(&Qs[kk * 132 + tx * 4]);
+        const float av[2] = {a2.x, a2.y}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        if (SELF) {
+          const int k = k0 + kk;
+          if (k >= s_lo && k < s_hi) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) sacc[i][j] = fmaf(av[i], bv[j], sacc[i][j]);
+          }
+        }
+      }
+    }
+    cached_slot = tl.x;
+    cached_n0 = static_cast<int>(n0);
+
+    // epilogue from the landed stage
+    const int s = it % kK5Stages;
+    mbar_wait(&full[s], (it / kK5Stages) & 1);
+    const float* st = ring + s * (kK5StageBytes / 4);
+    const int64_t col = n0 + tx * 4;
+    const int nv = col < t.b ? (int)(t.b - col < 4 ? t.b - col : 4) : 0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = ty * 2 + i;
+      const int64_t row = m0 + r;
+      float pd[4] = {0.f, 0.f, 0.f, 0.f}, an[4] = {0.f, 0.f, 0.f, 0.f},
+            ve[4] = {0.f, 0.f, 0.f, 0.f}, lo[4] = {0.f, 0.f, 0.f, 0.f};
+      const bool live = row < t.a && nv > 0;
+      if (live) {
+        const float4 a = *reinterpret_cast<const float4*>(st + (0 * 16 + r) * 128 + tx * 4);
+        const float4 b = *reinterpret_cast<const float4*>(st + (1 * 16 + r) * 128 + tx * 4);
+        const float4 c = *reinterpret_cast<const float4*>(st + (2 * 16 + r) * 128 + tx * 4);
+        pd[0] = a.x; pd[1] = a.y; pd[2] = a.z; pd[3] = a.w;
+        an[0] = b.x; an[1] = b.y; an[2] = b.z; an[3] = b.w;
+        ve[0] = c.x; ve[1] = c.y; ve[2] = c.z; ve[3] = c.w;
+        if (ovl) {
+          const float4 d = *reinterpret_cast<const float4*>(st + (3 * 16 + r) * 128 + tx * 4);
+          lo[0] = d.x; lo[1] = d.y; lo[2] = d.z; lo[3] = d.w;
+        }
+      }
+      float op[4], oa[4], ov[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float delta = __fmul_rn(acc[i][j], invD);
+        const EpiOut o = epilogue(delta, pd[j], an[j], lo[j], ve[j], mode, gamma, beta, classical);
+        op[j] = o.pend;
+        oa[j] = o.anchor;
+        ov[j] = o.v;
+        if (live && j < nv) {
+          if (SELF) {
+            const double df = (double)sacc[i][j] - (double)pd[j];
+            num += df * df;
+            den += (double)pd[j] * (double)pd[j];
+          }
+          en += (double)o.e * (double)o.e;
+          if (ovl) dn += (double)o.pend * (double)o.pend;
+          if (!isfinite(o.anchor)) nf += 1.0;
+        }
+      }
+      if (live) {
+        const int64_t base = t.off + row * t.b + col;
+        const bool full4 = nv == 4;
+        store4(pending + base, full4, nv, op);
+        store4(anchor + base, full4, nv, oa);
+        store4(velocity + base, full4, nv, ov);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  stats_add(stats, num, den, dn, en, nf, nullptr);
+}
+
+static size_t k5s_smem() {
+  return kK5Stages * kK5StageBytes + (32 * 132 + 32 * 20) * 4 + 2 * kK5Stages * 8 + 64;
+}
+
 void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                      int self_index, int mode, float* pending, float* anchor,
                      const float* local, float* velocity, float gamma, float beta,
@@ -215,10 +411,39 @@ void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered
   float* phat = static_cast<float*>(ctx->scratch("phat", sizeof(float) * P.pelems * D));
   float* qhat = static_cast<float*>(ctx->scratch("qhat", sizeof(float) * P.qelems * D));
   dequant_factors(P, D, gathered, P.payload_bytes, phat, qhat, 0, s);
-  k5_outer<<<P.k5_tiles.size(), 256, 0, s>>>(P.d_t2, P.d_k5_tiles, phat, qhat, D, self_index,
-                                            mode, pending, anchor, local, velocity, gamma, beta,
-                                            classical, stats);
-  DLX_LAUNCHED();
+  if (!P.k5s_tiles.empty()) {
+    static bool attr = false;
+    if (!attr) {
+      DLX_CUDA(cudaFuncSetAttribute(k5s_outer<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5s_smem()));
+      DLX_CUDA(cudaFuncSetAttribute(k5s_outer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5s_smem()));
+      attr = true;
+    }
+    int sms = 0, dev = 0;
+    DLX_CUDA(cudaGetDevice(&dev));
+    DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int n = static_cast<int>(P.k5s_tiles.size());
+    const int grid = std::min(n, sms);
+    if (self_index >= 0)
+      k5s_outer<true><<<grid, 288, k5s_smem(), s>>>(P.d_t2, P.d_k5s_tiles, n, phat, qhat, D,
+                                                    self_index, mode, pending, anchor, local,
+                                                    velocity, gamma, beta, classical, stats);
+    else
+      k5s_outer<false><<<grid, 288, k5s_smem(), s>>>(P.d_t2, P.d_k5s_tiles, n, phat, qhat, D,
+                                                     self_index, mode, pending, anchor, local,
+                                                     velocity, gamma, beta, classical, stats);
+    DLX_LAUNCHED();
+  }
+  if (!P.k5_tiles.empty()) {
+    if (self_index >= 0)
+      k5_outer<true><<<P.k5_tiles.size(), 256, 0, s>>>(P.d_t2, P.d_k5_tiles, phat, qhat, D,
+                                                       self_index, mode, pending, anchor, local,
+                                                       velocity, gamma, beta, classical, stats);
+    else
+      k5_outer<false><<<P.k5_tiles.size(), 256, 0, s>>>(P.d_t2, P.d_k5_tiles, phat, qhat, D,
+                                                        self_index, mode, pending, anchor, local,
+                                                        velocity, gamma, beta, classical, stats);
+    DLX_LAUNCHED();
+  }
 }
 
 // ------------------------------------------------------------------ 1-D tensors

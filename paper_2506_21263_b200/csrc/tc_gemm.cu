@@ -1,6 +1,9 @@
 // tc_gemm.cu — tcgen05 / TMEM / TMA power-iteration sweeps (lowrank_approx
 // compress.cpp:70-77):  K1  Y = delta Q  (A = delta, K-major)   and
-//                       K2  Z = delta^T P (A = delta^T, MN-major), deterministic split-K.
+//                       K2  Z = delta^T P (A = delta^T), deterministic split-K.
+// For K2 the delta tile arrives row-major (M contiguous); the split warps transpose it into
+// the canonical K-major SW128 layout while splitting, so both sweeps feed the tensor core
+// K-major operands (MN-major tf32 operands would need the 32B-atom swizzle variant).
 //
 // Both sweeps stream every element of delta from HBM exactly once; the factor operand
 // (Q or P, <= 256 columns) is the MMA N dimension. Precision: 3xTF32 — each fp32 operand
@@ -20,89 +23,9 @@
 #include <cstring>
 
 #include "dlx_internal.cuh"
+#include "ptx.cuh"
 
 namespace dlx {
-
-// ------------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.b32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(su32(b)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// Bounded wait: a pipeline bug traps (launch error) instead of hanging the device.
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  uint32_t n = 0;
-  while (!mbar_try(b, parity)) {
-    if (++n > (1u << 24)) __trap();
-  }
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 // Shared-memory matrix descriptor, SWIZZLE_128B (tcgen05 "version 1" layout).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -121,6 +44,16 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn, bool b_mn) {
          (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
 }
 
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void split4(const float4 x, float4& h, float4& l) {
+  h.x = tf32_hi(x.x); l.x = x.x - h.x;
+  h.y = tf32_hi(x.y); l.y = x.y - h.y;
+  h.z = tf32_hi(x.z); l.z = x.z - h.z;
+  h.w = tf32_hi(x.w); l.w = x.w - h.w;
+}
+
 // ------------------------------------------------------------------ kernel
 struct TcMaps {
   CUtensorMap a;  // delta: K1 box {32, 128} (K-major); K2 box {32, 32} (MN-major)
@@ -130,7 +63,8 @@ struct TcMaps {
 constexpr int kTcThreads = 192;
 constexpr uint32_t kAStage = 128 * 32 * 4;  // 16 KB
 
-// A_MN: false = K1 (A = delta rows, K-major), true = K2 (A = delta^T, MN-major).
+// A_MN: false = K1 (A = delta rows, already K-major), true = K2 (A = delta^T: the raw tile
+// is [k][m], transposed into K-major hi/lo by the split warps).
 template <bool A_MN>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_tc_sweep(const DevT2* __restrict__ T, const TcMaps* __restrict__ maps,
@@ -140,7 +74,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t b_bytes = static_cast<uint32_t>(N) * 128;
-  const uint32_t stage_bytes = 2 * kAStage + 2 * b_bytes;
+  const uint32_t stage_bytes = 2 * kAStage + 2 * b_bytes + (A_MN ? kAStage : 0u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
   uint64_t* full = bars;
   uint64_t* split = bars + stages;
@@ -207,8 +141,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tma_load_2d(st, &mp->a, &full[s], static_cast<int>(k), tl.y);  // {k, m0}
           } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)  // 4 MN blocks of 32 columns, 32 rows each
-              tma_load_2d(st + q * 4096, &mp->a, &full[s], tl.y + 32 * q, static_cast<int>(k));
+            for (int q = 0; q < 4; ++q)  // raw [k][m] tile: 4 boxes of 32 rows x 32 columns
+              tma_load_2d(st + 2 * kAStage + 2 * b_bytes + q * 4096, &mp->a, &full[s],
+                          tl.y + 32 * q, static_cast<int>(k));
           }
           tma_load_2d(st + 2 * kAStage, &mp->b, &full[s], static_cast<int>(k), 0);  // {k, n}
         }
@@ -217,7 +152,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(N, A_MN, false);
+      const uint32_t idesc = idesc_tf32(N, false, false);
       uint32_t it = 0, tphase = 0;
       for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
         const int4 tl = tiles[ti];
@@ -238,12 +173,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint32_t b_lo = b_hi + b_bytes;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            // K-major A: +32 B per 8-element k step inside the 128-B swizzle atom;
-            // MN-major A: one 8-row (1024-B) atom per k step, MN blocks 4096 B apart.
-            const uint32_t aoff = A_MN ? kk * 1024u : kk * 32u;
-            const uint32_t lbo = A_MN ? 4096u : 16u;
-            const uint64_t ah = sdesc(a_hi + aoff, lbo, 1024u);
-            const uint64_t al = sdesc(a_lo + aoff, lbo, 1024u);
+            // K-major SW128: +32 B per 8-element k step inside the 128-B swizzle atom
+            const uint64_t ah = sdesc(a_hi + kk * 32u, 16u, 1024u);
+            const uint64_t al = sdesc(a_lo + kk * 32u, 16u, 1024u);
             const uint64_t bh = sdesc(b_hi + kk * 32u, 16u, 1024u);
             const uint64_t bl = sdesc(b_lo + kk * 32u, 16u, 1024u);
             mma_tf32(tmem, ah, bh, idesc, first ? 0u : 1u);
@@ -273,27 +205,41 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t ph = (it / stages) & 1;
         mbar_wait(&full[s], ph);
         uint8_t* st = smem + s * stage_bytes;
-        // hi = tf32-exact truncation (written back), lo = x - hi
+        // hi = tf32-exact truncation, lo = x - hi
         float4* ah = reinterpret_cast<float4*>(st);
         float4* al = reinterpret_cast<float4*>(st + kAStage);
+        if (!A_MN) {  // in place: the TMA already wrote the K-major SW128 tile into A_hi
 #pragma unroll 4
-        for (int i = et; i < static_cast<int>(kAStage / 16); i += 128) {
-          float4 x = ah[i], h, l;
-          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u); l.x = x.x - h.x;
-          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u); l.y = x.y - h.y;
-          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u); l.z = x.z - h.z;
-          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u); l.w = x.w - h.w;
-          ah[i] = h;
-          al[i] = l;
+          for (int i = et; i < static_cast<int>(kAStage / 16); i += 128) {
+            float4 h, l;
+            split4(ah[i], h, l);
+            ah[i] = h;
+            al[i] = l;
+          }
+        } else {
+          // raw[q][k][mm] (m = 32q + mm) -> K-major SW128: row m, 16-B chunk c = k/4 stored
+          // at chunk c ^ (m % 8). Thread et owns row m = et.
+          const float* raw = reinterpret_cast<const float*>(st + 2 * kAStage + 2 * b_bytes);
+          const int m = et, q = m >> 5, mm = m & 31;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float4 x;
+            x.x = raw[q * 1024 + (4 * c + 0) * 32 + mm];
+            x.y = raw[q * 1024 + (4 * c + 1) * 32 + mm];
+            x.z = raw[q * 1024 + (4 * c + 2) * 32 + mm];
+            x.w = raw[q * 1024 + (4 * c + 3) * 32 + mm];
+            float4 h, l;
+            split4(x, h, l);
+            const int idx = m * 8 + (c ^ (m & 7));
+            ah[idx] = h;
+            al[idx] = l;
+          }
         }
         float4* bh = reinterpret_cast<float4*>(st + 2 * kAStage);
         float4* bl = reinterpret_cast<float4*>(st + 2 * kAStage + b_bytes);
         for (int i = et; i < static_cast<int>(b_bytes / 16); i += 128) {
-          float4 x = bh[i], h, l;
-          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u); l.x = x.x - h.x;
-          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u); l.y = x.y - h.y;
-          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u); l.z = x.z - h.z;
-          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u); l.w = x.w - h.w;
+          float4 h, l;
+          split4(bh[i], h, l);
           bh[i] = h;
           bl[i] = l;
         }
@@ -348,14 +294,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 static void encode(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t stride1_bytes,
-                   uint32_t b0, uint32_t b1) {
+                   uint32_t b0, uint32_t b1, bool swizzle = true) {
   const cuuint64_t dims[2] = {d0, d1};
   const cuuint64_t strides[1] = {stride1_bytes};
   const cuuint32_t box[2] = {b0, b1};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
@@ -420,7 +367,7 @@ static const TcMaps* tc_maps(const Plan& P, int which, const float* slab, const 
       encode(&m.a, A, t.b, t.a, t.b * 4, 32, 128);
       encode(&m.b, fac + t.qoff, t.b, t.r, t.ldb * 4, 32, N);
     } else {
-      encode(&m.a, A, t.b, t.a, t.b * 4, 32, 32);
+      encode(&m.a, A, t.b, t.a, t.b * 4, 32, 32, /*swizzle=*/false);
       encode(&m.b, fac + t.poff, t.a, t.r, t.lda * 4, 32, N);
     }
   }
@@ -432,13 +379,14 @@ static const TcMaps* tc_maps(const Plan& P, int which, const float* slab, const 
   return S.d_maps[which];
 }
 
-static int tc_stages(int N) {
-  const int stage = 2 * 16384 + 2 * N * 128;
-  return std::max(2, std::min(6, (200 * 1024) / stage));
+static int tc_stage_bytes(int N, bool a_mn) { return 2 * 16384 + 2 * N * 128 + (a_mn ? 16384 : 0); }
+
+static int tc_stages(int N, bool a_mn) {
+  return std::max(2, std::min(6, (200 * 1024) / tc_stage_bytes(N, a_mn)));
 }
 
-static size_t tc_smem(int N, int stages) {
-  return 1024 + static_cast<size_t>(stages) * (2 * 16384 + 2 * N * 128) + 8 * (3 * stages + 2) + 16;
+static size_t tc_smem(int N, bool a_mn, int stages) {
+  return 1024 + static_cast<size_t>(stages) * tc_stage_bytes(N, a_mn) + 8 * (3 * stages + 2) + 16;
 }
 
 static int num_sms() {
@@ -456,8 +404,8 @@ static void launch_sweep(const Plan& P, const TcMaps* maps, const std::vector<in
                          const int4* d_tiles, float* out, float* part, cudaStream_t s) {
   if (tiles.empty()) return;
   const int N = tc_n(P);
-  const int stages = tc_stages(N);
-  const size_t sm = tc_smem(N, stages);
+  const int stages = tc_stages(N, A_MN);
+  const size_t sm = tc_smem(N, A_MN, stages);
   static bool attr = false;
   if (!attr) {
     DLX_CUDA(cudaFuncSetAttribute(k_tc_sweep<A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
