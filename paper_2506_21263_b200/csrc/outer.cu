@@ -10,6 +10,10 @@
 //   nesterov_outer_step  optim.cpp:56-78        v = beta v + Delta; anchor -= gamma (Delta + beta v)
 // HBM traffic per element of a 2-D tensor: read pending, anchor, local, v; write pending,
 // anchor, v = 28 B; Delta itself never touches HBM.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
 #include "dlx_internal.cuh"
 #include "ptx.cuh"
 
@@ -214,17 +218,22 @@ __global__ void __launch_bounds__(256, 3) k5_outer(const DevT2* __restrict__ T,
 
 // ------------------------------------------------------------------ K5s: persistent, streamed
 // One CTA per SM loops over 16 x 128 tiles (ordered column-block-major so the Qhat tile is
-// reused across consecutive tiles). Warp 8 streams the tile's four operand row segments
-// (pending, anchor, local, velocity; 512 B each) into a 4-stage shared-memory ring with
-// cp.async.bulk (the Blackwell bulk-copy engine, mbarrier complete_tx); warps 0-7 compute
+// reused across consecutive tiles). Warp 8 streams the tile's four operand boxes
+// (pending, anchor, velocity, local; 16 rows x 512 B each) into a 4-stage shared-memory ring
+// with one TMA tensor copy per operand (mbarrier complete_tx); warps 0-7 compute
 // the factor GEMM for the tile while the copies land, then run the fused epilogue from
 // shared memory and store the three outputs (evict-first). Up to 4 x 32 KB of operand
 // traffic is in flight per SM.
 constexpr int kK5Stages = 4;
 constexpr int kK5StageBytes = 4 * 16 * 128 * 4;  // 4 streams x 16 rows x 128 floats
 
+struct K5Maps {
+  CUtensorMap m[4];  // pending, anchor, velocity, local: dims {b, a}, box {128, 16}
+};
+
 template <bool SELF>
 __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
+                                                    const K5Maps* __restrict__ maps,
                                                     const int4* __restrict__ tiles, int ntiles,
                                                     const float* __restrict__ phat,
                                                     const float* __restrict__ qhat, int D,
@@ -261,17 +270,13 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
         const DevT2 t = T[tl.x];
         const int s = it % kK5Stages;
         mbar_wait(&empty[s], ((it / kK5Stages) & 1) ^ 1);
-        const int rows = static_cast<int>(t.a - tl.y < 16 ? t.a - tl.y : 16);
-        const int cols = static_cast<int>(t.b - tl.z < 128 ? t.b - tl.z : 128);
-        const uint32_t seg = static_cast<uint32_t>(cols) * 4;
+        (void)t;
         const int nstreams = ovl ? 4 : 3;
-        mbar_expect_tx(&full[s], seg * rows * nstreams);
+        mbar_expect_tx(&full[s], 16 * 128 * 4 * nstreams);  // full boxes (OOB zero-filled)
         float* st = ring + s * (kK5StageBytes / 4);
-        const float* srcs[4] = {pending, anchor, velocity, local};
+        const K5Maps* mp = maps + tl.x;
         for (int q = 0; q < nstreams; ++q)
-          for (int r = 0; r < rows; ++r)
-            bulk_g2s(st + (q * 16 + r) * 128, srcs[q] + t.off + (tl.y + r) * t.b + tl.z, seg,
-                     &full[s]);
+          tma_load_2d(st + q * 16 * 128, &mp->m[q], &full[s], tl.z, tl.y);
       }
     }
     return;
@@ -399,6 +404,55 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
   stats_add(stats, num, den, dn, en, nf, nullptr);
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 k5_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    DLX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+struct K5MapCache {
+  const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
+  K5Maps* d = nullptr;
+  std::vector<K5Maps> h;
+};
+
+static const K5Maps* k5_maps(const Plan& P, const float* pending, const float* anchor,
+                             const float* velocity, const float* local, cudaStream_t s) {
+  static thread_local std::map<const Plan*, K5MapCache> cache;
+  K5MapCache& c = cache[&P];
+  const void* key[4] = {pending, anchor, velocity, local};
+  if (c.d && std::equal(key, key + 4, c.key)) return c.d;
+  if (!c.d) DLX_CUDA(cudaMalloc(&c.d, sizeof(K5Maps) * std::max<size_t>(P.t2.size(), 1)));
+  c.h.assign(P.t2.size(), K5Maps{});
+  for (size_t k = 0; k < P.t2.size(); ++k) {
+    const DevT2& t = P.t2[k];
+    if (t.b % 4 != 0) continue;
+    for (int q = 0; q < 4; ++q) {
+      if (!key[q]) continue;
+      const cuuint64_t dims[2] = {static_cast<cuuint64_t>(t.b), static_cast<cuuint64_t>(t.a)};
+      const cuuint64_t strides[1] = {static_cast<cuuint64_t>(t.b) * 4};
+      const cuuint32_t box[2] = {128, 16};
+      const cuuint32_t estr[2] = {1, 1};
+      CUresult r = k5_encode_fn()(&c.h[k].m[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                  const_cast<float*>(static_cast<const float*>(key[q])) + t.off,
+                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled (K5) failed");
+    }
+  }
+  DLX_CUDA(cudaMemcpyAsync(c.d, c.h.data(), sizeof(K5Maps) * P.t2.size(), cudaMemcpyHostToDevice, s));
+  DLX_CUDA(cudaStreamSynchronize(s));
+  std::copy(key, key + 4, c.key);
+  return c.d;
+}
+
 static size_t k5s_smem() {
   return kK5Stages * kK5StageBytes + (32 * 132 + 32 * 20) * 4 + 2 * kK5Stages * 8 + 64;
 }
@@ -423,12 +477,14 @@ void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered
     DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int n = static_cast<int>(P.k5s_tiles.size());
     const int grid = std::min(n, sms);
+    const K5Maps* maps = k5_maps(P, pending, anchor, velocity,
+                                 mode == DLX_MODE_OVERLAPPED ? local : nullptr, s);
     if (self_index >= 0)
-      k5s_outer<true><<<grid, 288, k5s_smem(), s>>>(P.d_t2, P.d_k5s_tiles, n, phat, qhat, D,
+      k5s_outer<true><<<grid, 288, k5s_smem(), s>>>(P.d_t2, maps, P.d_k5s_tiles, n, phat, qhat, D,
                                                     self_index, mode, pending, anchor, local,
                                                     velocity, gamma, beta, classical, stats);
     else
-      k5s_outer<false><<<grid, 288, k5s_smem(), s>>>(P.d_t2, P.d_k5s_tiles, n, phat, qhat, D,
+      k5s_outer<false><<<grid, 288, k5s_smem(), s>>>(P.d_t2, maps, P.d_k5s_tiles, n, phat, qhat, D,
                                                      self_index, mode, pending, anchor, local,
                                                      velocity, gamma, beta, classical, stats);
     DLX_LAUNCHED();

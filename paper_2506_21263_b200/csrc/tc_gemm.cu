@@ -56,15 +56,52 @@ __device__ __forceinline__ void split4(const float4 x, float4& h, float4& l) {
 
 // ------------------------------------------------------------------ kernel
 struct TcMaps {
-  CUtensorMap a;  // delta: K1 box {32, 128} (K-major); K2 box {32, 32} (MN-major)
-  CUtensorMap b;  // factor (Q for K1, P for K2): box {32, N}
+  CUtensorMap a;  // delta: K1 box {32, 128} SW128 (K-major); K2 box {32, 32} plain ([k][m])
+  CUtensorMap b;  // factor (Q for K1, P for K2): box {32, N} SW128 (K-major)
 };
 
 constexpr int kTcThreads = 192;
-constexpr uint32_t kAStage = 128 * 32 * 4;  // 16 KB
+constexpr uint32_t kAStage = 128 * 32 * 4;  // 16 KB raw delta tile per stage
+constexpr int kTcStages = 4;                // TMEM holds 4 stages of A hi/lo (64 cols each)
+constexpr uint32_t kTmemCols = 512;         // [0,256) accumulator, [256,512) A stages
 
-// A_MN: false = K1 (A = delta rows, already K-major), true = K2 (A = delta^T: the raw tile
-// is [k][m], transposed into K-major hi/lo by the split warps).
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem desc]
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// A_MN: false = K1 (A = delta rows: the TMA tile is already K-major SW128, row m = A row);
+// true = K2 (A = delta^T: the raw TMA tile is [k][m], column m = A row).
+// The split warps turn each landed A tile into tf32-exact hi and lo parts directly in TMEM
+// (tcgen05.st; one TMEM lane per A row), so the tensor core reads A from TMEM and only the
+// small factor operand B from shared memory (hi/lo split in place).
 template <bool A_MN>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_tc_sweep(const DevT2* __restrict__ T, const TcMaps* __restrict__ maps,
@@ -74,7 +111,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t b_bytes = static_cast<uint32_t>(N) * 128;
-  const uint32_t stage_bytes = 2 * kAStage + 2 * b_bytes + (A_MN ? kAStage : 0u);
+  const uint32_t stage_bytes = kAStage + 2 * b_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
   uint64_t* full = bars;
   uint64_t* split = bars + stages;
@@ -84,7 +121,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t tmem_cols = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -99,7 +135,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
-                 "r"(tmem_cols));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -142,10 +178,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           } else {
 #pragma unroll
             for (int q = 0; q < 4; ++q)  // raw [k][m] tile: 4 boxes of 32 rows x 32 columns
-              tma_load_2d(st + 2 * kAStage + 2 * b_bytes + q * 4096, &mp->a, &full[s],
-                          tl.y + 32 * q, static_cast<int>(k));
+              tma_load_2d(st + q * 4096, &mp->a, &full[s], tl.y + 32 * q, static_cast<int>(k));
           }
-          tma_load_2d(st + 2 * kAStage, &mp->b, &full[s], static_cast<int>(k), 0);  // {k, n}
+          tma_load_2d(st + kAStage, &mp->b, &full[s], static_cast<int>(k), 0);  // {k, n}
         }
       }
     }
@@ -167,20 +202,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(&split[s], ph);
           tc_fence_after();
-          const uint32_t a_hi = su32(smem + s * stage_bytes);
-          const uint32_t a_lo = a_hi + kAStage;
-          const uint32_t b_hi = a_hi + 2 * kAStage;
+          const uint32_t a_hi = tmem + 256u + static_cast<uint32_t>(s) * 64u;
+          const uint32_t a_lo = a_hi + 32u;
+          const uint32_t b_hi = su32(smem + s * stage_bytes + kAStage);
           const uint32_t b_lo = b_hi + b_bytes;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            // K-major SW128: +32 B per 8-element k step inside the 128-B swizzle atom
-            const uint64_t ah = sdesc(a_hi + kk * 32u, 16u, 1024u);
-            const uint64_t al = sdesc(a_lo + kk * 32u, 16u, 1024u);
             const uint64_t bh = sdesc(b_hi + kk * 32u, 16u, 1024u);
             const uint64_t bl = sdesc(b_lo + kk * 32u, 16u, 1024u);
-            mma_tf32(tmem, ah, bh, idesc, first ? 0u : 1u);
-            mma_tf32(tmem, ah, bl, idesc, 1u);
-            mma_tf32(tmem, al, bh, idesc, 1u);
+            mma_tf32_ts(tmem, a_hi + kk * 8u, bh, idesc, first ? 0u : 1u);
+            mma_tf32_ts(tmem, a_hi + kk * 8u, bl, idesc, 1u);
+            mma_tf32_ts(tmem, a_lo + kk * 8u, bh, idesc, 1u);
             first = false;
           }
           mma_commit(&empty[s]);
@@ -191,9 +223,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else {
     // ---------------------------------------------------------------- split + epilogue
-    const int et = threadIdx.x - 64;     // 0..127
-    const int quarter = warp % 4;        // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane; // accumulator row (M index) of this thread
+    const int et = threadIdx.x - 64;      // 0..127
+    const int quarter = warp % 4;         // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;  // A / accumulator row of this thread
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     uint32_t it = 0, tphase = 0;
     for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
       const int4 tl = tiles[ti];
@@ -205,45 +238,43 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t ph = (it / stages) & 1;
         mbar_wait(&full[s], ph);
         uint8_t* st = smem + s * stage_bytes;
-        // hi = tf32-exact truncation, lo = x - hi
-        float4* ah = reinterpret_cast<float4*>(st);
-        float4* al = reinterpret_cast<float4*>(st + kAStage);
-        if (!A_MN) {  // in place: the TMA already wrote the K-major SW128 tile into A_hi
-#pragma unroll 4
-          for (int i = et; i < static_cast<int>(kAStage / 16); i += 128) {
-            float4 h, l;
-            split4(ah[i], h, l);
-            ah[i] = h;
-            al[i] = l;
-          }
-        } else {
-          // raw[q][k][mm] (m = 32q + mm) -> K-major SW128: row m, 16-B chunk c = k/4 stored
-          // at chunk c ^ (m % 8). Thread et owns row m = et.
-          const float* raw = reinterpret_cast<const float*>(st + 2 * kAStage + 2 * b_bytes);
-          const int m = et, q = m >> 5, mm = m & 31;
+        // this thread's A row (32 values) -> hi / lo registers -> TMEM
+        float h[32], l[32];
+        if (!A_MN) {
+          const float4* rowp = reinterpret_cast<const float4*>(st) + row * 8;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            float4 x;
-            x.x = raw[q * 1024 + (4 * c + 0) * 32 + mm];
-            x.y = raw[q * 1024 + (4 * c + 1) * 32 + mm];
-            x.z = raw[q * 1024 + (4 * c + 2) * 32 + mm];
-            x.w = raw[q * 1024 + (4 * c + 3) * 32 + mm];
-            float4 h, l;
-            split4(x, h, l);
-            const int idx = m * 8 + (c ^ (m & 7));
-            ah[idx] = h;
-            al[idx] = l;
+            const float4 x = rowp[c ^ (row & 7)];  // SW128: chunk c stored at c ^ (row % 8)
+            float4 hh, ll;
+            split4(x, hh, ll);
+            h[4 * c + 0] = hh.x; h[4 * c + 1] = hh.y; h[4 * c + 2] = hh.z; h[4 * c + 3] = hh.w;
+            l[4 * c + 0] = ll.x; l[4 * c + 1] = ll.y; l[4 * c + 2] = ll.z; l[4 * c + 3] = ll.w;
+          }
+        } else {
+          const float* raw = reinterpret_cast<const float*>(st);
+          const int q = row >> 5, mm = row & 31;
+#pragma unroll
+          for (int kk = 0; kk < 32; ++kk) {
+            const float x = raw[q * 1024 + kk * 32 + mm];
+            h[kk] = tf32_hi(x);
+            l[kk] = x - h[kk];
           }
         }
-        float4* bh = reinterpret_cast<float4*>(st + 2 * kAStage);
-        float4* bl = reinterpret_cast<float4*>(st + 2 * kAStage + b_bytes);
+        const uint32_t a_col = 256u + static_cast<uint32_t>(s) * 64u;
+        tmem_st32(tmem + lane_base + a_col, h);
+        tmem_st32(tmem + lane_base + a_col + 32u, l);
+        // factor operand B: split in place in shared memory
+        float4* bh = reinterpret_cast<float4*>(st + kAStage);
+        float4* bl = reinterpret_cast<float4*>(st + kAStage + b_bytes);
         for (int i = et; i < static_cast<int>(b_bytes / 16); i += 128) {
-          float4 h, l;
-          split4(bh[i], h, l);
-          bh[i] = h;
-          bl[i] = l;
+          float4 hh, ll;
+          split4(bh[i], hh, ll);
+          bh[i] = hh;
+          bl[i] = ll;
         }
+        tmem_st_wait();
         fence_async_smem();
+        tc_fence_before();
         mbar_arrive(&split[s]);
       }
       // epilogue: TMEM -> column-major factor (or split-K partial)
@@ -260,7 +291,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       for (int c = 0; c < N; c += 16) {
         float v[16];
-        tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
+        tmem_ld16(tmem + lane_base + c, v);
         if (m < mlim) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
@@ -276,7 +307,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(tmem_cols));
+                 "r"(kTmemCols));
   }
 }
 
@@ -379,10 +410,12 @@ static const TcMaps* tc_maps(const Plan& P, int which, const float* slab, const 
   return S.d_maps[which];
 }
 
-static int tc_stage_bytes(int N, bool a_mn) { return 2 * 16384 + 2 * N * 128 + (a_mn ? 16384 : 0); }
+static int tc_stage_bytes(int N, bool) { return 16384 + 2 * N * 128; }
 
 static int tc_stages(int N, bool a_mn) {
-  return std::max(2, std::min(6, (200 * 1024) / tc_stage_bytes(N, a_mn)));
+  (void)N;
+  (void)a_mn;
+  return kTcStages;  // bounded by the TMEM A ring (4 x 64 columns)
 }
 
 static size_t tc_smem(int N, bool a_mn, int stages) {
