@@ -224,12 +224,23 @@ __global__ void __launch_bounds__(256, 3) k5_outer(const DevT2* __restrict__ T,
 // the factor GEMM for the tile while the copies land, then run the fused epilogue from
 // shared memory and store the three outputs (evict-first). Up to 4 x 32 KB of operand
 // traffic is in flight per SM.
-constexpr int kK5Stages = 4;
-constexpr int kK5StageBytes = 4 * 16 * 128 * 4;  // 4 streams x 16 rows x 128 floats
+constexpr int kK5Stages = 5;
+constexpr int kK5StreamBytes = 16 * 128 * 4;               // one operand box: 16 rows x 128
+constexpr int kK5StageBytes = 4 * kK5StreamBytes + 32 * 16 * 4;  // 4 operands + Phat tile
 
 struct K5Maps {
-  CUtensorMap m[4];  // pending, anchor, velocity, local: dims {b, a}, box {128, 16}
+  // pending, anchor, velocity, local: dims {b, a}, box {128, 16};
+  // [4] = this tensor's dequantised left factors Phat: dims {lda, D*r}, box {16, 32}
+  CUtensorMap m[5];
 };
+
+// Contiguous tile chunk of this CTA (tiles are column-block-major, so consecutive tiles share
+// the Qhat block and it is loaded once per block).
+__device__ __forceinline__ void k5_chunk(int ntiles, int& t0, int& t1) {
+  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+  t0 = blockIdx.x * per;
+  t1 = min(ntiles, t0 + per);
+}
 
 template <bool SELF>
 __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
@@ -237,7 +248,7 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
                                                     const int4* __restrict__ tiles, int ntiles,
                                                     const float* __restrict__ phat,
                                                     const float* __restrict__ qhat, int D,
-                                                    int self_index, int mode,
+                                                    int self_index, int mode, int ps_tma,
                                                     float* __restrict__ pending,
                                                     float* __restrict__ anchor,
                                                     const float* __restrict__ local,
@@ -245,10 +256,10 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
                                                     float beta, int classical,
                                                     dlx_round_stats* stats) {
   extern __shared__ __align__(128) uint8_t k5smem[];
-  float* ring = reinterpret_cast<float*>(k5smem);                         // [stage][stream][16][128]
+  float* ring = reinterpret_cast<float*>(k5smem);  // [stage]{[stream][16][128], Ps[32][16]}
   float* Qs = reinterpret_cast<float*>(k5smem + kK5Stages * kK5StageBytes);  // [32][132]
-  float* Ps = Qs + 32 * 132;                                                // [32][20]
-  uint64_t* full = reinterpret_cast<uint64_t*>(Ps + 32 * 20);
+  float* Pg = Qs + 32 * 132;                                                // [32][20]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Pg + 32 * 20);
   uint64_t* empty = full + kK5Stages;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const bool ovl = mode == DLX_MODE_OVERLAPPED;
@@ -260,23 +271,24 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  int t_begin, t_end;
+  k5_chunk(ntiles, t_begin, t_end);
 
   if (warp == 8) {
-    // ------------------------------------------------------------ producer (bulk copies)
+    // ------------------------------------------------------------ producer (TMA)
     if (lane == 0) {
       uint32_t it = 0;
-      for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+      for (int ti = t_begin; ti < t_end; ++ti, ++it) {
         const int4 tl = tiles[ti];
-        const DevT2 t = T[tl.x];
         const int s = it % kK5Stages;
         mbar_wait(&empty[s], ((it / kK5Stages) & 1) ^ 1);
-        (void)t;
         const int nstreams = ovl ? 4 : 3;
-        mbar_expect_tx(&full[s], 16 * 128 * 4 * nstreams);  // full boxes (OOB zero-filled)
+        mbar_expect_tx(&full[s], kK5StreamBytes * nstreams + (ps_tma ? 32 * 16 * 4 : 0));
         float* st = ring + s * (kK5StageBytes / 4);
         const K5Maps* mp = maps + tl.x;
         for (int q = 0; q < nstreams; ++q)
           tma_load_2d(st + q * 16 * 128, &mp->m[q], &full[s], tl.z, tl.y);
+        if (ps_tma) tma_load_2d(st + 4 * 16 * 128, &mp->m[4], &full[s], tl.y, 0);
       }
     }
     return;
@@ -288,7 +300,7 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
   const float invD = __fdiv_rn(1.0f, (float)D);
   int cached_slot = -1, cached_n0 = -1;
   uint32_t it = 0;
-  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+  for (int ti = t_begin; ti < t_end; ++ti, ++it) {
     const int4 tl = tiles[ti];
     const DevT2 t = T[tl.x];
     const int64_t m0 = tl.y, n0 = tl.z;
@@ -296,36 +308,51 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
     const float* Ph = phat + D * t.poff;
     const float* Qh = qhat + D * t.qoff;
     const int s_lo = SELF ? self_index * t.r : K, s_hi = s_lo + t.r;
+    const int s = it % kK5Stages;
+    const float* st = ring + s * (kK5StageBytes / 4);
     float acc[2][4], sacc[2][4];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j] = sacc[i][j] = 0.f;
-    const bool reuse_q = (tl.x == cached_slot && n0 == cached_n0 && K <= 32);
+    const bool one_chunk = K <= 32;
+    const bool reuse_q = one_chunk && tl.x == cached_slot && n0 == cached_n0;
     for (int k0 = 0; k0 < K; k0 += 32) {
-      named_bar(1, 256);  // previous users of Ps / Qs are done
-      if (tid < 128) {
-        const int kk = tid / 4, c4 = (tid % 4) * 4;
-        const int k = k0 + kk;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k < K) v = *reinterpret_cast<const float4*>(Ph + (int64_t)k * t.lda + m0 + c4);
-        *reinterpret_cast<float4*>(&Ps[kk * 20 + c4]) = v;
-      }
-      if (!reuse_q) {
-#pragma unroll
-        for (int l = 0; l < 4; ++l) {
-          const int e = tid + 256 * l, kk = e / 32, c4 = (e % 32) * 4;
+      const float* Ps;
+      int pstride;
+      if (!(reuse_q && ps_tma)) {
+        named_bar(1, 256);  // previous users of Pg / Qs are done
+        if (!ps_tma && tid < 128) {
+          const int kk = tid / 4, c4 = (tid % 4) * 4;
           const int k = k0 + kk;
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (k < K && n0 + c4 < t.ldb)
-            v = *reinterpret_cast<const float4*>(Qh + (int64_t)k * t.ldb + n0 + c4);
-          *reinterpret_cast<float4*>(&Qs[kk * 132 + c4]) = v;
+          if (k < K) v = *reinterpret_cast<const float4*>(Ph + (int64_t)k * t.lda + m0 + c4);
+          *reinterpret_cast<float4*>(&Pg[kk * 20 + c4]) = v;
         }
+        if (!reuse_q) {
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            const int e = tid + 256 * l, kk = e / 32, c4 = (e % 32) * 4;
+            const int k = k0 + kk;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (k < K && n0 + c4 < t.ldb)
+              v = *reinterpret_cast<const float4*>(Qh + (int64_t)k * t.ldb + n0 + c4);
+            *reinterpret_cast<float4*>(&Qs[kk * 132 + c4]) = v;
+          }
+        }
+        named_bar(1, 256);
       }
-      named_bar(1, 256);
+      if (ps_tma) {
+        if (k0 == 0) mbar_wait(&full[s], (it / kK5Stages) & 1);
+        Ps = st + 4 * 16 * 128;  // [k][16] from the TMA box
+        pstride = 16;
+      } else {
+        Ps = Pg;
+        pstride = 20;
+      }
       const int kmax = min(32, K - k0);
       for (int kk = 0; kk < kmax; ++kk) {
-        const float2 a2 = *reinterpret_cast<const float2*>(&Ps[kk * 20 + ty * 2]);
+        const float2 a2 = *reinterpret_cast<const float2*>(&Ps[kk * pstride + ty * 2]);
         const float4 b4 = *reinterpret_cast<const float4*>(&Qs[kk * 132 + tx * 4]);
         const float av[2] = {a2.x, a2.y}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
@@ -347,9 +374,7 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
     cached_n0 = static_cast<int>(n0);
 
     // epilogue from the landed stage
-    const int s = it % kK5Stages;
-    mbar_wait(&full[s], (it / kK5Stages) & 1);
-    const float* st = ring + s * (kK5StageBytes / 4);
+    if (!ps_tma) mbar_wait(&full[s], (it / kK5Stages) & 1);
     const int64_t col = n0 + tx * 4;
     const int nv = col < t.b ? (int)(t.b - col < 4 ? t.b - col : 4) : 0;
 #pragma unroll
@@ -417,17 +442,18 @@ static PFN_cuTensorMapEncodeTiled_v12000 k5_encode_fn() {
 }
 
 struct K5MapCache {
-  const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
+  const void* key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   K5Maps* d = nullptr;
   std::vector<K5Maps> h;
 };
 
-static const K5Maps* k5_maps(const Plan& P, const float* pending, const float* anchor,
-                             const float* velocity, const float* local, cudaStream_t s) {
+static const K5Maps* k5_maps(const Plan& P, int D, const float* pending, const float* anchor,
+                             const float* velocity, const float* local, const float* phat,
+                             cudaStream_t s) {
   static thread_local std::map<const Plan*, K5MapCache> cache;
   K5MapCache& c = cache[&P];
-  const void* key[4] = {pending, anchor, velocity, local};
-  if (c.d && std::equal(key, key + 4, c.key)) return c.d;
+  const void* key[6] = {pending, anchor, velocity, local, phat, reinterpret_cast<const void*>(static_cast<intptr_t>(D))};
+  if (c.d && std::equal(key, key + 6, c.key)) return c.d;
   if (!c.d) DLX_CUDA(cudaMalloc(&c.d, sizeof(K5Maps) * std::max<size_t>(P.t2.size(), 1)));
   c.h.assign(P.t2.size(), K5Maps{});
   for (size_t k = 0; k < P.t2.size(); ++k) {
@@ -446,10 +472,22 @@ static const K5Maps* k5_maps(const Plan& P, const float* pending, const float* a
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled (K5) failed");
     }
+    if (D * t.r <= 32) {  // Phat tile map (box 16 rows x 32 factor columns)
+      const cuuint64_t dims[2] = {static_cast<cuuint64_t>(t.lda), static_cast<cuuint64_t>(D * t.r)};
+      const cuuint64_t strides[1] = {static_cast<cuuint64_t>(t.lda) * 4};
+      const cuuint32_t box[2] = {16, 32};
+      const cuuint32_t estr[2] = {1, 1};
+      CUresult r = k5_encode_fn()(&c.h[k].m[4], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                  const_cast<float*>(phat) + D * t.poff, dims, strides, box, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled (K5 Phat) failed");
+    }
   }
   DLX_CUDA(cudaMemcpyAsync(c.d, c.h.data(), sizeof(K5Maps) * P.t2.size(), cudaMemcpyHostToDevice, s));
   DLX_CUDA(cudaStreamSynchronize(s));
-  std::copy(key, key + 4, c.key);
+  std::copy(key, key + 6, c.key);
   return c.d;
 }
 
@@ -477,15 +515,16 @@ void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered
     DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int n = static_cast<int>(P.k5s_tiles.size());
     const int grid = std::min(n, sms);
-    const K5Maps* maps = k5_maps(P, pending, anchor, velocity,
-                                 mode == DLX_MODE_OVERLAPPED ? local : nullptr, s);
+    const K5Maps* maps = k5_maps(P, D, pending, anchor, velocity,
+                                 mode == DLX_MODE_OVERLAPPED ? local : nullptr, phat, s);
+    const int ps_tma = D * P.rmax <= 32 ? 1 : 0;
     if (self_index >= 0)
       k5s_outer<true><<<grid, 288, k5s_smem(), s>>>(P.d_t2, maps, P.d_k5s_tiles, n, phat, qhat, D,
-                                                    self_index, mode, pending, anchor, local,
+                                                    self_index, mode, ps_tma, pending, anchor, local,
                                                     velocity, gamma, beta, classical, stats);
     else
       k5s_outer<false><<<grid, 288, k5s_smem(), s>>>(P.d_t2, maps, P.d_k5s_tiles, n, phat, qhat, D,
-                                                     self_index, mode, pending, anchor, local,
+                                                     self_index, mode, ps_tma, pending, anchor, local,
                                                      velocity, gamma, beta, classical, stats);
     DLX_LAUNCHED();
   }

@@ -62,7 +62,6 @@ struct TcMaps {
 
 constexpr int kTcThreads = 192;
 constexpr uint32_t kAStage = 128 * 32 * 4;  // 16 KB raw delta tile per stage
-constexpr int kTcStages = 4;                // TMEM holds 4 stages of A hi/lo (64 cols each)
 constexpr uint32_t kTmemCols = 512;         // [0,256) accumulator, [256,512) A stages
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
@@ -99,34 +98,41 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
 
 // A_MN: false = K1 (A = delta rows: the TMA tile is already K-major SW128, row m = A row);
 // true = K2 (A = delta^T: the raw TMA tile is [k][m], column m = A row).
-// The split warps turn each landed A tile into tf32-exact hi and lo parts directly in TMEM
-// (tcgen05.st; one TMEM lane per A row), so the tensor core reads A from TMEM and only the
-// small factor operand B from shared memory (hi/lo split in place).
+// Two rings decouple memory latency from the MMA: a deep LOAD ring (lr stages of raw A + B
+// in shared memory, filled by TMA) and a shallow COMPUTE ring (cr slots of A hi/lo in TMEM,
+// written with tcgen05.st, + B hi/lo in shared memory). The split warps move a landed load
+// stage into a compute slot and immediately release the load stage, so up to lr x 20 KB of
+// HBM traffic stays in flight per SM independently of the MMA pipeline.
 template <bool A_MN>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_tc_sweep(const DevT2* __restrict__ T, const TcMaps* __restrict__ maps,
-               const int4* __restrict__ tiles, int ntiles, int N, int stages,
+               const int4* __restrict__ tiles, int ntiles, int N, int lr, int cr,
                const int* __restrict__ splits, const int64_t* __restrict__ part_off,
                float* __restrict__ out, float* __restrict__ part) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t b_bytes = static_cast<uint32_t>(N) * 128;
-  const uint32_t stage_bytes = kAStage + 2 * b_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
-  uint64_t* full = bars;
-  uint64_t* split = bars + stages;
-  uint64_t* empty = bars + 2 * stages;
-  uint64_t* tfull = bars + 3 * stages;
+  const uint32_t ls_bytes = kAStage + b_bytes;  // load stage: raw A + raw B
+  uint8_t* cring = smem + lr * ls_bytes;        // compute slots: B hi + B lo
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cring + cr * 2 * b_bytes);
+  uint64_t* lfull = bars;
+  uint64_t* lempty = lfull + lr;
+  uint64_t* cfull = lempty + lr;
+  uint64_t* cempty = cfull + cr;
+  uint64_t* tfull = cempty + cr;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&split[s], 128);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < lr; ++s) {
+      mbar_init(&lfull[s], 1);
+      mbar_init(&lempty[s], 128);
+    }
+    for (int s = 0; s < cr; ++s) {
+      mbar_init(&cfull[s], 128);
+      mbar_init(&cempty[s], 1);
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 128);
@@ -168,19 +174,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         int64_t k0, k1;
         tile_k(tl, t, k0, k1);
         for (int64_t k = k0; k < k1; k += 32, ++it) {
-          const int s = it % stages;
-          const uint32_t ph = (it / stages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * stage_bytes;
-          mbar_expect_tx(&full[s], kAStage + b_bytes);
+          const int s = it % lr;
+          mbar_wait(&lempty[s], ((it / lr) & 1) ^ 1);
+          uint8_t* st = smem + s * ls_bytes;
+          mbar_expect_tx(&lfull[s], kAStage + b_bytes);
           if (!A_MN) {
-            tma_load_2d(st, &mp->a, &full[s], static_cast<int>(k), tl.y);  // {k, m0}
+            tma_load_2d(st, &mp->a, &lfull[s], static_cast<int>(k), tl.y);  // {k, m0}
           } else {
 #pragma unroll
             for (int q = 0; q < 4; ++q)  // raw [k][m] tile: 4 boxes of 32 rows x 32 columns
-              tma_load_2d(st + q * 4096, &mp->a, &full[s], tl.y + 32 * q, static_cast<int>(k));
+              tma_load_2d(st + q * 4096, &mp->a, &lfull[s], tl.y + 32 * q, static_cast<int>(k));
           }
-          tma_load_2d(st + kAStage, &mp->b, &full[s], static_cast<int>(k), 0);  // {k, n}
+          tma_load_2d(st + kAStage, &mp->b, &lfull[s], static_cast<int>(k), 0);  // {k, n}
         }
       }
     }
@@ -198,13 +203,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tc_fence_after();
         bool first = true;
         for (int64_t k = k0; k < k1; k += 32, ++it) {
-          const int s = it % stages;
-          const uint32_t ph = (it / stages) & 1;
-          mbar_wait(&split[s], ph);
+          const int c = it % cr;
+          mbar_wait(&cfull[c], (it / cr) & 1);
           tc_fence_after();
-          const uint32_t a_hi = tmem + 256u + static_cast<uint32_t>(s) * 64u;
+          const uint32_t a_hi = tmem + 256u + static_cast<uint32_t>(c) * 64u;
           const uint32_t a_lo = a_hi + 32u;
-          const uint32_t b_hi = su32(smem + s * stage_bytes + kAStage);
+          const uint32_t b_hi = su32(cring + c * 2 * b_bytes);
           const uint32_t b_lo = b_hi + b_bytes;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mma_tf32_ts(tmem, a_lo + kk * 8u, bh, idesc, 1u);
             first = false;
           }
-          mma_commit(&empty[s]);
+          mma_commit(&cempty[c]);
         }
         mma_commit(tfull);
         tphase ^= 1;
@@ -227,6 +231,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int quarter = warp % 4;         // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;  // A / accumulator row of this thread
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const int bvec = static_cast<int>(b_bytes / 16);
     uint32_t it = 0, tphase = 0;
     for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
       const int4 tl = tiles[ti];
@@ -234,21 +239,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int64_t k0, k1;
       tile_k(tl, t, k0, k1);
       for (int64_t k = k0; k < k1; k += 32, ++it) {
-        const int s = it % stages;
-        const uint32_t ph = (it / stages) & 1;
-        mbar_wait(&full[s], ph);
-        uint8_t* st = smem + s * stage_bytes;
-        // this thread's A row (32 values) -> hi / lo registers -> TMEM
+        const int s = it % lr, c = it % cr;
+        mbar_wait(&lfull[s], (it / lr) & 1);
+        const uint8_t* st = smem + s * ls_bytes;
+        // this thread's A row (32 values) -> hi / lo registers
         float h[32], l[32];
         if (!A_MN) {
           const float4* rowp = reinterpret_cast<const float4*>(st) + row * 8;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 x = rowp[c ^ (row & 7)];  // SW128: chunk c stored at c ^ (row % 8)
+          for (int q = 0; q < 8; ++q) {
+            const float4 x = rowp[q ^ (row & 7)];  // SW128: chunk q stored at q ^ (row % 8)
             float4 hh, ll;
             split4(x, hh, ll);
-            h[4 * c + 0] = hh.x; h[4 * c + 1] = hh.y; h[4 * c + 2] = hh.z; h[4 * c + 3] = hh.w;
-            l[4 * c + 0] = ll.x; l[4 * c + 1] = ll.y; l[4 * c + 2] = ll.z; l[4 * c + 3] = ll.w;
+            h[4 * q + 0] = hh.x; h[4 * q + 1] = hh.y; h[4 * q + 2] = hh.z; h[4 * q + 3] = hh.w;
+            l[4 * q + 0] = ll.x; l[4 * q + 1] = ll.y; l[4 * q + 2] = ll.z; l[4 * q + 3] = ll.w;
           }
         } else {
           const float* raw = reinterpret_cast<const float*>(st);
@@ -260,22 +264,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             l[kk] = x - h[kk];
           }
         }
-        const uint32_t a_col = 256u + static_cast<uint32_t>(s) * 64u;
-        tmem_st32(tmem + lane_base + a_col, h);
-        tmem_st32(tmem + lane_base + a_col + 32u, l);
-        // factor operand B: split in place in shared memory
-        float4* bh = reinterpret_cast<float4*>(st + kAStage);
-        float4* bl = reinterpret_cast<float4*>(st + kAStage + b_bytes);
-        for (int i = et; i < static_cast<int>(b_bytes / 16); i += 128) {
+        // B: raw (load stage) -> hi / lo (compute slot) once the slot is free
+        mbar_wait(&cempty[c], ((it / cr) & 1) ^ 1);
+        tc_fence_after();
+        const float4* braw = reinterpret_cast<const float4*>(st + kAStage);
+        float4* bh = reinterpret_cast<float4*>(cring + c * 2 * b_bytes);
+        float4* bl = reinterpret_cast<float4*>(cring + c * 2 * b_bytes + b_bytes);
+        for (int i = et; i < bvec; i += 128) {
           float4 hh, ll;
-          split4(bh[i], hh, ll);
+          split4(braw[i], hh, ll);
           bh[i] = hh;
           bl[i] = ll;
         }
+        mbar_arrive(&lempty[s]);  // raw stage consumed (A values are in registers)
+        const uint32_t a_col = 256u + static_cast<uint32_t>(c) * 64u;
+        tmem_st32(tmem + lane_base + a_col, h);
+        tmem_st32(tmem + lane_base + a_col + 32u, l);
         tmem_st_wait();
         fence_async_smem();
         tc_fence_before();
-        mbar_arrive(&split[s]);
+        mbar_arrive(&cfull[c]);
       }
       // epilogue: TMEM -> column-major factor (or split-K partial)
       mbar_wait(tfull, tphase);
@@ -289,13 +297,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       } else {
         dst = splits[tl.x] > 1 ? part + part_off[tl.x] + tl.w * (t.ldb * t.r) : out + t.qoff;
       }
-      for (int c = 0; c < N; c += 16) {
+      for (int cc = 0; cc < N; cc += 16) {
         float v[16];
-        tmem_ld16(tmem + lane_base + c, v);
+        tmem_ld16(tmem + lane_base + cc, v);
         if (m < mlim) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (c + j < t.r) dst[(c + j) * ld + m] = v[j];
+            if (cc + j < t.r) dst[(cc + j) * ld + m] = v[j];
         }
       }
       tc_fence_before();
@@ -410,16 +418,20 @@ static const TcMaps* tc_maps(const Plan& P, int which, const float* slab, const 
   return S.d_maps[which];
 }
 
-static int tc_stage_bytes(int N, bool) { return 16384 + 2 * N * 128; }
-
-static int tc_stages(int N, bool a_mn) {
-  (void)N;
-  (void)a_mn;
-  return kTcStages;  // bounded by the TMEM A ring (4 x 64 columns)
+// Ring sizes (load stages lr, compute slots cr) that fit ~220 KB of shared memory.
+static void tc_rings(int N, int& lr, int& cr) {
+  const int b = N * 128;
+  for (cr = 4; cr >= 2; cr -= 2) {
+    lr = (220 * 1024 - cr * 2 * b) / (16384 + b);
+    if (lr >= 3 || cr == 2) break;
+  }
+  lr = std::max(2, std::min(lr, 10));
 }
 
-static size_t tc_smem(int N, bool a_mn, int stages) {
-  return 1024 + static_cast<size_t>(stages) * tc_stage_bytes(N, a_mn) + 8 * (3 * stages + 2) + 16;
+static size_t tc_smem(int N, int lr, int cr) {
+  const int b = N * 128;
+  return 1024 + static_cast<size_t>(lr) * (16384 + b) + static_cast<size_t>(cr) * 2 * b +
+         8 * (2 * lr + 2 * cr + 2) + 16;
 }
 
 static int num_sms() {
@@ -437,8 +449,9 @@ static void launch_sweep(const Plan& P, const TcMaps* maps, const std::vector<in
                          const int4* d_tiles, float* out, float* part, cudaStream_t s) {
   if (tiles.empty()) return;
   const int N = tc_n(P);
-  const int stages = tc_stages(N, A_MN);
-  const size_t sm = tc_smem(N, A_MN, stages);
+  int lr = 0, cr = 0;
+  tc_rings(N, lr, cr);
+  const size_t sm = tc_smem(N, lr, cr);
   static bool attr = false;
   if (!attr) {
     DLX_CUDA(cudaFuncSetAttribute(k_tc_sweep<A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -447,7 +460,7 @@ static void launch_sweep(const Plan& P, const TcMaps* maps, const std::vector<in
   }
   const int grid = static_cast<int>(std::min<size_t>(tiles.size(), num_sms()));
   k_tc_sweep<A_MN><<<grid, kTcThreads, sm, s>>>(P.d_t2, maps, d_tiles, (int)tiles.size(), N,
-                                                stages, P.d_k2_splits, P.d_k2_part_off, out, part);
+                                                lr, cr, P.d_k2_splits, P.d_k2_part_off, out, part);
   DLX_LAUNCHED();
 }
 
