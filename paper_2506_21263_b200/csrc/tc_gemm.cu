@@ -20,6 +20,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 #include <cstring>
 
 #include "dlx_internal.cuh"
@@ -60,9 +63,9 @@ struct TcMaps {
   CUtensorMap b;  // factor (Q for K1, P for K2): box {32, N} SW128 (K-major)
 };
 
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;  // producer warp, MMA warp, 8 split/epilogue warps
 constexpr uint32_t kAStage = 128 * 32 * 4;  // 16 KB raw delta tile per stage
-constexpr uint32_t kTmemCols = 512;         // [0,256) accumulator, [256,512) A stages
+constexpr uint32_t kTmemCols = 512;  // [0,N) accumulator, then compute slots of A hi/lo (64 cols)
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
   asm volatile(
@@ -82,6 +85,18 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -96,6 +111,18 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       : "memory");
 }
 
+// Ring position (slot, phase) advanced without integer division.
+struct Ring {
+  int slot = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
 // A_MN: false = K1 (A = delta rows: the TMA tile is already K-major SW128, row m = A row);
 // true = K2 (A = delta^T: the raw TMA tile is [k][m], column m = A row).
 // Two rings decouple memory latency from the MMA: a deep LOAD ring (lr stages of raw A + B
@@ -106,9 +133,11 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
 template <bool A_MN>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_tc_sweep(const DevT2* __restrict__ T, const TcMaps* __restrict__ maps,
-               const int4* __restrict__ tiles, int ntiles, int N, int lr, int cr,
+               const int4* __restrict__ tiles, const int* __restrict__ cta_off, int N,
+               int lr, int cr,
                const int* __restrict__ splits, const int64_t* __restrict__ part_off,
-               float* __restrict__ out, float* __restrict__ part) {
+               float* __restrict__ out, float* __restrict__ part, int variant,
+               unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t b_bytes = static_cast<uint32_t>(N) * 128;
@@ -128,14 +157,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < lr; ++s) {
       mbar_init(&lfull[s], 1);
-      mbar_init(&lempty[s], 128);
+      mbar_init(&lempty[s], 256);
     }
     for (int s = 0; s < cr; ++s) {
-      mbar_init(&cfull[s], 128);
+      mbar_init(&cfull[s], 256);
       mbar_init(&cempty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 128);
+    mbar_init(tempty, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -148,6 +177,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t a_base = static_cast<uint32_t>((N + 31) / 32 * 32);  // A slots after the accumulator
   constexpr int64_t KC = 2048;
 
   // k-loop extent of a tile
@@ -163,20 +193,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-        const int4 tl = tiles[ti];
-        const DevT2 t = T[tl.x];
-        const TcMaps* mp = maps + tl.x;
+    // warp-uniform loop, one elected lane issues (TMA operands must be uniform)
+    Ring L;
+    for (int ti = cta_off[blockIdx.x]; ti < cta_off[blockIdx.x + 1]; ++ti) {
+      const int4 tl = tiles[ti];
+      const DevT2 t = T[tl.x];
+      const TcMaps* mp = maps + tl.x;
+      if (elect_one()) {
         prefetch_map(&mp->a);
         prefetch_map(&mp->b);
-        int64_t k0, k1;
-        tile_k(tl, t, k0, k1);
-        for (int64_t k = k0; k < k1; k += 32, ++it) {
-          const int s = it % lr;
-          mbar_wait(&lempty[s], ((it / lr) & 1) ^ 1);
-          uint8_t* st = smem + s * ls_bytes;
+      }
+      __syncwarp();
+      int64_t k0, k1;
+      tile_k(tl, t, k0, k1);
+      for (int64_t k = k0; k < k1; k += 32, L.next(lr)) {
+        const int s = L.slot;
+        mbar_wait(&lempty[s], L.phase ^ 1);
+        uint8_t* st = smem + s * ls_bytes;
+        if (elect_one()) {
           mbar_expect_tx(&lfull[s], kAStage + b_bytes);
           if (!A_MN) {
             tma_load_2d(st, &mp->a, &lfull[s], static_cast<int>(k), tl.y);  // {k, m0}
@@ -187,106 +221,138 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           tma_load_2d(st + kAStage, &mp->b, &lfull[s], static_cast<int>(k), 0);  // {k, n}
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(N, false, false);
-      uint32_t it = 0, tphase = 0;
-      for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-        const int4 tl = tiles[ti];
-        const DevT2 t = T[tl.x];
-        int64_t k0, k1;
-        tile_k(tl, t, k0, k1);
-        mbar_wait(tempty, tphase ^ 1);
-        tc_fence_after();
-        bool first = true;
-        for (int64_t k = k0; k < k1; k += 32, ++it) {
-          const int c = it % cr;
-          mbar_wait(&cfull[c], (it / cr) & 1);
-          tc_fence_after();
-          const uint32_t a_hi = tmem + 256u + static_cast<uint32_t>(c) * 64u;
-          const uint32_t a_lo = a_hi + 32u;
-          const uint32_t b_hi = su32(cring + c * 2 * b_bytes);
-          const uint32_t b_lo = b_hi + b_bytes;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t bh = sdesc(b_hi + kk * 32u, 16u, 1024u);
-            const uint64_t bl = sdesc(b_lo + kk * 32u, 16u, 1024u);
-            mma_tf32_ts(tmem, a_hi + kk * 8u, bh, idesc, first ? 0u : 1u);
-            mma_tf32_ts(tmem, a_hi + kk * 8u, bl, idesc, 1u);
-            mma_tf32_ts(tmem, a_lo + kk * 8u, bh, idesc, 1u);
-            first = false;
-          }
-          mma_commit(&cempty[c]);
-        }
-        mma_commit(tfull);
-        tphase ^= 1;
-      }
-    }
-  } else {
-    // ---------------------------------------------------------------- split + epilogue
-    const int et = threadIdx.x - 64;      // 0..127
-    const int quarter = warp % 4;         // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;  // A / accumulator row of this thread
-    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const int bvec = static_cast<int>(b_bytes / 16);
-    uint32_t it = 0, tphase = 0;
-    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    // The whole warp runs the (warp-uniform) loop so descriptors and TMEM addresses live in
+    // uniform registers; one elected lane issues each tcgen05.mma / commit.
+    const uint32_t idesc = idesc_tf32(N, false, false);
+    // the k step adds 32 B = 2 units of the 16-B start-address field
+    const uint64_t bdesc_hi0 = sdesc(su32(cring), 16u, 1024u);
+    const uint64_t bdesc_lo0 = sdesc(su32(cring) + b_bytes, 16u, 1024u);
+    const uint64_t slot_step = (2u * b_bytes) >> 4;  // start-address units per compute slot
+    uint32_t tphase = 0;
+    Ring C;
+    for (int ti = cta_off[blockIdx.x]; ti < cta_off[blockIdx.x + 1]; ++ti) {
       const int4 tl = tiles[ti];
       const DevT2 t = T[tl.x];
       int64_t k0, k1;
       tile_k(tl, t, k0, k1);
-      for (int64_t k = k0; k < k1; k += 32, ++it) {
-        const int s = it % lr, c = it % cr;
-        mbar_wait(&lfull[s], (it / lr) & 1);
+      {
+        const long long w0 = clock64();
+        mbar_wait(tempty, tphase ^ 1);
+        if (prof && lane == 0) atomicAdd(&prof[blockIdx.x * 8 + 2], (unsigned long long)(clock64() - w0));
+      }
+      tc_fence_after();
+      uint32_t acc = 0;
+      for (int64_t k = k0; k < k1; k += 32, C.next(cr)) {
+        const int c = C.slot;
+        const long long w0 = clock64();
+        mbar_wait(&cfull[c], C.phase);
+        if (prof && lane == 0) atomicAdd(&prof[blockIdx.x * 8 + 0], (unsigned long long)(clock64() - w0));
+        tc_fence_after();
+        const uint32_t a_hi = tmem + a_base + static_cast<uint32_t>(c) * 64u;
+        const uint32_t a_lo = a_hi + 32u;
+        const uint64_t bh = bdesc_hi0 + slot_step * c, bl = bdesc_lo0 + slot_step * c;
+        if (elect_one()) {
+          if (!(variant & 4)) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              mma_tf32_ts(tmem, a_hi + kk * 8u, bh + 2u * kk, idesc, acc | kk);
+              if (!(variant & 1)) {
+                mma_tf32_ts(tmem, a_hi + kk * 8u, bl + 2u * kk, idesc, 1u);
+                mma_tf32_ts(tmem, a_lo + kk * 8u, bh + 2u * kk, idesc, 1u);
+              }
+            }
+          }
+          mma_commit(&cempty[c]);
+        }
+        __syncwarp();
+        acc = 1u;
+        if (prof && lane == 0) atomicAdd(&prof[blockIdx.x * 8 + 1], (unsigned long long)(clock64() - w0));
+      }
+      if (elect_one()) mma_commit(tfull);
+      __syncwarp();
+      tphase ^= 1;
+    }
+  } else {
+    // ---------------------------------------------------------------- split + epilogue
+    // 8 warps: two per TMEM lane quarter; warp half h handles K columns [16h, 16h + 16)
+    const int et = threadIdx.x - 64;      // 0..255
+    const int quarter = warp % 4;         // TMEM lane quarter this warp may access
+    const int half = (warp - 2) / 4;      // 0 or 1
+    const int row = quarter * 32 + lane;  // A / accumulator row of this thread
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const int bvec = static_cast<int>(b_bytes / 16);
+    uint32_t tphase = 0;
+    Ring L, C;
+    for (int ti = cta_off[blockIdx.x]; ti < cta_off[blockIdx.x + 1]; ++ti) {
+      const int4 tl = tiles[ti];
+      const DevT2 t = T[tl.x];
+      int64_t k0, k1;
+      tile_k(tl, t, k0, k1);
+      for (int64_t k = k0; k < k1; k += 32, L.next(lr), C.next(cr)) {
+        const int s = L.slot, c = C.slot;
+        const bool pt = prof && et == 0;
+        long long w0 = pt ? clock64() : 0;
+        mbar_wait(&lfull[s], L.phase);
+        if (pt) { atomicAdd(&prof[blockIdx.x * 8 + 3], (unsigned long long)(clock64() - w0)); w0 = clock64(); }
         const uint8_t* st = smem + s * ls_bytes;
-        // this thread's A row (32 values) -> hi / lo registers
-        float h[32], l[32];
+        // 16 values of this thread's A row -> hi / lo registers
+        float h[16], l[16];
         if (!A_MN) {
           const float4* rowp = reinterpret_cast<const float4*>(st) + row * 8;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
+          for (int qq = 0; qq < 4; ++qq) {
+            const int q = half * 4 + qq;
             const float4 x = rowp[q ^ (row & 7)];  // SW128: chunk q stored at q ^ (row % 8)
             float4 hh, ll;
             split4(x, hh, ll);
-            h[4 * q + 0] = hh.x; h[4 * q + 1] = hh.y; h[4 * q + 2] = hh.z; h[4 * q + 3] = hh.w;
-            l[4 * q + 0] = ll.x; l[4 * q + 1] = ll.y; l[4 * q + 2] = ll.z; l[4 * q + 3] = ll.w;
+            h[4 * qq + 0] = hh.x; h[4 * qq + 1] = hh.y; h[4 * qq + 2] = hh.z; h[4 * qq + 3] = hh.w;
+            l[4 * qq + 0] = ll.x; l[4 * qq + 1] = ll.y; l[4 * qq + 2] = ll.z; l[4 * qq + 3] = ll.w;
           }
         } else {
           const float* raw = reinterpret_cast<const float*>(st);
           const int q = row >> 5, mm = row & 31;
 #pragma unroll
-          for (int kk = 0; kk < 32; ++kk) {
-            const float x = raw[q * 1024 + kk * 32 + mm];
+          for (int kk = 0; kk < 16; ++kk) {
+            const float x = raw[q * 1024 + (half * 16 + kk) * 32 + mm];
             h[kk] = tf32_hi(x);
             l[kk] = x - h[kk];
           }
         }
         // B: raw (load stage) -> hi / lo (compute slot) once the slot is free
-        mbar_wait(&cempty[c], ((it / cr) & 1) ^ 1);
+        if (pt) { atomicAdd(&prof[blockIdx.x * 8 + 4], (unsigned long long)(clock64() - w0)); w0 = clock64(); }
+        mbar_wait(&cempty[c], C.phase ^ 1);
+        if (pt) { atomicAdd(&prof[blockIdx.x * 8 + 5], (unsigned long long)(clock64() - w0)); w0 = clock64(); }
         tc_fence_after();
         const float4* braw = reinterpret_cast<const float4*>(st + kAStage);
         float4* bh = reinterpret_cast<float4*>(cring + c * 2 * b_bytes);
         float4* bl = reinterpret_cast<float4*>(cring + c * 2 * b_bytes + b_bytes);
-        for (int i = et; i < bvec; i += 128) {
+        for (int i = et; i < bvec; i += 256) {
           float4 hh, ll;
           split4(braw[i], hh, ll);
           bh[i] = hh;
           bl[i] = ll;
         }
         mbar_arrive(&lempty[s]);  // raw stage consumed (A values are in registers)
-        const uint32_t a_col = 256u + static_cast<uint32_t>(c) * 64u;
-        tmem_st32(tmem + lane_base + a_col, h);
-        tmem_st32(tmem + lane_base + a_col + 32u, l);
-        tmem_st_wait();
+        const uint32_t a_col = a_base + static_cast<uint32_t>(c) * 64u + half * 16u;
+        if (!(variant & 2)) {
+          tmem_st16(tmem + lane_base + a_col, h);
+          tmem_st16(tmem + lane_base + a_col + 32u, l);
+          tmem_st_wait();
+        }
         fence_async_smem();
         tc_fence_before();
         mbar_arrive(&cfull[c]);
+        if (pt) atomicAdd(&prof[blockIdx.x * 8 + 6], (unsigned long long)(clock64() - w0));
       }
-      // epilogue: TMEM -> column-major factor (or split-K partial)
+      // epilogue: TMEM -> column-major factor (or split-K partial); halves alternate 16-col chunks
+      const long long we = (prof && et == 0) ? clock64() : 0;
       mbar_wait(tfull, tphase);
+      if (prof && et == 0) atomicAdd(&prof[blockIdx.x * 8 + 7], (unsigned long long)(clock64() - we));
       tc_fence_after();
       const int64_t m = tl.y + row;
       const int64_t mlim = A_MN ? t.b : t.a;
@@ -297,7 +363,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       } else {
         dst = splits[tl.x] > 1 ? part + part_off[tl.x] + tl.w * (t.ldb * t.r) : out + t.qoff;
       }
-      for (int cc = 0; cc < N; cc += 16) {
+      for (int cc = half * 16; cc < N; cc += 32) {
         float v[16];
         tmem_ld16(tmem + lane_base + cc, v);
         if (m < mlim) {
@@ -350,10 +416,23 @@ bool tc_eligible(const DevT2& t) { return (t.b % 4) == 0 && t.r >= 1; }
 
 int tc_n(const Plan& P) { return static_cast<int>(std::max<int64_t>(16, round_up(P.rmax, 16))); }
 
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    DLX_CUDA(cudaGetDevice(&dev));
+    DLX_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
 struct TcState {
-  std::vector<int4> k1, k2;
+  std::vector<int4> k1, k2;  // tiles grouped per CTA (balanced, see balance())
+  std::vector<int> off1, off2;
   int4* d_k1 = nullptr;
   int4* d_k2 = nullptr;
+  int* d_off1 = nullptr;
+  int* d_off2 = nullptr;
   TcMaps* d_maps[2] = {nullptr, nullptr};
   const void* key[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
   std::vector<TcMaps> host[2];
@@ -373,15 +452,46 @@ static TcState& tc_state(const Plan& P) {
       for (int q = 0; q < sp; ++q)
         for (int64_t j0 = 0; j0 < t.b; j0 += 128) s->k2.push_back(make_int4((int)k, (int)j0, 0, q));
     }
-    auto up = [](const std::vector<int4>& v) {
-      int4* d = nullptr;
+    // Longest-processing-time assignment of tiles to persistent CTAs: tile costs differ 4x
+    // (K = 8192 vs 2048 columns), so a round-robin split leaves some SMs with 1.5x the work.
+    const int G = num_sms();
+    auto balance = [&](std::vector<int4>& tl, std::vector<int>& off, bool k2) {
+      std::vector<std::pair<int64_t, int>> cost;
+      for (size_t i = 0; i < tl.size(); ++i) {
+        const DevT2& t = P.t2[tl[i].x];
+        const int64_t kl = k2 ? std::min<int64_t>(KC, t.a - int64_t(tl[i].w) * KC) : t.b;
+        cost.push_back({ceil_div(kl, 32) + 8, static_cast<int>(i)});  // + epilogue overhead
+      }
+      std::stable_sort(cost.begin(), cost.end(), [](auto& x, auto& y) { return x.first > y.first; });
+      const int g = static_cast<int>(std::min<size_t>(tl.size(), G));
+      std::vector<std::vector<int4>> bins(std::max(g, 1));
+      std::vector<int64_t> load(std::max(g, 1), 0);
+      for (auto& c : cost) {
+        const int b = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+        load[b] += c.first;
+        bins[b].push_back(tl[c.second]);
+      }
+      tl.clear();
+      off.assign(1, 0);
+      for (auto& b : bins) {
+        tl.insert(tl.end(), b.begin(), b.end());
+        off.push_back(static_cast<int>(tl.size()));
+      }
+    };
+    balance(s->k1, s->off1, false);
+    balance(s->k2, s->off2, true);
+    auto up = [](const auto& v) {
+      using T = typename std::decay_t<decltype(v)>::value_type;
+      T* d = nullptr;
       if (v.empty()) return d;
-      DLX_CUDA(cudaMalloc(&d, sizeof(int4) * v.size()));
-      DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(int4) * v.size(), cudaMemcpyHostToDevice));
+      DLX_CUDA(cudaMalloc(&d, sizeof(T) * v.size()));
+      DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
       return d;
     };
     s->d_k1 = up(s->k1);
     s->d_k2 = up(s->k2);
+    s->d_off1 = up(s->off1);
+    s->d_off2 = up(s->off2);
     for (int w = 0; w < 2; ++w) {
       DLX_CUDA(cudaMalloc(&s->d_maps[w], sizeof(TcMaps) * std::max<size_t>(P.t2.size(), 1)));
       s->host[w].resize(P.t2.size());
@@ -421,11 +531,12 @@ static const TcMaps* tc_maps(const Plan& P, int which, const float* slab, const 
 // Ring sizes (load stages lr, compute slots cr) that fit ~220 KB of shared memory.
 static void tc_rings(int N, int& lr, int& cr) {
   const int b = N * 128;
-  for (cr = 4; cr >= 2; cr -= 2) {
+  const int a_base = (N + 31) / 32 * 32;
+  for (cr = std::min(7, (512 - a_base) / 64); cr >= 2; --cr) {
     lr = (220 * 1024 - cr * 2 * b) / (16384 + b);
-    if (lr >= 3 || cr == 2) break;
+    if (lr >= 4 || cr == 2) break;
   }
-  lr = std::max(2, std::min(lr, 10));
+  lr = std::max(2, std::min(lr, 8));
 }
 
 static size_t tc_smem(int N, int lr, int cr) {
@@ -434,19 +545,11 @@ static size_t tc_smem(int N, int lr, int cr) {
          8 * (2 * lr + 2 * cr + 2) + 16;
 }
 
-static int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    DLX_CUDA(cudaGetDevice(&dev));
-    DLX_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-  }
-  return n;
-}
 
 template <bool A_MN>
 static void launch_sweep(const Plan& P, const TcMaps* maps, const std::vector<int4>& tiles,
-                         const int4* d_tiles, float* out, float* part, cudaStream_t s) {
+                         const int4* d_tiles, const std::vector<int>& off, const int* d_off,
+                         float* out, float* part, cudaStream_t s) {
   if (tiles.empty()) return;
   const int N = tc_n(P);
   int lr = 0, cr = 0;
@@ -458,9 +561,31 @@ static void launch_sweep(const Plan& P, const TcMaps* maps, const std::vector<in
                                   227 * 1024));
     attr = true;
   }
-  const int grid = static_cast<int>(std::min<size_t>(tiles.size(), num_sms()));
-  k_tc_sweep<A_MN><<<grid, kTcThreads, sm, s>>>(P.d_t2, maps, d_tiles, (int)tiles.size(), N,
-                                                lr, cr, P.d_k2_splits, P.d_k2_part_off, out, part);
+  const int grid = static_cast<int>(off.size()) - 1;
+  static const int variant = [] {
+    const char* e = getenv("DLX_SWEEP_VARIANT");  // experiments only: 1 = 1xTF32, 2 = no TMEM
+    return e ? atoi(e) : 0;                       // stores, 4 = no MMA, 8 = lr=2
+  }();
+  if (variant & 8) lr = 2;
+  static unsigned long long* prof = nullptr;
+  if ((variant & 16) && !prof) {
+    DLX_CUDA(cudaMalloc(&prof, 8 * 8 * 1024));
+  }
+  if (prof) DLX_CUDA(cudaMemsetAsync(prof, 0, 8 * 8 * 1024, s));
+  k_tc_sweep<A_MN><<<grid, kTcThreads, sm, s>>>(P.d_t2, maps, d_tiles, d_off, N,
+                                                lr, cr, P.d_k2_splits, P.d_k2_part_off, out, part,
+                                                variant, (variant & 16) ? prof : nullptr);
+  if (variant & 16) {
+    std::vector<unsigned long long> h(8 * grid);
+    DLX_CUDA(cudaMemcpyAsync(h.data(), prof, 8 * 8 * grid, cudaMemcpyDeviceToHost, s));
+    DLX_CUDA(cudaStreamSynchronize(s));
+    double t[8] = {0};
+    for (int b = 0; b < grid; ++b)
+      for (int i = 0; i < 8; ++i) t[i] += h[b * 8 + i] / (double)grid;
+    fprintf(stderr, "[tc_sweep<%d> lr=%d cr=%d] per-CTA cycles: mma_wait_cfull=%.0f mma_stage_total=%.0f "
+                    "mma_wait_tempty=%.0f | split(lane0): wait_lfull=%.0f splitA=%.0f wait_cempty=%.0f "
+                    "rest=%.0f wait_tfull=%.0f\n", (int)A_MN, lr, cr, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+  }
   DLX_LAUNCHED();
 }
 
@@ -471,14 +596,14 @@ bool tc_supported(const Plan& P) { return P.rmax >= 1 && P.rmax <= 256; }
 void launch_k1_tc(const Plan& P, const float* slab, const float* q, float* y, cudaStream_t s) {
   TcState& S = tc_state(P);
   const TcMaps* maps = tc_maps(P, 0, slab, q, s);
-  launch_sweep<false>(P, maps, S.k1, S.d_k1, y, nullptr, s);
+  launch_sweep<false>(P, maps, S.k1, S.d_k1, S.off1, S.d_off1, y, nullptr, s);
 }
 
 void launch_k2_tc(const Plan& P, const float* slab, const float* p, float* z, float* part,
                   cudaStream_t s) {
   TcState& S = tc_state(P);
   const TcMaps* maps = tc_maps(P, 1, slab, p, s);
-  launch_sweep<true>(P, maps, S.k2, S.d_k2, z, part, s);
+  launch_sweep<true>(P, maps, S.k2, S.d_k2, S.off2, S.d_off2, z, part, s);
 }
 
 }  // namespace dlx
