@@ -47,8 +47,7 @@ static GramJob* make_job(const std::vector<DevMat>& mats) {
     J->nparts.push_back(cnt);
     J->total_parts += cnt;
     for (int64_t r0 = 0; r0 < m.n; r0 += 128)
-      for (int cb = 0; cb < m.r; cb += 32)
-        J->apply.push_back(make_int4(static_cast<int>(e), static_cast<int>(r0), cb / 32, 0));
+      J->apply.push_back(make_int4(static_cast<int>(e), static_cast<int>(r0), 0, 0));
   }
   auto up = [](auto& v) {
     using T = typename std::decay_t<decltype(v)>::value_type;
@@ -95,12 +94,14 @@ constexpr int kGramRows = 32;
 __global__ void __launch_bounds__(256) k_gram(const DevMat* __restrict__ mats,
                                               const int4* __restrict__ splits,
                                               const float* __restrict__ buf, int rr,
-                                              double* __restrict__ partial) {
+                                              double* __restrict__ partial,
+                                              const int* __restrict__ only) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int4 sp = splits[blockIdx.x];
+  if (only && !only[sp.x]) return;  // entry not selected for this pass
   const DevMat m = mats[sp.x];
   const int nb = (m.r + 3) / 4, nblk = nb * (nb + 1) / 2;
-  float* Ys = reinterpret_cast<float*>(smem_raw);  // [rpad][kGramRows]
+  float* Ys = reinterpret_cast<float*>(smem_raw);  // [rpad][kGramRows + 1] (padded: no bank conflicts)
   const int rpad = nb * 4;
   // thread -> (block, group); block index across grid.y passes when nblk > 256
   const int groups = nblk >= 256 ? 1 : 256 / nblk;
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(256) k_gram(const DevMat* __restrict__ mats,
     for (int e = threadIdx.x; e < rpad * kGramRows; e += 256) {
       const int c = e / kGramRows, rr0 = e % kGramRows;
       const int row = r0 + rr0;
-      Ys[e] = (c < m.r && row < sp.z) ? Y[(int64_t)c * m.ld + row] : 0.f;
+      Ys[c * (kGramRows + 1) + rr0] = (c < m.r && row < sp.z) ? Y[(int64_t)c * m.ld + row] : 0.f;
     }
     __syncthreads();
     if (active) {
@@ -137,8 +138,8 @@ __global__ void __launch_bounds__(256) k_gram(const DevMat* __restrict__ mats,
         double a[4], b[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          a[i] = (double)Ys[(jb * 4 + i) * kGramRows + rr0];
-          b[i] = (double)Ys[(kb * 4 + i) * kGramRows + rr0];
+          a[i] = (double)Ys[(jb * 4 + i) * (kGramRows + 1) + rr0];
+          b[i] = (double)Ys[(kb * 4 + i) * (kGramRows + 1) + rr0];
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -175,10 +176,11 @@ __global__ void __launch_bounds__(256) k_gram(const DevMat* __restrict__ mats,
 
 static size_t gram_smem(int rmax) {
   const int rpad = (rmax + 3) / 4 * 4;
-  return std::max<size_t>(sizeof(float) * rpad * kGramRows, sizeof(double) * 16 * 256);
+  return std::max<size_t>(sizeof(float) * rpad * (kGramRows + 1), sizeof(double) * 16 * 256);
 }
 
-static void launch_gram(const GramJob& J, const float* buf, double* partial, cudaStream_t s) {
+static void launch_gram(const GramJob& J, const float* buf, double* partial, cudaStream_t s,
+                        const int* only = nullptr) {
   const int nb = (J.rmax + 3) / 4, nblk = nb * (nb + 1) / 2;
   const int gy = nblk >= 256 ? (nblk + 255) / 256 : 1;
   const size_t sm = gram_smem(J.rmax);
@@ -187,27 +189,44 @@ static void launch_gram(const GramJob& J, const float* buf, double* partial, cud
     DLX_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr = true;
   }
-  k_gram<<<dim3(J.splits.size(), gy), 256, sm, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial);
+  k_gram<<<dim3(J.splits.size(), gy), 256, sm, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial,
+                                                     only);
   DLX_LAUNCHED();
 }
 
 // ------------------------------------------------------------------ Cholesky + R^-1
-// G = sum_p partial[p] (fixed order); upper Cholesky G = R^T R in place; flag the entry if
-// a pivot is within 10x of the reference dependence tolerance; Rinv = R^-1 (upper).
+// G = sum_p partial[p] (fixed order); upper Cholesky G = R^T R; Rinv = R^-1 (upper).
+// flags[e] = 1 if a pivot is within 10x of the reference dependence tolerance (exact MGS2
+// fallback). need2[e] = 1 if the factor is ill-conditioned enough that a second CholQR pass
+// is needed (cond_F(R) > 2e3): with an fp64 Gram of fp32 data, fp64 Cholesky and fp64 apply,
+// one pass is already orthonormal to fp32 precision below that. Matrices live in shared
+// memory for r <= 64, in the global work buffer otherwise.
 __global__ void __launch_bounds__(256) k_chol(const DevMat* __restrict__ mats,
                                               const int* __restrict__ part0,
                                               const int* __restrict__ nparts, int rr,
                                               const double* __restrict__ partial,
                                               double* __restrict__ work,
                                               double* __restrict__ rinv,
-                                              int* __restrict__ flags) {
+                                              int* __restrict__ flags,
+                                              int* __restrict__ need2,
+                                              const int* __restrict__ only) {
+  extern __shared__ __align__(16) unsigned char chol_smem[];
   __shared__ int s_flag;
-  __shared__ double s_thr;
+  __shared__ double s_thr, red[8];
   const int e = blockIdx.x;
+  if (only && !only[e]) {
+    if (threadIdx.x == 0) {
+      flags[e] = 0;
+      if (need2) need2[e] = 0;
+    }
+    return;
+  }
   const DevMat m = mats[e];
   const int r = m.r;
-  double* W = work + (int64_t)e * rr * rr;
-  double* X = rinv + (int64_t)e * rr * rr;
+  const bool in_smem = rr <= 64;  // launch-uniform: dynamic smem is sized for rr
+  const int ld = in_smem ? r : rr;
+  double* W = in_smem ? reinterpret_cast<double*>(chol_smem) : work + (int64_t)e * rr * rr;
+  double* X = in_smem ? W + r * r : rinv + (int64_t)e * rr * rr;
   const double* src = partial + (int64_t)part0[e] * rr * rr;
   const int np = nparts[e];
   for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
@@ -215,12 +234,12 @@ __global__ void __launch_bounds__(256) k_chol(const DevMat* __restrict__ mats,
     if (k < j) continue;
     double g = 0.0;
     for (int p = 0; p < np; ++p) g += src[(int64_t)p * rr * rr + j * rr + k];
-    W[j * rr + k] = g;
+    W[j * ld + k] = g;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     double mx = 0.0;
-    for (int j = 0; j < r; ++j) mx = fmax(mx, W[j * rr + j]);
+    for (int j = 0; j < r; ++j) mx = fmax(mx, W[j * ld + j]);
     const double big = sqrt(mx);
     const double tol = 1e-7 * fmax(1.0, big);
     s_thr = (10.0 * tol) * (10.0 * tol);
@@ -229,76 +248,121 @@ __global__ void __launch_bounds__(256) k_chol(const DevMat* __restrict__ mats,
   __syncthreads();
   for (int j = 0; j < r; ++j) {
     if (threadIdx.x == 0) {
-      const double d = W[j * rr + j];
+      const double d = W[j * ld + j];
       if (!(d > s_thr)) s_flag = 1;
     }
     __syncthreads();
     if (s_flag) break;
-    const double rjj = sqrt(W[j * rr + j]);
+    const double rjj = sqrt(W[j * ld + j]);
     const double inv = 1.0 / rjj;
     __syncthreads();
-    for (int k = j + 1 + threadIdx.x; k < r; k += blockDim.x) W[j * rr + k] *= inv;
-    if (threadIdx.x == 0) W[j * rr + j] = rjj;
+    for (int k = j + 1 + threadIdx.x; k < r; k += blockDim.x) W[j * ld + k] *= inv;
+    if (threadIdx.x == 0) W[j * ld + j] = rjj;
     __syncthreads();
     const int rem = r - j - 1;
     for (int idx = threadIdx.x; idx < rem * rem; idx += blockDim.x) {
       const int i = j + 1 + idx / rem, k = j + 1 + idx % rem;
       if (k < i) continue;
-      W[i * rr + k] -= W[j * rr + i] * W[j * rr + k];
+      W[i * ld + k] -= W[j * ld + i] * W[j * ld + k];
     }
     __syncthreads();
   }
   if (threadIdx.x == 0) flags[e] = s_flag;
-  if (s_flag) return;
+  if (s_flag) {
+    if (need2 && threadIdx.x == 0) need2[e] = 0;
+    return;
+  }
   // upper-triangular inverse, one column per thread (back substitution)
+  double xf = 0.0, rf = 0.0;
   for (int c = threadIdx.x; c < r; c += blockDim.x) {
-    X[c * rr + c] = 1.0 / W[c * rr + c];
+    X[c * ld + c] = 1.0 / W[c * ld + c];
     for (int i = c - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int k = i + 1; k <= c; ++k) s += W[i * rr + k] * X[k * rr + c];
-      X[i * rr + c] = -s / W[i * rr + i];
+      double sum = 0.0;
+      for (int k = i + 1; k <= c; ++k) sum += W[i * ld + k] * X[k * ld + c];
+      X[i * ld + c] = -sum / W[i * ld + i];
     }
-    for (int i = c + 1; i < r; ++i) X[i * rr + c] = 0.0;
+    for (int i = c + 1; i < r; ++i) X[i * ld + c] = 0.0;
+    for (int i = 0; i <= c; ++i) {
+      xf += X[i * ld + c] * X[i * ld + c];
+      rf += W[i * ld + c] * W[i * ld + c];
+    }
+  }
+  if (need2) {
+    double v[2] = {xf, rf};
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red[threadIdx.x / 32] = v[0];
+    }
+    __syncthreads();
+    double xs = 0.0;
+    for (int i = 0; i < 8; ++i) xs += red[i];
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = v[1];
+    __syncthreads();
+    double rs = 0.0;
+    for (int i = 0; i < 8; ++i) rs += red[i];
+    if (threadIdx.x == 0) need2[e] = (sqrt(xs) * sqrt(rs) > 2e3) ? 1 : 0;
+  }
+  if (in_smem) {
+    __syncthreads();
+    double* G = rinv + (int64_t)e * rr * rr;
+    for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) G[(idx / r) * rr + idx % r] = X[idx];
   }
 }
 
-// ------------------------------------------------------------------ apply: out = Y R^-1
+// ------------------------------------------------------------------ apply: Y <- Y R^-1
+// One CTA per 128-row tile of a factor, all columns: the tile is staged in shared memory
+// first, so the update is in place. fp64 accumulation, R^-1 upper triangular.
 __global__ void __launch_bounds__(128) k_apply(const DevMat* __restrict__ mats,
                                                const int4* __restrict__ jobs, int rr,
                                                const double* __restrict__ rinv,
-                                               const int* __restrict__ flags,
-                                               const float* __restrict__ in,
-                                               float* __restrict__ out) {
-  __shared__ double Rs[32][33];
+                                               const int* __restrict__ skip,
+                                               const int* __restrict__ only,
+                                               float* __restrict__ buf) {
+  extern __shared__ __align__(16) unsigned char ap_smem[];
   const int4 jb = jobs[blockIdx.x];
+  if (skip[jb.x] || (only && !only[jb.x])) return;
   const DevMat m = mats[jb.x];
-  if (flags[jb.x]) return;
-  const int cb = jb.z;
+  const int r = m.r;
+  double* Rs = reinterpret_cast<double*>(ap_smem);  // [32][33]
+  float* Ys = reinterpret_cast<float*>(Rs + 32 * 33);  // [r][129]
   const int64_t row = jb.y + threadIdx.x;
   const bool live = row < m.n;
+  float* Y = buf + m.off;
   const double* X = rinv + (int64_t)jb.x * rr * rr;
-  const float* Y = in + m.off;
-  double acc[32];
+  for (int idx = threadIdx.x; idx < r * 128; idx += 128) {
+    const int c = idx / 128, i = idx % 128;
+    Ys[c * 129 + i] = (jb.y + i < m.n) ? Y[(int64_t)c * m.ld + jb.y + i] : 0.f;
+  }
+  __syncthreads();
+  for (int cb = 0; cb * 32 < r; ++cb) {
+    double acc[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
-  for (int kb = 0; kb <= cb; ++kb) {
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < 32 * 32; idx += 128) {
-      const int k = kb * 32 + idx / 32, j = cb * 32 + idx % 32;
-      Rs[idx / 32][idx % 32] = (k < m.r && j < m.r) ? X[k * rr + j] : 0.0;
+    for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+    for (int kb = 0; kb <= cb; ++kb) {
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < 32 * 32; idx += 128) {
+        const int k = kb * 32 + idx / 32, j = cb * 32 + idx % 32;
+        Rs[(idx / 32) * 33 + idx % 32] = (k < r && j < r) ? X[k * rr + j] : 0.0;
+      }
+      __syncthreads();
+      const int kmax = min(32, r - kb * 32);
+      for (int k = 0; k < kmax; ++k) {
+        const double y = (double)Ys[(kb * 32 + k) * 129 + threadIdx.x];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = fma(y, Rs[k * 33 + j], acc[j]);
+      }
     }
-    __syncthreads();
-    const int kmax = min(32, m.r - kb * 32);
-    for (int k = 0; k < kmax; ++k) {
-      const double y = live ? (double)Y[(int64_t)(kb * 32 + k) * m.ld + row] : 0.0;
+    if (live) {
+      const int jmax = min(32, r - cb * 32);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = fma(y, Rs[k][j], acc[j]);
+      for (int j = 0; j < 32; ++j)
+        if (j < jmax) Y[(int64_t)(cb * 32 + j) * m.ld + row] = (float)acc[j];
     }
   }
-  if (!live) return;
-  float* O = out + m.off;
-  const int jmax = min(32, m.r - cb * 32);
-  for (int j = 0; j < jmax; ++j) O[(int64_t)(cb * 32 + j) * m.ld + row] = (float)acc[j];
 }
 
 // ------------------------------------------------------------------ exact MGS2 fallback
@@ -358,7 +422,9 @@ __global__ void __launch_bounds__(1024) k_mgs_fallback(const DevMat* __restrict_
 }
 
 // ------------------------------------------------------------------ driver
-static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* tmp, const std::string& tag,
+static size_t apply_smem(int rmax) { return 32 * 33 * sizeof(double) + sizeof(float) * rmax * 129; }
+
+static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* /*tmp*/, const std::string& tag,
                     int64_t buf_elems, cudaStream_t s) {
   const int rr = J.rmax;
   const size_t ne = J.mats.size();
@@ -366,18 +432,29 @@ static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* tmp, const std:
   auto* work = static_cast<double*>(ctx->scratch("chol_work", sizeof(double) * ne * rr * rr));
   auto* rinv = static_cast<double*>(ctx->scratch("chol_rinv", sizeof(double) * ne * rr * rr));
   auto* flags1 = static_cast<int*>(ctx->scratch("ortho_flags1" + tag, sizeof(int) * ne));
+  auto* need2 = static_cast<int*>(ctx->scratch("ortho_need2" + tag, sizeof(int) * ne));
   auto* flags2 = static_cast<int*>(ctx->scratch("ortho_flags2" + tag, sizeof(int) * ne));
-  // pass 1: buf -> tmp
+  static bool attr = false;
+  if (!attr) {
+    DLX_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    DLX_CUDA(cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+    attr = true;
+  }
+  const size_t csm = rr <= 64 ? 2 * sizeof(double) * rr * rr : 0;
+  const size_t asm_ = apply_smem(rr);
+  // pass 1 (every factor), in place
   launch_gram(J, buf, partial, s);
-  k_chol<<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags1);
+  k_chol<<<ne, 256, csm, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags1,
+                              need2, nullptr);
   DLX_LAUNCHED();
-  k_apply<<<J.apply.size(), 128, 0, s>>>(J.d_mats, J.d_apply, rr, rinv, flags1, buf, tmp);
+  k_apply<<<J.apply.size(), 128, asm_, s>>>(J.d_mats, J.d_apply, rr, rinv, flags1, nullptr, buf);
   DLX_LAUNCHED();
-  // pass 2: tmp -> buf (entries flagged in pass 1 are skipped by both applies)
-  launch_gram(J, tmp, partial, s);
-  k_chol<<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags2);
+  // pass 2 only for factors whose conditioning needs it (need2), in place
+  launch_gram(J, buf, partial, s, need2);
+  k_chol<<<ne, 256, csm, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags2,
+                              nullptr, need2);
   DLX_LAUNCHED();
-  k_apply<<<J.apply.size(), 128, 0, s>>>(J.d_mats, J.d_apply, rr, rinv, flags1, tmp, buf);
+  k_apply<<<J.apply.size(), 128, asm_, s>>>(J.d_mats, J.d_apply, rr, rinv, flags2, need2, buf);
   DLX_LAUNCHED();
   // exact MGS2 for flagged entries (pass-1 flags: buf still holds their input)
   auto* dscr = static_cast<double*>(ctx->scratch("mgs_scratch", sizeof(double) * buf_elems));
