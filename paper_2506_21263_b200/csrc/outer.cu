@@ -167,17 +167,25 @@ __global__ void __launch_bounds__(256, 3) k5_outer(const DevT2* __restrict__ T,
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-      if (SELF) {
-        const int k = k0 + kk;
-        if (k >= s_lo && k < s_hi) {
+      // own-payload terms (measure_error), accumulated separately so Delta's summation order
+      // never depends on self_index (bitwise-identical Delta on every rank); at D = 1 the
+      // own payload is the whole sum and sacc is taken from acc after the loop
+      const int k = k0 + kk;
+      if (SELF && D > 1 && k >= s_lo && k < s_hi) {  // CTA-uniform branch
 #pragma unroll
-          for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) sacc[i][j] = fmaf(av[i], bv[j], sacc[i][j]);
-        }
+          for (int j = 0; j < 4; ++j) sacc[i][j] = fmaf(av[i], bv[j], sacc[i][j]);
       }
     }
     __syncthreads();
+  }
+
+  if (SELF && D == 1) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sacc[i][j] = acc[i][j];
   }
 
   // 3. fused epilogue
@@ -359,19 +367,26 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
         for (int i = 0; i < 2; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-        if (SELF) {
-          const int k = k0 + kk;
-          if (k >= s_lo && k < s_hi) {
+        // own-payload terms (measure_error), accumulated separately so Delta's summation order
+        // never depends on self_index (bitwise-identical Delta on every rank); at D = 1 the
+        // own payload is the whole sum and sacc is taken from acc after the loop
+        const int k = k0 + kk;
+        if (SELF && D > 1 && k >= s_lo && k < s_hi) {  // CTA-uniform branch
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+          for (int i = 0; i < 2; ++i)
 #pragma unroll
-              for (int j = 0; j < 4; ++j) sacc[i][j] = fmaf(av[i], bv[j], sacc[i][j]);
-          }
+            for (int j = 0; j < 4; ++j) sacc[i][j] = fmaf(av[i], bv[j], sacc[i][j]);
         }
       }
     }
     cached_slot = tl.x;
     cached_n0 = static_cast<int>(n0);
+    if (SELF && D == 1) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sacc[i][j] = acc[i][j];
+    }
 
     // epilogue from the landed stage
     if (!ps_tma) mbar_wait(&full[s], (it / kK5Stages) & 1);
@@ -397,6 +412,8 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
         }
       }
       float op[4], oa[4], ov[4];
+      float fnum = 0.f, fden = 0.f, fen = 0.f, fdn = 0.f;  // per-row partials (fp32), folded
+      int bad = 0;                                         // into fp64 once per row
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float delta = __fmul_rn(acc[i][j], invD);
@@ -406,15 +423,20 @@ __global__ void __launch_bounds__(288, 1) k5s_outer(const DevT2* __restrict__ T,
         ov[j] = o.v;
         if (live && j < nv) {
           if (SELF) {
-            const double df = (double)sacc[i][j] - (double)pd[j];
-            num += df * df;
-            den += (double)pd[j] * (double)pd[j];
+            const float df = sacc[i][j] - pd[j];
+            fnum = fmaf(df, df, fnum);
+            fden = fmaf(pd[j], pd[j], fden);
           }
-          en += (double)o.e * (double)o.e;
-          if (ovl) dn += (double)o.pend * (double)o.pend;
-          if (!isfinite(o.anchor)) nf += 1.0;
+          fen = fmaf(o.e, o.e, fen);
+          if (ovl) fdn = fmaf(o.pend, o.pend, fdn);
+          bad |= !isfinite(o.anchor);
         }
       }
+      num += fnum;
+      den += fden;
+      en += fen;
+      dn += fdn;
+      nf += bad;
       if (live) {
         const int64_t base = t.off + row * t.b + col;
         const bool full4 = nv == 4;

@@ -343,3 +343,31 @@ def test_tensor_core_sweeps_match_simt(ctx, oracle, rank):
     cb, _ = decode_payload(L, outs[0].payload, rank, 8)
     assert (ca == ref["codes"]).mean() >= 0.95
     assert (cb == ref["codes"]).mean() >= 0.95
+
+
+def test_outer_update_identical_on_every_rank(ctx, oracle):
+    """Every rank reconstructs the same Delta and anchor bit for bit (SPEC anchor
+    consistency): the fused update must not depend on which worker's measure_error it
+    also accumulates (self_index) — the distributed race/divergence detector."""
+    from paper_2506_21263_b200 import api
+    import torch
+    shapes = [(64, 256), (256,), (300, 128)]
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    rank, q, D = 8, 4, 3
+    ranks = t.ranks(rank)
+    pays = []
+    for w in range(D):
+        d = oracle.gaussian(oracle.stream(w, 6), t.numel())[0]
+        c = oracle.compress(t, d, rank, q, 0, 2, oracle.stream(7, 7))
+        pays.append(_payload_from_oracle(L, oracle, t, ranks, rank, q, c["codes"], c["scales"]))
+    gathered = torch.cat(pays)
+    anchor, local, vel, pend = _rand_state(oracle, L, 5)
+    outs = []
+    for self_index in (-1, 0, 1, 2):
+        dA, dL, dV, dP = L.pack(anchor), L.pack(local), L.pack(vel), L.pack(pend)
+        api.outer_update(L, gathered, D, rank, q, dP, dA, dL, dV, 0.7, 0.9, False,
+                         mode=api.OVERLAPPED, self_index=self_index)
+        outs.append(torch.cat([dA, dV]).cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
