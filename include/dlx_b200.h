@@ -175,8 +175,10 @@ int64_t dlx_serialize(const dlx_layout* layout, int rank, int qbits, const char*
 dlx_status dlx_parse(const dlx_layout* layout, int rank, int qbits, const uint8_t* bytes,
                      int64_t size, uint8_t* h_payload);
 
-/* Runtime options. "tensor_cores" (default 1): 0 routes the power-iteration sweeps through
- * the SIMT kernels instead of the tcgen05 ones (A/B testing; also env DLX_TENSOR_CORES=0). */
+/* Runtime options (A/B testing). "tensor_cores" (default 1): 0 routes the power-iteration
+ * sweeps through the SIMT kernels instead of the tcgen05 ones (env DLX_TENSOR_CORES=0).
+ * "outer_tensor_cores" (default 1): 0 runs the fused outer update with the SIMT factor GEMM
+ * instead of the tcgen05/TMA kernel (env DLX_OUTER_TC=0). */
 dlx_status dlx_set_option(const char* key, int value);
 
 /* Test hook: one power-iteration sweep — which = 0: out = delta * in (K1, in = Q factors),

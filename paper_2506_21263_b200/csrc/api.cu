@@ -295,6 +295,8 @@ dlx_status dlx_set_option(const char* key, int value) {
     const std::string k = key ? key : "";
     if (k == "tensor_cores") {
       option_tensor_cores() = value != 0;
+    } else if (k == "outer_tensor_cores") {
+      option_outer_tc() = value != 0;
     } else {
       raise(DLX_ERR_VALIDATION, "unknown option: " + k);
     }

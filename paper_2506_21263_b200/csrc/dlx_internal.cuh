@@ -190,6 +190,7 @@ void launch_k1_tc(const Plan& P, const float* slab, const float* q, float* y, cu
 void launch_k2_tc(const Plan& P, const float* slab, const float* p, float* z, float* part,
                   cudaStream_t s);
 bool& option_tensor_cores();
+bool& option_outer_tc();
 void launch_k2(const Plan& P, const float* slab, const float* p, float* z, float* part,
                cudaStream_t s);
 void orthonormalize_batched(dlx_ctx* ctx, const Plan& P, int side, float* buf, float* tmp,

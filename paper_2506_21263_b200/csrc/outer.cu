@@ -13,36 +13,13 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "dlx_internal.cuh"
 #include "ptx.cuh"
+#include "epilogue.cuh"
 
 namespace dlx {
-
-struct EpiOut {
-  float pend, anchor, v, e;
-};
-
-// One element of the fused epilogue given Delta (all roundings explicit).
-__device__ __forceinline__ EpiOut epilogue(float delta, float pend, float anchor, float local,
-                                           float v, int mode, float gamma, float beta,
-                                           int classical) {
-  EpiOut o;
-  if (mode == DLX_MODE_OVERLAPPED) {
-    o.e = __fsub_rn(pend, delta);
-    o.pend = __fadd_rn(__fsub_rn(anchor, local), o.e);
-  } else {
-    o.e = __fsub_rn(pend, delta);
-    o.pend = o.e;
-  }
-  o.v = __fadd_rn(__fmul_rn(beta, v), delta);
-  if (classical) {
-    o.anchor = __fsub_rn(anchor, __fmul_rn(gamma, o.v));
-  } else {
-    o.anchor = __fsub_rn(anchor, __fmul_rn(gamma, __fadd_rn(delta, __fmul_rn(beta, o.v))));
-  }
-  return o;
-}
 
 __device__ __forceinline__ void stats_add(dlx_round_stats* st, double num, double den,
                                           double dn, double en, double nf, double* red) {
@@ -517,11 +494,30 @@ static size_t k5s_smem() {
   return kK5Stages * kK5StageBytes + (32 * 132 + 32 * 20) * 4 + 2 * kK5Stages * 8 + 64;
 }
 
+bool o5_eligible(const Plan& P, int D, int self_index);
+void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
+                        int self_index, int mode, float* pending, float* anchor,
+                        const float* local, float* velocity, float gamma, float beta,
+                        int classical, dlx_round_stats* stats, cudaStream_t s);
+
+bool& option_outer_tc() {
+  static bool on = [] {
+    const char* e = getenv("DLX_OUTER_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                      int self_index, int mode, float* pending, float* anchor,
                      const float* local, float* velocity, float gamma, float beta,
                      int classical, dlx_round_stats* stats, cudaStream_t s) {
   if (P.t2.empty()) return;
+  if (option_outer_tc() && o5_eligible(P, D, self_index)) {
+    launch_outer_2d_tc(ctx, P, D, gathered, self_index, mode, pending, anchor, local, velocity,
+                       gamma, beta, classical, stats, s);
+    return;
+  }
   float* phat = static_cast<float*>(ctx->scratch("phat", sizeof(float) * P.pelems * D));
   float* qhat = static_cast<float*>(ctx->scratch("qhat", sizeof(float) * P.qelems * D));
   dequant_factors(P, D, gathered, P.payload_bytes, phat, qhat, 0, s);

@@ -371,3 +371,59 @@ def test_outer_update_identical_on_every_rank(ctx, oracle):
         outs.append(torch.cat([dA, dV]).cpu().numpy())
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("D,rank", [(1, 8), (1, 32), (2, 16), (2, 32)])
+def test_outer_update_tensor_core_path(ctx, oracle, D, rank):
+    """tcgen05/TMA fused outer update (eligible layouts: b % 4 == 0, D*r <= 64) against the
+    oracle's allreduce_avg and the reference epilogue, with the SIMT path run side by side."""
+    from paper_2506_21263_b200 import api
+    import torch
+    shapes = [(40, 36), (36,), (200, 64), (64,), (300, 96), (129, 160)]
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    q = 4
+    ranks = t.ranks(rank)
+    codes, scales, pays = [], [], []
+    for w in range(D):
+        d = oracle.gaussian(oracle.stream(w, 16), t.numel())[0]
+        c = oracle.compress(t, d, rank, q, 0, 2, oracle.stream(7, 8))
+        codes.append(c["codes"]); scales.append(c["scales"])
+        pays.append(_payload_from_oracle(L, oracle, t, ranks, rank, q, c["codes"], c["scales"]))
+    gathered = torch.cat(pays)
+    ref = oracle.allreduce_avg(t, ranks, codes, scales)
+    anchor, local, vel, pend = _rand_state(oracle, L, 9)
+    res = {}
+    for tc in (1, 0):
+        api.set_option("outer_tensor_cores", tc)
+        try:
+            z = L.empty(); a0 = L.empty(); v0 = L.empty()
+            api.outer_update(L, gathered, D, rank, q, z, a0, None, v0, 0.7, 0.9, False, mode=api.SYNC)
+            dg = -L.unpack(z)
+            dA, dL, dV, dP = L.pack(anchor), L.pack(local), L.pack(vel), L.pack(pend)
+            stats = torch.zeros(8, dtype=torch.float64, device="cuda")
+            api.outer_update(L, gathered, D, rank, q, dP, dA, dL, dV, 0.7, 0.9, False,
+                             mode=api.OVERLAPPED, self_index=0, stats=stats)
+            res[tc] = (dg, L.unpack(dP), L.unpack(dA), L.unpack(dV), stats.cpu().numpy())
+        finally:
+            api.set_option("outer_tensor_cores", 1)
+    f = np.float32
+    for tc in (1, 0):
+        dg = res[tc][0]
+        for i, (x, y) in enumerate(zip(split_dense(shapes, dg), split_dense(shapes, ref))):
+            if len(shapes[i]) == 1:
+                assert np.array_equal(x, y), (tc, i)
+            else:
+                assert rel_fro(x, y) <= TOL_RECON, (tc, i, rel_fro(x, y))
+                assert np.abs(x - y).max() <= TOL_RECON * np.abs(y).max(), (tc, i)
+        dgf = dg.astype(np.float32)
+        e = (pend - dgf).astype(f)
+        want_p = ((anchor - local).astype(f) + e).astype(f)
+        want_v = ((f(0.9) * vel).astype(f) + dgf).astype(f)
+        want_a = (anchor - (f(0.7) * (dgf + (f(0.9) * want_v).astype(f)).astype(f)).astype(f)).astype(f)
+        assert np.array_equal(res[tc][1], want_p), tc
+        assert np.array_equal(res[tc][3], want_v), tc
+        assert np.array_equal(res[tc][2], want_a), tc
+        st = res[tc][4]
+        ce = oracle.measure_error(t, pend, ranks, codes[0], scales[0])
+        assert abs(st[0] / st[1] - ce) <= 1e-4 * max(ce, 1e-12), tc
