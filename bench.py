@@ -32,12 +32,14 @@ METRIC = "outer-sync ms/round & params/s (compress→allreduce→Nesterov), 1/2/
 # bounded CPU sample: a 512-row slab of an OPT-1.3B 2048x2048 attention-projection delta
 # plus its 2048 bias (1 050 624 params), full reference round with the adaptive SVD
 CPU_SAMPLE = [(512, 2048), (2048,)]
+# dominant kernels timed with per-launch CUDA events (dlx_kernel_time)
+KERNELS = ("k_o5", "k_tc_sweep_k1", "k_tc_sweep_k2")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="opt-1.3b")
@@ -47,7 +49,7 @@ def parse():
     ap.add_argument("--follow-controller", action="store_true",
                     help="apply the adaptive controller's rank (default: measure r' and run the "
                          "controller every round but time at rank1 = 32, the configured rank)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -63,13 +65,14 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
-        self.lines = []
+        self.lines = []  # (monotonic time, csv line)
+        self.window = (0.0, float("inf"))
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -79,7 +82,18 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def wait_first(self, timeout=5.0):
+        t = time.monotonic() + timeout
+        while self.proc and not self.lines and time.monotonic() < t:
+            time.sleep(0.02)
+
+    def start(self):
+        self.window = (time.monotonic(), float("inf"))
+
+    def stop(self):
+        self.window = (self.window[0], time.monotonic())
 
     def __exit__(self, *a):
         if self.proc:
@@ -92,7 +106,8 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inside = [ln for t, ln in self.lines if self.window[0] <= t <= self.window[1]]
+        for ln in inside:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 6:
                 continue
@@ -215,8 +230,13 @@ def main():
     eng.side_events = []
     recs = []
     api.take_launch_count()
+    api.set_option("kernel_events", 1)  # per-launch CUDA events on the launching stream
+    for k in KERNELS:
+        api.kernel_time(k)
     barrier()
     with ClockSampler(local_rank) as clocks:
+        clocks.wait_first()
+        clocks.start()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
@@ -224,7 +244,10 @@ def main():
             recs.append(eng.step(local))
         t1.record(stream)
         barrier()
+        clocks.stop()
     launches = api.take_launch_count()
+    ktimes = {k: api.kernel_time(k) for k in KERNELS}
+    api.set_option("kernel_events", 0)
     ms = t0.elapsed_time(t1)
     if world > 1:
         m = torch.tensor([ms], device=dev)
@@ -245,42 +268,59 @@ def main():
         phases["effective_rank(side)"] = sum(a.elapsed_time(b) for a, b in eng.side_events) / args.steps
     eng.phase_events = None
 
-    # ---------------- roofline of the dominant kernel group
+    # ---------------- roofline of the dominant kernel (CUDA events around each launch)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else \
+        "fallback (B200_PROFILING.md)"
     iters = cfg.power_iters
-    bytes_per_param = {"compress": 4.0 * (2 * iters + 1), "outer_update": 28.0}
-    phase_bw = {k: (bytes_per_param[k] * P / (phases[k] / 1e3) / 1e9) for k in bytes_per_param
-                if phases.get(k)}
-    dom = max(bytes_per_param, key=lambda k: phases.get(k, 0.0))
-    achieved = phase_bw.get(dom, 0.0)
-    roofline = {"bound": "hbm", "kernel": "fused outer update (dequant + K5 + 1-D)" if dom ==
-                "outer_update" else "compress (5 delta sweeps + CholQR2 + quantise)",
-                "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "peak_source": peak_src, "traffic": None,
-                "algorithmic_bytes_per_param": bytes_per_param[dom],
-                "per_phase_GBps": phase_bw}
+    per_kernel = {}
+    for k, (kms, kbytes, kn) in ktimes.items():
+        if kn:
+            per_kernel[k] = {"launches": kn, "ms_per_launch": kms / kn,
+                             "bytes_per_launch": kbytes / kn,
+                             "GBps": kbytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0,
+                             "share_of_step": kms / ms}
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["share_of_step"]) if per_kernel else None
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        t = prof.get("kernels", {}).get(dom)
+        if t and prof.get("workload") == f"{args.config} r={args.rank} q={args.qbits} D={world}":
+            traffic = t["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    achieved = per_kernel[dom]["GBps"] if dom else 0.0
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
+                "unit": "GB/s", "frac": achieved / hbm_peak, "peak_source": peak_src,
+                "traffic": traffic,
+                "algorithmic_bytes_per_launch": per_kernel[dom]["bytes_per_launch"] if dom else None,
+                "kernels": per_kernel,
+                "phase_GBps": {k: (b * P / (phases[k] / 1e3) / 1e9) for k, b in
+                               (("compress", 4.0 * (2 * iters + 1)), ("outer_update", 28.0))
+                               if phases.get(k)}}
 
     # ---------------- end-to-end through the public API with host buffers
-    # each step: H2D of the round's local parameters (pinned) -> round -> D2H of the new
-    # anchor (theta_global); optimiser state stays device-resident in the engine.
+    # each step: H2D of the round's local parameters from pinned host memory -> round ->
+    # D2H of the new anchor (theta_global) into pinned host memory (OuterSync.step_host:
+    # the copies run on copy streams overlapping compress); optimiser state stays resident.
     h_local = torch.empty(L.slab_elems, dtype=torch.float32, pin_memory=True)
     h_local.copy_(local)
-    h_anchor = torch.empty_like(h_local)
+    h_anchor = torch.empty(L.slab_elems, dtype=torch.float32, pin_memory=True)
     ke = max(1, args.e2e_steps)
+    eng.step_host(h_local, h_anchor)  # warm the copy streams / staging buffer
+    eng.host_wait()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(ke):
-        local.copy_(h_local, non_blocking=True)
-        eng.step(local)
-        h_anchor.copy_(eng.anchor, non_blocking=True)
+        eng.step_host(h_local, h_anchor)
+    eng.host_wait(stream)
     e1.record(stream)
     barrier()
     ms_e2e = e0.elapsed_time(e1)

@@ -178,8 +178,16 @@ dlx_status dlx_parse(const dlx_layout* layout, int rank, int qbits, const uint8_
 /* Runtime options (A/B testing). "tensor_cores" (default 1): 0 routes the power-iteration
  * sweeps through the SIMT kernels instead of the tcgen05 ones (env DLX_TENSOR_CORES=0).
  * "outer_tensor_cores" (default 1): 0 runs the fused outer update with the SIMT factor GEMM
- * instead of the tcgen05/TMA kernel (env DLX_OUTER_TC=0). */
+ * instead of the tcgen05/TMA kernel (env DLX_OUTER_TC=0). "kernel_events" (default 0): 1
+ * brackets each launch of the dominant kernels (k_o5, k_tc_sweep K1/K2) with CUDA events on
+ * the launching stream, for dlx_kernel_time. */
 dlx_status dlx_set_option(const char* key, int value);
+
+/* Device time (ms, from the CUDA events), algorithmic HBM bytes and launch count of every
+ * recorded launch of kernel `name` ("k_o5", "k_tc_sweep_k1", "k_tc_sweep_k2") since the last
+ * call; synchronises on those events and clears them. Needs "kernel_events" = 1. */
+dlx_status dlx_kernel_time(const char* name, double* ms_total, double* bytes_total,
+                           int64_t* launches);
 
 /* Test hook: one power-iteration sweep — which = 0: out = delta * in (K1, in = Q factors),
  * which = 1: out = delta^T * in (K2, in = P factors) — on the tcgen05 (use_tc = 1) or SIMT

@@ -84,6 +84,7 @@ PROTOS = {
     "dlx_parse": (_i32, [_vp, _i32, _i32, _vp, _i64, _vp]),
     "dlx_take_launch_count": (_u64, []),
     "dlx_set_option": (_i32, [C.c_char_p, _i32]),
+    "dlx_kernel_time": (_i32, [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dlx_debug_sweep": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
 }
 

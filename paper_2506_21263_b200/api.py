@@ -382,6 +382,14 @@ def set_option(key: str, value: int) -> None:
     check(lib().dlx_set_option(key.encode(), int(value)))
 
 
+def kernel_time(name: str):
+    """dlx_kernel_time: (device ms, algorithmic bytes, launches) of the recorded launches of
+    kernel `name` since the last call (needs set_option("kernel_events", 1))."""
+    ms, by, n = C.c_double(0.0), C.c_double(0.0), C.c_int64(0)
+    check(lib().dlx_kernel_time(name.encode(), C.byref(ms), C.byref(by), C.byref(n)))
+    return ms.value, by.value, n.value
+
+
 def debug_sweep(layout: Layout, rank: int, which: int, slab: torch.Tensor, fac_in: torch.Tensor,
                 use_tc: bool, stream=None) -> torch.Tensor:
     """Test hook: one K1 (which=0, out = delta Q) or K2 (which=1, out = delta^T P) sweep."""

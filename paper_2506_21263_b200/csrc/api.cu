@@ -19,6 +19,30 @@ void check_cuda(cudaError_t e, const char* what) {
 
 void count_launch(int n) { g_launches += static_cast<uint64_t>(n); }
 
+namespace {
+struct TimedLaunch {
+  std::string name;
+  double bytes;
+  cudaEvent_t a, b;
+};
+bool g_kernel_events = false;
+std::vector<TimedLaunch> g_timed;  // recorded launches (events owned, destroyed on read)
+}  // namespace
+
+KernelTimer::KernelTimer(const char* name, double bytes, cudaStream_t s) : stream(s) {
+  if (!g_kernel_events) return;
+  TimedLaunch t{name, bytes, nullptr, nullptr};
+  DLX_CUDA(cudaEventCreate(&t.a));
+  DLX_CUDA(cudaEventCreate(&t.b));
+  DLX_CUDA(cudaEventRecord(t.a, s));
+  slot = static_cast<int>(g_timed.size());
+  g_timed.push_back(t);
+}
+
+KernelTimer::~KernelTimer() {
+  if (slot >= 0) cudaEventRecord(g_timed[slot].b, stream);
+}
+
 template <class F>
 static dlx_status guard(F&& f) {
   try {
@@ -297,6 +321,8 @@ dlx_status dlx_set_option(const char* key, int value) {
       option_tensor_cores() = value != 0;
     } else if (k == "outer_tensor_cores") {
       option_outer_tc() = value != 0;
+    } else if (k == "kernel_events") {
+      g_kernel_events = value != 0;
     } else {
       raise(DLX_ERR_VALIDATION, "unknown option: " + k);
     }
@@ -319,6 +345,34 @@ dlx_status dlx_debug_sweep(dlx_ctx* ctx, const dlx_layout* layout, int rank, int
       launch_k2(P, d_slab, d_in, d_out, part, s);
     }
     option_tensor_cores() = saved;
+  });
+}
+
+dlx_status dlx_kernel_time(const char* name, double* ms_total, double* bytes_total,
+                           int64_t* launches) {
+  return guard([&] {
+    const std::string n = name ? name : "";
+    double ms = 0.0, bytes = 0.0;
+    int64_t cnt = 0;
+    std::vector<TimedLaunch> keep;
+    for (TimedLaunch& t : g_timed) {
+      if (t.name != n) {
+        keep.push_back(t);
+        continue;
+      }
+      DLX_CUDA(cudaEventSynchronize(t.b));
+      float x = 0.f;
+      DLX_CUDA(cudaEventElapsedTime(&x, t.a, t.b));
+      ms += x;
+      bytes += t.bytes;
+      ++cnt;
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    g_timed.swap(keep);
+    if (ms_total) *ms_total = ms;
+    if (bytes_total) *bytes_total = bytes;
+    if (launches) *launches = cnt;
   });
 }
 

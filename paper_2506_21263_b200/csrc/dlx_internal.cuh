@@ -191,6 +191,16 @@ void launch_k2_tc(const Plan& P, const float* slab, const float* p, float* z, fl
                   cudaStream_t s);
 bool& option_tensor_cores();
 bool& option_outer_tc();
+
+// Optional CUDA-event timing of the dominant kernels (dlx_set_option("kernel_events", 1)):
+// events recorded on the launching stream around one launch, with the launch's algorithmic
+// HBM bytes; read back (and cleared) by dlx_kernel_time. Off by default (no events).
+struct KernelTimer {
+  KernelTimer(const char* name, double bytes, cudaStream_t s);
+  ~KernelTimer();
+  int slot = -1;
+  cudaStream_t stream = nullptr;
+};
 void launch_k2(const Plan& P, const float* slab, const float* p, float* z, float* part,
                cudaStream_t s);
 void orthonormalize_batched(dlx_ctx* ctx, const Plan& P, int side, float* buf, float* tmp,

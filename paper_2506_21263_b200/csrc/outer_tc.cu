@@ -375,6 +375,7 @@ struct O5State {
   int4* d_rows = nullptr;
   std::vector<int64_t> aoff, boff;  // per slot: element offsets of A [lda][KA], B [ldb][KA]
   int64_t a_elems = 0, b_elems = 0;
+  int64_t params = 0;  // 2-D parameters covered
   int64_t* d_aoff = nullptr;
   int64_t* d_boff = nullptr;
   O5Maps* d_maps = nullptr;
@@ -412,6 +413,7 @@ static O5State& o5_state(const Plan& P, int D) {
       const int64_t ld = side == 0 ? t.lda : t.ldb;
       for (int64_t r = 0; r < ld; ++r) S.rows.push_back(make_int4(static_cast<int>(k), side, static_cast<int>(r), 0));
     }
+    S.params += t.a * t.b;
     S.aoff.push_back(S.a_elems);
     S.boff.push_back(S.b_elems);
     S.a_elems += t.lda * S.KA;
@@ -482,6 +484,9 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
     DLX_CUDA(cudaFuncSetAttribute(k_o5<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
+  // algorithmic bytes: read pending, anchor, velocity (+ local in overlapped mode), write
+  // pending, anchor, velocity — 28 B/param overlapped, 24 B/param sync
+  KernelTimer timer("k_o5", (mode == DLX_MODE_OVERLAPPED ? 28.0 : 24.0) * S.params, s);
   if (self_index >= 0)
     k_o5<true><<<grid, kO5Threads, smem, s>>>(P.d_t2, S.d_maps, S.d_tiles, S.d_off, D, KA,
                                              self_index, mode, gamma, beta, classical, stats);

@@ -400,6 +400,7 @@ static int num_sms() {
 }
 
 struct TcState {
+  int64_t swept_params = 0;  // delta elements one sweep reads on the tensor-core path
   std::vector<int4> k1, k2;  // tiles grouped per CTA (balanced, see balance())
   std::vector<int> off1, off2;
   int4* d_k1 = nullptr;
@@ -420,6 +421,7 @@ static TcState& tc_state(const Plan& P) {
     for (size_t k = 0; k < P.t2.size(); ++k) {
       const DevT2& t = P.t2[k];
       if (!tc_eligible(t)) continue;
+      s->swept_params += t.a * t.b;
       for (int64_t m0 = 0; m0 < t.a; m0 += 128) s->k1.push_back(make_int4((int)k, (int)m0, 0, 0));
       const int sp = static_cast<int>(ceil_div(t.a, KC));
       for (int q = 0; q < sp; ++q)
@@ -545,6 +547,8 @@ static void launch_sweep(const Plan& P, const TcMaps* maps, const std::vector<in
     DLX_CUDA(cudaMalloc(&prof, 8 * 8 * 1024));
   }
   if (prof) DLX_CUDA(cudaMemsetAsync(prof, 0, 8 * 8 * 1024, s));
+  // algorithmic bytes: one fp32 read of every swept delta element (factors are L2-resident)
+  KernelTimer timer(A_MN ? "k_tc_sweep_k2" : "k_tc_sweep_k1", 4.0 * tc_state(P).swept_params, s);
   k_tc_sweep<A_MN><<<grid, kTcThreads, sm, s>>>(P.d_t2, maps, d_tiles, d_off, N,
                                                 lr, cr, P.d_k2_splits, P.d_k2_part_off, out, part,
                                                 variant, (variant & 16) ? prof : nullptr);

@@ -101,6 +101,17 @@ class OuterSync:
         self.last = RoundRecord()
         self.phase_events = None  # optional: list collecting (name, event) on the main stream
         self.side_events: list = []  # (start, end) of the effective rank on the side stream
+        # host-resident parameter pipeline (step_host): copy streams + staging buffer
+        self._h2d = self._d2h = None
+        self._dev_local = None
+        self._d2h_ev = None
+        self._pre_update: list = []  # events the next read of local / write of anchor waits on
+
+    def _wait_pre_update(self):
+        cur = torch.cuda.current_stream()
+        for e in self._pre_update:
+            cur.wait_event(e)
+        self._pre_update = []
 
     def _ev(self, name: str):
         if self.phase_events is None:
@@ -170,6 +181,7 @@ class OuterSync:
                 self.energy_host.copy_(energy, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(side)
+        self._wait_pre_update()
         api.outer_update(L, gathered, self.world, r, q, self.pending, self.anchor, local,
                          self.velocity, cfg.outer_lr, cfg.outer_momentum, cfg.outer_classical,
                          mode=mode, self_index=self.rank if cfg.measure_error else -1,
@@ -232,6 +244,7 @@ class OuterSync:
                 self._push_window(rec.r_prime)
         else:
             rec = RoundRecord(round=self.round, r_t=self.r_t, H_t=self.H_t)
+            self._wait_pre_update()
             api.stage_deltas(self.L, self.anchor, local, None, self.pending, None)
         r_next, h_next = self._adapt()
         self.has_pending = True
@@ -243,6 +256,7 @@ class OuterSync:
         """run_round_sync (engine.cpp:423-456): stage with the carried error, average the
         fresh delta, then Nesterov (pending carries e between rounds)."""
         self.round += 1
+        self._wait_pre_update()
         api.stage_deltas(self.L, self.anchor, local, self.pending if self.has_pending else None,
                          self.pending, None)
         self.has_pending = True
@@ -257,3 +271,37 @@ class OuterSync:
 
     def step(self, local: torch.Tensor) -> RoundRecord:
         return self.round_overlapped(local) if self.cfg.overlap else self.round_sync(local)
+
+    def step_host(self, h_local: torch.Tensor, h_anchor_out: torch.Tensor | None = None
+                  ) -> RoundRecord:
+        """One round with the worker's local parameters in (pinned) host memory — the
+        drop-in call a host-resident reference engine makes. The H2D copy of `h_local` runs
+        on a copy stream concurrently with compress (overlapped mode reads local only in the
+        fused outer update); the new anchor is copied into `h_anchor_out` on a second copy
+        stream that overlaps the next round's compress. host_wait() orders the caller's
+        stream after the last D2H."""
+        dev = self.anchor.device
+        if self._h2d is None:
+            self._h2d = torch.cuda.Stream(device=dev)
+            self._d2h = torch.cuda.Stream(device=dev)
+            self._dev_local = torch.empty_like(self.anchor)
+        cur = torch.cuda.current_stream()
+        self._h2d.wait_stream(cur)  # the previous round's reads of the staging buffer
+        with torch.cuda.stream(self._h2d):
+            self._dev_local.copy_(h_local, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(self._h2d)
+        self._pre_update = [ev] + ([self._d2h_ev] if self._d2h_ev is not None else [])
+        rec = self.step(self._dev_local)
+        if h_anchor_out is not None:
+            self._d2h.wait_stream(cur)
+            with torch.cuda.stream(self._d2h):
+                h_anchor_out.copy_(self.anchor, non_blocking=True)
+            self._d2h_ev = torch.cuda.Event()
+            self._d2h_ev.record(self._d2h)
+        return rec
+
+    def host_wait(self, stream=None):
+        """Make `stream` (default: current) wait for the last step_host D2H."""
+        if self._d2h_ev is not None:
+            (stream or torch.cuda.current_stream()).wait_event(self._d2h_ev)
