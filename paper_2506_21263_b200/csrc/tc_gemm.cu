@@ -98,24 +98,28 @@ struct Ring {
 
 // A_MN: false = K1 (A = delta rows: the TMA tile is already K-major SW128, row m = A row);
 // true = K2 (A = delta^T: the raw TMA tile is [k][m], column m = A row).
+// KB: 32-column k boxes per pipeline stage (a 16 KB stage costs one mbarrier round trip per
+// 16 KB and caps the stream near 5.5 TB/s; 32 KB stages reach the HBM roofline).
 // Two rings decouple memory latency from the MMA: a deep LOAD ring (lr stages of raw A + B
 // in shared memory, filled by TMA) and a shallow COMPUTE ring (cr slots of A hi/lo in TMEM,
 // written with tcgen05.st, + B hi/lo in shared memory). The split warps move a landed load
-// stage into a compute slot and immediately release the load stage, so up to lr x 20 KB of
-// HBM traffic stays in flight per SM independently of the MMA pipeline.
-template <bool A_MN>
+// stage into a compute slot and immediately release the load stage, so up to lr stages of
+// HBM traffic stay in flight per SM independently of the MMA pipeline.
+template <bool A_MN, int KB>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_tc_sweep(const DevT2* __restrict__ T, const TcMaps* __restrict__ maps,
                const int4* __restrict__ tiles, const int* __restrict__ cta_off, int N,
                int lr, int cr,
                const int* __restrict__ splits, const int64_t* __restrict__ part_off,
-               float* __restrict__ out, float* __restrict__ part, int variant,
-               unsigned long long* __restrict__ prof) {
+               float* __restrict__ out, float* __restrict__ part) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t b_bytes = static_cast<uint32_t>(N) * 128;
-  const uint32_t ls_bytes = kAStage + b_bytes;  // load stage: raw A + raw B
-  uint8_t* cring = smem + lr * ls_bytes;        // compute slots: B hi + B lo
+  constexpr uint32_t kA = KB * kAStage;          // raw A bytes per stage
+  constexpr int KS = 32 * KB;                    // k extent of a stage
+  const uint32_t b_box = static_cast<uint32_t>(N) * 128;  // one 32-k box of B (N rows x 128 B)
+  const uint32_t b_bytes = KB * b_box;
+  const uint32_t ls_bytes = kA + b_bytes;        // load stage: raw A + raw B
+  uint8_t* cring = smem + lr * ls_bytes;         // compute slots: B hi + B lo
   uint64_t* bars = reinterpret_cast<uint64_t*>(cring + cr * 2 * b_bytes);
   uint64_t* lfull = bars;
   uint64_t* lempty = lfull + lr;
@@ -151,6 +155,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t a_base = static_cast<uint32_t>((N + 31) / 32 * 32);  // A slots after the accumulator
+  constexpr uint32_t kSlotCols = 64u * KB;  // TMEM columns per compute slot (hi + lo per box)
   constexpr int64_t KC = 2048;
 
   // k-loop extent of a tile
@@ -179,20 +184,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __syncwarp();
       int64_t k0, k1;
       tile_k(tl, t, k0, k1);
-      for (int64_t k = k0; k < k1; k += 32, L.next(lr)) {
+      for (int64_t k = k0; k < k1; k += KS, L.next(lr)) {
         const int s = L.slot;
         mbar_wait(&lempty[s], L.phase ^ 1);
         uint8_t* st = smem + s * ls_bytes;
         if (elect_one()) {
-          mbar_expect_tx(&lfull[s], kAStage + b_bytes);
-          if (!A_MN) {
-            tma_load_2d(st, &mp->a, &lfull[s], static_cast<int>(k), tl.y);  // {k, m0}
-          } else {
+          const int nb = static_cast<int>(min(static_cast<int64_t>(KB), (k1 - k + 31) / 32));  // boxes inside the tile
+          mbar_expect_tx(&lfull[s], static_cast<uint32_t>(nb) * (kAStage + b_box));
 #pragma unroll
-            for (int q = 0; q < 4; ++q)  // raw [k][m] tile: 4 boxes of 32 rows x 32 columns
-              tma_load_2d(st + q * 4096, &mp->a, &lfull[s], tl.y + 32 * q, static_cast<int>(k));
+          for (int j = 0; j < KB; ++j) {
+            if (j < nb) {
+              const int kj = static_cast<int>(k) + 32 * j;
+              if (!A_MN) {
+                tma_load_2d(st + j * kAStage, &mp->a, &lfull[s], kj, tl.y);  // {k, m0}
+              } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)  // raw [k][m] tile: 4 boxes of 32 rows x 32 columns
+                  tma_load_2d(st + j * kAStage + q * 4096, &mp->a, &lfull[s], tl.y + 32 * q, kj);
+              }
+              tma_load_2d(st + kA + j * b_box, &mp->b, &lfull[s], kj, 0);  // {k, n}
+            }
           }
-          tma_load_2d(st + kAStage, &mp->b, &lfull[s], static_cast<int>(k), 0);  // {k, n}
         }
         __syncwarp();
       }
@@ -206,6 +218,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint64_t bdesc_hi0 = sdesc(su32(cring), 16u, 1024u);
     const uint64_t bdesc_lo0 = sdesc(su32(cring) + b_bytes, 16u, 1024u);
     const uint64_t slot_step = (2u * b_bytes) >> 4;  // start-address units per compute slot
+    const uint64_t box_step = b_box >> 4;
     uint32_t tphase = 0;
     Ring C;
     for (int ti = cta_off[blockIdx.x]; ti < cta_off[blockIdx.x + 1]; ++ti) {
@@ -213,28 +226,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const DevT2 t = T[tl.x];
       int64_t k0, k1;
       tile_k(tl, t, k0, k1);
-      {
-        const long long w0 = clock64();
-        mbar_wait(tempty, tphase ^ 1);
-        if (prof && lane == 0) atomicAdd(&prof[blockIdx.x * 8 + 2], (unsigned long long)(clock64() - w0));
-      }
+      mbar_wait(tempty, tphase ^ 1);
       tc_fence_after();
       uint32_t acc = 0;
-      for (int64_t k = k0; k < k1; k += 32, C.next(cr)) {
+      for (int64_t k = k0; k < k1; k += KS, C.next(cr)) {
         const int c = C.slot;
-        const long long w0 = clock64();
         mbar_wait(&cfull[c], C.phase);
-        if (prof && lane == 0) atomicAdd(&prof[blockIdx.x * 8 + 0], (unsigned long long)(clock64() - w0));
         tc_fence_after();
-        const uint32_t a_hi = tmem + a_base + static_cast<uint32_t>(c) * 64u;
-        const uint32_t a_lo = a_hi + 32u;
-        const uint64_t bh = bdesc_hi0 + slot_step * c, bl = bdesc_lo0 + slot_step * c;
+        const int nb = static_cast<int>(min(static_cast<int64_t>(KB), (k1 - k + 31) / 32));
         if (elect_one()) {
-          if (!(variant & 4)) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              mma_tf32_ts(tmem, a_hi + kk * 8u, bh + 2u * kk, idesc, acc | kk);
-              if (!(variant & 1)) {
+          for (int j = 0; j < KB; ++j) {
+            if (j < nb) {
+              const uint32_t a_hi = tmem + a_base + static_cast<uint32_t>(c) * kSlotCols + 64u * j;
+              const uint32_t a_lo = a_hi + 32u;
+              const uint64_t bh = bdesc_hi0 + slot_step * c + box_step * j;
+              const uint64_t bl = bdesc_lo0 + slot_step * c + box_step * j;
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                mma_tf32_ts(tmem, a_hi + kk * 8u, bh + 2u * kk, idesc, (acc | kk | j) ? 1u : 0u);
                 mma_tf32_ts(tmem, a_hi + kk * 8u, bl + 2u * kk, idesc, 1u);
                 mma_tf32_ts(tmem, a_lo + kk * 8u, bh + 2u * kk, idesc, 1u);
               }
@@ -244,7 +254,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         __syncwarp();
         acc = 1u;
-        if (prof && lane == 0) atomicAdd(&prof[blockIdx.x * 8 + 1], (unsigned long long)(clock64() - w0));
       }
       if (elect_one()) mma_commit(tfull);
       __syncwarp();
@@ -252,7 +261,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else {
     // ---------------------------------------------------------------- split + epilogue
-    // 8 warps: two per TMEM lane quarter; warp half h handles K columns [16h, 16h + 16)
+    // 8 warps: two per TMEM lane quarter; warp half h handles columns [16h, 16h + 16) of
+    // every 32-column box
     const int et = threadIdx.x - 64;      // 0..255
     const int quarter = warp % 4;         // TMEM lane quarter this warp may access
     const int half = (warp - 2) / 4;      // 0 or 1
@@ -266,66 +276,69 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const DevT2 t = T[tl.x];
       int64_t k0, k1;
       tile_k(tl, t, k0, k1);
-      for (int64_t k = k0; k < k1; k += 32, L.next(lr), C.next(cr)) {
+      for (int64_t k = k0; k < k1; k += KS, L.next(lr), C.next(cr)) {
         const int s = L.slot, c = C.slot;
-        const bool pt = prof && et == 0;
-        long long w0 = pt ? clock64() : 0;
         mbar_wait(&lfull[s], L.phase);
-        if (pt) { atomicAdd(&prof[blockIdx.x * 8 + 3], (unsigned long long)(clock64() - w0)); w0 = clock64(); }
         const uint8_t* st = smem + s * ls_bytes;
-        // 16 values of this thread's A row -> hi / lo registers
-        float h[16], l[16];
-        if (!A_MN) {
-          const float4* rowp = reinterpret_cast<const float4*>(st) + row * 8;
+        const int nb = static_cast<int>(min(static_cast<int64_t>(KB), (k1 - k + 31) / 32));
+        // 16 values per box of this thread's A row -> hi / lo registers
+        float h[KB][16], l[KB][16];
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int q = half * 4 + qq;
-            const float4 x = rowp[q ^ (row & 7)];  // SW128: chunk q stored at q ^ (row % 8)
-            float4 hh, ll;
-            split4(x, hh, ll);
-            h[4 * qq + 0] = hh.x; h[4 * qq + 1] = hh.y; h[4 * qq + 2] = hh.z; h[4 * qq + 3] = hh.w;
-            l[4 * qq + 0] = ll.x; l[4 * qq + 1] = ll.y; l[4 * qq + 2] = ll.z; l[4 * qq + 3] = ll.w;
-          }
-        } else {
-          const float* raw = reinterpret_cast<const float*>(st);
-          const int q = row >> 5, mm = row & 31;
+        for (int j = 0; j < KB; ++j) {
+          if (j < nb) {
+            const uint8_t* sj = st + j * kAStage;
+            if (!A_MN) {
+              const float4* rowp = reinterpret_cast<const float4*>(sj) + row * 8;
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk) {
-            const float x = raw[q * 1024 + (half * 16 + kk) * 32 + mm];
-            h[kk] = tf32_hi(x);
-            l[kk] = x - h[kk];
+              for (int qq = 0; qq < 4; ++qq) {
+                const int q = half * 4 + qq;
+                const float4 x = rowp[q ^ (row & 7)];  // SW128: chunk q stored at q ^ (row % 8)
+                float4 hh, ll;
+                split4(x, hh, ll);
+                h[j][4 * qq + 0] = hh.x; h[j][4 * qq + 1] = hh.y; h[j][4 * qq + 2] = hh.z; h[j][4 * qq + 3] = hh.w;
+                l[j][4 * qq + 0] = ll.x; l[j][4 * qq + 1] = ll.y; l[j][4 * qq + 2] = ll.z; l[j][4 * qq + 3] = ll.w;
+              }
+            } else {
+              const float* raw = reinterpret_cast<const float*>(sj);
+              const int q = row >> 5, mm = row & 31;
+#pragma unroll
+              for (int kk = 0; kk < 16; ++kk) {
+                const float x = raw[q * 1024 + (half * 16 + kk) * 32 + mm];
+                h[j][kk] = tf32_hi(x);
+                l[j][kk] = x - h[j][kk];
+              }
+            }
           }
         }
         // B: raw (load stage) -> hi / lo (compute slot) once the slot is free
-        if (pt) { atomicAdd(&prof[blockIdx.x * 8 + 4], (unsigned long long)(clock64() - w0)); w0 = clock64(); }
         mbar_wait(&cempty[c], C.phase ^ 1);
-        if (pt) { atomicAdd(&prof[blockIdx.x * 8 + 5], (unsigned long long)(clock64() - w0)); w0 = clock64(); }
         tc_fence_after();
-        const float4* braw = reinterpret_cast<const float4*>(st + kAStage);
+        const float4* braw = reinterpret_cast<const float4*>(st + kA);
         float4* bh = reinterpret_cast<float4*>(cring + c * 2 * b_bytes);
         float4* bl = reinterpret_cast<float4*>(cring + c * 2 * b_bytes + b_bytes);
-        for (int i = et; i < bvec; i += 256) {
+        const int bv = bvec / KB * nb;
+        for (int i = et; i < bv; i += 256) {
           float4 hh, ll;
           split4(braw[i], hh, ll);
           bh[i] = hh;
           bl[i] = ll;
         }
         mbar_arrive(&lempty[s]);  // raw stage consumed (A values are in registers)
-        const uint32_t a_col = a_base + static_cast<uint32_t>(c) * 64u + half * 16u;
-        if (!(variant & 2)) {
-          tmem_st16(tmem + lane_base + a_col, h);
-          tmem_st16(tmem + lane_base + a_col + 32u, l);
-          tmem_st_wait();
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+          if (j < nb) {
+            const uint32_t a_col = a_base + static_cast<uint32_t>(c) * kSlotCols + 64u * j + half * 16u;
+            tmem_st16(tmem + lane_base + a_col, h[j]);
+            tmem_st16(tmem + lane_base + a_col + 32u, l[j]);
+          }
         }
+        tmem_st_wait();
         fence_async_smem();
         tc_fence_before();
         mbar_arrive(&cfull[c]);
-        if (pt) atomicAdd(&prof[blockIdx.x * 8 + 6], (unsigned long long)(clock64() - w0));
       }
       // epilogue: TMEM -> column-major factor (or split-K partial); halves alternate 16-col chunks
-      const long long we = (prof && et == 0) ? clock64() : 0;
       mbar_wait(tfull, tphase);
-      if (prof && et == 0) atomicAdd(&prof[blockIdx.x * 8 + 7], (unsigned long long)(clock64() - we));
       tc_fence_after();
       const int64_t m = tl.y + row;
       const int64_t mlim = A_MN ? t.b : t.a;
@@ -503,66 +516,57 @@ static const TcMaps* tc_maps(const Plan& P, int which, const float* slab, const 
   return S.d_maps[which];
 }
 
-// Ring sizes (load stages lr, compute slots cr) that fit ~220 KB of shared memory.
-static void tc_rings(int N, int& lr, int& cr) {
-  const int b = N * 128;
+// Boxes per stage: 2 (32 KB of delta per stage) while the rings still fit; 1 for wide N.
+static int tc_kb(int N) { return N <= 64 ? 2 : 1; }
+
+// Ring sizes (load stages lr, compute slots cr) that fit ~220 KB of shared memory and the
+// 512 TMEM columns (accumulator N + cr slots of 64 * kb columns).
+static void tc_rings(int N, int kb, int& lr, int& cr) {
+  const int b = N * 128 * kb;
+  const int a = 16384 * kb;
   const int a_base = (N + 31) / 32 * 32;
-  for (cr = std::min(7, (512 - a_base) / 64); cr >= 2; --cr) {
-    lr = (220 * 1024 - cr * 2 * b) / (16384 + b);
-    if (lr >= 4 || cr == 2) break;
+  for (cr = std::min(kb == 1 ? 7 : 3, (512 - a_base) / (64 * kb)); cr >= 2; --cr) {
+    lr = (220 * 1024 - cr * 2 * b) / (a + b);
+    if (lr >= (kb == 1 ? 4 : 3) || cr == 2) break;
   }
   lr = std::max(2, std::min(lr, 8));
 }
 
-static size_t tc_smem(int N, int lr, int cr) {
-  const int b = N * 128;
-  return 1024 + static_cast<size_t>(lr) * (16384 + b) + static_cast<size_t>(cr) * 2 * b +
+static size_t tc_smem(int N, int kb, int lr, int cr) {
+  const int b = N * 128 * kb;
+  return 1024 + static_cast<size_t>(lr) * (16384 * kb + b) + static_cast<size_t>(cr) * 2 * b +
          8 * (2 * lr + 2 * cr + 2) + 16;
 }
 
+template <bool A_MN, int KB>
+static void launch_sweep_kb(const Plan& P, const TcMaps* maps, const int4* d_tiles, int grid,
+                            const int* d_off, float* out, float* part, cudaStream_t s) {
+  const int N = tc_n(P);
+  int lr = 0, cr = 0;
+  tc_rings(N, KB, lr, cr);
+  const size_t sm = tc_smem(N, KB, lr, cr);
+  static bool attr = false;
+  if (!attr) {
+    DLX_CUDA(cudaFuncSetAttribute(k_tc_sweep<A_MN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    attr = true;
+  }
+  k_tc_sweep<A_MN, KB><<<grid, kTcThreads, sm, s>>>(P.d_t2, maps, d_tiles, d_off, N, lr, cr,
+                                                    P.d_k2_splits, P.d_k2_part_off, out, part);
+}
 
 template <bool A_MN>
 static void launch_sweep(const Plan& P, const TcMaps* maps, const std::vector<int4>& tiles,
                          const int4* d_tiles, const std::vector<int>& off, const int* d_off,
                          float* out, float* part, cudaStream_t s) {
   if (tiles.empty()) return;
-  const int N = tc_n(P);
-  int lr = 0, cr = 0;
-  tc_rings(N, lr, cr);
-  const size_t sm = tc_smem(N, lr, cr);
-  static bool attr = false;
-  if (!attr) {
-    DLX_CUDA(cudaFuncSetAttribute(k_tc_sweep<A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
-    attr = true;
-  }
   const int grid = static_cast<int>(off.size()) - 1;
-  static const int variant = [] {
-    const char* e = getenv("DLX_SWEEP_VARIANT");  // experiments only: 1 = 1xTF32, 2 = no TMEM
-    return e ? atoi(e) : 0;                       // stores, 4 = no MMA, 8 = lr=2
-  }();
-  if (variant & 8) lr = 2;
-  static unsigned long long* prof = nullptr;
-  if ((variant & 16) && !prof) {
-    DLX_CUDA(cudaMalloc(&prof, 8 * 8 * 1024));
-  }
-  if (prof) DLX_CUDA(cudaMemsetAsync(prof, 0, 8 * 8 * 1024, s));
   // algorithmic bytes: one fp32 read of every swept delta element (factors are L2-resident)
   KernelTimer timer(A_MN ? "k_tc_sweep_k2" : "k_tc_sweep_k1", 4.0 * tc_state(P).swept_params, s);
-  k_tc_sweep<A_MN><<<grid, kTcThreads, sm, s>>>(P.d_t2, maps, d_tiles, d_off, N,
-                                                lr, cr, P.d_k2_splits, P.d_k2_part_off, out, part,
-                                                variant, (variant & 16) ? prof : nullptr);
-  if (variant & 16) {
-    std::vector<unsigned long long> h(8 * grid);
-    DLX_CUDA(cudaMemcpyAsync(h.data(), prof, 8 * 8 * grid, cudaMemcpyDeviceToHost, s));
-    DLX_CUDA(cudaStreamSynchronize(s));
-    double t[8] = {0};
-    for (int b = 0; b < grid; ++b)
-      for (int i = 0; i < 8; ++i) t[i] += h[b * 8 + i] / (double)grid;
-    fprintf(stderr, "[tc_sweep<%d> lr=%d cr=%d] per-CTA cycles: mma_wait_cfull=%.0f mma_stage_total=%.0f "
-                    "mma_wait_tempty=%.0f | split(lane0): wait_lfull=%.0f splitA=%.0f wait_cempty=%.0f "
-                    "rest=%.0f wait_tfull=%.0f\n", (int)A_MN, lr, cr, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
-  }
+  if (tc_kb(tc_n(P)) == 2)
+    launch_sweep_kb<A_MN, 2>(P, maps, d_tiles, grid, d_off, out, part, s);
+  else
+    launch_sweep_kb<A_MN, 1>(P, maps, d_tiles, grid, d_off, out, part, s);
   DLX_LAUNCHED();
 }
 

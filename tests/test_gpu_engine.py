@@ -80,7 +80,9 @@ def test_step_host_matches_step(ctx, oracle):
         r2 = e2.step_host(h, h_anchor)
         e2.host_wait()
         torch.cuda.synchronize()
-        assert r1.comp_error == r2.comp_error and r1.r_prime == r2.r_prime
+        # stats are fp64 atomics (diagnostics; summation order not fixed)
+        assert abs(r1.comp_error - r2.comp_error) <= 1e-12 * abs(r1.comp_error)
+        assert r1.r_prime == r2.r_prime
         assert torch.equal(e1.anchor, e2.anchor)
         assert torch.equal(e1.velocity, e2.velocity)
         assert torch.equal(e1.pending, e2.pending)
