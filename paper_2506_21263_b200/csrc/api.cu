@@ -66,7 +66,15 @@ static T* upload(const std::vector<T>& v) {
   return d;
 }
 
+void* Plan::dev_alloc(size_t bytes) const {
+  void* p = nullptr;
+  DLX_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+  const_cast<Plan*>(this)->owned.push_back(p);
+  return p;
+}
+
 Plan::~Plan() {
+  for (void* p : owned) cudaFree(p);
   void* ptrs[] = {d_t2, d_t1, d_chunks, d_streams, d_mats[0], d_mats[1], d_k1_tiles,
                   d_k2_tiles, d_k2_part_off, d_k2_splits, d_k5_tiles, d_cold_base_spec[0],
                   d_cold_base_spec[1], d_k1_rest, d_k2_rest, d_k5s_tiles};

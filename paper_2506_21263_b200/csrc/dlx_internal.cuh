@@ -1,6 +1,7 @@
 // dlx_internal.cuh — shared device/host definitions of the B200 outer-sync library.
 #pragma once
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <stdint.h>
 
 #include <map>
@@ -128,11 +129,21 @@ struct dlx_layout {
   std::vector<int64_t> offsets;  // slab offsets
   int64_t slab = 0;
   std::map<std::pair<int, int>, std::unique_ptr<dlx::Plan>> plans;
+  void* d_spans = nullptr;  // staging-kernel tensor table (device), freed with the layout
   dlx::Plan& plan(int rank, int qbits);
+  ~dlx_layout() {
+    if (d_spans) cudaFree(d_spans);
+  }
   int64_t numel(int i) const { return ndim[i] == 2 ? dims[2 * i] * dims[2 * i + 1] : dims[2 * i]; }
 };
 
 namespace dlx {
+
+// Derived per-plan state (tile tables, tensor-map caches) owned by the Plan; its device
+// buffers come from Plan::dev_alloc and are freed with the plan (no address-keyed caches).
+struct PlanExt {
+  virtual ~PlanExt() = default;
+};
 
 // Host + device description of (layout, rank, qbits).
 struct Plan {
@@ -175,8 +186,31 @@ struct Plan {
   // chunk), [1] nearest (exact: quantisation draws nothing)
   std::vector<int64_t> cold_base_spec[2];
   int64_t* d_cold_base_spec[2] = {nullptr, nullptr};
+  // derived state + device buffers owned by the plan
+  std::map<std::string, std::unique_ptr<PlanExt>> ext;
+  std::vector<void*> owned;
+  void* dev_alloc(size_t bytes) const;  // cudaMalloc, freed in ~Plan
   ~Plan();
 };
+
+// Typed ext slot: created empty (default-constructed) on first use; *fresh tells the caller.
+template <class T>
+T& plan_ext(const Plan& P, const std::string& key, bool* fresh = nullptr) {
+  auto& e = const_cast<Plan&>(P).ext[key];
+  if (fresh) *fresh = !e;
+  if (!e) e.reset(new T());
+  return *static_cast<T*>(e.get());
+}
+
+// Upload a host vector into a plan-owned device buffer (at least min_elems elements).
+template <class T>
+T* plan_upload(const Plan& P, const std::vector<T>& v, size_t min_elems = 0) {
+  const size_t n = std::max(v.size(), min_elems);
+  if (n == 0) return nullptr;
+  T* d = static_cast<T*>(P.dev_alloc(sizeof(T) * n));
+  if (!v.empty()) DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return d;
+}
 
 // Kernel launchers (csrc/*.cu)
 void launch_fill_gaussian(const dlx_layout& L, float* out, const float* base, float scale,

@@ -27,77 +27,229 @@ __device__ double er_block_sum(double v, double* red) {
   return s;
 }
 
+// ------------------------------------------------------------------ integer code Grams
+// For K = D r <= 64 the factor Grams come straight from the packed codes: C^T C over the
+// gathered codes of one side of one tensor is an exact integer (|c| <= 2^(q-1), int32 per
+// 1024-row chunk, int64 across chunks), and G = diag(s) C^T C diag(s) with the column scales
+// is formed in fp64 inside k_effrank — no dequantised factor copies, no fp64 Gram sweep.
+constexpr int kCgChunk = 1024;  // rows per k_code_gram block
+constexpr int kCgTile = 64;     // rows staged in shared memory per pass
+constexpr int kCgMaxK = 64;
+
+struct CodeGramJob : PlanExt {
+  std::vector<int4> chunks;  // (t2 slot, side, row0, row1)
+  int4* d = nullptr;
+};
+
+__global__ void __launch_bounds__(256) k_code_gram(const DevT2* __restrict__ T,
+                                                   const int4* __restrict__ chunks,
+                                                   const uint8_t* __restrict__ gathered,
+                                                   int64_t pay_bytes, int qbits, int D, int kst,
+                                                   unsigned long long* __restrict__ G) {
+  __shared__ int tile[kCgMaxK][kCgTile + 1];           // [k][row]
+  __shared__ int red[256 * 16];                        // per-thread 4x4 partials
+  const int4 ch = chunks[blockIdx.x];
+  const DevT2& t = T[ch.x];
+  const int side = ch.y, r = t.r, K = D * r;
+  const int64_t n = side == 0 ? t.a : t.b;
+  const int nb = (K + 3) / 4;             // 4-wide blocks per dimension
+  const int NB = nb * (nb + 1) / 2;       // upper block triangle
+  const int S = max(1, 256 / NB);         // row slices
+  const int bidx = threadIdx.x % NB, slice = threadIdx.x / NB;
+  const bool active = slice < S;
+  int bi = 0, rem = bidx;
+  while (rem >= nb - bi) {
+    rem -= nb - bi;
+    ++bi;
+  }
+  const int bj = bi + rem;
+  int acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0;
+  const uint32_t mask = (1u << qbits) - 1u;
+  const int sh = 32 - qbits;
+  // decode assignment: thread -> row rl = tid % 64 of columns k = tid / 64 + 4 m (fixed
+  // across tiles, so the column addressing is hoisted)
+  const int rl = threadIdx.x % kCgTile, k0 = threadIdx.x / kCgTile;
+  const int ncol = nb;  // columns per thread: k0, k0 + 4, ..., < 4 nb
+  const uint8_t* cseg[kCgMaxK / 4];
+  int64_t cbit[kCgMaxK / 4];
+#pragma unroll
+  for (int m = 0; m < kCgMaxK / 4; ++m) {
+    const int k = k0 + 4 * m;
+    cseg[m] = nullptr;
+    cbit[m] = 0;
+    if (m < ncol && k < K) {
+      const int w = k / r, j = k % r;
+      cseg[m] = gathered + w * pay_bytes + (side == 0 ? t.seg_pc : t.seg_qc);
+      cbit[m] = (int64_t)j * n * qbits;
+    }
+  }
+  const int64_t rend = min((int64_t)ch.w, n);
+  for (int64_t row0 = ch.z; row0 < ch.w; row0 += kCgTile) {
+    __syncthreads();
+    const int64_t row = row0 + rl;
+#pragma unroll
+    for (int m = 0; m < kCgMaxK / 4; ++m) {
+      if (m >= ncol) break;
+      int c = 0;
+      if (cseg[m] && row < rend) {
+        const int64_t bit = cbit[m] + row * qbits;
+        const uint32_t word = static_cast<uint32_t>(cseg[m][bit >> 3]) |
+                              (static_cast<uint32_t>(cseg[m][(bit >> 3) + 1]) << 8);
+        c = static_cast<int>(((word >> (bit & 7)) & mask) << sh) >> sh;  // sign-extend
+      }
+      tile[k0 + 4 * m][rl] = c;
+    }
+    __syncthreads();
+    if (active) {
+      for (int rl = slice; rl < kCgTile; rl += S) {
+        int a[4], b[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          a[x] = tile[4 * bi + x][rl];
+          b[x] = tile[4 * bj + x][rl];
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] += a[x] * b[y];
+      }
+    }
+  }
+  // fold the row slices (fixed order; integer sums are exact anyway), one atomic per entry
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) red[threadIdx.x * 16 + x * 4 + y] = active ? acc[x][y] : 0;
+  __syncthreads();
+  unsigned long long* g = G + ((int64_t)ch.x * 2 + side) * kst * kst;
+  for (int e = threadIdx.x; e < NB * 16; e += 256) {
+    const int b = e / 16, xy = e % 16, x = xy / 4, y = xy % 4;
+    long long sum = 0;
+    for (int sl = 0; sl < S; ++sl) sum += red[(sl * NB + b) * 16 + xy];
+    int ci = 0, rm = b;
+    while (rm >= nb - ci) {
+      rm -= nb - ci;
+      ++ci;
+    }
+    const int cj = ci + rm;
+    const int i = 4 * ci + x, j = 4 * cj + y;
+    if (i < K && j < K && i <= j && sum != 0)
+      atomicAdd(&g[i * kst + j], static_cast<unsigned long long>(sum));
+  }
+}
+
+// ------------------------------------------------------------------ eigenproblem
+constexpr int kErSmemDim = 64;  // L, G_A L and M staged in shared memory when n2 <= 64
+constexpr size_t kErSmemBytes = 3 * kErSmemDim * (kErSmemDim + 1) * sizeof(double);
+// (the launch sizes the staging for the largest n2 so small problems fit several CTAs / SM)
+
+// Per tensor: G_B = L L^T (semidefinite Cholesky), M = L^T G_A L, cyclic parallel Jacobi,
+// prefix energy. Grams come either as fp64 matrices (GA, GB; row stride rr) or as integer
+// code Grams (GI, upper triangle, stride rr) scaled by the payload's column scales.
 __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, int D, int rr,
                                                  const double* __restrict__ GA,
                                                  const double* __restrict__ GB,
+                                                 const long long* __restrict__ GI,
+                                                 const uint8_t* __restrict__ gathered,
+                                                 int64_t pay_bytes, int sdim,
                                                  double* __restrict__ work, double tau,
                                                  int* __restrict__ per,
                                                  double* __restrict__ energy) {
+  extern __shared__ double er_sm[];
   __shared__ double red[32];
   __shared__ double cs[1024], sn[1024];
   __shared__ int pp[1024], qq[1024];
   __shared__ int s_k;
   __shared__ double s_tot;
   const int e = blockIdx.x;
-  const int K = D * T[e].r;
+  const DevT2& t = T[e];
+  const int K = D * t.r;
   const int n2 = K + (K & 1);
   const int64_t mat = (int64_t)rr * rr;
-  const double* Ga = GA + e * mat;
-  double* Lm = work + (3 * e + 0) * mat;  // L (lower), from G_B
-  double* Tm = work + (3 * e + 1) * mat;  // G_A L
-  double* M = work + (3 * e + 2) * mat;   // L^T G_A L  (n2 x n2, row stride rr)
-  // 1. semidefinite Cholesky of G_B (lower), columns with vanishing pivot dropped
-  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x)
-    Lm[(idx / K) * rr + idx % K] = GB[e * mat + (idx / K) * rr + idx % K];
+  const bool in_smem = n2 <= sdim;
+  const int ld = in_smem ? sdim + 1 : rr;
+  const int64_t ms = in_smem ? (int64_t)sdim * (sdim + 1) : mat;
+  double* base = in_smem ? er_sm : work + 3 * e * mat;
+  double* Lm = base;           // L (lower), from G_B
+  double* Tm = base + ms;      // G_A L
+  double* M = base + 2 * ms;   // G_A, then L^T G_A L (n2 x n2)
+  // 0. stage G_B -> Lm, G_A -> M
+  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) {
+    const int i = idx / K, k = idx % K;
+    double gb, ga;
+    if (GI) {
+      const int lo = min(i, k), hi = max(i, k);
+      const long long* gi = GI + (int64_t)e * 2 * mat;
+      const int wi = i / t.r, ji = i % t.r, wk = k / t.r, jk = k % t.r;
+      const uint8_t* pi = gathered + wi * pay_bytes;
+      const uint8_t* pk = gathered + wk * pay_bytes;
+      const double sai = *reinterpret_cast<const float*>(pi + t.seg_ps + 4 * ji);
+      const double sak = *reinterpret_cast<const float*>(pk + t.seg_ps + 4 * jk);
+      const double sbi = *reinterpret_cast<const float*>(pi + t.seg_qs + 4 * ji);
+      const double sbk = *reinterpret_cast<const float*>(pk + t.seg_qs + 4 * jk);
+      ga = (double)gi[lo * rr + hi] * sai * sak;
+      gb = (double)gi[mat + lo * rr + hi] * sbi * sbk;
+    } else {
+      ga = GA[e * mat + i * rr + k];
+      gb = GB[e * mat + i * rr + k];
+    }
+    Lm[i * ld + k] = gb;
+    M[i * ld + k] = ga;
+  }
   __syncthreads();
+  // 1. semidefinite Cholesky of G_B (lower), columns with vanishing pivot dropped
   double dmax = 0.0;
-  for (int j = 0; j < K; ++j) dmax = fmax(dmax, Lm[j * rr + j]);
+  for (int j = 0; j < K; ++j) dmax = fmax(dmax, Lm[j * ld + j]);
   const double floor_piv = 1e-14 * dmax;
   for (int j = 0; j < K; ++j) {
-    const double d = Lm[j * rr + j];
+    const double d = Lm[j * ld + j];
     const bool keep = d > floor_piv && d > 0.0;
     const double ljj = keep ? sqrt(d) : 0.0;
     __syncthreads();
     for (int i = j + 1 + threadIdx.x; i < K; i += blockDim.x)
-      Lm[i * rr + j] = keep ? Lm[i * rr + j] / ljj : 0.0;
-    if (threadIdx.x == 0) Lm[j * rr + j] = ljj;
+      Lm[i * ld + j] = keep ? Lm[i * ld + j] / ljj : 0.0;
+    if (threadIdx.x == 0) Lm[j * ld + j] = ljj;
     __syncthreads();
     const int rem = K - j - 1;
     for (int idx = threadIdx.x; idx < rem * rem; idx += blockDim.x) {
       const int i = j + 1 + idx / rem, k = j + 1 + idx % rem;
       if (k > i) continue;
-      Lm[i * rr + k] -= Lm[i * rr + j] * Lm[k * rr + j];
+      Lm[i * ld + k] -= Lm[i * ld + j] * Lm[k * ld + j];
     }
     __syncthreads();
   }
   for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) {  // zero the strict upper part
     const int i = idx / K, k = idx % K;
-    if (k > i) Lm[i * rr + k] = 0.0;
+    if (k > i) Lm[i * ld + k] = 0.0;
   }
   __syncthreads();
   // 2. Tm = G_A L ; M = L^T Tm
   for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) {
     const int i = idx / K, j = idx % K;
     double s = 0.0;
-    for (int k = j; k < K; ++k) s = fma(Ga[i * rr + k], Lm[k * rr + j], s);
-    Tm[i * rr + j] = s;
+    for (int k = j; k < K; ++k) s = fma(M[i * ld + k], Lm[k * ld + j], s);
+    Tm[i * ld + j] = s;
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < n2 * n2; idx += blockDim.x) {
     const int i = idx / n2, j = idx % n2;
     double s = 0.0;
     if (i < K && j < K)
-      for (int k = i; k < K; ++k) s = fma(Lm[k * rr + i], Tm[k * rr + j], s);
-    M[i * rr + j] = s;
+      for (int k = i; k < K; ++k) s = fma(Lm[k * ld + i], Tm[k * ld + j], s);
+    M[i * ld + j] = s;
   }
   __syncthreads();
   // symmetrise (rounding) and 3. parallel cyclic Jacobi (round-robin pairing)
   for (int idx = threadIdx.x; idx < n2 * n2; idx += blockDim.x) {
     const int i = idx / n2, j = idx % n2;
     if (j > i) {
-      const double v = 0.5 * (M[i * rr + j] + M[j * rr + i]);
-      M[i * rr + j] = v;
-      M[j * rr + i] = v;
+      const double v = 0.5 * (M[i * ld + j] + M[j * ld + i]);
+      M[i * ld + j] = v;
+      M[j * ld + i] = v;
     }
   }
   __syncthreads();
@@ -106,7 +258,7 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
     double off = 0.0, dg = 0.0;
     for (int idx = threadIdx.x; idx < n2 * n2; idx += blockDim.x) {
       const int i = idx / n2, j = idx % n2;
-      const double v = M[i * rr + j];
+      const double v = M[i * ld + j];
       if (i == j) dg += v * v; else off += v * v;
     }
     off = er_block_sum(off, red);
@@ -117,10 +269,10 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
         int a = (rd + i) % (n2 - 1);
         int b = i == 0 ? n2 - 1 : (rd - i + n2 - 1) % (n2 - 1);
         const int p = min(a, b), q = max(a, b);
-        const double apq = M[p * rr + q];
+        const double apq = M[p * ld + q];
         double c = 1.0, s = 0.0;
         if (apq != 0.0) {
-          const double theta = (M[q * rr + q] - M[p * rr + p]) / (2.0 * apq);
+          const double theta = (M[q * ld + q] - M[p * ld + p]) / (2.0 * apq);
           const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
           c = 1.0 / sqrt(t * t + 1.0);
           s = t * c;
@@ -135,18 +287,18 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
         const int i = idx / n2, k = idx % n2;
         const int p = pp[i], q = qq[i];
         const double c = cs[i], s = sn[i];
-        const double ap = M[p * rr + k], aq = M[q * rr + k];
-        M[p * rr + k] = c * ap - s * aq;
-        M[q * rr + k] = s * ap + c * aq;
+        const double ap = M[p * ld + k], aq = M[q * ld + k];
+        M[p * ld + k] = c * ap - s * aq;
+        M[q * ld + k] = s * ap + c * aq;
       }
       __syncthreads();
       for (int idx = threadIdx.x; idx < half * n2; idx += blockDim.x) {  // columns
         const int i = idx / n2, k = idx % n2;
         const int p = pp[i], q = qq[i];
         const double c = cs[i], s = sn[i];
-        const double ap = M[k * rr + p], aq = M[k * rr + q];
-        M[k * rr + p] = c * ap - s * aq;
-        M[k * rr + q] = s * ap + c * aq;
+        const double ap = M[k * ld + p], aq = M[k * ld + q];
+        M[k * ld + p] = c * ap - s * aq;
+        M[k * ld + q] = s * ap + c * aq;
       }
       __syncthreads();
     }
@@ -154,10 +306,10 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
   // 4. eigenvalues (clamped >= 0) sorted descending by rank counting; prefix energy
   double* ev = Tm;  // reuse: ev[rank] = value
   for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    const double v = fmax(M[i * rr + i], 0.0);
+    const double v = fmax(M[i * ld + i], 0.0);
     int rank = 0;
     for (int j = 0; j < n2; ++j) {
-      const double w = fmax(M[j * rr + j], 0.0);
+      const double w = fmax(M[j * ld + j], 0.0);
       rank += (w > v) || (w == v && j < i);
     }
     ev[rank] = v;
@@ -185,31 +337,72 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
   }
 }
 
+static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const double* GB,
+                           const long long* GI, const uint8_t* gathered, double* W, double tau,
+                           int* d_per, double* d_energy, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    DLX_CUDA(cudaFuncSetAttribute(k_effrank, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kErSmemBytes)));
+    attr = true;
+  }
+  int n2max = 0;
+  for (const DevT2& t : P.t2) n2max = std::max(n2max, D * t.r + ((D * t.r) & 1));
+  const int sdim = n2max <= kErSmemDim ? n2max : 0;
+  const size_t smem = 3 * static_cast<size_t>(sdim) * (sdim + 1) * sizeof(double);
+  k_effrank<<<P.t2.size(), 256, smem, s>>>(P.d_t2, D, rr, GA, GB, GI, gathered, P.payload_bytes,
+                                           sdim, W, tau, d_per, d_energy);
+  DLX_LAUNCHED();
+}
+
 void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                             double tau, int* d_per, double* d_energy, cudaStream_t s) {
   if (P.t2.empty()) return;
+  int K = 0;
+  for (const DevT2& t : P.t2) K = std::max(K, D * t.r);
+  if (K > 2048) raise(DLX_ERR_VALIDATION, "effective_rank: D * rank above 2048 unsupported");
+  const int64_t mat = static_cast<int64_t>(K) * K;
+  const size_t ne = P.t2.size();
+  auto* W = static_cast<double*>(ctx->scratch("er_W", sizeof(double) * mat * ne * 3));
+  if (K <= kCgMaxK) {
+    // integer code Grams straight from the gathered payloads
+    bool fresh = false;
+    CodeGramJob& J = plan_ext<CodeGramJob>(P, "code_gram", &fresh);
+    if (fresh) {
+      for (size_t k = 0; k < ne; ++k)
+        for (int side = 0; side < 2; ++side) {
+          const int64_t n = side == 0 ? P.t2[k].a : P.t2[k].b;
+          for (int64_t r0 = 0; r0 < n; r0 += kCgChunk)
+            J.chunks.push_back(make_int4(static_cast<int>(k), side, static_cast<int>(r0),
+                                         static_cast<int>(std::min(n, r0 + kCgChunk))));
+        }
+      J.d = plan_upload(P, J.chunks);
+    }
+    auto* GI = static_cast<unsigned long long*>(
+        ctx->scratch("er_GI", sizeof(unsigned long long) * mat * ne * 2));
+    DLX_CUDA(cudaMemsetAsync(GI, 0, sizeof(unsigned long long) * mat * ne * 2, s));
+    k_code_gram<<<J.chunks.size(), 256, 0, s>>>(P.d_t2, J.d, gathered, P.payload_bytes, P.qbits,
+                                                D, K, GI);
+    DLX_LAUNCHED();
+    launch_effrank(P, D, K, nullptr, nullptr, reinterpret_cast<const long long*>(GI), gathered,
+                   W, tau, d_per, d_energy, s);
+    return;
+  }
   float* phat = static_cast<float*>(ctx->scratch("er_phat", sizeof(float) * P.pelems * D));
   float* qhat = static_cast<float*>(ctx->scratch("er_qhat", sizeof(float) * P.qelems * D));
   dequant_factors(P, D, gathered, P.payload_bytes, phat, qhat, 0, s);
   std::vector<DevMat> A, B;
-  int K = 0;
   for (size_t k = 0; k < P.t2.size(); ++k) {
     const DevT2& t = P.t2[k];
     A.push_back(DevMat{D * t.poff, t.a, t.lda, D * t.r, static_cast<int>(k)});
     B.push_back(DevMat{D * t.qoff, t.b, t.ldb, D * t.r, static_cast<int>(k)});
-    K = std::max(K, D * t.r);
   }
-  if (K > 2048) raise(DLX_ERR_VALIDATION, "effective_rank: D * rank above 2048 unsupported");
-  const int64_t mat = static_cast<int64_t>(K) * K;
-  const size_t ne = P.t2.size();
   auto* GA = static_cast<double*>(ctx->scratch("er_GA", sizeof(double) * mat * ne));
   auto* GB = static_cast<double*>(ctx->scratch("er_GB", sizeof(double) * mat * ne));
-  auto* W = static_cast<double*>(ctx->scratch("er_W", sizeof(double) * mat * ne * 3));
   const std::string tag = std::to_string(D);
   gram_batched(ctx, P, "erA" + tag, A, phat, GA, s);
   gram_batched(ctx, P, "erB" + tag, B, qhat, GB, s);
-  k_effrank<<<ne, 256, 0, s>>>(P.d_t2, D, K, GA, GB, W, tau, d_per, d_energy);
-  DLX_LAUNCHED();
+  launch_effrank(P, D, K, GA, GB, nullptr, nullptr, W, tau, d_per, d_energy, s);
 }
 
 }  // namespace dlx

@@ -15,7 +15,7 @@
 namespace dlx {
 
 // ------------------------------------------------------------------ job tables
-struct GramJob {
+struct GramJob : PlanExt {
   std::vector<DevMat> mats;
   DevMat* d_mats = nullptr;
   std::vector<int4> splits;  // (entry, row0, row1, part index)
@@ -30,8 +30,7 @@ struct GramJob {
   int total_parts = 0;
 };
 
-static GramJob* make_job(const std::vector<DevMat>& mats) {
-  auto* J = new GramJob();
+static void make_job(const Plan& P, GramJob* J, const std::vector<DevMat>& mats) {
   J->mats = mats;
   for (size_t e = 0; e < mats.size(); ++e) {
     const DevMat& m = mats[e];
@@ -49,28 +48,19 @@ static GramJob* make_job(const std::vector<DevMat>& mats) {
     for (int64_t r0 = 0; r0 < m.n; r0 += 128)
       J->apply.push_back(make_int4(static_cast<int>(e), static_cast<int>(r0), 0, 0));
   }
-  auto up = [](auto& v) {
-    using T = typename std::decay_t<decltype(v)>::value_type;
-    T* d = nullptr;
-    if (v.empty()) return d;
-    DLX_CUDA(cudaMalloc(&d, sizeof(T) * v.size()));
-    DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
-    return d;
-  };
-  J->d_mats = up(J->mats);
-  J->d_splits = up(J->splits);
-  J->d_apply = up(J->apply);
-  J->d_part0 = up(J->part0);
-  J->d_nparts = up(J->nparts);
-  return J;
+  J->d_mats = plan_upload(P, J->mats);
+  J->d_splits = plan_upload(P, J->splits);
+  J->d_apply = plan_upload(P, J->apply);
+  J->d_part0 = plan_upload(P, J->part0);
+  J->d_nparts = plan_upload(P, J->nparts);
 }
 
 static GramJob& job_for(const Plan& P, const std::string& key,
                         const std::vector<DevMat>& mats) {
-  static thread_local std::map<std::pair<const Plan*, std::string>, std::unique_ptr<GramJob>> cache;
-  auto& slot = cache[{&P, key}];
-  if (!slot) slot.reset(make_job(mats));
-  return *slot;
+  bool fresh = false;
+  GramJob& J = plan_ext<GramJob>(P, "gram:" + key, &fresh);
+  if (fresh) make_job(P, &J, mats);
+  return J;
 }
 
 // ------------------------------------------------------------------ deterministic reduce

@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <map>
+
 #include "dlx_internal.cuh"
 #include "ptx.cuh"
 #include "epilogue.cuh"
@@ -440,7 +442,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 k5_encode_fn() {
   return fn;
 }
 
-struct K5MapCache {
+struct K5MapCache : PlanExt {
   const void* key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   K5Maps* d = nullptr;
   std::vector<K5Maps> h;
@@ -449,11 +451,10 @@ struct K5MapCache {
 static const K5Maps* k5_maps(const Plan& P, int D, const float* pending, const float* anchor,
                              const float* velocity, const float* local, const float* phat,
                              cudaStream_t s) {
-  static thread_local std::map<const Plan*, K5MapCache> cache;
-  K5MapCache& c = cache[&P];
+  K5MapCache& c = plan_ext<K5MapCache>(P, "k5_maps");
   const void* key[6] = {pending, anchor, velocity, local, phat, reinterpret_cast<const void*>(static_cast<intptr_t>(D))};
   if (c.d && std::equal(key, key + 6, c.key)) return c.d;
-  if (!c.d) DLX_CUDA(cudaMalloc(&c.d, sizeof(K5Maps) * std::max<size_t>(P.t2.size(), 1)));
+  if (!c.d) c.d = static_cast<K5Maps*>(P.dev_alloc(sizeof(K5Maps) * std::max<size_t>(P.t2.size(), 1)));
   c.h.assign(P.t2.size(), K5Maps{});
   for (size_t k = 0; k < P.t2.size(); ++k) {
     const DevT2& t = P.t2[k];
@@ -581,17 +582,25 @@ __device__ __forceinline__ float avg_1d(const uint8_t* gathered, int64_t pay_byt
   return (float)__dmul_rn(acc, 1.0 / (double)D);
 }
 
+constexpr int kOuter1dElems = 1024;  // elements per k_outer_1d block (4 per thread)
+
+// One block per 1024-element chunk of a 1-D tensor (host-built chunk table), block-reduced
+// stats: one atomic per statistic per block.
 __global__ void __launch_bounds__(256) k_outer_1d(const DevT1* __restrict__ T,
+                                                  const int2* __restrict__ chunks,
                                                   const uint8_t* __restrict__ gathered,
                                                   int64_t pay_bytes, int qbits, int D,
                                                   int self_index, int mode, float* pending,
                                                   float* anchor, const float* local,
                                                   float* velocity, float gamma, float beta,
                                                   int classical, dlx_round_stats* stats) {
-  const DevT1 t = T[blockIdx.y];
-  double num = 0.0, den = 0.0, dn = 0.0, en = 0.0, nf = 0.0;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < t.n;
-       k += (int64_t)gridDim.x * blockDim.x) {
+  const int2 ch = chunks[blockIdx.x];  // (tensor, first element)
+  const DevT1 t = T[ch.x];
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // num, den, delta_norm, err_norm, nonfinite
+#pragma unroll
+  for (int u = 0; u < kOuter1dElems / 256; ++u) {
+    const int64_t k = ch.y + u * 256 + threadIdx.x;
+    if (k >= t.n) break;
     const float delta = avg_1d(gathered, pay_bytes, t, k, D, qbits);
     const int64_t i = t.off + k;
     const float pd = pending[i];
@@ -602,17 +611,36 @@ __global__ void __launch_bounds__(256) k_outer_1d(const DevT1* __restrict__ T,
       const float rec = __fmul_rn((float)code_at(pay + t.seg_c, k, qbits),
                                   *reinterpret_cast<const float*>(pay + t.seg_s));
       const double df = (double)rec - (double)pd;
-      num += df * df;
-      den += (double)pd * (double)pd;
+      v[0] += df * df;
+      v[1] += (double)pd * (double)pd;
     }
-    en += (double)o.e * (double)o.e;
-    if (mode == DLX_MODE_OVERLAPPED) dn += (double)o.pend * (double)o.pend;
-    if (!isfinite(o.anchor)) nf += 1.0;
+    v[3] += (double)o.e * (double)o.e;
+    if (mode == DLX_MODE_OVERLAPPED) v[2] += (double)o.pend * (double)o.pend;
+    if (!isfinite(o.anchor)) v[4] += 1.0;
     pending[i] = o.pend;
     anchor[i] = o.anchor;
     velocity[i] = o.v;
   }
-  stats_add(stats, num, den, dn, en, nf, nullptr);
+  __shared__ double red[8][5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  }
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) red[threadIdx.x >> 5][q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0 && stats) {
+    double sum[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int w = 0; w < 8; ++w)
+      for (int q = 0; q < 5; ++q) sum[q] += red[w][q];
+    if (sum[0] != 0.0) atomicAdd(&stats->err_num, sum[0]);
+    if (sum[1] != 0.0) atomicAdd(&stats->err_den, sum[1]);
+    if (sum[2] != 0.0) atomicAdd(&stats->delta_norm_sq, sum[2]);
+    if (sum[3] != 0.0) atomicAdd(&stats->err_norm_sq, sum[3]);
+    if (sum[4] != 0.0) atomicAdd(&stats->nonfinite, sum[4]);
+  }
 }
 
 void launch_outer_1d(const Plan& P, int D, const uint8_t* gathered, int self_index, int mode,
@@ -620,12 +648,24 @@ void launch_outer_1d(const Plan& P, int D, const uint8_t* gathered, int self_ind
                      float gamma, float beta, int classical, dlx_round_stats* stats,
                      cudaStream_t s) {
   if (P.t1.empty()) return;
-  int64_t mx = 1;
-  for (const DevT1& t : P.t1) mx = std::max(mx, t.n);
-  const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 64));
-  k_outer_1d<<<dim3(gx, P.t1.size()), 256, 0, s>>>(P.d_t1, gathered, P.payload_bytes, P.qbits,
-                                                   D, self_index, mode, pending, anchor, local,
-                                                   velocity, gamma, beta, classical, stats);
+  struct Chunks1d : PlanExt {
+    int2* d = nullptr;
+    int n = 0;
+  };
+  bool fresh = false;
+  Chunks1d& tb = plan_ext<Chunks1d>(P, "outer_1d", &fresh);
+  if (fresh) {
+    std::vector<int2> ch;
+    for (size_t i = 0; i < P.t1.size(); ++i)
+      for (int64_t k = 0; k < P.t1[i].n; k += kOuter1dElems)
+        ch.push_back(make_int2(static_cast<int>(i), static_cast<int>(k)));
+    tb.d = plan_upload(P, ch);
+    tb.n = static_cast<int>(ch.size());
+  }
+  if (tb.n == 0) return;
+  k_outer_1d<<<tb.n, 256, 0, s>>>(P.d_t1, tb.d, gathered, P.payload_bytes, P.qbits, D,
+                                       self_index, mode, pending, anchor, local, velocity, gamma,
+                                       beta, classical, stats);
   DLX_LAUNCHED();
 }
 
@@ -719,11 +759,11 @@ void launch_stage(const dlx_layout& L, const float* anchor, const float* local,
     spans[i] = {L.offsets[i], L.numel(i)};
     mx = std::max(mx, spans[i].n);
   }
-  static thread_local std::map<const dlx_layout*, Span*> cache;
-  Span*& d = cache[&L];
+  Span* d = static_cast<Span*>(L.d_spans);
   if (!d) {
     DLX_CUDA(cudaMalloc(&d, sizeof(Span) * L.nt));
     DLX_CUDA(cudaMemcpy(d, spans.data(), sizeof(Span) * L.nt, cudaMemcpyHostToDevice));
+    const_cast<dlx_layout&>(L).d_spans = d;
   }
   const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 1024));
   k_stage<<<dim3(gx, L.nt), 256, 0, s>>>(d, anchor, local, err, pending, norm_sq);

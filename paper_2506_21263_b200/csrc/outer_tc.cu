@@ -38,47 +38,64 @@ struct O5Maps {
 
 // ------------------------------------------------------------------ prep: A and B operands
 // One thread per (slot, side, row, w): writes K-major rows of A (side 0) or B hi/lo (side 1).
-__global__ void k_o5_prep(const DevT2* __restrict__ T, const int4* __restrict__ rows, int nrows,
-                          const int64_t* __restrict__ aoff, const int64_t* __restrict__ boff,
-                          const uint8_t* __restrict__ gathered, int64_t pay_bytes, int qbits,
-                          int D, int KA, float* __restrict__ A, float* __restrict__ Bh,
-                          float* __restrict__ Bl) {
-  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= nrows) return;
-  const int4 rw = rows[g];  // (slot, side, row, -)
-  const DevT2 t = T[rw.x];
-  const int side = rw.y, row = rw.z;
-  const int64_t n = side == 0 ? t.a : t.b;
+constexpr int kPrepRows = 64;  // factor rows per k_o5_prep block
+
+// Block = 64 consecutive factor rows: codes are decoded column by column (coalesced over
+// rows), staged in shared memory, and written row-major [row][KA] with coalesced stores.
+__global__ void __launch_bounds__(256) k_o5_prep(
+    const DevT2* __restrict__ T, const int4* __restrict__ rows, int nrows,
+    const int64_t* __restrict__ aoff, const int64_t* __restrict__ boff,
+    const uint8_t* __restrict__ gathered, int64_t pay_bytes, int qbits, int D, int KA,
+    float* __restrict__ A, float* __restrict__ Bh, float* __restrict__ Bl) {
+  __shared__ float tile[kPrepRows][65];
+  const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kPrepRows;
   const float invD = __fdiv_rn(1.0f, (float)D);
-  float* dst_a = A + aoff[rw.x] + (int64_t)row * KA;   // [lda rows][KA]
-  float* dst_h = Bh + boff[rw.x] + (int64_t)row * KA;  // [ldb rows][KA]
-  float* dst_l = Bl + boff[rw.x] + (int64_t)row * KA;
-  for (int k = 0; k < KA; ++k) {
-    const int w = k / t.r, j = k % t.r;
-    float v = 0.f;
-    if (w < D && row < n) {
-      const uint8_t* pay = gathered + w * pay_bytes;
-      const int64_t idx = (int64_t)j * n + row;  // column-major code index within the factor
-      const uint8_t* seg = pay + (side == 0 ? t.seg_pc : t.seg_qc);
-      const int64_t bit = idx * qbits;
-      const uint32_t word = static_cast<uint32_t>(seg[bit >> 3]) |
-                            (static_cast<uint32_t>(seg[(bit >> 3) + 1]) << 8);
-      int c = static_cast<int>((word >> (bit & 7)) & ((1u << qbits) - 1u));
-      if (c & (1 << (qbits - 1))) c -= 1 << qbits;
-      if (side == 0) {
-        v = static_cast<float>(c);
-      } else {
-        const float sp = *reinterpret_cast<const float*>(pay + t.seg_ps + 4 * j);
-        const float sq = *reinterpret_cast<const float*>(pay + t.seg_qs + 4 * j);
-        v = __fmul_rn(static_cast<float>(c), __fmul_rn(__fmul_rn(sp, sq), invD));
+  {
+    const int rl = threadIdx.x % kPrepRows;
+    const int64_t g = g0 + rl;
+    if (g < nrows) {
+      const int4 rw = rows[g];  // (slot, side, row, -)
+      const DevT2& t = T[rw.x];
+      const int side = rw.y, row = rw.z;
+      const int64_t n = side == 0 ? t.a : t.b;
+      for (int k = threadIdx.x / kPrepRows; k < KA; k += 256 / kPrepRows) {
+        const int w = k / t.r, j = k % t.r;
+        float v = 0.f;
+        if (w < D && row < n) {
+          const uint8_t* pay = gathered + w * pay_bytes;
+          const int64_t idx = (int64_t)j * n + row;  // column-major code index within the factor
+          const uint8_t* seg = pay + (side == 0 ? t.seg_pc : t.seg_qc);
+          const int64_t bit = idx * qbits;
+          const uint32_t word = static_cast<uint32_t>(seg[bit >> 3]) |
+                                (static_cast<uint32_t>(seg[(bit >> 3) + 1]) << 8);
+          int c = static_cast<int>((word >> (bit & 7)) & ((1u << qbits) - 1u));
+          if (c & (1 << (qbits - 1))) c -= 1 << qbits;
+          if (side == 0) {
+            v = static_cast<float>(c);
+          } else {
+            const float sp = *reinterpret_cast<const float*>(pay + t.seg_ps + 4 * j);
+            const float sq = *reinterpret_cast<const float*>(pay + t.seg_qs + 4 * j);
+            v = __fmul_rn(static_cast<float>(c), __fmul_rn(__fmul_rn(sp, sq), invD));
+          }
+        }
+        tile[rl][k] = v;
       }
     }
-    if (side == 0) {
-      dst_a[k] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kPrepRows * KA; e += 256) {
+    const int rl = e / KA, k = e - rl * KA;
+    const int64_t g = g0 + rl;
+    if (g >= nrows) break;
+    const int4 rw = rows[g];
+    const float v = tile[rl][k];
+    if (rw.y == 0) {
+      A[aoff[rw.x] + static_cast<int64_t>(rw.z) * KA + k] = v;
     } else {
+      const int64_t o = boff[rw.x] + static_cast<int64_t>(rw.z) * KA + k;
       const float h = tf32_hi(v);
-      dst_h[k] = h;
-      dst_l[k] = v - h;
+      Bh[o] = h;
+      Bl[o] = v - h;
     }
   }
 }
@@ -138,6 +155,8 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     // ---------------------------------------------------------------- TMA producer
     int s = 0, a = -1;
     uint32_t sph = 0, aph[2] = {0, 0};
+    // (L2 eviction hints on these loads / the stores measured 10 % slower: none)
+
     int band_slot = -1, band_m0 = -1;
     for (int ti = t0; ti < t1; ++ti) {
       const int4 tl = tiles[ti];
@@ -365,7 +384,7 @@ static void o5_encode_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_
   if (r != CUDA_SUCCESS) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled (K5 tc) failed");
 }
 
-struct O5State {
+struct O5State : PlanExt {
   int D = 0, KA = 0;
   std::vector<int4> tiles;
   std::vector<int> off;
@@ -396,11 +415,9 @@ bool o5_eligible(const Plan& P, int D, int self_index) {
 }
 
 static O5State& o5_state(const Plan& P, int D) {
-  static thread_local std::map<std::pair<const Plan*, int>, std::unique_ptr<O5State>> cache;
-  auto& up = cache[{&P, D}];
-  if (up) return *up;
-  up.reset(new O5State());
-  O5State& S = *up;
+  bool fresh = false;
+  O5State& S = plan_ext<O5State>(P, "o5:" + std::to_string(D), &fresh);
+  if (!fresh) return S;
   S.D = D;
   S.KA = static_cast<int>(round_up(D * P.rmax, 32));
   // tiles: per tensor, row band (128) major, then 32-column blocks; balanced contiguous chunks
@@ -425,19 +442,12 @@ static O5State& o5_state(const Plan& P, int D) {
   const int g = static_cast<int>(std::min<size_t>(S.tiles.size(), sms));
   S.off.resize(g + 1);
   for (int b = 0; b <= g; ++b) S.off[b] = static_cast<int>(S.tiles.size() * b / g);
-  auto upl = [](const auto& v) {
-    using T = typename std::decay_t<decltype(v)>::value_type;
-    T* d = nullptr;
-    DLX_CUDA(cudaMalloc(&d, sizeof(T) * std::max<size_t>(v.size(), 1)));
-    if (!v.empty()) DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
-    return d;
-  };
-  S.d_tiles = upl(S.tiles);
-  S.d_off = upl(S.off);
-  S.d_rows = upl(S.rows);
-  S.d_aoff = upl(S.aoff);
-  S.d_boff = upl(S.boff);
-  DLX_CUDA(cudaMalloc(&S.d_maps, sizeof(O5Maps) * P.t2.size()));
+  S.d_tiles = plan_upload(P, S.tiles, 1);
+  S.d_off = plan_upload(P, S.off, 1);
+  S.d_rows = plan_upload(P, S.rows, 1);
+  S.d_aoff = plan_upload(P, S.aoff, 1);
+  S.d_boff = plan_upload(P, S.boff, 1);
+  S.d_maps = static_cast<O5Maps*>(P.dev_alloc(sizeof(O5Maps) * P.t2.size()));
   S.h_maps.resize(P.t2.size());
   return S;
 }
@@ -451,7 +461,7 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   float* A = static_cast<float*>(ctx->scratch("o5_A", sizeof(float) * (S.a_elems + 1024)));
   float* Bh = static_cast<float*>(ctx->scratch("o5_Bh", sizeof(float) * (S.b_elems + 1024)));
   float* Bl = static_cast<float*>(ctx->scratch("o5_Bl", sizeof(float) * (S.b_elems + 1024)));
-  k_o5_prep<<<static_cast<unsigned>(ceil_div(S.rows.size(), 128)), 128, 0, s>>>(
+  k_o5_prep<<<static_cast<unsigned>(ceil_div(S.rows.size(), kPrepRows)), 256, 0, s>>>(
       P.d_t2, S.d_rows, static_cast<int>(S.rows.size()), S.d_aoff, S.d_boff, gathered,
       P.payload_bytes, P.qbits, D, KA, A, Bh, Bl);
   DLX_LAUNCHED();

@@ -345,12 +345,13 @@ void launch_k2(const Plan& P, const float* slab, const float* p, float* z, float
       mx = std::max(mx, P.t2[k].ldb * P.t2[k].r);
     }
   if (slots.empty()) return;
-  static thread_local std::map<const Plan*, int*> cache;
-  int*& d = cache[&P];
-  if (!d) {
-    DLX_CUDA(cudaMalloc(&d, sizeof(int) * slots.size()));
-    DLX_CUDA(cudaMemcpy(d, slots.data(), sizeof(int) * slots.size(), cudaMemcpyHostToDevice));
-  }
+  struct Slots : PlanExt {
+    int* d = nullptr;
+  };
+  bool fresh = false;
+  Slots& sl = plan_ext<Slots>(P, "k2_reduce", &fresh);
+  if (fresh) sl.d = plan_upload(P, slots);
+  int* d = sl.d;
   const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 1024));
   k2_reduce<<<dim3(gx, slots.size()), 256, 0, s>>>(P.d_t2, d, P.d_k2_splits, P.d_k2_part_off,
                                                   part, z);

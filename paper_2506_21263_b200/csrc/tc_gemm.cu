@@ -172,6 +172,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     // warp-uniform loop, one elected lane issues (TMA operands must be uniform)
+    // delta streams through once; the factor chunks are re-read by every row band
+    const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
     Ring L;
     for (int ti = cta_off[blockIdx.x]; ti < cta_off[blockIdx.x + 1]; ++ti) {
       const int4 tl = tiles[ti];
@@ -196,13 +198,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (j < nb) {
               const int kj = static_cast<int>(k) + 32 * j;
               if (!A_MN) {
-                tma_load_2d(st + j * kAStage, &mp->a, &lfull[s], kj, tl.y);  // {k, m0}
+                tma_load_2d_hint(st + j * kAStage, &mp->a, &lfull[s], kj, tl.y, pol_stream);  // {k, m0}
               } else {
 #pragma unroll
                 for (int q = 0; q < 4; ++q)  // raw [k][m] tile: 4 boxes of 32 rows x 32 columns
-                  tma_load_2d(st + j * kAStage + q * 4096, &mp->a, &lfull[s], tl.y + 32 * q, kj);
+                  tma_load_2d_hint(st + j * kAStage + q * 4096, &mp->a, &lfull[s], tl.y + 32 * q, kj,
+                                   pol_stream);
               }
-              tma_load_2d(st + kA + j * b_box, &mp->b, &lfull[s], kj, 0);  // {k, n}
+              tma_load_2d_hint(st + kA + j * b_box, &mp->b, &lfull[s], kj, 0, pol_keep);  // {k, n}
             }
           }
         }
@@ -412,7 +415,7 @@ static int num_sms() {
   return n;
 }
 
-struct TcState {
+struct TcState : PlanExt {
   int64_t swept_params = 0;  // delta elements one sweep reads on the tensor-core path
   std::vector<int4> k1, k2;  // tiles grouped per CTA (balanced, see balance())
   std::vector<int> off1, off2;
@@ -426,10 +429,9 @@ struct TcState {
 };
 
 static TcState& tc_state(const Plan& P) {
-  static thread_local std::map<const Plan*, std::unique_ptr<TcState>> cache;
-  auto& s = cache[&P];
-  if (!s) {
-    s.reset(new TcState());
+  bool fresh = false;
+  TcState* s = &plan_ext<TcState>(P, "tc_sweep", &fresh);
+  if (fresh) {
     constexpr int64_t KC = 2048;
     for (size_t k = 0; k < P.t2.size(); ++k) {
       const DevT2& t = P.t2[k];
@@ -468,20 +470,12 @@ static TcState& tc_state(const Plan& P) {
     };
     balance(s->k1, s->off1, false);
     balance(s->k2, s->off2, true);
-    auto up = [](const auto& v) {
-      using T = typename std::decay_t<decltype(v)>::value_type;
-      T* d = nullptr;
-      if (v.empty()) return d;
-      DLX_CUDA(cudaMalloc(&d, sizeof(T) * v.size()));
-      DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
-      return d;
-    };
-    s->d_k1 = up(s->k1);
-    s->d_k2 = up(s->k2);
-    s->d_off1 = up(s->off1);
-    s->d_off2 = up(s->off2);
+    s->d_k1 = plan_upload(P, s->k1);
+    s->d_k2 = plan_upload(P, s->k2);
+    s->d_off1 = plan_upload(P, s->off1);
+    s->d_off2 = plan_upload(P, s->off2);
     for (int w = 0; w < 2; ++w) {
-      DLX_CUDA(cudaMalloc(&s->d_maps[w], sizeof(TcMaps) * std::max<size_t>(P.t2.size(), 1)));
+      s->d_maps[w] = static_cast<TcMaps*>(P.dev_alloc(sizeof(TcMaps) * std::max<size_t>(P.t2.size(), 1)));
       s->host[w].resize(P.t2.size());
     }
   }

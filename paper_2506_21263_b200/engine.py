@@ -24,6 +24,25 @@ from . import api
 from .api import NEAREST, OVERLAPPED, STOCHASTIC, SYNC, QuantSpec
 
 
+def exchange(payload: torch.Tensor, gathered: torch.Tensor, warm_q: torch.Tensor | None,
+             world: int, group=None) -> torch.Tensor:
+    """The round's only data exchange (collective_average, engine.cpp:215-263): all-gather
+    of every worker's compressed payload into `gathered` — worker w's bytes at
+    [w * len(payload), (w + 1) * len(payload)), worker order = rank order, the order
+    allreduce_avg sums in (collective.cpp:17-46) — and broadcast of worker 0's float Q
+    factors as everyone's next warm start (engine.cpp:498-501). Byte-format agnostic; NCCL
+    over NVLink on GPUs, gloo on CPU tensors."""
+    if world == 1:
+        return payload
+    import torch.distributed as dist
+    pb = payload.numel()
+    g = gathered[:world * pb]
+    dist.all_gather_into_tensor(g, payload, group=group)
+    if warm_q is not None and warm_q.numel() > 0:
+        dist.broadcast(warm_q, src=0, group=group)
+    return g
+
+
 @dataclass
 class OuterConfig:
     """The config keys the path accepts (config.cpp:209-235); defaults engine.hpp:21-36,
@@ -137,14 +156,8 @@ class OuterSync:
 
     def _exchange(self, pb: int, qel: int):
         """All-gather payloads; broadcast worker-0 Q (warm start) — NCCL over NVLink."""
-        if self.world == 1:
-            return self.payload[:pb]
-        import torch.distributed as dist
-        g = self.gathered[:self.world * pb]
-        dist.all_gather_into_tensor(g, self.payload[:pb], group=self.group)
-        if qel > 0:
-            dist.broadcast(self.warm_q[:qel], src=0, group=self.group)
-        return g
+        return exchange(self.payload[:pb], self.gathered, self.warm_q[:qel] if qel > 0 else None,
+                        self.world, self.group)
 
     def collective_average(self, local: torch.Tensor | None, mode: int) -> RoundRecord:
         """Compress (shared stream per round), exchange, measure, fused outer update."""

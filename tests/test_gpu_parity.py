@@ -265,13 +265,15 @@ def test_compress_larger_shapes(ctx, oracle):
         _check_compress(L, t, oracle, ref, res, rank, 8, st)
 
 
-def test_effective_rank_factor_space(ctx, oracle):
+@pytest.mark.parametrize("rank,q,D", [(6, 8, 3), (16, 2, 1), (32, 4, 2), (30, 4, 3)])
+def test_effective_rank_factor_space(ctx, oracle, rank, q, D):
+    """Factor-space r' (integer code Grams for D*r <= 64, fp64 dequantised Grams above) vs
+    the reference's dense SVD of the averaged Delta; energy = ||Delta||_F^2."""
     from paper_2506_21263_b200 import api
     import torch
-    shapes = [(48, 40), (40,), (30, 64), (20, 20)]
+    shapes = [(48, 40), (40,), (30, 64), (20, 20), (70, 36)]
     t = Table(shapes)
     L = mk(ctx, shapes)
-    rank, q, D = 6, 8, 3
     ranks = t.ranks(rank)
     codes, scales, pays = [], [], []
     for w in range(D):
@@ -280,11 +282,17 @@ def test_effective_rank_factor_space(ctx, oracle):
         codes.append(c["codes"]); scales.append(c["scales"])
         pays.append(_payload_from_oracle(L, oracle, t, ranks, rank, q, c["codes"], c["scales"]))
     avg = oracle.allreduce_avg(t, ranks, codes, scales)
+    dense = [x for x, s in zip(split_dense(shapes, avg), shapes) if len(s) == 2]
     for tau in (0.3, 0.5, 0.9):
         per, agg, allz = oracle.effective_rank(t, avg, tau, rank)
         er = api.effective_rank(L, torch.cat(pays), D, rank, q, tau, rank)
         assert [k for _, k in er.per_tensor] == per.tolist()
         assert er.aggregate == agg and er.all_zero == allz
+    per_d, energy_d = api.effective_rank_device(L, torch.cat(pays), D, rank, q, 0.5)
+    en = energy_d.cpu().numpy()
+    for x, e in zip(dense, en):
+        f = float(np.sum(x.astype(np.float64) ** 2))
+        assert abs(e - f) <= 1e-5 * f
 
 
 def test_errors_are_typed(ctx):
@@ -427,3 +435,22 @@ def test_outer_update_tensor_core_path(ctx, oracle, D, rank):
         st = res[tc][4]
         ce = oracle.measure_error(t, pend, ranks, codes[0], scales[0])
         assert abs(st[0] / st[1] - ce) <= 1e-4 * max(ce, 1e-12), tc
+
+
+def test_layouts_recreated_after_close(ctx, oracle):
+    """Derived per-plan state (tile tables, tensor maps) lives in the plan: closing a layout
+    and building a differently shaped one (allocator address reuse) must not pick up stale
+    tables."""
+    from paper_2506_21263_b200 import api
+    rank, q = 8, 4
+    for it, shapes in enumerate([[(300, 64), (64,)], [(96, 128), (128,), (40, 36)],
+                                 [(300, 64), (64,)], [(64, 256), (512, 32)]]):
+        t = Table(shapes)
+        L = mk(ctx, shapes)
+        flat = oracle.gaussian(oracle.stream(it, 3), t.numel())[0]
+        st = oracle.stream(5, it)
+        res = api.compress(L, L.pack(flat), rank, api.QuantSpec(q, 0), None, 0, 2, st)
+        ref = oracle.compress(t, flat, rank, q, 0, 2, st)
+        ca, _ = decode_payload(L, res.payload, rank, q)
+        assert (ca == ref["codes"]).mean() >= 0.99, it
+        L.close()
