@@ -140,6 +140,17 @@ dlx_status dlx_outer_update(dlx_ctx* ctx, const dlx_layout* layout, int rank, in
                             float* d_velocity, float gamma, float beta, int classical,
                             dlx_round_stats* d_stats, void* stream);
 
+/* dlx_outer_update restricted to the layout tensors [t_begin, t_end) (all state buffers are
+ * still full slabs; only that range is read and written). d_stats is zeroed only when
+ * t_begin == 0, so consecutive ranges accumulate one round's statistics — the host pipeline
+ * (OuterSync.step_host) updates each range as soon as its H2D copy has landed. */
+dlx_status dlx_outer_update_range(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
+                                  int D, const uint8_t* d_gathered, int self_index, int mode,
+                                  float* d_pending, float* d_anchor, const float* d_local,
+                                  float* d_velocity, float gamma, float beta, int classical,
+                                  dlx_round_stats* d_stats, int t_begin, int t_end,
+                                  void* stream);
+
 /* stage_deltas (engine.cpp:266-276): pending <- (anchor - local) + (d_err ? d_err : 0).
  * d_err may alias d_pending. d_norm_sq (nullable device double) gets ||pending||^2. */
 dlx_status dlx_stage_deltas(dlx_ctx* ctx, const dlx_layout* layout, const float* d_anchor,

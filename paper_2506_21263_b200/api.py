@@ -293,13 +293,21 @@ def outer_update(layout: Layout, gathered: torch.Tensor, D: int, rank: int, qbit
                  pending: torch.Tensor, anchor: torch.Tensor, local: torch.Tensor | None,
                  velocity: torch.Tensor, gamma: float, beta: float, classical: bool = False,
                  mode: int = OVERLAPPED, self_index: int = -1, stats: torch.Tensor | None = None,
-                 stream=None):
+                 stream=None, tensors: tuple[int, int] | None = None):
     """Fused reconstruct + error feedback + stage + Nesterov (engine.cpp:254-276,
-    optim.cpp:56-78). stats: device float64[8] (dlx_round_stats) or None."""
-    check(lib().dlx_outer_update(layout.ctx.h, layout.h, rank, qbits, D, _ptr(gathered),
-                                 self_index, mode, _ptr(pending), _ptr(anchor), _ptr(local),
-                                 _ptr(velocity), gamma, beta, int(classical), _ptr(stats),
-                                 _stream(stream)))
+    optim.cpp:56-78). stats: device float64[8] (dlx_round_stats) or None. tensors=(t0, t1)
+    restricts the update to layout tensors [t0, t1) (stats zeroed only when t0 == 0)."""
+    if tensors is None:
+        check(lib().dlx_outer_update(layout.ctx.h, layout.h, rank, qbits, D, _ptr(gathered),
+                                     self_index, mode, _ptr(pending), _ptr(anchor), _ptr(local),
+                                     _ptr(velocity), gamma, beta, int(classical), _ptr(stats),
+                                     _stream(stream)))
+    else:
+        check(lib().dlx_outer_update_range(layout.ctx.h, layout.h, rank, qbits, D, _ptr(gathered),
+                                           self_index, mode, _ptr(pending), _ptr(anchor),
+                                           _ptr(local), _ptr(velocity), gamma, beta,
+                                           int(classical), _ptr(stats), int(tensors[0]),
+                                           int(tensors[1]), _stream(stream)))
 
 
 def stage_deltas(layout: Layout, anchor, local, err, pending, norm_sq=None, stream=None):

@@ -621,11 +621,12 @@ dlx_status dlx_allreduce_avg(dlx_ctx* ctx, const dlx_layout* layout, int rank, i
   });
 }
 
-dlx_status dlx_outer_update(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits, int D,
-                            const uint8_t* d_gathered, int self_index, int mode,
-                            float* d_pending, float* d_anchor, const float* d_local,
-                            float* d_velocity, float gamma, float beta, int classical,
-                            dlx_round_stats* d_stats, void* stream) {
+dlx_status dlx_outer_update_range(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
+                                  int D, const uint8_t* d_gathered, int self_index, int mode,
+                                  float* d_pending, float* d_anchor, const float* d_local,
+                                  float* d_velocity, float gamma, float beta, int classical,
+                                  dlx_round_stats* d_stats, int t_begin, int t_end,
+                                  void* stream) {
   return guard([&] {
     set_device(ctx);
     validate_quant(rank, qbits);
@@ -637,12 +638,25 @@ dlx_status dlx_outer_update(dlx_ctx* ctx, const dlx_layout* layout, int rank, in
       raise(DLX_ERR_VALIDATION, "overlapped mode needs the local parameters");
     Plan& P = const_cast<dlx_layout*>(layout)->plan(rank, qbits);
     cudaStream_t s = as_stream(stream);
-    if (d_stats) DLX_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(dlx_round_stats), s));
+    if (t_begin < 0 || t_end > layout->nt || t_begin > t_end)
+      raise(DLX_ERR_VALIDATION, "outer_update: tensor range out of bounds");
+    const SlotRange R = slot_range(P, t_begin, t_end);
+    if (d_stats && t_begin == 0) DLX_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(dlx_round_stats), s));
     launch_outer_2d(ctx, P, D, d_gathered, self_index, mode, d_pending, d_anchor, d_local,
-                    d_velocity, gamma, beta, classical, d_stats, s);
+                    d_velocity, gamma, beta, classical, d_stats, R, s);
     launch_outer_1d(P, D, d_gathered, self_index, mode, d_pending, d_anchor, d_local,
-                    d_velocity, gamma, beta, classical, d_stats, s);
+                    d_velocity, gamma, beta, classical, d_stats, R, s);
   });
+}
+
+dlx_status dlx_outer_update(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits, int D,
+                            const uint8_t* d_gathered, int self_index, int mode,
+                            float* d_pending, float* d_anchor, const float* d_local,
+                            float* d_velocity, float gamma, float beta, int classical,
+                            dlx_round_stats* d_stats, void* stream) {
+  return dlx_outer_update_range(ctx, layout, rank, qbits, D, d_gathered, self_index, mode,
+                                d_pending, d_anchor, d_local, d_velocity, gamma, beta, classical,
+                                d_stats, 0, layout ? layout->nt : 0, stream);
 }
 
 dlx_status dlx_stage_deltas(dlx_ctx* ctx, const dlx_layout* layout, const float* d_anchor,

@@ -245,14 +245,29 @@ void quantize_all(dlx_ctx* ctx, const Plan& P, const float* pbuf, const float* q
                   int* d_mismatch, int64_t* d_cold_base_actual, cudaStream_t s);
 void dequant_factors(const Plan& P, int D, const uint8_t* gathered, int64_t pay_bytes,
                      float* phat, float* qhat, int64_t lda_tot, cudaStream_t s);
+// Slot ranges of one outer-update call: 2-D slots [s0, s1), 1-D slots [u0, u1) (the tensors
+// of a layout index range; the whole layout by default).
+struct SlotRange {
+  int s0 = 0, s1 = 0, u0 = 0, u1 = 0;
+  bool full(const Plan& P) const {
+    return s0 == 0 && s1 == static_cast<int>(P.t2.size()) && u0 == 0 &&
+           u1 == static_cast<int>(P.t1.size());
+  }
+  std::string key() const {
+    return std::to_string(s0) + ":" + std::to_string(s1) + ":" + std::to_string(u0) + ":" +
+           std::to_string(u1);
+  }
+};
+SlotRange slot_range(const Plan& P, int t_begin, int t_end);
+
 void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                      int self_index, int mode, float* pending, float* anchor,
                      const float* local, float* velocity, float gamma, float beta,
-                     int classical, dlx_round_stats* stats, cudaStream_t s);
+                     int classical, dlx_round_stats* stats, const SlotRange& R, cudaStream_t s);
 void launch_outer_1d(const Plan& P, int D, const uint8_t* gathered, int self_index, int mode,
                      float* pending, float* anchor, const float* local, float* velocity,
                      float gamma, float beta, int classical, dlx_round_stats* stats,
-                     cudaStream_t s);
+                     const SlotRange& R, cudaStream_t s);
 void launch_reconstruct_dense(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                               float* out, cudaStream_t s);
 void launch_stage(const dlx_layout& L, const float* anchor, const float* local,

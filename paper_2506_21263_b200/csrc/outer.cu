@@ -499,7 +499,34 @@ bool o5_eligible(const Plan& P, int D, int self_index);
 void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                         int self_index, int mode, float* pending, float* anchor,
                         const float* local, float* velocity, float gamma, float beta,
-                        int classical, dlx_round_stats* stats, cudaStream_t s);
+                        int classical, dlx_round_stats* stats, const SlotRange& R,
+                        cudaStream_t s);
+
+SlotRange slot_range(const Plan& P, int t_begin, int t_end) {
+  SlotRange R;
+  auto lo2 = [&](int t) {
+    int k = 0;
+    while (k < static_cast<int>(P.t2.size()) && P.t2[k].idx < t) ++k;
+    return k;
+  };
+  auto lo1 = [&](int t) {
+    int k = 0;
+    while (k < static_cast<int>(P.t1.size()) && P.t1[k].idx < t) ++k;
+    return k;
+  };
+  R.s0 = lo2(t_begin);
+  R.s1 = lo2(t_end);
+  R.u0 = lo1(t_begin);
+  R.u1 = lo1(t_end);
+  return R;
+}
+
+// SIMT K5 tiles of a slot range (the plan's full lists when the range is the whole layout)
+struct K5RangeTiles : PlanExt {
+  std::vector<int4> k5s, k5;
+  int4* d_k5s = nullptr;
+  int4* d_k5 = nullptr;
+};
 
 bool& option_outer_tc() {
   static bool on = [] {
@@ -512,17 +539,38 @@ bool& option_outer_tc() {
 void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                      int self_index, int mode, float* pending, float* anchor,
                      const float* local, float* velocity, float gamma, float beta,
-                     int classical, dlx_round_stats* stats, cudaStream_t s) {
-  if (P.t2.empty()) return;
+                     int classical, dlx_round_stats* stats, const SlotRange& R,
+                     cudaStream_t s) {
+  if (P.t2.empty() || R.s1 <= R.s0) return;
   if (option_outer_tc() && o5_eligible(P, D, self_index)) {
     launch_outer_2d_tc(ctx, P, D, gathered, self_index, mode, pending, anchor, local, velocity,
-                       gamma, beta, classical, stats, s);
+                       gamma, beta, classical, stats, R, s);
     return;
+  }
+  const std::vector<int4>* k5s_tiles = &P.k5s_tiles;
+  const std::vector<int4>* k5_tiles = &P.k5_tiles;
+  const int4* d_k5s_tiles = P.d_k5s_tiles;
+  const int4* d_k5_tiles = P.d_k5_tiles;
+  if (!R.full(P)) {
+    bool fresh = false;
+    K5RangeTiles& T = plan_ext<K5RangeTiles>(P, "k5_range:" + R.key(), &fresh);
+    if (fresh) {
+      for (const int4& t : P.k5s_tiles)
+        if (t.x >= R.s0 && t.x < R.s1) T.k5s.push_back(t);
+      for (const int4& t : P.k5_tiles)
+        if (t.x >= R.s0 && t.x < R.s1) T.k5.push_back(t);
+      T.d_k5s = plan_upload(P, T.k5s);
+      T.d_k5 = plan_upload(P, T.k5);
+    }
+    k5s_tiles = &T.k5s;
+    k5_tiles = &T.k5;
+    d_k5s_tiles = T.d_k5s;
+    d_k5_tiles = T.d_k5;
   }
   float* phat = static_cast<float*>(ctx->scratch("phat", sizeof(float) * P.pelems * D));
   float* qhat = static_cast<float*>(ctx->scratch("qhat", sizeof(float) * P.qelems * D));
   dequant_factors(P, D, gathered, P.payload_bytes, phat, qhat, 0, s);
-  if (!P.k5s_tiles.empty()) {
+  if (!k5s_tiles->empty()) {
     static bool attr = false;
     if (!attr) {
       DLX_CUDA(cudaFuncSetAttribute(k5s_outer<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5s_smem()));
@@ -532,28 +580,28 @@ void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered
     int sms = 0, dev = 0;
     DLX_CUDA(cudaGetDevice(&dev));
     DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int n = static_cast<int>(P.k5s_tiles.size());
+    const int n = static_cast<int>(k5s_tiles->size());
     const int grid = std::min(n, sms);
     const K5Maps* maps = k5_maps(P, D, pending, anchor, velocity,
                                  mode == DLX_MODE_OVERLAPPED ? local : nullptr, phat, s);
     const int ps_tma = D * P.rmax <= 32 ? 1 : 0;
     if (self_index >= 0)
-      k5s_outer<true><<<grid, 288, k5s_smem(), s>>>(P.d_t2, maps, P.d_k5s_tiles, n, phat, qhat, D,
+      k5s_outer<true><<<grid, 288, k5s_smem(), s>>>(P.d_t2, maps, d_k5s_tiles, n, phat, qhat, D,
                                                     self_index, mode, ps_tma, pending, anchor, local,
                                                     velocity, gamma, beta, classical, stats);
     else
-      k5s_outer<false><<<grid, 288, k5s_smem(), s>>>(P.d_t2, maps, P.d_k5s_tiles, n, phat, qhat, D,
+      k5s_outer<false><<<grid, 288, k5s_smem(), s>>>(P.d_t2, maps, d_k5s_tiles, n, phat, qhat, D,
                                                      self_index, mode, ps_tma, pending, anchor, local,
                                                      velocity, gamma, beta, classical, stats);
     DLX_LAUNCHED();
   }
-  if (!P.k5_tiles.empty()) {
+  if (!k5_tiles->empty()) {
     if (self_index >= 0)
-      k5_outer<true><<<P.k5_tiles.size(), 256, 0, s>>>(P.d_t2, P.d_k5_tiles, phat, qhat, D,
+      k5_outer<true><<<k5_tiles->size(), 256, 0, s>>>(P.d_t2, d_k5_tiles, phat, qhat, D,
                                                        self_index, mode, pending, anchor, local,
                                                        velocity, gamma, beta, classical, stats);
     else
-      k5_outer<false><<<P.k5_tiles.size(), 256, 0, s>>>(P.d_t2, P.d_k5_tiles, phat, qhat, D,
+      k5_outer<false><<<k5_tiles->size(), 256, 0, s>>>(P.d_t2, d_k5_tiles, phat, qhat, D,
                                                         self_index, mode, pending, anchor, local,
                                                         velocity, gamma, beta, classical, stats);
     DLX_LAUNCHED();
@@ -646,17 +694,17 @@ __global__ void __launch_bounds__(256) k_outer_1d(const DevT1* __restrict__ T,
 void launch_outer_1d(const Plan& P, int D, const uint8_t* gathered, int self_index, int mode,
                      float* pending, float* anchor, const float* local, float* velocity,
                      float gamma, float beta, int classical, dlx_round_stats* stats,
-                     cudaStream_t s) {
-  if (P.t1.empty()) return;
+                     const SlotRange& R, cudaStream_t s) {
+  if (P.t1.empty() || R.u1 <= R.u0) return;
   struct Chunks1d : PlanExt {
     int2* d = nullptr;
     int n = 0;
   };
   bool fresh = false;
-  Chunks1d& tb = plan_ext<Chunks1d>(P, "outer_1d", &fresh);
+  Chunks1d& tb = plan_ext<Chunks1d>(P, "outer_1d:" + R.key(), &fresh);
   if (fresh) {
     std::vector<int2> ch;
-    for (size_t i = 0; i < P.t1.size(); ++i)
+    for (size_t i = R.u0; i < static_cast<size_t>(R.u1); ++i)
       for (int64_t k = 0; k < P.t1[i].n; k += kOuter1dElems)
         ch.push_back(make_int2(static_cast<int>(i), static_cast<int>(k)));
     tb.d = plan_upload(P, ch);

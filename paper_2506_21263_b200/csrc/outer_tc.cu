@@ -395,6 +395,7 @@ struct O5State : PlanExt {
   std::vector<int64_t> aoff, boff;  // per slot: element offsets of A [lda][KA], B [ldb][KA]
   int64_t a_elems = 0, b_elems = 0;
   int64_t params = 0;  // 2-D parameters covered
+  int s0 = 0, s1 = 0;  // slot range
   int64_t* d_aoff = nullptr;
   int64_t* d_boff = nullptr;
   O5Maps* d_maps = nullptr;
@@ -414,23 +415,29 @@ bool o5_eligible(const Plan& P, int D, int self_index) {
   return true;
 }
 
-static O5State& o5_state(const Plan& P, int D) {
+static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   bool fresh = false;
-  O5State& S = plan_ext<O5State>(P, "o5:" + std::to_string(D), &fresh);
+  O5State& S = plan_ext<O5State>(P, "o5:" + std::to_string(D) + ":" + R.key(), &fresh);
   if (!fresh) return S;
   S.D = D;
   S.KA = static_cast<int>(round_up(D * P.rmax, 32));
-  // tiles: per tensor, row band (128) major, then 32-column blocks; balanced contiguous chunks
+  S.s0 = R.s0;
+  S.s1 = R.s1;
+  // tiles: per tensor, row band (128) major, then 32-column blocks; balanced contiguous chunks.
+  // A / B staging offsets cover every slot (shared buffers); tiles and rows only the range.
   for (size_t k = 0; k < P.t2.size(); ++k) {
     const DevT2& t = P.t2[k];
-    for (int64_t m0 = 0; m0 < t.a; m0 += 128)
-      for (int64_t n0 = 0; n0 < t.b; n0 += 32)
-        S.tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0), static_cast<int>(n0), 0));
-    for (int side = 0; side < 2; ++side) {
-      const int64_t ld = side == 0 ? t.lda : t.ldb;
-      for (int64_t r = 0; r < ld; ++r) S.rows.push_back(make_int4(static_cast<int>(k), side, static_cast<int>(r), 0));
+    const bool in = static_cast<int>(k) >= R.s0 && static_cast<int>(k) < R.s1;
+    if (in) {
+      for (int64_t m0 = 0; m0 < t.a; m0 += 128)
+        for (int64_t n0 = 0; n0 < t.b; n0 += 32)
+          S.tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0), static_cast<int>(n0), 0));
+      for (int side = 0; side < 2; ++side) {
+        const int64_t ld = side == 0 ? t.lda : t.ldb;
+        for (int64_t r = 0; r < ld; ++r) S.rows.push_back(make_int4(static_cast<int>(k), side, static_cast<int>(r), 0));
+      }
+      S.params += t.a * t.b;
     }
-    S.params += t.a * t.b;
     S.aoff.push_back(S.a_elems);
     S.boff.push_back(S.b_elems);
     S.a_elems += t.lda * S.KA;
@@ -455,8 +462,10 @@ static O5State& o5_state(const Plan& P, int D) {
 void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                         int self_index, int mode, float* pending, float* anchor,
                         const float* local, float* velocity, float gamma, float beta,
-                        int classical, dlx_round_stats* stats, cudaStream_t s) {
-  O5State& S = o5_state(P, D);
+                        int classical, dlx_round_stats* stats, const SlotRange& R,
+                        cudaStream_t s) {
+  O5State& S = o5_state(P, D, R);
+  if (S.tiles.empty()) return;
   const int KA = S.KA;
   float* A = static_cast<float*>(ctx->scratch("o5_A", sizeof(float) * (S.a_elems + 1024)));
   float* Bh = static_cast<float*>(ctx->scratch("o5_Bh", sizeof(float) * (S.b_elems + 1024)));
@@ -467,7 +476,7 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   DLX_LAUNCHED();
   const void* key[7] = {pending, anchor, velocity, mode == DLX_MODE_OVERLAPPED ? local : nullptr, A, Bh, Bl};
   if (!std::equal(key, key + 7, S.key)) {
-    for (size_t k = 0; k < P.t2.size(); ++k) {
+    for (size_t k = S.s0; k < static_cast<size_t>(S.s1); ++k) {
       const DevT2& t = P.t2[k];
       O5Maps& m = S.h_maps[k];
       std::memset(&m, 0, sizeof(m));

@@ -125,6 +125,9 @@ class OuterSync:
         self._dev_local = None
         self._d2h_ev = None
         self._pre_update: list = []  # events the next read of local / write of anchor waits on
+        self._host_job = None        # per-step chunk schedule while step_host runs
+        self.host_chunks = 8         # tensor groups of the chunked host pipeline
+        self._groups = None
 
     def _wait_pre_update(self):
         cur = torch.cuda.current_stream()
@@ -194,11 +197,7 @@ class OuterSync:
                 self.energy_host.copy_(energy, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(side)
-        self._wait_pre_update()
-        api.outer_update(L, gathered, self.world, r, q, self.pending, self.anchor, local,
-                         self.velocity, cfg.outer_lr, cfg.outer_momentum, cfg.outer_classical,
-                         mode=mode, self_index=self.rank if cfg.measure_error else -1,
-                         stats=self.stats, stream=cur)
+        self._outer_update(gathered, r, q, local, mode, cur)
         self._ev("end")
         self.stats_host.copy_(self.stats, non_blocking=True)
         rec = RoundRecord(round=self.round, r_t=r, H_t=self.H_t, averaged=True,
@@ -211,6 +210,38 @@ class OuterSync:
             cur.wait_stream(self.side or cur)
         self.warm_rank = r
         return rec
+
+    def _outer_update(self, gathered, r: int, q: int, local, mode: int, cur):
+        cfg, L = self.cfg, self.L
+        kw = dict(mode=mode, self_index=self.rank if cfg.measure_error else -1,
+                  stats=self.stats, stream=cur)
+        job = self._host_job
+        if job is None:
+            self._wait_pre_update()
+            api.outer_update(L, gathered, self.world, r, q, self.pending, self.anchor, local,
+                             self.velocity, cfg.outer_lr, cfg.outer_momentum,
+                             cfg.outer_classical, **kw)
+            return
+        # chunked host pipeline: each tensor group is updated as soon as its H2D copy has
+        # landed, and its new anchor starts back to the host right after
+        for e in job["prev"]:
+            cur.wait_event(e)
+        self._pre_update = []
+        for (t0, t1, e0, e1), ev in zip(self._groups, job["h2d"]):
+            cur.wait_event(ev)
+            api.outer_update(L, gathered, self.world, r, q, self.pending, self.anchor, local,
+                             self.velocity, cfg.outer_lr, cfg.outer_momentum,
+                             cfg.outer_classical, tensors=(t0, t1), **kw)
+            if job["out"] is not None:
+                ue = torch.cuda.Event()
+                ue.record(cur)
+                self._d2h.wait_event(ue)
+                with torch.cuda.stream(self._d2h):
+                    job["out"][e0:e1].copy_(self.anchor[e0:e1], non_blocking=True)
+        if job["out"] is not None:
+            self._d2h_ev = torch.cuda.Event()
+            self._d2h_ev.record(self._d2h)
+        job["done"] = True
 
     def _finish(self, rec: RoundRecord, mode: int) -> RoundRecord:
         torch.cuda.current_stream().synchronize()
@@ -285,28 +316,55 @@ class OuterSync:
     def step(self, local: torch.Tensor) -> RoundRecord:
         return self.round_overlapped(local) if self.cfg.overlap else self.round_sync(local)
 
+    def _host_groups(self):
+        """Contiguous tensor groups of ~equal slab size: (t0, t1, e0, e1) with slab element
+        range [e0, e1) (the last group runs to the end of the slab)."""
+        if self._groups is None:
+            L = self.L
+            nt = len(L.shapes)
+            target = L.slab_elems / max(1, self.host_chunks)
+            groups, t0 = [], 0
+            for t in range(1, nt + 1):
+                end = int(L.offsets[t]) if t < nt else L.slab_elems
+                if t == nt or end - int(L.offsets[t0]) >= target:
+                    groups.append((t0, t, int(L.offsets[t0]) if t0 else 0, end))
+                    t0 = t
+            self._groups = groups
+        return self._groups
+
     def step_host(self, h_local: torch.Tensor, h_anchor_out: torch.Tensor | None = None
                   ) -> RoundRecord:
         """One round with the worker's local parameters in (pinned) host memory — the
-        drop-in call a host-resident reference engine makes. The H2D copy of `h_local` runs
-        on a copy stream concurrently with compress (overlapped mode reads local only in the
-        fused outer update); the new anchor is copied into `h_anchor_out` on a second copy
-        stream that overlaps the next round's compress. host_wait() orders the caller's
-        stream after the last D2H."""
+        drop-in call a host-resident reference engine makes. The local parameters go to the
+        device in tensor groups on a copy stream while compress runs (overlapped mode reads
+        local only in the fused outer update); each group's outer update starts as soon as
+        its copy has landed, and its new anchor goes back to `h_anchor_out` on a second copy
+        stream right after, overlapping the remaining copies and the next round. host_wait()
+        orders the caller's stream after the last D2H."""
         dev = self.anchor.device
         if self._h2d is None:
             self._h2d = torch.cuda.Stream(device=dev)
             self._d2h = torch.cuda.Stream(device=dev)
             self._dev_local = torch.empty_like(self.anchor)
+        groups = self._host_groups()
         cur = torch.cuda.current_stream()
         self._h2d.wait_stream(cur)  # the previous round's reads of the staging buffer
+        evs = []
         with torch.cuda.stream(self._h2d):
-            self._dev_local.copy_(h_local, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(self._h2d)
-        self._pre_update = [ev] + ([self._d2h_ev] if self._d2h_ev is not None else [])
-        rec = self.step(self._dev_local)
-        if h_anchor_out is not None:
+            for _, _, e0, e1 in groups:
+                self._dev_local[e0:e1].copy_(h_local[e0:e1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self._h2d)
+                evs.append(ev)
+        prev = [self._d2h_ev] if self._d2h_ev is not None else []
+        self._pre_update = evs + prev  # for the un-chunked paths (staging round, sync mode)
+        job = {"h2d": evs, "prev": prev, "out": h_anchor_out, "done": False}
+        self._host_job = job if self.cfg.overlap else None
+        try:
+            rec = self.step(self._dev_local)
+        finally:
+            self._host_job = None
+        if h_anchor_out is not None and not job["done"]:
             self._d2h.wait_stream(cur)
             with torch.cuda.stream(self._d2h):
                 h_anchor_out.copy_(self.anchor, non_blocking=True)
