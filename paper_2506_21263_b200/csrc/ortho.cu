@@ -164,6 +164,82 @@ __global__ void __launch_bounds__(256) k_gram(const DevMat* __restrict__ mats,
   }
 }
 
+// r <= 32 fast path on the fp64 tensor cores (mma.sync m8n8k4 f64, DMMA): 64-row tiles of
+// Y staged once as fp64 in shared memory, next tile prefetched into registers; warp w owns
+// one 8x8 block (ci <= cj) of the upper block triangle of G = Y^T Y and accumulates it over
+// every 4-row k step (A = Y^T block, B = Y block: the same fragment shape).
+constexpr int kGdRows = 64;
+constexpr int kGdLd = kGdRows + 4;  // [col][row] stride: conflict-free fragment loads
+
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(320) k_gram_dmma(const DevMat* __restrict__ mats,
+                                                   const int4* __restrict__ splits,
+                                                   const float* __restrict__ buf, int rr,
+                                                   double* __restrict__ partial,
+                                                   const int* __restrict__ only) {
+  __shared__ double Ys[32 * kGdLd];
+  const int4 sp = splits[blockIdx.x];
+  if (only && !only[sp.x]) return;
+  const DevMat m = mats[sp.x];
+  const int nb = (m.r + 7) / 8, nblk = nb * (nb + 1) / 2;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int ci = 0, cj = 0;
+  {
+    int rem = warp;
+    while (ci < nb && rem >= nb - ci) {
+      rem -= nb - ci;
+      ++ci;
+    }
+    cj = ci + rem;
+  }
+  const bool active = warp < nblk;
+  double acc[2] = {0.0, 0.0};
+  const float* Y = buf + m.off;
+  const int cols = nb * 8;
+  const int per = (cols * kGdRows + 319) / 320;  // staged elements per thread (<= 7)
+  float pre[7];
+  auto fetch = [&](int r0) {
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      const int e = threadIdx.x + 320 * i;
+      const int c = e / kGdRows, rl = e % kGdRows;
+      const int row = r0 + rl;
+      pre[i] = (i < per && c < m.r && row < sp.z) ? __ldg(&Y[(int64_t)c * m.ld + row]) : 0.f;
+    }
+  };
+  fetch(sp.y);
+  for (int r0 = sp.y; r0 < sp.z; r0 += kGdRows) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      const int e = threadIdx.x + 320 * i;
+      if (i < per && e < cols * kGdRows) Ys[(e / kGdRows) * kGdLd + e % kGdRows] = (double)pre[i];
+    }
+    __syncthreads();
+    if (r0 + kGdRows < sp.z) fetch(r0 + kGdRows);
+    if (active) {
+      const double* pa = Ys + (ci * 8 + lane / 4) * kGdLd + lane % 4;
+      const double* pb = Ys + (cj * 8 + lane / 4) * kGdLd + lane % 4;
+#pragma unroll 4
+      for (int k = 0; k < kGdRows; k += 4) dmma_8x8x4(acc, pa[k], pb[k]);
+    }
+  }
+  if (active) {
+    double* out = partial + (int64_t)sp.w * rr * rr;
+    const int gj = ci * 8 + lane / 4;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int gk = cj * 8 + 2 * (lane % 4) + q;
+      if (gj < m.r && gk < m.r && gj <= gk) out[gj * rr + gk] = acc[q];
+    }
+  }
+}
+
 static size_t gram_smem(int rmax) {
   const int rpad = (rmax + 3) / 4 * 4;
   return std::max<size_t>(sizeof(float) * rpad * (kGramRows + 1), sizeof(double) * 16 * 256);
@@ -171,6 +247,11 @@ static size_t gram_smem(int rmax) {
 
 static void launch_gram(const GramJob& J, const float* buf, double* partial, cudaStream_t s,
                         const int* only = nullptr) {
+  if (J.rmax <= 32) {
+    k_gram_dmma<<<J.splits.size(), 320, 0, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial, only);
+    DLX_LAUNCHED();
+    return;
+  }
   const int nb = (J.rmax + 3) / 4, nblk = nb * (nb + 1) / 2;
   const int gy = nblk >= 256 ? (nblk + 255) / 256 : 1;
   const size_t sm = gram_smem(J.rmax);
@@ -355,6 +436,90 @@ __global__ void __launch_bounds__(128) k_apply(const DevMat* __restrict__ mats,
   }
 }
 
+// r <= 32 fast path on DMMA: Y <- Y R^-1 for one 128-row tile. The tile (fp64, [row][k])
+// and R^-1 (upper, zero-padded) are staged in shared memory; warp w owns rows
+// [32 w, 32 w + 32) = four 8-row blocks, and column block cj only needs the k steps
+// k < 8 (cj + 1) (triangular).
+constexpr int kAdLdY = 36;  // [row][k] stride: conflict-free A fragments
+constexpr int kAdLdR = 40;  // [k][col] stride: conflict-free B fragments
+
+__global__ void __launch_bounds__(128) k_apply_dmma(const DevMat* __restrict__ mats,
+                                                    const int4* __restrict__ jobs, int njobs,
+                                                    int per_cta, int rr,
+                                                    const double* __restrict__ rinv,
+                                                    const int* __restrict__ skip,
+                                                    const int* __restrict__ only,
+                                                    float* __restrict__ buf) {
+  // A run of consecutive 128-row tiles per CTA: the next tile's rows are loaded into
+  // registers while the current one is multiplied; R^-1 is restaged only when the tile
+  // run crosses into another factor.
+  __shared__ __align__(16) double Ys[128 * kAdLdY];
+  __shared__ double Rs[32 * kAdLdR];
+  const int j0 = blockIdx.x * per_cta, j1 = min(njobs, j0 + per_cta);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  auto live_job = [&](int j) {
+    const int e = jobs[j].x;
+    return !skip[e] && !(only && !only[e]);
+  };
+  float v[32];
+  auto fetch = [&](int j) {
+    const int4 jb = jobs[j];
+    const DevMat& m = mats[jb.x];
+    const int64_t row = jb.y + threadIdx.x;
+    const bool live = row < m.n;
+    const float* Y = buf + m.off;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = (k < m.r && live) ? Y[(int64_t)k * m.ld + row] : 0.f;
+  };
+  int cur = -1;
+  int j = j0;
+  while (j < j1 && !live_job(j)) ++j;
+  if (j < j1) fetch(j);
+  while (j < j1) {
+    const int4 jb = jobs[j];
+    const DevMat m = mats[jb.x];
+    const int r = m.r, nb = (r + 7) / 8;
+    __syncthreads();  // previous tile's fragments consumed
+    if (jb.x != cur) {
+      const double* X = rinv + (int64_t)jb.x * rr * rr;
+      for (int idx = threadIdx.x; idx < 32 * 32; idx += 128) {
+        const int k = idx / 32, c = idx % 32;
+        Rs[k * kAdLdR + c] = (k < r && c < r && k <= c) ? X[k * rr + c] : 0.0;
+      }
+      cur = jb.x;
+    }
+    {
+      double* dst = Ys + threadIdx.x * kAdLdY;
+#pragma unroll
+      for (int k = 0; k < 32; k += 2) *reinterpret_cast<double2*>(dst + k) = make_double2(v[k], v[k + 1]);
+    }
+    __syncthreads();
+    int jn = j + 1;
+    while (jn < j1 && !live_job(jn)) ++jn;
+    if (jn < j1) fetch(jn);
+    float* Y = buf + m.off;
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) {
+      const int rl = warp * 32 + rb * 8;  // first tile row of this 8-row block
+      const double* pa = Ys + (rl + lane / 4) * kAdLdY + lane % 4;
+      for (int cj = 0; cj < nb; ++cj) {
+        double acc[2] = {0.0, 0.0};
+        const double* pb = Rs + (lane % 4) * kAdLdR + cj * 8 + lane / 4;
+        for (int k = 0; k < 8 * (cj + 1); k += 4) dmma_8x8x4(acc, pa[k], pb[k * kAdLdR]);
+        const int64_t row = jb.y + rl + lane / 4;
+        if (row < m.n) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int col = cj * 8 + 2 * (lane % 4) + q;
+            if (col < r) Y[(int64_t)col * m.ld + row] = (float)acc[q];
+          }
+        }
+      }
+    }
+    j = jn;
+  }
+}
+
 // ------------------------------------------------------------------ exact MGS2 fallback
 __global__ void __launch_bounds__(1024) k_mgs_fallback(const DevMat* __restrict__ mats,
                                                        const int* __restrict__ flags,
@@ -414,6 +579,19 @@ __global__ void __launch_bounds__(1024) k_mgs_fallback(const DevMat* __restrict_
 // ------------------------------------------------------------------ driver
 static size_t apply_smem(int rmax) { return 32 * 33 * sizeof(double) + sizeof(float) * rmax * 129; }
 
+static void launch_apply(const GramJob& J, int rr, const double* rinv, const int* skip,
+                         const int* only, float* buf, size_t asm_, cudaStream_t s) {
+  if (rr <= 32) {
+    const int nj = static_cast<int>(J.apply.size());
+    const int per = std::max(1, (nj + 4 * 148 - 1) / (4 * 148));
+    k_apply_dmma<<<(nj + per - 1) / per, 128, 0, s>>>(J.d_mats, J.d_apply, nj, per, rr, rinv, skip,
+                                                      only, buf);
+  }
+  else
+    k_apply<<<J.apply.size(), 128, asm_, s>>>(J.d_mats, J.d_apply, rr, rinv, skip, only, buf);
+  DLX_LAUNCHED();
+}
+
 static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* /*tmp*/, const std::string& tag,
                     int64_t buf_elems, cudaStream_t s) {
   const int rr = J.rmax;
@@ -437,15 +615,13 @@ static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* /*tmp*/, const 
   k_chol<<<ne, 256, csm, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags1,
                               need2, nullptr);
   DLX_LAUNCHED();
-  k_apply<<<J.apply.size(), 128, asm_, s>>>(J.d_mats, J.d_apply, rr, rinv, flags1, nullptr, buf);
-  DLX_LAUNCHED();
+  launch_apply(J, rr, rinv, flags1, nullptr, buf, asm_, s);
   // pass 2 only for factors whose conditioning needs it (need2), in place
   launch_gram(J, buf, partial, s, need2);
   k_chol<<<ne, 256, csm, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags2,
                               nullptr, need2);
   DLX_LAUNCHED();
-  k_apply<<<J.apply.size(), 128, asm_, s>>>(J.d_mats, J.d_apply, rr, rinv, flags2, need2, buf);
-  DLX_LAUNCHED();
+  launch_apply(J, rr, rinv, flags2, need2, buf, asm_, s);
   // exact MGS2 for flagged entries (pass-1 flags: buf still holds their input)
   auto* dscr = static_cast<double*>(ctx->scratch("mgs_scratch", sizeof(double) * buf_elems));
   k_mgs_fallback<<<ne, 1024, 0, s>>>(J.d_mats, flags1, buf, dscr);

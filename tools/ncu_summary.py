@@ -54,11 +54,16 @@ def launches(path, out):
     rows = [r for r in csv.reader(open(path)) if len(r) > 14 and r[0].isdigit()]
     seq = [(re.sub(r"\(.*", "", r[4]).replace("void ", "").strip(), r[6], float(r[14]) / 1e3)
            for r in rows]
-    # one steady-state round = between the last two fused outer-update launches
-    o5 = [i for i, (n, _, _) in enumerate(seq) if n.startswith("dlx::k_o5<") or
-          n.startswith("dlx::k5")]
-    a, b = (o5[-3], o5[-2]) if len(o5) >= 3 else (0, len(seq) - 1)
-    rnd = seq[a + 1:b + 1]
+    # one steady-state round: from a quantiser launch (end of compress) to the next one,
+    # taking the last such segment with exactly one fused outer-update launch (the device-
+    # resident rounds; the host-pipeline rounds update in tensor groups)
+    qp = [i for i, (n, _, _) in enumerate(seq) if n.startswith("dlx::k_quant_pack")]
+    rnd = seq
+    for a, b in reversed(list(zip(qp, qp[1:]))):
+        seg = seq[a + 1:b + 1]
+        if sum(1 for n, _, _ in seg if n.startswith("dlx::k_o5<") or n.startswith("dlx::k5")) == 1:
+            rnd = seg
+            break
     agg = OrderedDict()
     for n, s, t in rnd:
         k = (n, s)
@@ -68,8 +73,9 @@ def launches(path, out):
     main = sum(t for n, s, t in rnd if s == rnd[-1][1])
     lines = [f"# Launch list of one steady-state round (`{path.split('/')[-1]}`)", "",
              "`ncu --metrics gpu__time_duration.sum --clock-control none` over "
-             "`bench.py --steps 2 --warmup 3`; launches between two consecutive fused outer "
-             "updates. Serialised and cold-cache: use the shares.", "",
+             "`bench.py --steps 2 --warmup 3`; launches from one round's quantiser to the next "
+             "(effective rank + outer update of round t, compress of round t+1). Serialised "
+             "and cold-cache: use the shares.", "",
              f"Sum of kernel times: {total:.1f} us ({main:.1f} us on the main stream).", "",
              "| kernel | stream | launches | total us | share |", "|---|---|---|---|---|"]
     for (n, s), (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
