@@ -384,6 +384,112 @@ __global__ void __launch_bounds__(256) k_chol(const DevMat* __restrict__ mats,
   }
 }
 
+// r <= 32 fast path: the partial Grams are folded by the whole CTA, then one warp factors
+// in registers — lane c holds column c of the (upper) matrix, the pivot row is broadcast
+// with shuffles, so a step costs no block barrier — and inverts R from shared memory (lane
+// c back-substitutes column c of R^-1). Same pivot test / flags / need2 as k_chol.
+__global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
+                                                const int* __restrict__ part0,
+                                                const int* __restrict__ nparts, int rr,
+                                                const double* __restrict__ partial,
+                                                double* __restrict__ rinv,
+                                                int* __restrict__ flags,
+                                                int* __restrict__ need2,
+                                                const int* __restrict__ only) {
+  __shared__ double G[32][33];
+  __shared__ double dinv[32];
+  const int e = blockIdx.x;
+  if (only && !only[e]) {
+    if (threadIdx.x == 0) {
+      flags[e] = 0;
+      if (need2) need2[e] = 0;
+    }
+    return;
+  }
+  const DevMat m = mats[e];
+  const int r = m.r;
+  const double* src = partial + (int64_t)part0[e] * rr * rr;
+  const int np = nparts[e];
+  // fold; columns >= r are padded with the identity so the factorisation below runs all 32
+  // steps without data-dependent branches
+  for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
+    const int j = idx / 32, k = idx % 32;
+    double g = (j == k && j >= r) ? 1.0 : 0.0;
+    if (j < r && k < r && k >= j)
+      for (int p = 0; p < np; ++p) g += src[(int64_t)p * rr * rr + j * rr + k];
+    G[j][k] = g;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int c = threadIdx.x;
+  double w[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) w[i] = (i <= c) ? G[i][c] : 0.0;  // column c, upper part
+  double mx = 0.0;
+  for (int j = 0; j < r; ++j) mx = fmax(mx, G[j][j]);
+  const double tol = 1e-7 * fmax(1.0, sqrt(mx));
+  const double thr = (10.0 * tol) * (10.0 * tol);
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double d = __shfl_sync(0xffffffffu, w[j], j);  // W[j][j] from lane j
+    bad |= !(d > thr);
+    const double rjj = sqrt(d);
+    const double inv = 1.0 / rjj;
+    if (c == j) {
+      w[j] = rjj;
+      dinv[j] = inv;
+    }
+    if (c > j) w[j] *= inv;  // R[j][c]
+#pragma unroll
+    for (int i = j + 1; i < 32; ++i) {  // W[i][c] -= R[j][i] R[j][c], j < i <= c
+      const double rji = __shfl_sync(0xffffffffu, w[j], i);
+      if (i <= c) w[i] = fma(-rji, w[j], w[i]);
+    }
+  }
+  const int flag = __any_sync(0xffffffffu, bad) ? 1 : 0;
+  if (c == 0) flags[e] = flag;
+  if (flag) {
+    if (need2 && c == 0) need2[e] = 0;
+    return;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) G[i][c] = (i <= c) ? w[i] : 0.0;  // R, upper
+  __syncwarp();
+  // X = R^-1: lane c solves R x = e_c by back substitution (rolled over i)
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (i == c) ? dinv[c] : 0.0;
+#pragma unroll
+  for (int i = 30; i >= 0; --i) {
+    double sum = 0.0;
+#pragma unroll
+    for (int k = i + 1; k < 32; ++k) sum = fma(G[i][k], x[k], sum);
+    if (i < c) x[i] = -sum * dinv[i];
+  }
+  double xf = 0.0, rf = 0.0;
+  if (c < r) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      xf = fma(x[i], x[i], xf);
+      rf = fma(G[i][c], G[i][c], rf);
+    }
+  }
+  double* X = rinv + (int64_t)e * rr * rr;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < r && c < r) X[i * rr + c] = x[i];
+  if (need2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      xf += __shfl_xor_sync(0xffffffffu, xf, o);
+      rf += __shfl_xor_sync(0xffffffffu, rf, o);
+    }
+    if (c == 0) need2[e] = (sqrt(xf) * sqrt(rf) > 2e3) ? 1 : 0;
+  }
+}
+
 // ------------------------------------------------------------------ apply: Y <- Y R^-1
 // One CTA per 128-row tile of a factor, all columns: the tile is staged in shared memory
 // first, so the update is in place. fp64 accumulation, R^-1 upper triangular.
@@ -592,6 +698,19 @@ static void launch_apply(const GramJob& J, int rr, const double* rinv, const int
   DLX_LAUNCHED();
 }
 
+static void launch_chol(const GramJob& J, int rr, const double* partial, double* work,
+                        double* rinv, int* flags, int* need2, const int* only, size_t csm,
+                        cudaStream_t s) {
+  const int ne = static_cast<int>(J.mats.size());
+  if (rr <= 32)
+    k_chol32<<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, rinv, flags, need2,
+                                only);
+  else
+    k_chol<<<ne, 256, csm, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags,
+                                need2, only);
+  DLX_LAUNCHED();
+}
+
 static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* /*tmp*/, const std::string& tag,
                     int64_t buf_elems, cudaStream_t s) {
   const int rr = J.rmax;
@@ -612,15 +731,11 @@ static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* /*tmp*/, const 
   const size_t asm_ = apply_smem(rr);
   // pass 1 (every factor), in place
   launch_gram(J, buf, partial, s);
-  k_chol<<<ne, 256, csm, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags1,
-                              need2, nullptr);
-  DLX_LAUNCHED();
+  launch_chol(J, rr, partial, work, rinv, flags1, need2, nullptr, csm, s);
   launch_apply(J, rr, rinv, flags1, nullptr, buf, asm_, s);
   // pass 2 only for factors whose conditioning needs it (need2), in place
   launch_gram(J, buf, partial, s, need2);
-  k_chol<<<ne, 256, csm, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags2,
-                              nullptr, need2);
-  DLX_LAUNCHED();
+  launch_chol(J, rr, partial, work, rinv, flags2, nullptr, need2, csm, s);
   launch_apply(J, rr, rinv, flags2, need2, buf, asm_, s);
   // exact MGS2 for flagged entries (pass-1 flags: buf still holds their input)
   auto* dscr = static_cast<double*>(ctx->scratch("mgs_scratch", sizeof(double) * buf_elems));
