@@ -9,6 +9,7 @@
 // eigenproblem (cyclic parallel Jacobi, one CTA per tensor). r' can differ from the dense
 // reference only where the prefix energy lands within rounding of tau (ties).
 #include "dlx_internal.cuh"
+#include "ptx.cuh"
 
 namespace dlx {
 
@@ -27,13 +28,17 @@ __device__ double er_block_sum(double v, double* red) {
   return s;
 }
 
-// ------------------------------------------------------------------ integer code Grams
+// ------------------------------------------------------------------ code Grams
 // For K = D r <= 64 the factor Grams come straight from the packed codes: C^T C over the
-// gathered codes of one side of one tensor is an exact integer (|c| <= 2^(q-1), int32 per
-// 1024-row chunk, int64 across chunks), and G = diag(s) C^T C diag(s) with the column scales
-// is formed in fp64 inside k_effrank — no dequantised factor copies, no fp64 Gram sweep.
+// gathered codes of one side of one tensor is an integer matrix (|c| <= 2^(q-1)), formed on
+// the fp64 tensor cores (DMMA) from exactly converted codes — every partial sum is an
+// integer below 2^53, so the chunk sums added with fp64 atomics are exact and independent of
+// their order. G = diag(s) C^T C diag(s) with the column scales is formed inside k_effrank.
+// No dequantised factor copies, no fp32 Gram sweep; the kernel's footprint (320 threads,
+// 35 KB) lets it share an SM with the fused outer update it overlaps.
 constexpr int kCgChunk = 1024;  // rows per k_code_gram block
 constexpr int kCgTile = 64;     // rows staged in shared memory per pass
+constexpr int kCgLd = kCgTile + 4;
 constexpr int kCgMaxK = 64;
 
 struct CodeGramJob : PlanExt {
@@ -41,104 +46,117 @@ struct CodeGramJob : PlanExt {
   int4* d = nullptr;
 };
 
-__global__ void __launch_bounds__(256) k_code_gram(const DevT2* __restrict__ T,
+// Decode task = 8 consecutive rows of one column: their 8 q-bit codes are one <= 64-bit field
+// read with three aligned 32-bit loads (prefetched one pass ahead).
+struct CgTask {
+  uint32_t w0, w1, w2;
+};
+
+__global__ void __launch_bounds__(320) k_code_gram(const DevT2* __restrict__ T,
                                                    const int4* __restrict__ chunks,
                                                    const uint8_t* __restrict__ gathered,
                                                    int64_t pay_bytes, int qbits, int D, int kst,
-                                                   unsigned long long* __restrict__ G) {
-  __shared__ int tile[kCgMaxK][kCgTile + 1];           // [k][row]
-  __shared__ int red[256 * 16];                        // per-thread 4x4 partials
+                                                   double* __restrict__ G) {
+  __shared__ double tile[kCgMaxK * kCgLd];  // [k][row]
   const int4 ch = chunks[blockIdx.x];
   const DevT2& t = T[ch.x];
   const int side = ch.y, r = t.r, K = D * r;
   const int64_t n = side == 0 ? t.a : t.b;
-  const int nb = (K + 3) / 4;             // 4-wide blocks per dimension
-  const int NB = nb * (nb + 1) / 2;       // upper block triangle
-  const int S = max(1, 256 / NB);         // row slices
-  const int bidx = threadIdx.x % NB, slice = threadIdx.x / NB;
-  const bool active = slice < S;
-  int bi = 0, rem = bidx;
-  while (rem >= nb - bi) {
-    rem -= nb - bi;
-    ++bi;
-  }
-  const int bj = bi + rem;
-  int acc[4][4];
+  const int nb = (K + 7) / 8, nblk = nb * (nb + 1) / 2;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(gathered);
+  const int64_t nwords = D * pay_bytes / 4;
+  // tasks: (column k, 8-row group g) for k < 8 nb, g < 8; two per thread at most
+  const int ntask = 8 * nb * 8;
+  int tk[2], tg[2];
+  int64_t tbit[2];
 #pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) acc[x][y] = 0;
-  const uint32_t mask = (1u << qbits) - 1u;
-  const int sh = 32 - qbits;
-  // decode assignment: thread -> row rl = tid % 64 of columns k = tid / 64 + 4 m (fixed
-  // across tiles, so the column addressing is hoisted)
-  const int rl = threadIdx.x % kCgTile, k0 = threadIdx.x / kCgTile;
-  const int ncol = nb;  // columns per thread: k0, k0 + 4, ..., < 4 nb
-  const uint8_t* cseg[kCgMaxK / 4];
-  int64_t cbit[kCgMaxK / 4];
-#pragma unroll
-  for (int m = 0; m < kCgMaxK / 4; ++m) {
-    const int k = k0 + 4 * m;
-    cseg[m] = nullptr;
-    cbit[m] = 0;
-    if (m < ncol && k < K) {
-      const int w = k / r, j = k % r;
-      cseg[m] = gathered + w * pay_bytes + (side == 0 ? t.seg_pc : t.seg_qc);
-      cbit[m] = (int64_t)j * n * qbits;
+  for (int u = 0; u < 2; ++u) {
+    const int id = threadIdx.x + 320 * u;
+    tk[u] = id < ntask ? id / 8 : -1;
+    tg[u] = id % 8;
+    tbit[u] = -1;
+    if (tk[u] >= 0 && tk[u] < K) {
+      const int w = tk[u] / r, j = tk[u] % r;
+      tbit[u] = (w * pay_bytes + (side == 0 ? t.seg_pc : t.seg_qc)) * 8 + (int64_t)j * n * qbits;
     }
   }
   const int64_t rend = min((int64_t)ch.w, n);
+  CgTask pre[2];
+  auto fetch = [&](int64_t row0) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      pre[u] = {0u, 0u, 0u};
+      const int64_t row = row0 + 8 * tg[u];
+      if (tbit[u] >= 0 && row < rend) {
+        const int64_t bit = tbit[u] + row * qbits;
+        const int64_t wi = bit >> 5;
+        pre[u].w0 = words[wi];
+        pre[u].w1 = wi + 1 < nwords ? words[wi + 1] : 0u;
+        pre[u].w2 = wi + 2 < nwords ? words[wi + 2] : 0u;
+      }
+    }
+  };
+  double acc[4][2];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) acc[b][0] = acc[b][1] = 0.0;
+  const uint32_t mask = (1u << qbits) - 1u;
+  const int sh = 32 - qbits;
+  fetch(ch.z);
   for (int64_t row0 = ch.z; row0 < ch.w; row0 += kCgTile) {
     __syncthreads();
-    const int64_t row = row0 + rl;
 #pragma unroll
-    for (int m = 0; m < kCgMaxK / 4; ++m) {
-      if (m >= ncol) break;
-      int c = 0;
-      if (cseg[m] && row < rend) {
-        const int64_t bit = cbit[m] + row * qbits;
-        const uint32_t word = static_cast<uint32_t>(cseg[m][bit >> 3]) |
-                              (static_cast<uint32_t>(cseg[m][(bit >> 3) + 1]) << 8);
-        c = static_cast<int>(((word >> (bit & 7)) & mask) << sh) >> sh;  // sign-extend
+    for (int u = 0; u < 2; ++u) {
+      if (tk[u] < 0) continue;
+      const int64_t rowg = row0 + 8 * tg[u];
+      const int s = tbit[u] >= 0 ? static_cast<int>((tbit[u] + rowg * qbits) & 31) : 0;
+      const uint64_t lo = static_cast<uint64_t>(pre[u].w0) | (static_cast<uint64_t>(pre[u].w1) << 32);
+      const uint64_t v = (lo >> s) | (s ? (static_cast<uint64_t>(pre[u].w2) << (64 - s)) : 0ull);
+      double* dst = tile + tk[u] * kCgLd + 8 * tg[u];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        int c = static_cast<int>((static_cast<uint32_t>(v >> (i * qbits)) & mask) << sh) >> sh;
+        if (tbit[u] < 0 || rowg + i >= rend) c = 0;
+        dst[i] = static_cast<double>(c);
       }
-      tile[k0 + 4 * m][rl] = c;
     }
     __syncthreads();
-    if (active) {
-      for (int rl = slice; rl < kCgTile; rl += S) {
-        int a[4], b[4];
+    if (row0 + kCgTile < ch.w) fetch(row0 + kCgTile);
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          a[x] = tile[4 * bi + x][rl];
-          b[x] = tile[4 * bj + x][rl];
+    for (int b = 0; b < 4; ++b) {
+      const int blk = warp + 10 * b;
+      if (blk < nblk) {
+        int bi = 0, rem = blk;
+        while (rem >= nb - bi) {
+          rem -= nb - bi;
+          ++bi;
         }
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y) acc[x][y] += a[x] * b[y];
+        const int bj = bi + rem;
+        const double* pa = tile + (bi * 8 + lane / 4) * kCgLd + lane % 4;
+        const double* pb = tile + (bj * 8 + lane / 4) * kCgLd + lane % 4;
+#pragma unroll 4
+        for (int k = 0; k < kCgTile; k += 4) dmma_8x8x4(acc[b], pa[k], pb[k]);
       }
     }
   }
-  // fold the row slices (fixed order; integer sums are exact anyway), one atomic per entry
+  double* g = G + ((int64_t)ch.x * 2 + side) * kst * kst;
 #pragma unroll
-  for (int x = 0; x < 4; ++x)
+  for (int b = 0; b < 4; ++b) {
+    const int blk = warp + 10 * b;
+    if (blk < nblk) {
+      int bi = 0, rem = blk;
+      while (rem >= nb - bi) {
+        rem -= nb - bi;
+        ++bi;
+      }
+      const int bj = bi + rem;
+      const int i = bi * 8 + lane / 4;
 #pragma unroll
-    for (int y = 0; y < 4; ++y) red[threadIdx.x * 16 + x * 4 + y] = active ? acc[x][y] : 0;
-  __syncthreads();
-  unsigned long long* g = G + ((int64_t)ch.x * 2 + side) * kst * kst;
-  for (int e = threadIdx.x; e < NB * 16; e += 256) {
-    const int b = e / 16, xy = e % 16, x = xy / 4, y = xy % 4;
-    long long sum = 0;
-    for (int sl = 0; sl < S; ++sl) sum += red[(sl * NB + b) * 16 + xy];
-    int ci = 0, rm = b;
-    while (rm >= nb - ci) {
-      rm -= nb - ci;
-      ++ci;
+      for (int q = 0; q < 2; ++q) {
+        const int j = bj * 8 + 2 * (lane % 4) + q;
+        if (i < K && j < K && i <= j && acc[b][q] != 0.0) atomicAdd(&g[i * kst + j], acc[b][q]);
+      }
     }
-    const int cj = ci + rm;
-    const int i = 4 * ci + x, j = 4 * cj + y;
-    if (i < K && j < K && i <= j && sum != 0)
-      atomicAdd(&g[i * kst + j], static_cast<unsigned long long>(sum));
   }
 }
 
@@ -153,16 +171,20 @@ constexpr size_t kErSmemBytes = 3 * kErSmemDim * (kErSmemDim + 1) * sizeof(doubl
 __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, int D, int rr,
                                                  const double* __restrict__ GA,
                                                  const double* __restrict__ GB,
-                                                 const long long* __restrict__ GI,
+                                                 const double* __restrict__ GI,
                                                  const uint8_t* __restrict__ gathered,
-                                                 int64_t pay_bytes, int sdim,
+                                                 int64_t pay_bytes, int sdim, int hmax,
                                                  double* __restrict__ work, double tau,
                                                  int* __restrict__ per,
                                                  double* __restrict__ energy) {
   extern __shared__ double er_sm[];
   __shared__ double red[32];
-  __shared__ double cs[1024], sn[1024];
-  __shared__ int pp[1024], qq[1024];
+  // dynamic shared memory: [L | G_A L | M] (when staged) then the rotation table of a round
+  const int64_t stage = sdim > 0 ? 3 * (int64_t)sdim * (sdim + 1) : 0;
+  double* cs = er_sm + stage;
+  double* sn = cs + hmax;
+  int* pp = reinterpret_cast<int*>(sn + hmax);
+  int* qq = pp + hmax;
   __shared__ int s_k;
   __shared__ double s_tot;
   const int e = blockIdx.x;
@@ -183,7 +205,7 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
     double gb, ga;
     if (GI) {
       const int lo = min(i, k), hi = max(i, k);
-      const long long* gi = GI + (int64_t)e * 2 * mat;
+      const double* gi = GI + (int64_t)e * 2 * mat;
       const int wi = i / t.r, ji = i % t.r, wk = k / t.r, jk = k % t.r;
       const uint8_t* pi = gathered + wi * pay_bytes;
       const uint8_t* pk = gathered + wk * pay_bytes;
@@ -191,8 +213,8 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
       const double sak = *reinterpret_cast<const float*>(pk + t.seg_ps + 4 * jk);
       const double sbi = *reinterpret_cast<const float*>(pi + t.seg_qs + 4 * ji);
       const double sbk = *reinterpret_cast<const float*>(pk + t.seg_qs + 4 * jk);
-      ga = (double)gi[lo * rr + hi] * sai * sak;
-      gb = (double)gi[mat + lo * rr + hi] * sbi * sbk;
+      ga = gi[lo * rr + hi] * sai * sak;
+      gb = gi[mat + lo * rr + hi] * sbi * sbk;
     } else {
       ga = GA[e * mat + i * rr + k];
       gb = GB[e * mat + i * rr + k];
@@ -338,20 +360,22 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
 }
 
 static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const double* GB,
-                           const long long* GI, const uint8_t* gathered, double* W, double tau,
+                           const double* GI, const uint8_t* gathered, double* W, double tau,
                            int* d_per, double* d_energy, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     DLX_CUDA(cudaFuncSetAttribute(k_effrank, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kErSmemBytes)));
+                                  static_cast<int>(kErSmemBytes + 1024 * 24)));
     attr = true;
   }
   int n2max = 0;
   for (const DevT2& t : P.t2) n2max = std::max(n2max, D * t.r + ((D * t.r) & 1));
   const int sdim = n2max <= kErSmemDim ? n2max : 0;
-  const size_t smem = 3 * static_cast<size_t>(sdim) * (sdim + 1) * sizeof(double);
+  const int hmax = std::max(1, n2max / 2);
+  const size_t smem = 3 * static_cast<size_t>(sdim) * (sdim + 1) * sizeof(double) +
+                      static_cast<size_t>(hmax) * (2 * sizeof(double) + 2 * sizeof(int));
   k_effrank<<<P.t2.size(), 256, smem, s>>>(P.d_t2, D, rr, GA, GB, GI, gathered, P.payload_bytes,
-                                           sdim, W, tau, d_per, d_energy);
+                                           sdim, hmax, W, tau, d_per, d_energy);
   DLX_LAUNCHED();
 }
 
@@ -378,13 +402,12 @@ void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* g
         }
       J.d = plan_upload(P, J.chunks);
     }
-    auto* GI = static_cast<unsigned long long*>(
-        ctx->scratch("er_GI", sizeof(unsigned long long) * mat * ne * 2));
-    DLX_CUDA(cudaMemsetAsync(GI, 0, sizeof(unsigned long long) * mat * ne * 2, s));
-    k_code_gram<<<J.chunks.size(), 256, 0, s>>>(P.d_t2, J.d, gathered, P.payload_bytes, P.qbits,
+    auto* GI = static_cast<double*>(ctx->scratch("er_GI", sizeof(double) * mat * ne * 2));
+    DLX_CUDA(cudaMemsetAsync(GI, 0, sizeof(double) * mat * ne * 2, s));
+    k_code_gram<<<J.chunks.size(), 320, 0, s>>>(P.d_t2, J.d, gathered, P.payload_bytes, P.qbits,
                                                 D, K, GI);
     DLX_LAUNCHED();
-    launch_effrank(P, D, K, nullptr, nullptr, reinterpret_cast<const long long*>(GI), gathered,
+    launch_effrank(P, D, K, nullptr, nullptr, GI, gathered,
                    W, tau, d_per, d_energy, s);
     return;
   }

@@ -11,6 +11,7 @@
 // stream_key({n, r, j, attempt}))). That path only triggers on (near) rank-deficient
 // inputs such as all-zero tensors.
 #include "dlx_internal.cuh"
+#include "ptx.cuh"
 
 namespace dlx {
 
@@ -171,11 +172,6 @@ __global__ void __launch_bounds__(256) k_gram(const DevMat* __restrict__ mats,
 constexpr int kGdRows = 64;
 constexpr int kGdLd = kGdRows + 4;  // [col][row] stride: conflict-free fragment loads
 
-__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
-}
 
 __global__ void __launch_bounds__(320) k_gram_dmma(const DevMat* __restrict__ mats,
                                                    const int4* __restrict__ splits,
