@@ -51,6 +51,8 @@ def parse():
                          "controller every round but time at rank1 = 32, the configured rank)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-side-stream", action="store_true",
+                    help="run the effective-rank measurement on the main stream")
     return ap.parse_args()
 
 
@@ -212,7 +214,7 @@ def main():
     cfg = OuterConfig(rank1=args.rank, qbits=args.qbits, adaptive=not args.no_adaptive,
                       H1=125, window_c=5, tau=0.5, power_iters=2, seed=1, overlap=True,
                       hold_rank=not args.follow_controller)
-    eng = OuterSync(L, cfg, anchor, world=world, rank=rank)
+    eng = OuterSync(L, cfg, anchor, world=world, rank=rank, side_stream=not args.no_side_stream)
     stream = torch.cuda.current_stream()
 
     def barrier():

@@ -275,66 +275,182 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
     }
   }
   __syncthreads();
-  const int half = n2 / 2;
-  for (int sweep = 0; sweep < 40 && n2 > 1; ++sweep) {
-    double off = 0.0, dg = 0.0;
-    for (int idx = threadIdx.x; idx < n2 * n2; idx += blockDim.x) {
-      const int i = idx / n2, j = idx % n2;
-      const double v = M[i * ld + j];
-      if (i == j) dg += v * v; else off += v * v;
-    }
-    off = er_block_sum(off, red);
-    dg = er_block_sum(dg, red);
-    if (off <= 1e-30 * dg || off == 0.0) break;
-    for (int rd = 0; rd < n2 - 1; ++rd) {
-      for (int i = threadIdx.x; i < half; i += blockDim.x) {
-        int a = (rd + i) % (n2 - 1);
-        int b = i == 0 ? n2 - 1 : (rd - i + n2 - 1) % (n2 - 1);
-        const int p = min(a, b), q = max(a, b);
-        const double apq = M[p * ld + q];
-        double c = 1.0, s = 0.0;
-        if (apq != 0.0) {
-          const double theta = (M[q * ld + q] - M[p * ld + p]) / (2.0 * apq);
-          const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          c = 1.0 / sqrt(t * t + 1.0);
-          s = t * c;
+  __shared__ double tri[4 * 64];  // V | A v / H | diagonal | squared off-diagonal
+  double* ev = in_smem ? tri : Tm;  // eigenvalues, descending
+  if (in_smem) {
+    // 3a. Householder tridiagonalisation (P = I - v v^T / H, A <- P A P) in shared memory
+    __shared__ double s_H, s_alpha, s_K;
+    double* V = tri;        // Householder vector
+    double* Pv = tri + 64;  // A v / H
+    const int n = n2;
+    const int tid = threadIdx.x;
+    for (int k = 0; k + 2 < n; ++k) {
+      if (tid < 32) {
+        double ss = 0.0;
+        for (int i = k + 1 + tid; i < n; i += 32) {
+          const double x = M[i * ld + k];
+          ss += x * x;
         }
-        cs[i] = c;
-        sn[i] = s;
-        pp[i] = p;
-        qq[i] = q;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (tid == 0) {
+          const double x0 = M[(k + 1) * ld + k];
+          const double nrm = sqrt(ss);
+          if (!(ss - x0 * x0 > 1e-300 * ss) || nrm == 0.0) {
+            s_H = 0.0;  // column already reduced
+            s_alpha = x0;
+          } else {
+            const double alpha = x0 > 0.0 ? -nrm : nrm;
+            s_alpha = alpha;
+            s_H = ss - x0 * alpha;  // ||v||^2 / 2
+          }
+        }
       }
       __syncthreads();
-      for (int idx = threadIdx.x; idx < half * n2; idx += blockDim.x) {  // rows
-        const int i = idx / n2, k = idx % n2;
-        const int p = pp[i], q = qq[i];
-        const double c = cs[i], s = sn[i];
-        const double ap = M[p * ld + k], aq = M[q * ld + k];
-        M[p * ld + k] = c * ap - s * aq;
-        M[q * ld + k] = s * ap + c * aq;
+      const double H = s_H;
+      if (H == 0.0) {  // uniform
+        __syncthreads();
+        continue;
+      }
+      for (int i = k + 1 + tid; i < n; i += blockDim.x)
+        V[i] = i == k + 1 ? M[i * ld + k] - s_alpha : M[i * ld + k];
+      __syncthreads();
+      {
+        const int row = k + 1 + tid / 4, part = tid % 4;
+        double acc = 0.0;
+        if (row < n)
+          for (int j = k + 1 + part; j < n; j += 4) acc = fma(M[row * ld + j], V[j], acc);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (row < n && part == 0) Pv[row] = acc / H;
       }
       __syncthreads();
-      for (int idx = threadIdx.x; idx < half * n2; idx += blockDim.x) {  // columns
-        const int i = idx / n2, k = idx % n2;
-        const int p = pp[i], q = qq[i];
-        const double c = cs[i], s = sn[i];
-        const double ap = M[k * ld + p], aq = M[k * ld + q];
-        M[k * ld + p] = c * ap - s * aq;
-        M[k * ld + q] = s * ap + c * aq;
+      if (tid < 32) {
+        double acc = 0.0;
+        for (int i = k + 1 + tid; i < n; i += 32) acc = fma(V[i], Pv[i], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (tid == 0) s_K = acc / (2.0 * H);
       }
+      __syncthreads();
+      const double Kc = s_K;
+      const int mm = n - k - 1;
+      for (int idx = tid; idx < mm * mm; idx += blockDim.x) {
+        const int i = k + 1 + idx / mm, j = k + 1 + idx % mm;
+        const double wi = Pv[i] - Kc * V[i], wj = Pv[j] - Kc * V[j];
+        M[i * ld + j] -= V[i] * wj + wi * V[j];
+      }
+      if (tid == 0) M[(k + 1) * ld + k] = s_alpha;
       __syncthreads();
     }
-  }
-  // 4. eigenvalues (clamped >= 0) sorted descending by rank counting; prefix energy
-  double* ev = Tm;  // reuse: ev[rank] = value
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    const double v = fmax(M[i * ld + i], 0.0);
-    int rank = 0;
-    for (int j = 0; j < n2; ++j) {
-      const double w = fmax(M[j * ld + j], 0.0);
-      rank += (w > v) || (w == v && j < i);
+    // 3b. eigenvalues of the tridiagonal (d, e) by multisection on Sturm counts: a group of
+    // G lanes per eigenvalue evaluates G interior points per step (log2(G+1) bits / step)
+    double* Dg = Pv + 64;
+    double* E2 = Dg + 64;
+    for (int i = tid; i < n; i += blockDim.x) {
+      Dg[i] = M[i * ld + i];
+      E2[i] = i + 1 < n ? M[(i + 1) * ld + i] * M[(i + 1) * ld + i] : 0.0;
     }
-    ev[rank] = v;
+    __syncthreads();
+    double lo = 0.0, hi = 0.0, amax = 0.0;
+    for (int i = 0; i < n; ++i) {  // Gershgorin (every thread, uniform)
+      const double r0 = i > 0 ? sqrt(E2[i - 1]) : 0.0, r1 = i + 1 < n ? sqrt(E2[i]) : 0.0;
+      lo = fmin(lo, Dg[i] - r0 - r1);
+      hi = fmax(hi, Dg[i] + r0 + r1);
+      amax = fmax(amax, fabs(Dg[i]) + r0 + r1);
+    }
+    hi += 1e-14 * amax + 1e-300;
+    lo -= 1e-14 * amax + 1e-300;
+    const double pivmin = 1e-290 + 1e-30 * amax * amax;
+    int G = 1;
+    while (G * 2 <= 32 && G * 2 * n <= static_cast<int>(blockDim.x)) G *= 2;
+    const int idx = tid / G, l = tid % G;
+    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((tid % 32) / G * G);
+    const int iters = G >= 16 ? 12 : G >= 8 ? 15 : G >= 4 ? 20 : G >= 2 ? 29 : 50;
+    for (int it = 0; it < iters; ++it) {
+      const double sig = lo + (hi - lo) * (double)(l + 1) / (double)(G + 1);
+      int c = 0;
+      {
+        double q = Dg[0] - sig;
+        c += q < 0.0;
+        for (int j = 1; j < n; ++j) {
+          if (fabs(q) < pivmin) q = -pivmin;
+          q = (Dg[j] - sig) - E2[j - 1] / q;
+          c += q < 0.0;
+        }
+      }
+      const unsigned below = __ballot_sync(0xffffffffu, c <= idx) & gmask;
+      const int L = __popc(below);
+      const int base = (tid % 32) / G * G;
+      const double s_lo = __shfl_sync(0xffffffffu, sig, base + max(L - 1, 0));
+      const double s_hi = __shfl_sync(0xffffffffu, sig, base + min(L, G - 1));
+      if (L > 0) lo = s_lo;
+      if (L < G) hi = s_hi;
+    }
+    __syncthreads();
+    if (l == 0 && idx < n) ev[n - 1 - idx] = fmax(0.5 * (lo + hi), 0.0);
+  } else {
+    const int half = n2 / 2;
+    for (int sweep = 0; sweep < 40 && n2 > 1; ++sweep) {
+      double off = 0.0, dg = 0.0;
+      for (int idx = threadIdx.x; idx < n2 * n2; idx += blockDim.x) {
+        const int i = idx / n2, j = idx % n2;
+        const double v = M[i * ld + j];
+        if (i == j) dg += v * v; else off += v * v;
+      }
+      off = er_block_sum(off, red);
+      dg = er_block_sum(dg, red);
+      if (off <= 1e-30 * dg || off == 0.0) break;
+      for (int rd = 0; rd < n2 - 1; ++rd) {
+        for (int i = threadIdx.x; i < half; i += blockDim.x) {
+          int a = (rd + i) % (n2 - 1);
+          int b = i == 0 ? n2 - 1 : (rd - i + n2 - 1) % (n2 - 1);
+          const int p = min(a, b), q = max(a, b);
+          const double apq = M[p * ld + q];
+          double c = 1.0, s = 0.0;
+          if (apq != 0.0) {
+            const double theta = (M[q * ld + q] - M[p * ld + p]) / (2.0 * apq);
+            const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+          }
+          cs[i] = c;
+          sn[i] = s;
+          pp[i] = p;
+          qq[i] = q;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < half * n2; idx += blockDim.x) {  // rows
+          const int i = idx / n2, k = idx % n2;
+          const int p = pp[i], q = qq[i];
+          const double c = cs[i], s = sn[i];
+          const double ap = M[p * ld + k], aq = M[q * ld + k];
+          M[p * ld + k] = c * ap - s * aq;
+          M[q * ld + k] = s * ap + c * aq;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < half * n2; idx += blockDim.x) {  // columns
+          const int i = idx / n2, k = idx % n2;
+          const int p = pp[i], q = qq[i];
+          const double c = cs[i], s = sn[i];
+          const double ap = M[k * ld + p], aq = M[k * ld + q];
+          M[k * ld + p] = c * ap - s * aq;
+          M[k * ld + q] = s * ap + c * aq;
+        }
+        __syncthreads();
+      }
+    }
+    // 4. eigenvalues (clamped >= 0) sorted descending by rank counting; prefix energy
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+      const double v = fmax(M[i * ld + i], 0.0);
+      int rank = 0;
+      for (int j = 0; j < n2; ++j) {
+        const double w = fmax(M[j * ld + j], 0.0);
+        rank += (w > v) || (w == v && j < i);
+      }
+      ev[rank] = v;
+    }
+
   }
   __syncthreads();
   if (threadIdx.x == 0) {
