@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) k_o5_prep(
 template <bool SELF>
 __global__ void __launch_bounds__(kO5Threads, 1)
     k_o5(const DevT2* __restrict__ T, const O5Maps* __restrict__ maps,
-         const int4* __restrict__ tiles, const int* __restrict__ cta_off, int D, int KA,
+         const int2* __restrict__ bands, int nbands, int* __restrict__ band_ctr, int D, int KA,
          int self_index, int mode, float gamma, float beta, int classical,
          dlx_round_stats* stats) {
   extern __shared__ __align__(1024) uint8_t o5smem[];
@@ -122,6 +122,9 @@ __global__ void __launch_bounds__(kO5Threads, 1)
   uint64_t* accfull = aempty + 2;          // [2]
   uint64_t* accempty = accfull + 2;        // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+  // per-stage tile descriptor written by the producer before the stage's arrive:
+  // (t2 slot or -1 = end, row m0, column n0, A slot | 2 first-of-band | 4 last-of-band)
+  int4* sinfo = reinterpret_cast<int4*>(tmem_slot + 4);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const bool ovl = mode == DLX_MODE_OVERLAPPED;
   const int nstreams = ovl ? 4 : 3;
@@ -149,7 +152,6 @@ __global__ void __launch_bounds__(kO5Threads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;  // acc c: cols [64c, 64c+32) Delta, [64c+32, 64c+64) self
-  const int t0 = cta_off[blockIdx.x], t1 = cta_off[blockIdx.x + 1];
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -157,59 +159,70 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     uint32_t sph = 0, aph[2] = {0, 0};
     // (L2 eviction hints on these loads / the stores measured 10 % slower: none)
 
-    int band_slot = -1, band_m0 = -1;
-    for (int ti = t0; ti < t1; ++ti) {
-      const int4 tl = tiles[ti];
-      const O5Maps* mp = maps + tl.x;
-      if (tl.x != band_slot || tl.y != band_m0) {  // new row band: load A
-        band_slot = tl.x;
-        band_m0 = tl.y;
-        a = (a + 1) & 1;
-        mbar_wait(&aempty[a], aph[a] ^ 1);
-        aph[a] ^= 1;
-        if (elect_one()) {
-          mbar_expect_tx(&afull[a], aband_bytes);
-          for (int kc = 0; kc < nkc; ++kc)
-            tma_load_2d(abuf + a * aband_bytes + kc * kO5StreamBox, &mp->a, &afull[a], 32 * kc, tl.y);
-        }
-        __syncwarp();
-      }
-      mbar_wait(&sempty[s], sph ^ 1);
+    // Row bands are claimed dynamically (one atomic per band) in the global band order, so
+    // all CTAs work on neighbouring bands: the factor tiles of the few tensors in flight stay
+    // in L2, and CTAs that start late (side-stream work on their SM) simply take fewer bands.
+    for (;;) {
+      int band = 0;
+      if (lane == 0) band = atomicAdd(band_ctr, 1);
+      band = __shfl_sync(0xffffffffu, band, 0);
+      if (band >= nbands) break;
+      const int2 bd = bands[band];
+      const O5Maps* mp = maps + bd.x;
+      const int ntile = static_cast<int>((T[bd.x].b + 31) / 32);
+      a = (a + 1) & 1;
+      mbar_wait(&aempty[a], aph[a] ^ 1);
+      aph[a] ^= 1;
       if (elect_one()) {
-        uint8_t* st = smem + s * stage_bytes;
-        mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox + 2 * nkc * b_bytes);
-        for (int q = 0; q < nstreams; ++q)
-          tma_load_2d(st + q * kO5StreamBox, &mp->s[q], &sfull[s], tl.z, tl.y);
-        uint8_t* bb = st + 4 * kO5StreamBox;
-        for (int kc = 0; kc < nkc; ++kc) {
-          tma_load_2d(bb + kc * b_bytes, &mp->bh, &sfull[s], 32 * kc, tl.z);
-          tma_load_2d(bb + (nkc + kc) * b_bytes, &mp->bl, &sfull[s], 32 * kc, tl.z);
-        }
+        mbar_expect_tx(&afull[a], aband_bytes);
+        for (int kc = 0; kc < nkc; ++kc)
+          tma_load_2d(abuf + a * aband_bytes + kc * kO5StreamBox, &mp->a, &afull[a], 32 * kc, bd.y);
       }
       __syncwarp();
-      if (++s == kO5Stages) {
-        s = 0;
-        sph ^= 1;
+      for (int n = 0; n < ntile; ++n) {
+        mbar_wait(&sempty[s], sph ^ 1);
+        if (elect_one()) {
+          sinfo[s] = make_int4(bd.x, bd.y, 32 * n, a | (n == 0 ? 2 : 0) | (n == ntile - 1 ? 4 : 0));
+          uint8_t* st = smem + s * stage_bytes;
+          mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox + 2 * nkc * b_bytes);
+          for (int q = 0; q < nstreams; ++q)
+            tma_load_2d(st + q * kO5StreamBox, &mp->s[q], &sfull[s], 32 * n, bd.y);
+          uint8_t* bb = st + 4 * kO5StreamBox;
+          for (int kc = 0; kc < nkc; ++kc) {
+            tma_load_2d(bb + kc * b_bytes, &mp->bh, &sfull[s], 32 * kc, 32 * n);
+            tma_load_2d(bb + (nkc + kc) * b_bytes, &mp->bl, &sfull[s], 32 * kc, 32 * n);
+          }
+        }
+        __syncwarp();
+        if (++s == kO5Stages) {
+          s = 0;
+          sph ^= 1;
+        }
       }
     }
+    // end marker: one more stage whose descriptor says "done" (no bytes)
+    mbar_wait(&sempty[s], sph ^ 1);
+    if (elect_one()) {
+      sinfo[s] = make_int4(-1, 0, 0, 0);
+      mbar_arrive(&sfull[s]);
+    }
+    __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     const uint32_t idesc = idesc_tf32(32, false, false);
-    int s = 0, a = -1, c = 0;
+    int s = 0, a = 0, c = 0;
     uint32_t sph = 0, cph = 0, aph[2] = {0, 0};
-    int band_slot = -1, band_m0 = -1;
-    for (int ti = t0; ti < t1; ++ti) {
-      const int4 tl = tiles[ti];
+    for (;;) {
+      mbar_wait(&sfull[s], sph);
+      const int4 tl = sinfo[s];
+      if (tl.x < 0) break;
       const DevT2 t = T[tl.x];
-      const bool last_in_band = (ti + 1 == t1) || tiles[ti + 1].x != tl.x || tiles[ti + 1].y != tl.y;
-      if (tl.x != band_slot || tl.y != band_m0) {
-        band_slot = tl.x;
-        band_m0 = tl.y;
-        a = (a + 1) & 1;
+      const bool last_in_band = tl.w & 4;
+      if (tl.w & 2) {
+        a = tl.w & 1;
         mbar_wait(&afull[a], aph[a]);
         aph[a] ^= 1;
       }
-      mbar_wait(&sfull[s], sph);
       mbar_wait(&accempty[c], cph ^ 1);
       tc_fence_after();
       const uint32_t abase = su32(abuf + a * aband_bytes);
@@ -260,11 +273,12 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     double num = 0.0, den = 0.0, dn = 0.0, en = 0.0, nf = 0.0;
     int s = 0, c = 0;
     uint32_t sph = 0, cph = 0;
-    for (int ti = t0; ti < t1; ++ti) {
-      const int4 tl = tiles[ti];
+    for (;;) {
+      mbar_wait(&sfull[s], sph);
+      const int4 tl = sinfo[s];
+      if (tl.x < 0) break;
       const DevT2 t = T[tl.x];
       mbar_wait(&accfull[c], cph);
-      mbar_wait(&sfull[s], sph);
       tc_fence_after();
       float dv[16], sv[16];
       tmem_ld16(tmem + lane_base + 64u * c + 16u * half, dv);
@@ -396,6 +410,9 @@ struct O5State : PlanExt {
   int64_t a_elems = 0, b_elems = 0;
   int64_t params = 0;  // 2-D parameters covered
   int s0 = 0, s1 = 0;  // slot range
+  std::vector<int2> bands;  // (t2 slot, m0) in claim order
+  int2* d_bands = nullptr;
+  int* d_ctr = nullptr;
   int64_t* d_aoff = nullptr;
   int64_t* d_boff = nullptr;
   O5Maps* d_maps = nullptr;
@@ -449,6 +466,10 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   const int g = static_cast<int>(std::min<size_t>(S.tiles.size(), sms));
   S.off.resize(g + 1);
   for (int b = 0; b <= g; ++b) S.off[b] = static_cast<int>(S.tiles.size() * b / g);
+  for (const int4& tl : S.tiles)
+    if (tl.z == 0) S.bands.push_back(make_int2(tl.x, tl.y));
+  S.d_bands = plan_upload(P, S.bands, 1);
+  S.d_ctr = static_cast<int*>(P.dev_alloc(sizeof(int)));
   S.d_tiles = plan_upload(P, S.tiles, 1);
   S.d_off = plan_upload(P, S.off, 1);
   S.d_rows = plan_upload(P, S.rows, 1);
@@ -495,8 +516,10 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   }
   const int nkc = KA / 32;
   const size_t smem = 1024 + kO5Stages * (4 * kO5StreamBox + 2 * nkc * 4096) +
-                      2 * nkc * kO5StreamBox + 12 * 8 + 16;
-  const int grid = static_cast<int>(S.off.size()) - 1;
+                      2 * nkc * kO5StreamBox + 12 * 8 + 16 + 16 * kO5Stages;
+  const int grid = std::min(static_cast<int>(S.bands.size()), static_cast<int>(S.off.size()) - 1);
+  const int nbands = static_cast<int>(S.bands.size());
+  DLX_CUDA(cudaMemsetAsync(S.d_ctr, 0, sizeof(int), s));
   static bool attr = false;
   if (!attr) {
     DLX_CUDA(cudaFuncSetAttribute(k_o5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -507,10 +530,10 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   // pending, anchor, velocity — 28 B/param overlapped, 24 B/param sync
   KernelTimer timer("k_o5", (mode == DLX_MODE_OVERLAPPED ? 28.0 : 24.0) * S.params, s);
   if (self_index >= 0)
-    k_o5<true><<<grid, kO5Threads, smem, s>>>(P.d_t2, S.d_maps, S.d_tiles, S.d_off, D, KA,
+    k_o5<true><<<grid, kO5Threads, smem, s>>>(P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, KA,
                                              self_index, mode, gamma, beta, classical, stats);
   else
-    k_o5<false><<<grid, kO5Threads, smem, s>>>(P.d_t2, S.d_maps, S.d_tiles, S.d_off, D, KA,
+    k_o5<false><<<grid, kO5Threads, smem, s>>>(P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, KA,
                                               self_index, mode, gamma, beta, classical, stats);
   DLX_LAUNCHED();
 }
