@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdlx_b200.so")
+# DLX_LIB overrides the library path (A/B experiments between two builds)
+LIB_PATH = os.environ.get("DLX_LIB") or os.path.join(HERE, "libdlx_b200.so")
 
 # Exception taxonomy of the reference (errors.hpp:8-34) + device/collective failures.
 class Error(RuntimeError):

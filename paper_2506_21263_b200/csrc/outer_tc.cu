@@ -27,13 +27,16 @@
 namespace dlx {
 
 constexpr int kO5Threads = 320;
-constexpr int kO5Stages = 2;
-constexpr uint32_t kO5StreamBox = 128 * 32 * 4;  // 16 KB: 128 rows x 32 columns fp32 (SW128)
+constexpr int kO5MaxStages = 6;
+constexpr int kO5TileN = 16;                          // tile = 128 rows x 16 columns
+constexpr uint32_t kO5StreamBox = 128 * kO5TileN * 4;  // 8 KB per streamed operand (SW64)
+constexpr uint32_t kO5ABox = 128 * 32 * 4;            // 16 KB: 128 rows x 32 K of A (SW128)
+constexpr uint32_t kO5BBox = kO5TileN * 32 * 4;       // 2 KB: 16 rows x 32 K of B (SW128)
 
 struct O5Maps {
-  CUtensorMap s[4];  // pending, anchor, velocity, local: dims {b, a}, box {32, 128}, SW128
+  CUtensorMap s[4];  // pending, anchor, velocity, local: dims {b, a}, box {16, 128}, SW64
   CUtensorMap a;     // A (codes of P): dims {KA, lda}, box {32, 128}, SW128
-  CUtensorMap bh, bl;  // B hi / lo: dims {KA, ldb}, box {32, 32}, SW128
+  CUtensorMap bh, bl;  // B hi / lo: dims {KA, ldb}, box {32, 16}, SW128
 };
 
 // ------------------------------------------------------------------ prep: A and B operands
@@ -101,26 +104,27 @@ __global__ void __launch_bounds__(256) k_o5_prep(
 }
 
 // ------------------------------------------------------------------ the kernel
+// 16-column tiles keep 4-5 stages (36 KB each at K = 32) in flight per SM while one is in
+// the epilogue, so the HBM stream does not stall behind a stage that is being written back.
 template <bool SELF>
 __global__ void __launch_bounds__(kO5Threads, 1)
     k_o5(const DevT2* __restrict__ T, const O5Maps* __restrict__ maps,
-         const int2* __restrict__ bands, int nbands, int* __restrict__ band_ctr, int D, int KA,
-         int self_index, int mode, float gamma, float beta, int classical,
+         const int4* __restrict__ bands, int nbands, int* __restrict__ band_ctr, int D, int KA,
+         int nst, int self_index, int mode, float gamma, float beta, int classical,
          dlx_round_stats* stats) {
   extern __shared__ __align__(1024) uint8_t o5smem[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(o5smem) + 1023) & ~uintptr_t(1023));
-  const int nkc = KA / 32;                              // 32-wide K chunks
-  const uint32_t b_bytes = 32u * 32u * 4u;              // one B chunk: 32 rows x 32 K
-  const uint32_t stage_bytes = 4 * kO5StreamBox + 2 * nkc * b_bytes;
-  const uint32_t aband_bytes = nkc * kO5StreamBox;      // 128 rows x KA
-  uint8_t* abuf = smem + kO5Stages * stage_bytes;
+  const int nkc = KA / 32;                                 // 32-wide K chunks
+  const uint32_t stage_bytes = 4 * kO5StreamBox + 2 * nkc * kO5BBox;
+  const uint32_t aband_bytes = nkc * kO5ABox;              // 128 rows x KA
+  uint8_t* abuf = smem + nst * stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(abuf + 2 * aband_bytes);
-  uint64_t* sfull = bars;                  // [2]
-  uint64_t* sempty = sfull + kO5Stages;    // [2]
-  uint64_t* afull = sempty + kO5Stages;    // [2]
-  uint64_t* aempty = afull + 2;            // [2]
-  uint64_t* accfull = aempty + 2;          // [2]
-  uint64_t* accempty = accfull + 2;        // [2]
+  uint64_t* sfull = bars;                // [nst]
+  uint64_t* sempty = sfull + nst;        // [nst]
+  uint64_t* afull = sempty + nst;        // [2]
+  uint64_t* aempty = afull + 2;          // [2]
+  uint64_t* accfull = aempty + 2;        // [2]
+  uint64_t* accempty = accfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
   // per-stage tile descriptor written by the producer before the stage's arrive:
   // (t2 slot or -1 = end, row m0, column n0, A slot | 2 first-of-band | 4 last-of-band)
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(kO5Threads, 1)
   const int nstreams = ovl ? 4 : 3;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < kO5Stages; ++i) {
+    for (int i = 0; i < nst; ++i) {
       mbar_init(&sfull[i], 1);
       mbar_init(&sempty[i], 1);
     }
@@ -145,56 +149,58 @@ __global__ void __launch_bounds__(kO5Threads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
-                 "r"(128));
+                 "r"(64));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // acc c: cols [64c, 64c+32) Delta, [64c+32, 64c+64) self
+  const uint32_t tmem = *tmem_slot;  // acc c: cols [32c, 32c+16) Delta, [32c+16, 32c+32) self
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     int s = 0, a = -1;
     uint32_t sph = 0, aph[2] = {0, 0};
     // (L2 eviction hints on these loads / the stores measured 10 % slower: none)
-
-    // Row bands are claimed dynamically (one atomic per band) in the global band order, so
-    // all CTAs work on neighbouring bands: the factor tiles of the few tensors in flight stay
-    // in L2, and CTAs that start late (side-stream work on their SM) simply take fewer bands.
+    // Work is claimed dynamically (one atomic per chunk of 128 columns of a row band) in the
+    // global band-major order, so concurrently active CTAs stream ADJACENT column chunks of
+    // the same rows (DRAM row-buffer locality: a band per CTA measured 5.5 vs 6.6 TB/s on
+    // this 4-read / 3-write mix), the factor tiles of the few tensors in flight stay in L2,
+    // and CTAs that start late (side-stream work on their SM) simply take fewer chunks.
     for (;;) {
       int band = 0;
       if (lane == 0) band = atomicAdd(band_ctr, 1);
       band = __shfl_sync(0xffffffffu, band, 0);
       if (band >= nbands) break;
-      const int2 bd = bands[band];
+      const int4 bd = bands[band];  // (slot, m0, first column, columns)
       const O5Maps* mp = maps + bd.x;
-      const int ntile = static_cast<int>((T[bd.x].b + 31) / 32);
+      const int ntile = (bd.w + kO5TileN - 1) / kO5TileN;
       a = (a + 1) & 1;
       mbar_wait(&aempty[a], aph[a] ^ 1);
       aph[a] ^= 1;
       if (elect_one()) {
         mbar_expect_tx(&afull[a], aband_bytes);
         for (int kc = 0; kc < nkc; ++kc)
-          tma_load_2d(abuf + a * aband_bytes + kc * kO5StreamBox, &mp->a, &afull[a], 32 * kc, bd.y);
+          tma_load_2d(abuf + a * aband_bytes + kc * kO5ABox, &mp->a, &afull[a], 32 * kc, bd.y);
       }
       __syncwarp();
       for (int n = 0; n < ntile; ++n) {
         mbar_wait(&sempty[s], sph ^ 1);
         if (elect_one()) {
-          sinfo[s] = make_int4(bd.x, bd.y, 32 * n, a | (n == 0 ? 2 : 0) | (n == ntile - 1 ? 4 : 0));
+          const int n0 = bd.z + kO5TileN * n;
+          sinfo[s] = make_int4(bd.x, bd.y, n0, a | (n == 0 ? 2 : 0) | (n == ntile - 1 ? 4 : 0));
           uint8_t* st = smem + s * stage_bytes;
-          mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox + 2 * nkc * b_bytes);
+          mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox + 2 * nkc * kO5BBox);
           for (int q = 0; q < nstreams; ++q)
-            tma_load_2d(st + q * kO5StreamBox, &mp->s[q], &sfull[s], 32 * n, bd.y);
+            tma_load_2d(st + q * kO5StreamBox, &mp->s[q], &sfull[s], n0, bd.y);
           uint8_t* bb = st + 4 * kO5StreamBox;
           for (int kc = 0; kc < nkc; ++kc) {
-            tma_load_2d(bb + kc * b_bytes, &mp->bh, &sfull[s], 32 * kc, 32 * n);
-            tma_load_2d(bb + (nkc + kc) * b_bytes, &mp->bl, &sfull[s], 32 * kc, 32 * n);
+            tma_load_2d(bb + kc * kO5BBox, &mp->bh, &sfull[s], 32 * kc, n0);
+            tma_load_2d(bb + (nkc + kc) * kO5BBox, &mp->bl, &sfull[s], 32 * kc, n0);
           }
         }
         __syncwarp();
-        if (++s == kO5Stages) {
+        if (++s == nst) {
           s = 0;
           sph ^= 1;
         }
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    const uint32_t idesc = idesc_tf32(32, false, false);
+    const uint32_t idesc = idesc_tf32(kO5TileN, false, false);
     int s = 0, a = 0, c = 0;
     uint32_t sph = 0, cph = 0, aph[2] = {0, 0};
     for (;;) {
@@ -229,8 +235,8 @@ __global__ void __launch_bounds__(kO5Threads, 1)
       const uint32_t bbase = su32(smem + s * stage_bytes + 4 * kO5StreamBox);
       const uint64_t a0 = sdesc(abase, 16u, 1024u);
       const uint64_t bh0 = sdesc(bbase, 16u, 1024u);
-      const uint64_t bl0 = sdesc(bbase + nkc * b_bytes, 16u, 1024u);
-      const uint32_t dacc = tmem + 64u * c, sacc = dacc + 32u;
+      const uint64_t bl0 = sdesc(bbase + nkc * kO5BBox, 16u, 1024u);
+      const uint32_t dacc = tmem + 32u * c, sacc = dacc + 16u;
       const int K = D * t.r;
       const int s_lo = self_index * t.r, s_hi = s_lo + t.r;
       if (elect_one()) {
@@ -239,9 +245,9 @@ __global__ void __launch_bounds__(kO5Threads, 1)
           for (int kk = 0; kk < 4; ++kk) {
             const int k = 32 * kc + 8 * kk;
             if (k >= K) break;
-            const uint64_t ad = a0 + (uint64_t)((kc * kO5StreamBox + kk * 32) >> 4);
-            const uint64_t bh = bh0 + (uint64_t)((kc * b_bytes + kk * 32) >> 4);
-            const uint64_t bl = bl0 + (uint64_t)((kc * b_bytes + kk * 32) >> 4);
+            const uint64_t ad = a0 + (uint64_t)((kc * kO5ABox + kk * 32) >> 4);
+            const uint64_t bh = bh0 + (uint64_t)((kc * kO5BBox + kk * 32) >> 4);
+            const uint64_t bl = bl0 + (uint64_t)((kc * kO5BBox + kk * 32) >> 4);
             const uint32_t first = (kc == 0 && kk == 0) ? 0u : 1u;
             mma_tf32(dacc, ad, bh, idesc, first);
             mma_tf32(dacc, ad, bl, idesc, 1u);
@@ -256,7 +262,7 @@ __global__ void __launch_bounds__(kO5Threads, 1)
         if (last_in_band) mma_commit(&aempty[a]);
       }
       __syncwarp();
-      if (++s == kO5Stages) {
+      if (++s == nst) {
         s = 0;
         sph ^= 1;
       }
@@ -269,9 +275,8 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     const int quarter = warp % 4, half = (warp - 2) / 4;
     const int row = quarter * 32 + lane;  // tile row (TMEM lane)
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const float invD = __fdiv_rn(1.0f, (float)D);
     double num = 0.0, den = 0.0, dn = 0.0, en = 0.0, nf = 0.0;
-    int s = 0, c = 0;
+    int s = 0, c = 0, prev_s = -1;
     uint32_t sph = 0, cph = 0;
     for (;;) {
       mbar_wait(&sfull[s], sph);
@@ -280,21 +285,21 @@ __global__ void __launch_bounds__(kO5Threads, 1)
       const DevT2 t = T[tl.x];
       mbar_wait(&accfull[c], cph);
       tc_fence_after();
-      float dv[16], sv[16];
-      tmem_ld16(tmem + lane_base + 64u * c + 16u * half, dv);
-      if (SELF && D > 1) tmem_ld16(tmem + lane_base + 64u * c + 32u + 16u * half, sv);
+      float dv[8], sv[8];
+      tmem_ld8(tmem + lane_base + 32u * c + 8u * half, dv);
+      if (SELF && D > 1) tmem_ld8(tmem + lane_base + 32u * c + 16u + 8u * half, sv);
       tc_fence_before();
       mbar_arrive(&accempty[c]);
       uint8_t* st = smem + s * stage_bytes;
       const int64_t grow = tl.y + row;
-      const int64_t col0 = tl.z + 16 * half;
+      const int64_t col0 = tl.z + 8 * half;
       const bool live_row = grow < t.a;
       float fnum = 0.f, fden = 0.f, fen = 0.f, fdn = 0.f;
       int bad = 0;
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const int chunk = 4 * half + q4;  // 16-B chunk of the 128-B row
-        const uint32_t off = row * 128u + ((chunk ^ (row & 7)) * 16u);
+      for (int q2 = 0; q2 < 2; ++q2) {
+        const int chunk = 2 * half + q2;  // 16-B chunk of the 64-B row (SW64)
+        const uint32_t off = row * 64u + ((chunk ^ ((row >> 1) & 3)) * 16u);
         float4* pp = reinterpret_cast<float4*>(st + 0 * kO5StreamBox + off);
         float4* pa = reinterpret_cast<float4*>(st + 1 * kO5StreamBox + off);
         float4* pv = reinterpret_cast<float4*>(st + 2 * kO5StreamBox + off);
@@ -306,15 +311,15 @@ __global__ void __launch_bounds__(kO5Threads, 1)
         float op[4], oa[4], ov[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float delta = dv[4 * q4 + j];
+          const float delta = dv[4 * q2 + j];
           const EpiOut o = epilogue(delta, ip[j], ia[j], il[j], iv[j], mode, gamma, beta, classical);
           op[j] = o.pend;
           oa[j] = o.anchor;
           ov[j] = o.v;
-          const bool live = live_row && (col0 + 4 * q4 + j) < t.b;
+          const bool live = live_row && (col0 + 4 * q2 + j) < t.b;
           if (live) {
             if (SELF) {
-              const float rec = D > 1 ? __fmul_rn(sv[4 * q4 + j], (float)D) : __fmul_rn(delta, (float)D);
+              const float rec = D > 1 ? __fmul_rn(sv[4 * q2 + j], (float)D) : __fmul_rn(delta, (float)D);
               const float df = rec - ip[j];
               fnum = fmaf(df, df, fnum);
               fden = fmaf(ip[j], ip[j], fden);
@@ -328,7 +333,6 @@ __global__ void __launch_bounds__(kO5Threads, 1)
         *pa = make_float4(oa[0], oa[1], oa[2], oa[3]);
         *pv = make_float4(ov[0], ov[1], ov[2], ov[3]);
       }
-      (void)invD;
       num += fnum;
       den += fden;
       en += fen;
@@ -340,10 +344,15 @@ __global__ void __launch_bounds__(kO5Threads, 1)
         const O5Maps* mp = maps + tl.x;
         for (int q = 0; q < 3; ++q) tma_store_2d(&mp->s[q], st + q * kO5StreamBox, tl.z, tl.y);
         bulk_commit();
-        bulk_wait_read0();  // the stage may be refilled once the stores have read it
-        mbar_arrive(&sempty[s]);
+        // a stage may be refilled once its stores have read it: release the previous tile's
+        // stage (its store group is the older one), keeping the store latency off this path
+        if (prev_s >= 0) {
+          bulk_wait_read1();
+          mbar_arrive(&sempty[prev_s]);
+        }
+        prev_s = s;
       }
-      if (++s == kO5Stages) {
+      if (++s == nst) {
         s = 0;
         sph ^= 1;
       }
@@ -368,7 +377,7 @@ __global__ void __launch_bounds__(kO5Threads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
   }
 }
 
@@ -386,14 +395,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 o5_encode() {
 }
 
 static void o5_encode_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1,
-                          uint64_t stride_bytes, uint32_t b0, uint32_t b1) {
+                          uint64_t stride_bytes, uint32_t b0, uint32_t b1,
+                          CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   const cuuint64_t dims[2] = {d0, d1};
   const cuuint64_t strides[1] = {stride_bytes};
   const cuuint32_t box[2] = {b0, b1};
   const cuuint32_t es[2] = {1, 1};
   CUresult r = o5_encode()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled (K5 tc) failed");
 }
@@ -410,8 +420,8 @@ struct O5State : PlanExt {
   int64_t a_elems = 0, b_elems = 0;
   int64_t params = 0;  // 2-D parameters covered
   int s0 = 0, s1 = 0;  // slot range
-  std::vector<int2> bands;  // (t2 slot, m0) in claim order
-  int2* d_bands = nullptr;
+  std::vector<int4> bands;  // (t2 slot, m0, first column, columns) in claim order
+  int4* d_bands = nullptr;
   int* d_ctr = nullptr;
   int64_t* d_aoff = nullptr;
   int64_t* d_boff = nullptr;
@@ -466,8 +476,12 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   const int g = static_cast<int>(std::min<size_t>(S.tiles.size(), sms));
   S.off.resize(g + 1);
   for (int b = 0; b <= g; ++b) S.off[b] = static_cast<int>(S.tiles.size() * b / g);
+  constexpr int kChunkCols = 128;
   for (const int4& tl : S.tiles)
-    if (tl.z == 0) S.bands.push_back(make_int2(tl.x, tl.y));
+    if (tl.z % kChunkCols == 0) {
+      const int64_t b = P.t2[tl.x].b;
+      S.bands.push_back(make_int4(tl.x, tl.y, tl.z, static_cast<int>(std::min<int64_t>(kChunkCols, b - tl.z))));
+    }
   S.d_bands = plan_upload(P, S.bands, 1);
   S.d_ctr = static_cast<int*>(P.dev_alloc(sizeof(int)));
   S.d_tiles = plan_upload(P, S.tiles, 1);
@@ -504,10 +518,11 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
       const float* srcs[4] = {pending, anchor, velocity, local};
       for (int q = 0; q < 4; ++q)
         if (srcs[q] && (q < 3 || mode == DLX_MODE_OVERLAPPED))
-          o5_encode_map(&m.s[q], srcs[q] + t.off, t.b, t.a, t.b * 4, 32, 128);
+          o5_encode_map(&m.s[q], srcs[q] + t.off, t.b, t.a, t.b * 4, kO5TileN, 128,
+                        CU_TENSOR_MAP_SWIZZLE_64B);
       o5_encode_map(&m.a, A + S.aoff[k], KA, t.lda, KA * 4, 32, 128);
-      o5_encode_map(&m.bh, Bh + S.boff[k], KA, t.ldb, KA * 4, 32, 32);
-      o5_encode_map(&m.bl, Bl + S.boff[k], KA, t.ldb, KA * 4, 32, 32);
+      o5_encode_map(&m.bh, Bh + S.boff[k], KA, t.ldb, KA * 4, 32, kO5TileN);
+      o5_encode_map(&m.bl, Bl + S.boff[k], KA, t.ldb, KA * 4, 32, kO5TileN);
     }
     DLX_CUDA(cudaMemcpyAsync(S.d_maps, S.h_maps.data(), sizeof(O5Maps) * P.t2.size(),
                              cudaMemcpyHostToDevice, s));
@@ -515,8 +530,11 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
     std::copy(key, key + 7, S.key);
   }
   const int nkc = KA / 32;
-  const size_t smem = 1024 + kO5Stages * (4 * kO5StreamBox + 2 * nkc * 4096) +
-                      2 * nkc * kO5StreamBox + 12 * 8 + 16 + 16 * kO5Stages;
+  const size_t stage = 4 * kO5StreamBox + 2 * nkc * kO5BBox;
+  const size_t fixed = 1024 + 2 * nkc * kO5ABox + 16;
+  const int nst = static_cast<int>(std::min<size_t>(
+      kO5MaxStages, (215 * 1024 - fixed) / (stage + 2 * 8 + 16)));
+  const size_t smem = fixed + nst * (stage + 2 * 8 + 16) + 8 * 8;
   const int grid = std::min(static_cast<int>(S.bands.size()), static_cast<int>(S.off.size()) - 1);
   const int nbands = static_cast<int>(S.bands.size());
   DLX_CUDA(cudaMemsetAsync(S.d_ctr, 0, sizeof(int), s));
@@ -531,10 +549,10 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   KernelTimer timer("k_o5", (mode == DLX_MODE_OVERLAPPED ? 28.0 : 24.0) * S.params, s);
   if (self_index >= 0)
     k_o5<true><<<grid, kO5Threads, smem, s>>>(P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, KA,
-                                             self_index, mode, gamma, beta, classical, stats);
+                                             nst, self_index, mode, gamma, beta, classical, stats);
   else
     k_o5<false><<<grid, kO5Threads, smem, s>>>(P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, KA,
-                                              self_index, mode, gamma, beta, classical, stats);
+                                              nst, self_index, mode, gamma, beta, classical, stats);
   DLX_LAUNCHED();
 }
 
