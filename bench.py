@@ -51,8 +51,8 @@ def parse():
                          "controller every round but time at rank1 = 32, the configured rank)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-side-stream", action="store_true",
-                    help="run the effective-rank measurement on the main stream")
+    ap.add_argument("--side-stream", action="store_true",
+                    help="run the effective-rank measurement on a side stream")
     return ap.parse_args()
 
 
@@ -214,7 +214,7 @@ def main():
     cfg = OuterConfig(rank1=args.rank, qbits=args.qbits, adaptive=not args.no_adaptive,
                       H1=125, window_c=5, tau=0.5, power_iters=2, seed=1, overlap=True,
                       hold_rank=not args.follow_controller)
-    eng = OuterSync(L, cfg, anchor, world=world, rank=rank, side_stream=not args.no_side_stream)
+    eng = OuterSync(L, cfg, anchor, world=world, rank=rank, side_stream=args.side_stream)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -267,7 +267,8 @@ def main():
         phases[n0] = phases.get(n0, 0.0) + e0.elapsed_time(e1)
     phases = {k: v / args.steps for k, v in phases.items()}
     if eng.side_events:
-        phases["effective_rank(side)"] = sum(a.elapsed_time(b) for a, b in eng.side_events) / args.steps
+        phases["effective_rank (" + ("side stream" if args.side_stream else "inside outer_update") + ")"] = \
+            sum(a.elapsed_time(b) for a, b in eng.side_events) / args.steps
     eng.phase_events = None
 
     # ---------------- roofline of the dominant kernel (CUDA events around each launch)

@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "dlx_internal.cuh"
@@ -532,8 +533,12 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   const int nkc = KA / 32;
   const size_t stage = 4 * kO5StreamBox + 2 * nkc * kO5BBox;
   const size_t fixed = 1024 + 2 * nkc * kO5ABox + 16;
+  static const size_t budget = [] {  // experiments: DLX_O5_SMEM_KB
+    const char* e = getenv("DLX_O5_SMEM_KB");
+    return static_cast<size_t>(e ? atoi(e) : 190) * 1024;
+  }();
   const int nst = static_cast<int>(std::min<size_t>(
-      kO5MaxStages, (215 * 1024 - fixed) / (stage + 2 * 8 + 16)));
+      kO5MaxStages, (budget - fixed) / (stage + 2 * 8 + 16)));
   const size_t smem = fixed + nst * (stage + 2 * 8 + 16) + 8 * 8;
   const int grid = std::min(static_cast<int>(S.bands.size()), static_cast<int>(S.off.size()) - 1);
   const int nbands = static_cast<int>(S.bands.size());
