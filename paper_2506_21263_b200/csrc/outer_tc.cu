@@ -535,7 +535,7 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   const size_t fixed = 1024 + 2 * nkc * kO5ABox + 16;
   static const size_t budget = [] {  // experiments: DLX_O5_SMEM_KB
     const char* e = getenv("DLX_O5_SMEM_KB");
-    return static_cast<size_t>(e ? atoi(e) : 190) * 1024;
+    return static_cast<size_t>(e ? atoi(e) : 215) * 1024;
   }();
   const int nst = static_cast<int>(std::min<size_t>(
       kO5MaxStages, (budget - fixed) / (stage + 2 * 8 + 16)));
