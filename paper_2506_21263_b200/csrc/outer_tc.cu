@@ -16,10 +16,12 @@
 // A-band buffers and two TMEM accumulators keep loads, MMAs and epilogues overlapped.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "dlx_internal.cuh"
 #include "ptx.cuh"
@@ -31,27 +33,49 @@ constexpr int kO5Threads = 320;
 constexpr int kO5MaxStages = 6;
 constexpr int kO5TileN = 16;                          // tile = 128 rows x 16 columns
 constexpr uint32_t kO5StreamBox = 128 * kO5TileN * 4;  // 8 KB per streamed operand (SW64)
-constexpr uint32_t kO5ABox = 128 * 32 * 4;            // 16 KB: 128 rows x 32 K of A (SW128)
-constexpr uint32_t kO5BBox = kO5TileN * 32 * 4;       // 2 KB: 16 rows x 32 K of B (SW128)
+constexpr uint32_t kO5ABox = 128 * 128;               // 16 KB: 128 rows x 128 B of K (SW128)
+constexpr uint32_t kO5BBox = kO5TileN * 128;          // 2 KB: 16 rows x 128 B of K (SW128)
+
+// Operand kinds of the factor GEMM. K = D r <= 32: tf32, A exact, B = hi + lo (2 MMAs per
+// k-step of 8). K > 32 (more workers): bf16, A exact (|code| <= 127), B = b1 + b2 + b3 with
+// each term the bf16 rounding of the remainder (24 significant bits, 3 MMAs per k-step of
+// 16) — half the operand bytes per K, so K = 256 (D = 8 at r = 32) still fits the stages.
+template <bool BF>
+struct O5Kind {
+  static constexpr int ES = BF ? 2 : 4;    // bytes per operand element
+  static constexpr int AK = 128 / ES;      // K elements per 128-B swizzle atom row
+  static constexpr int KS = BF ? 16 : 8;   // MMA K per instruction (32 B)
+  static constexpr int NBP = BF ? 3 : 2;   // B planes
+};
 
 struct O5Maps {
   CUtensorMap s[4];  // pending, anchor, velocity, local: dims {b, a}, box {16, 128}, SW64
-  CUtensorMap a;     // A (codes of P): dims {KA, lda}, box {32, 128}, SW128
-  CUtensorMap bh, bl;  // B hi / lo: dims {KA, ldb}, box {32, 16}, SW128
+  CUtensorMap a;     // A (codes of P): dims {KA, lda}, box {AK, 128}, SW128
+  CUtensorMap b[3];  // B planes: dims {KA, ldb}, box {AK, 16}, SW128
 };
 
 // ------------------------------------------------------------------ prep: A and B operands
-// One thread per (slot, side, row, w): writes K-major rows of A (side 0) or B hi/lo (side 1).
-constexpr int kPrepRows = 64;  // factor rows per k_o5_prep block
+template <bool BF>
+constexpr int prep_rows() { return BF ? 32 : 64; }  // factor rows per k_o5_prep block
+
+__device__ __forceinline__ void o5_store(float* p, float v) { *p = v; }
+__device__ __forceinline__ void o5_store(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
 
 // Block = 64 consecutive factor rows: codes are decoded column by column (coalesced over
 // rows), staged in shared memory, and written row-major [row][KA] with coalesced stores.
+// A = code of P (exact); B = code_Q * s_P * s_Q / D split into NBP planes.
+template <bool BF>
 __global__ void __launch_bounds__(256) k_o5_prep(
     const DevT2* __restrict__ T, const int4* __restrict__ rows, int nrows,
     const int64_t* __restrict__ aoff, const int64_t* __restrict__ boff,
     const uint8_t* __restrict__ gathered, int64_t pay_bytes, int qbits, int D, int KA,
-    float* __restrict__ A, float* __restrict__ Bh, float* __restrict__ Bl) {
-  __shared__ float tile[kPrepRows][65];
+    void* __restrict__ A_, void* __restrict__ B0_, void* __restrict__ B1_,
+    void* __restrict__ B2_) {
+  using E = typename std::conditional<BF, __nv_bfloat16, float>::type;
+  E* A = static_cast<E*>(A_);
+  E* Bp[3] = {static_cast<E*>(B0_), static_cast<E*>(B1_), static_cast<E*>(B2_)};
+  constexpr int kPrepRows = prep_rows<BF>();
+  __shared__ float tile[kPrepRows][BF ? 257 : 65];
   const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kPrepRows;
   const float invD = __fdiv_rn(1.0f, (float)D);
   {
@@ -94,12 +118,22 @@ __global__ void __launch_bounds__(256) k_o5_prep(
     const int4 rw = rows[g];
     const float v = tile[rl][k];
     if (rw.y == 0) {
-      A[aoff[rw.x] + static_cast<int64_t>(rw.z) * KA + k] = v;
+      o5_store(&A[aoff[rw.x] + static_cast<int64_t>(rw.z) * KA + k], v);
     } else {
       const int64_t o = boff[rw.x] + static_cast<int64_t>(rw.z) * KA + k;
-      const float h = tf32_hi(v);
-      Bh[o] = h;
-      Bl[o] = v - h;
+      if (!BF) {
+        const float h = tf32_hi(v);
+        o5_store(&Bp[0][o], h);
+        o5_store(&Bp[1][o], v - h);
+      } else {
+        float rem = v;
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl) {
+          const __nv_bfloat16 b = __float2bfloat16_rn(rem);
+          reinterpret_cast<__nv_bfloat16*>(Bp[pl])[o] = b;
+          rem = rem - __bfloat162float(b);  // exact
+        }
+      }
     }
   }
 }
@@ -107,19 +141,20 @@ __global__ void __launch_bounds__(256) k_o5_prep(
 // ------------------------------------------------------------------ the kernel
 // 16-column tiles keep 4-5 stages (36 KB each at K = 32) in flight per SM while one is in
 // the epilogue, so the HBM stream does not stall behind a stage that is being written back.
-template <bool SELF>
+template <bool SELF, bool BF>
 __global__ void __launch_bounds__(kO5Threads, 1)
     k_o5(const DevT2* __restrict__ T, const O5Maps* __restrict__ maps,
          const int4* __restrict__ bands, int nbands, int* __restrict__ band_ctr, int D, int KA,
-         int nst, int self_index, int mode, float gamma, float beta, int classical,
+         int nst, int nab, int self_index, int mode, float gamma, float beta, int classical,
          dlx_round_stats* stats) {
+  using KD = O5Kind<BF>;
   extern __shared__ __align__(1024) uint8_t o5smem[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(o5smem) + 1023) & ~uintptr_t(1023));
-  const int nkc = KA / 32;                                 // 32-wide K chunks
-  const uint32_t stage_bytes = 4 * kO5StreamBox + 2 * nkc * kO5BBox;
+  const int nkc = KA / KD::AK;                             // 128-B K chunks
+  const uint32_t stage_bytes = 4 * kO5StreamBox + KD::NBP * nkc * kO5BBox;
   const uint32_t aband_bytes = nkc * kO5ABox;              // 128 rows x KA
   uint8_t* abuf = smem + nst * stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(abuf + 2 * aband_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(abuf + nab * aband_bytes);
   uint64_t* sfull = bars;                // [nst]
   uint64_t* sempty = sfull + nst;        // [nst]
   uint64_t* afull = sempty + nst;        // [2]
@@ -176,13 +211,13 @@ __global__ void __launch_bounds__(kO5Threads, 1)
       const int4 bd = bands[band];  // (slot, m0, first column, columns)
       const O5Maps* mp = maps + bd.x;
       const int ntile = (bd.w + kO5TileN - 1) / kO5TileN;
-      a = (a + 1) & 1;
+      a = nab == 2 ? (a + 1) & 1 : 0;
       mbar_wait(&aempty[a], aph[a] ^ 1);
       aph[a] ^= 1;
       if (elect_one()) {
         mbar_expect_tx(&afull[a], aband_bytes);
         for (int kc = 0; kc < nkc; ++kc)
-          tma_load_2d(abuf + a * aband_bytes + kc * kO5ABox, &mp->a, &afull[a], 32 * kc, bd.y);
+          tma_load_2d(abuf + a * aband_bytes + kc * kO5ABox, &mp->a, &afull[a], KD::AK * kc, bd.y);
       }
       __syncwarp();
       for (int n = 0; n < ntile; ++n) {
@@ -191,14 +226,13 @@ __global__ void __launch_bounds__(kO5Threads, 1)
           const int n0 = bd.z + kO5TileN * n;
           sinfo[s] = make_int4(bd.x, bd.y, n0, a | (n == 0 ? 2 : 0) | (n == ntile - 1 ? 4 : 0));
           uint8_t* st = smem + s * stage_bytes;
-          mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox + 2 * nkc * kO5BBox);
+          mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox + KD::NBP * nkc * kO5BBox);
           for (int q = 0; q < nstreams; ++q)
             tma_load_2d(st + q * kO5StreamBox, &mp->s[q], &sfull[s], n0, bd.y);
           uint8_t* bb = st + 4 * kO5StreamBox;
-          for (int kc = 0; kc < nkc; ++kc) {
-            tma_load_2d(bb + kc * kO5BBox, &mp->bh, &sfull[s], 32 * kc, n0);
-            tma_load_2d(bb + (nkc + kc) * kO5BBox, &mp->bl, &sfull[s], 32 * kc, n0);
-          }
+          for (int pl = 0; pl < KD::NBP; ++pl)
+            for (int kc = 0; kc < nkc; ++kc)
+              tma_load_2d(bb + (pl * nkc + kc) * kO5BBox, &mp->b[pl], &sfull[s], KD::AK * kc, n0);
         }
         __syncwarp();
         if (++s == nst) {
@@ -216,7 +250,7 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    const uint32_t idesc = idesc_tf32(kO5TileN, false, false);
+    const uint32_t idesc = BF ? idesc_bf16(kO5TileN) : idesc_tf32(kO5TileN, false, false);
     int s = 0, a = 0, c = 0;
     uint32_t sph = 0, cph = 0, aph[2] = {0, 0};
     for (;;) {
@@ -235,27 +269,33 @@ __global__ void __launch_bounds__(kO5Threads, 1)
       const uint32_t abase = su32(abuf + a * aband_bytes);
       const uint32_t bbase = su32(smem + s * stage_bytes + 4 * kO5StreamBox);
       const uint64_t a0 = sdesc(abase, 16u, 1024u);
-      const uint64_t bh0 = sdesc(bbase, 16u, 1024u);
-      const uint64_t bl0 = sdesc(bbase + nkc * kO5BBox, 16u, 1024u);
+      uint64_t b0[KD::NBP];
+#pragma unroll
+      for (int pl = 0; pl < KD::NBP; ++pl) b0[pl] = sdesc(bbase + pl * nkc * kO5BBox, 16u, 1024u);
       const uint32_t dacc = tmem + 32u * c, sacc = dacc + 16u;
       const int K = D * t.r;
       const int s_lo = self_index * t.r, s_hi = s_lo + t.r;
+      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc) {
+        if (BF)
+          mma_bf16(d, ad, bd, idesc, acc);
+        else
+          mma_tf32(d, ad, bd, idesc, acc);
+      };
       if (elect_one()) {
         for (int kc = 0; kc < nkc; ++kc) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const int k = 32 * kc + 8 * kk;
+            const int k = KD::AK * kc + KD::KS * kk;
             if (k >= K) break;
             const uint64_t ad = a0 + (uint64_t)((kc * kO5ABox + kk * 32) >> 4);
-            const uint64_t bh = bh0 + (uint64_t)((kc * kO5BBox + kk * 32) >> 4);
-            const uint64_t bl = bl0 + (uint64_t)((kc * kO5BBox + kk * 32) >> 4);
+            const uint64_t boff = (uint64_t)((kc * kO5BBox + kk * 32) >> 4);
             const uint32_t first = (kc == 0 && kk == 0) ? 0u : 1u;
-            mma_tf32(dacc, ad, bh, idesc, first);
-            mma_tf32(dacc, ad, bl, idesc, 1u);
+#pragma unroll
+            for (int pl = 0; pl < KD::NBP; ++pl) mma(dacc, ad, b0[pl] + boff, pl == 0 ? first : 1u);
             if (SELF && D > 1 && k >= s_lo && k < s_hi) {
               const uint32_t sfirst = k == s_lo ? 0u : 1u;
-              mma_tf32(sacc, ad, bh, idesc, sfirst);
-              mma_tf32(sacc, ad, bl, idesc, 1u);
+#pragma unroll
+              for (int pl = 0; pl < KD::NBP; ++pl) mma(sacc, ad, b0[pl] + boff, pl == 0 ? sfirst : 1u);
             }
           }
         }
@@ -397,24 +437,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 o5_encode() {
 
 static void o5_encode_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1,
                           uint64_t stride_bytes, uint32_t b0, uint32_t b1,
-                          CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                          CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+                          CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
   const cuuint64_t dims[2] = {d0, d1};
   const cuuint64_t strides[1] = {stride_bytes};
   const cuuint32_t box[2] = {b0, b1};
   const cuuint32_t es[2] = {1, 1};
-  CUresult r = o5_encode()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
-                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = o5_encode()(m, dt, 2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled (K5 tc) failed");
 }
 
+constexpr int kO5MaxK = 256;
+
 struct O5State : PlanExt {
   int D = 0, KA = 0;
-  std::vector<int4> tiles;
-  std::vector<int> off;
-  int4* d_tiles = nullptr;
-  int* d_off = nullptr;
+  bool bf = false;         // bf16 x 3 operands (K > 32) vs tf32 x 2
+  int nab = 2, nst = 0;    // A-band buffers, stream stages
+  size_t smem = 0;
   std::vector<int4> rows;
   int4* d_rows = nullptr;
   std::vector<int64_t> aoff, boff;  // per slot: element offsets of A [lda][KA], B [ldb][KA]
@@ -428,18 +469,19 @@ struct O5State : PlanExt {
   int64_t* d_boff = nullptr;
   O5Maps* d_maps = nullptr;
   std::vector<O5Maps> h_maps;
-  const void* key[7] = {};
+  const void* key[8] = {};
 };
 
 bool o5_eligible(const Plan& P, int D, int self_index) {
   if (P.t2.empty()) return false;
   const int K = D * P.rmax;
-  if (K > 64) return false;  // A band (128 x K) and B (32 x K hi/lo) staging budget
+  if (K > kO5MaxK) return false;  // A band (128 x K) + B stages must fit shared memory
   for (const DevT2& t : P.t2)
     if (t.b % 4 != 0) return false;
+  const int ks = K > 32 ? 16 : 8;  // MMA K step of the operand kind
   if (self_index >= 0 && D > 1)
     for (const DevT2& t : P.t2)
-      if (t.r % 8 != 0) return false;  // own-payload k steps must align with MMA k = 8
+      if (t.r % ks != 0) return false;  // own-payload k steps must align with the MMA K
   return true;
 }
 
@@ -448,18 +490,41 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   O5State& S = plan_ext<O5State>(P, "o5:" + std::to_string(D) + ":" + R.key(), &fresh);
   if (!fresh) return S;
   S.D = D;
-  S.KA = static_cast<int>(round_up(D * P.rmax, 32));
+  const int K = D * P.rmax;
+  S.bf = K > 32;
+  const int ak = S.bf ? O5Kind<true>::AK : O5Kind<false>::AK;
+  const int nbp = S.bf ? 3 : 2;
+  S.KA = static_cast<int>(round_up(K, ak));
   S.s0 = R.s0;
   S.s1 = R.s1;
-  // tiles: per tensor, row band (128) major, then 32-column blocks; balanced contiguous chunks.
-  // A / B staging offsets cover every slot (shared buffers); tiles and rows only the range.
+  // shared-memory plan: A band buffers (double if 3+ stream stages still fit) + stages
+  static const size_t budget = [] {  // experiments: DLX_O5_SMEM_KB
+    const char* e = getenv("DLX_O5_SMEM_KB");
+    return static_cast<size_t>(e ? atoi(e) : 215) * 1024;
+  }();
+  const int nkc = S.KA / ak;
+  const size_t stage = 4 * kO5StreamBox + nbp * nkc * kO5BBox + 2 * 8 + 16;
+  const size_t aband = static_cast<size_t>(nkc) * kO5ABox;
+  auto stages = [&](int nab) {
+    const size_t fixed = 1024 + nab * aband + 16 + 8 * 8;
+    return budget > fixed ? static_cast<int>(std::min<size_t>(kO5MaxStages, (budget - fixed) / stage)) : 0;
+  };
+  S.nab = stages(2) >= 3 ? 2 : 1;
+  S.nst = stages(S.nab);
+  if (S.nst < 2) raise(DLX_ERR_VALIDATION, "outer update: K too large for the tensor-core path");
+  S.smem = 1024 + S.nab * aband + 16 + 8 * 8 + S.nst * stage;
+  // A / B staging offsets cover every slot (shared buffers); bands and rows only the range.
+  // Work unit = a chunk of a row band (128 rows x chunk columns); chunks are claimed in
+  // band-major order so concurrently active CTAs read adjacent columns of the same rows.
+  const int64_t chunk = S.nab == 2 ? 128 : 256;  // single A buffer: amortise its reload
   for (size_t k = 0; k < P.t2.size(); ++k) {
     const DevT2& t = P.t2[k];
     const bool in = static_cast<int>(k) >= R.s0 && static_cast<int>(k) < R.s1;
     if (in) {
       for (int64_t m0 = 0; m0 < t.a; m0 += 128)
-        for (int64_t n0 = 0; n0 < t.b; n0 += 32)
-          S.tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0), static_cast<int>(n0), 0));
+        for (int64_t n0 = 0; n0 < t.b; n0 += chunk)
+          S.bands.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0),
+                                      static_cast<int>(n0), static_cast<int>(std::min(chunk, t.b - n0))));
       for (int side = 0; side < 2; ++side) {
         const int64_t ld = side == 0 ? t.lda : t.ldb;
         for (int64_t r = 0; r < ld; ++r) S.rows.push_back(make_int4(static_cast<int>(k), side, static_cast<int>(r), 0));
@@ -471,22 +536,8 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
     S.a_elems += t.lda * S.KA;
     S.b_elems += t.ldb * S.KA;
   }
-  int dev = 0, sms = 0;
-  DLX_CUDA(cudaGetDevice(&dev));
-  DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int g = static_cast<int>(std::min<size_t>(S.tiles.size(), sms));
-  S.off.resize(g + 1);
-  for (int b = 0; b <= g; ++b) S.off[b] = static_cast<int>(S.tiles.size() * b / g);
-  constexpr int kChunkCols = 128;
-  for (const int4& tl : S.tiles)
-    if (tl.z % kChunkCols == 0) {
-      const int64_t b = P.t2[tl.x].b;
-      S.bands.push_back(make_int4(tl.x, tl.y, tl.z, static_cast<int>(std::min<int64_t>(kChunkCols, b - tl.z))));
-    }
   S.d_bands = plan_upload(P, S.bands, 1);
   S.d_ctr = static_cast<int*>(P.dev_alloc(sizeof(int)));
-  S.d_tiles = plan_upload(P, S.tiles, 1);
-  S.d_off = plan_upload(P, S.off, 1);
   S.d_rows = plan_upload(P, S.rows, 1);
   S.d_aoff = plan_upload(P, S.aoff, 1);
   S.d_boff = plan_upload(P, S.boff, 1);
@@ -495,23 +546,47 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   return S;
 }
 
+template <bool SELF, bool BF>
+static void launch_o5(const Plan& P, const O5State& S, int grid, int nbands, int D, int self_index,
+                      int mode, float gamma, float beta, int classical, dlx_round_stats* stats,
+                      cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    DLX_CUDA(cudaFuncSetAttribute(k_o5<SELF, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  k_o5<SELF, BF><<<grid, kO5Threads, S.smem, s>>>(P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D,
+                                                  S.KA, S.nst, S.nab, self_index, mode, gamma,
+                                                  beta, classical, stats);
+}
+
 void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                         int self_index, int mode, float* pending, float* anchor,
                         const float* local, float* velocity, float gamma, float beta,
                         int classical, dlx_round_stats* stats, const SlotRange& R,
                         cudaStream_t s) {
   O5State& S = o5_state(P, D, R);
-  if (S.tiles.empty()) return;
+  if (S.bands.empty()) return;
   const int KA = S.KA;
-  float* A = static_cast<float*>(ctx->scratch("o5_A", sizeof(float) * (S.a_elems + 1024)));
-  float* Bh = static_cast<float*>(ctx->scratch("o5_Bh", sizeof(float) * (S.b_elems + 1024)));
-  float* Bl = static_cast<float*>(ctx->scratch("o5_Bl", sizeof(float) * (S.b_elems + 1024)));
-  k_o5_prep<<<static_cast<unsigned>(ceil_div(S.rows.size(), kPrepRows)), 256, 0, s>>>(
-      P.d_t2, S.d_rows, static_cast<int>(S.rows.size()), S.d_aoff, S.d_boff, gathered,
-      P.payload_bytes, P.qbits, D, KA, A, Bh, Bl);
+  const size_t es = S.bf ? 2 : 4;
+  void* A = ctx->scratch("o5_A", es * (S.a_elems + 1024));
+  void* B[3] = {ctx->scratch("o5_B0", es * (S.b_elems + 1024)),
+                ctx->scratch("o5_B1", es * (S.b_elems + 1024)),
+                S.bf ? ctx->scratch("o5_B2", es * (S.b_elems + 1024)) : nullptr};
+  if (S.bf)
+    k_o5_prep<true><<<static_cast<unsigned>(ceil_div(S.rows.size(), prep_rows<true>())), 256, 0, s>>>(
+        P.d_t2, S.d_rows, static_cast<int>(S.rows.size()), S.d_aoff, S.d_boff, gathered,
+        P.payload_bytes, P.qbits, D, KA, A, B[0], B[1], B[2]);
+  else
+    k_o5_prep<false><<<static_cast<unsigned>(ceil_div(S.rows.size(), prep_rows<false>())), 256, 0, s>>>(
+        P.d_t2, S.d_rows, static_cast<int>(S.rows.size()), S.d_aoff, S.d_boff, gathered,
+        P.payload_bytes, P.qbits, D, KA, A, B[0], B[1], B[2]);
   DLX_LAUNCHED();
-  const void* key[7] = {pending, anchor, velocity, mode == DLX_MODE_OVERLAPPED ? local : nullptr, A, Bh, Bl};
-  if (!std::equal(key, key + 7, S.key)) {
+  const void* key[8] = {pending, anchor, velocity, mode == DLX_MODE_OVERLAPPED ? local : nullptr,
+                        A, B[0], B[1], B[2]};
+  if (!std::equal(key, key + 8, S.key)) {
+    const CUtensorMapDataType dt = S.bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const uint32_t ak = S.bf ? O5Kind<true>::AK : O5Kind<false>::AK;
     for (size_t k = S.s0; k < static_cast<size_t>(S.s1); ++k) {
       const DevT2& t = P.t2[k];
       O5Maps& m = S.h_maps[k];
@@ -521,43 +596,37 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
         if (srcs[q] && (q < 3 || mode == DLX_MODE_OVERLAPPED))
           o5_encode_map(&m.s[q], srcs[q] + t.off, t.b, t.a, t.b * 4, kO5TileN, 128,
                         CU_TENSOR_MAP_SWIZZLE_64B);
-      o5_encode_map(&m.a, A + S.aoff[k], KA, t.lda, KA * 4, 32, 128);
-      o5_encode_map(&m.bh, Bh + S.boff[k], KA, t.ldb, KA * 4, 32, kO5TileN);
-      o5_encode_map(&m.bl, Bl + S.boff[k], KA, t.ldb, KA * 4, 32, kO5TileN);
+      o5_encode_map(&m.a, static_cast<uint8_t*>(A) + es * S.aoff[k], KA, t.lda, KA * es, ak, 128,
+                    CU_TENSOR_MAP_SWIZZLE_128B, dt);
+      for (int pl = 0; pl < (S.bf ? 3 : 2); ++pl)
+        o5_encode_map(&m.b[pl], static_cast<uint8_t*>(B[pl]) + es * S.boff[k], KA, t.ldb, KA * es, ak,
+                      kO5TileN, CU_TENSOR_MAP_SWIZZLE_128B, dt);
     }
     DLX_CUDA(cudaMemcpyAsync(S.d_maps, S.h_maps.data(), sizeof(O5Maps) * P.t2.size(),
                              cudaMemcpyHostToDevice, s));
     DLX_CUDA(cudaStreamSynchronize(s));
-    std::copy(key, key + 7, S.key);
+    std::copy(key, key + 8, S.key);
   }
-  const int nkc = KA / 32;
-  const size_t stage = 4 * kO5StreamBox + 2 * nkc * kO5BBox;
-  const size_t fixed = 1024 + 2 * nkc * kO5ABox + 16;
-  static const size_t budget = [] {  // experiments: DLX_O5_SMEM_KB
-    const char* e = getenv("DLX_O5_SMEM_KB");
-    return static_cast<size_t>(e ? atoi(e) : 215) * 1024;
-  }();
-  const int nst = static_cast<int>(std::min<size_t>(
-      kO5MaxStages, (budget - fixed) / (stage + 2 * 8 + 16)));
-  const size_t smem = fixed + nst * (stage + 2 * 8 + 16) + 8 * 8;
-  const int grid = std::min(static_cast<int>(S.bands.size()), static_cast<int>(S.off.size()) - 1);
+  int dev = 0, sms = 0;
+  DLX_CUDA(cudaGetDevice(&dev));
+  DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int nbands = static_cast<int>(S.bands.size());
+  const int grid = std::min(nbands, sms);
   DLX_CUDA(cudaMemsetAsync(S.d_ctr, 0, sizeof(int), s));
-  static bool attr = false;
-  if (!attr) {
-    DLX_CUDA(cudaFuncSetAttribute(k_o5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    DLX_CUDA(cudaFuncSetAttribute(k_o5<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
   // algorithmic bytes: read pending, anchor, velocity (+ local in overlapped mode), write
   // pending, anchor, velocity — 28 B/param overlapped, 24 B/param sync
   KernelTimer timer("k_o5", (mode == DLX_MODE_OVERLAPPED ? 28.0 : 24.0) * S.params, s);
-  if (self_index >= 0)
-    k_o5<true><<<grid, kO5Threads, smem, s>>>(P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, KA,
-                                             nst, self_index, mode, gamma, beta, classical, stats);
-  else
-    k_o5<false><<<grid, kO5Threads, smem, s>>>(P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, KA,
-                                              nst, self_index, mode, gamma, beta, classical, stats);
+  if (self_index >= 0) {
+    if (S.bf)
+      launch_o5<true, true>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, stats, s);
+    else
+      launch_o5<true, false>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, stats, s);
+  } else {
+    if (S.bf)
+      launch_o5<false, true>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, stats, s);
+    else
+      launch_o5<false, false>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, stats, s);
+  }
   DLX_LAUNCHED();
 }
 

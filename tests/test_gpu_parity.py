@@ -381,10 +381,11 @@ def test_outer_update_identical_on_every_rank(ctx, oracle):
         assert np.array_equal(o, outs[0])
 
 
-@pytest.mark.parametrize("D,rank", [(1, 8), (1, 32), (2, 16), (2, 32)])
+@pytest.mark.parametrize("D,rank", [(1, 8), (1, 32), (2, 16), (2, 32), (3, 32), (4, 32), (8, 32)])
 def test_outer_update_tensor_core_path(ctx, oracle, D, rank):
-    """tcgen05/TMA fused outer update (eligible layouts: b % 4 == 0, D*r <= 64) against the
-    oracle's allreduce_avg and the reference epilogue, with the SIMT path run side by side."""
+    """tcgen05/TMA fused outer update (eligible layouts: b % 4 == 0, K = D*r <= 256; tf32 x 2
+    operands for K <= 32, bf16 x 3 above) against the oracle's allreduce_avg and the reference
+    epilogue, with the SIMT path run side by side."""
     from paper_2506_21263_b200 import api
     import torch
     shapes = [(40, 36), (36,), (200, 64), (64,), (300, 96), (129, 160)]
