@@ -8,6 +8,8 @@
 // per-tensor work is two fp64 Gram matrices (tall-skinny, batched) and one K x K symmetric
 // eigenproblem (cyclic parallel Jacobi, one CTA per tensor). r' can differ from the dense
 // reference only where the prefix energy lands within rounding of tau (ties).
+#include <cuda_bf16.h>
+
 #include "dlx_internal.cuh"
 #include "ptx.cuh"
 
@@ -160,47 +162,207 @@ __global__ void __launch_bounds__(320) k_code_gram(const DevT2* __restrict__ T,
   }
 }
 
-// ------------------------------------------------------------------ eigenproblem
-constexpr int kErSmemDim = 64;  // L, G_A L and M staged in shared memory when n2 <= 64
-constexpr size_t kErSmemBytes = 3 * kErSmemDim * (kErSmemDim + 1) * sizeof(double);
-// (the launch sizes the staging for the largest n2 so small problems fit several CTAs / SM)
+// K up to 256: the same integer Gram on the bf16 tensor cores (mma.sync m16n8k16, fp32
+// accumulate). Codes are exact in bf16 and every per-chunk partial sum is an integer below
+// 1024 * 127^2 < 2^24, so the fp32 accumulation is exact; chunk sums are added as fp64 (exact,
+// order-independent). Block = (1024-row chunk of one factor side, group of 32x32 output
+// tiles of the upper block triangle); 64 rows are decoded per pass into Ct[k][row] (bf16).
+constexpr int kCgmRows = 64;
+constexpr int kCgmLd = kCgmRows + 8;  // bf16 row stride of Ct: conflict-free ldmatrix
+constexpr int kCgmTilesPerWarp = 2;
+constexpr int kCgmWarps = 8;
 
-// Per tensor: G_B = L L^T (semidefinite Cholesky), M = L^T G_A L, cyclic parallel Jacobi,
-// prefix energy. Grams come either as fp64 matrices (GA, GB; row stride rr) or as integer
-// code Grams (GI, upper triangle, stride rr) scaled by the payload's column scales.
-__global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, int D, int rr,
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(su32(p)));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r[0]), "=r"(r[1])
+               : "r"(su32(p)));
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4],
+                                               const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+__global__ void __launch_bounds__(256) k_code_gram_mma(const DevT2* __restrict__ T,
+                                                       const int4* __restrict__ chunks,
+                                                       const uint8_t* __restrict__ gathered,
+                                                       int64_t pay_bytes, int qbits, int D,
+                                                       int kst, double* __restrict__ G) {
+  __shared__ __align__(16) __nv_bfloat16 Ct[256 * kCgmLd];
+  const int4 ch = chunks[blockIdx.x];
+  const DevT2& t = T[ch.x];
+  const int side = ch.y, r = t.r, K = D * r;
+  const int64_t n = side == 0 ? t.a : t.b;
+  const int KP = (K + 31) / 32 * 32;  // padded to whole 32x32 tiles
+  const int nt32 = KP / 32, ntiles = nt32 * (nt32 + 1) / 2;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tile0 = blockIdx.y * kCgmWarps * kCgmTilesPerWarp;
+  if (tile0 >= ntiles) return;  // uniform
+  // decode tasks: (column k, 8-row group) -> one <= 64-bit field of 8 codes
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(gathered);
+  const int64_t nwords = D * pay_bytes / 4;
+  const uint32_t mask = (1u << qbits) - 1u;
+  const int sh = 32 - qbits;
+  const int64_t rend = min((int64_t)ch.w, n);
+  // this warp's output tiles (ti <= tj in 32-blocks)
+  int tI[kCgmTilesPerWarp], tJ[kCgmTilesPerWarp];
+  bool tv[kCgmTilesPerWarp];
+#pragma unroll
+  for (int u = 0; u < kCgmTilesPerWarp; ++u) {
+    const int id = tile0 + warp + kCgmWarps * u;
+    tv[u] = id < ntiles;
+    int bi = 0, rem = tv[u] ? id : 0;
+    while (rem >= nt32 - bi) {
+      rem -= nt32 - bi;
+      ++bi;
+    }
+    tI[u] = bi;
+    tJ[u] = bi + rem;
+  }
+  float acc[kCgmTilesPerWarp][2][4][4];
+#pragma unroll
+  for (int u = 0; u < kCgmTilesPerWarp; ++u)
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[u][a][b][c] = 0.f;
+  const int ntask = KP * (kCgmRows / 8);
+  for (int64_t row0 = ch.z; row0 < ch.w; row0 += kCgmRows) {
+    __syncthreads();
+    for (int task = threadIdx.x; task < ntask; task += 256) {
+      const int k = task / (kCgmRows / 8), tg = task % (kCgmRows / 8);
+      const int64_t rowg = row0 + 8 * tg;
+      uint32_t packed[4] = {0u, 0u, 0u, 0u};
+      if (k < K && rowg < rend) {
+        const int w = k / r, j = k % r;
+        const int64_t bit = ((w * pay_bytes + (side == 0 ? t.seg_pc : t.seg_qc)) * 8 +
+                             (int64_t)j * n * qbits) + rowg * qbits;
+        const int64_t wi = bit >> 5;
+        const uint32_t w0 = words[wi];
+        const uint32_t w1 = wi + 1 < nwords ? words[wi + 1] : 0u;
+        const uint32_t w2 = wi + 2 < nwords ? words[wi + 2] : 0u;
+        const int s = static_cast<int>(bit & 31);
+        const uint64_t lo = static_cast<uint64_t>(w0) | (static_cast<uint64_t>(w1) << 32);
+        const uint64_t v = (lo >> s) | (s ? (static_cast<uint64_t>(w2) << (64 - s)) : 0ull);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          int c = static_cast<int>((static_cast<uint32_t>(v >> (i * qbits)) & mask) << sh) >> sh;
+          if (rowg + i >= rend) c = 0;
+          const uint32_t hb = __bfloat16_as_ushort(__int2bfloat16_rn(c));
+          packed[i / 2] |= hb << (16 * (i % 2));
+        }
+      }
+      *reinterpret_cast<uint4*>(&Ct[k * kCgmLd + 8 * tg]) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kCgmTilesPerWarp; ++u) {
+      if (!tv[u]) continue;
+      const int i0 = 32 * tI[u], j0 = 32 * tJ[u];
+#pragma unroll
+      for (int k0 = 0; k0 < kCgmRows; k0 += 16) {
+        uint32_t af[2][4], bf[4][2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int rr_ = i0 + 16 * a + (lane % 8) + 8 * ((lane / 8) % 2);
+          const int cc = k0 + 8 * (lane / 16);
+          ldsm_x4(af[a], &Ct[rr_ * kCgmLd + cc]);
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int rr_ = j0 + 8 * b + (lane % 8);
+          const int cc = k0 + 8 * ((lane / 8) % 2);
+          ldsm_x2(bf[b], &Ct[rr_ * kCgmLd + cc]);
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) mma_bf16_16816(acc[u][a][b], af[a], bf[b]);
+      }
+    }
+  }
+  // accumulator fragment (m16n8): c0,c1 at row g, cols 2q, 2q+1; c2,c3 at row g + 8
+  double* g = G + ((int64_t)ch.x * 2 + side) * kst * kst;
+#pragma unroll
+  for (int u = 0; u < kCgmTilesPerWarp; ++u) {
+    if (!tv[u]) continue;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i = 32 * tI[u] + 16 * a + lane / 4 + 8 * (c / 2);
+          const int j = 32 * tJ[u] + 8 * b + 2 * (lane % 4) + (c % 2);
+          const float v = acc[u][a][b][c];
+          if (i < K && j < K && i <= j && v != 0.f) atomicAdd(&g[i * kst + j], static_cast<double>(v));
+        }
+  }
+}
+
+// ------------------------------------------------------------------ eigenproblem
+// Per tensor: G_B = L L^T (semidefinite Cholesky), M = L^T G_A L (K x K, K = D r), Householder
+// tridiagonalisation, eigenvalues by Sturm-count multisection, prefix energy. Working set:
+// L, G_A L and M all in shared memory for n <= 64; M alone in shared memory for n <= 128 (L
+// and G_A L in the global work buffer, L2-resident); everything in the work buffer above.
+// Grams come either as fp64 matrices (GA, GB; row stride rr) or as integer code Grams (GI,
+// upper triangle, stride rr) scaled by the payload's column scales.
+constexpr int kErAllSmem = 64;   // n <= 64: L, G_A L, M staged in shared memory
+constexpr int kErMSmem = 128;    // n <= 128: M staged in shared memory
+constexpr int kErMaxN = 256;     // tridiagonal scratch size
+
+__global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, int D, int rr,
                                                  const double* __restrict__ GA,
                                                  const double* __restrict__ GB,
                                                  const double* __restrict__ GI,
                                                  const uint8_t* __restrict__ gathered,
-                                                 int64_t pay_bytes, int sdim, int hmax,
+                                                 int64_t pay_bytes, int sdim, int mdim,
                                                  double* __restrict__ work, double tau,
                                                  int* __restrict__ per,
                                                  double* __restrict__ energy) {
   extern __shared__ double er_sm[];
   __shared__ double red[32];
-  // dynamic shared memory: [L | G_A L | M] (when staged) then the rotation table of a round
-  const int64_t stage = sdim > 0 ? 3 * (int64_t)sdim * (sdim + 1) : 0;
-  double* cs = er_sm + stage;
-  double* sn = cs + hmax;
-  int* pp = reinterpret_cast<int*>(sn + hmax);
-  int* qq = pp + hmax;
+  __shared__ double tri[4 * kErMaxN];  // V | A v / H | diagonal | squared off-diagonal
+  __shared__ double s_H, s_alpha, s_K, s_tot;
   __shared__ int s_k;
-  __shared__ double s_tot;
   const int e = blockIdx.x;
   const DevT2& t = T[e];
   const int K = D * t.r;
   const int n2 = K + (K & 1);
+  const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t mat = (int64_t)rr * rr;
-  const bool in_smem = n2 <= sdim;
-  const int ld = in_smem ? sdim + 1 : rr;
-  const int64_t ms = in_smem ? (int64_t)sdim * (sdim + 1) : mat;
-  double* base = in_smem ? er_sm : work + 3 * e * mat;
-  double* Lm = base;           // L (lower), from G_B
-  double* Tm = base + ms;      // G_A L
-  double* M = base + 2 * ms;   // G_A, then L^T G_A L (n2 x n2)
+  double* gw = work + 3 * e * mat;
+  double *Lm, *Tm, *M;
+  int ldl, ldm;
+  if (n2 <= sdim) {  // all three in shared memory (launch sized for sdim)
+    ldl = ldm = sdim + 1;
+    Lm = er_sm;
+    Tm = er_sm + (int64_t)sdim * ldl;
+    M = er_sm + 2 * (int64_t)sdim * ldl;
+  } else if (n2 <= mdim) {  // M in shared memory (launch sized for mdim)
+    ldl = rr;
+    ldm = mdim + 1;
+    Lm = gw;
+    Tm = gw + mat;
+    M = er_sm;
+  } else {
+    ldl = ldm = rr;
+    Lm = gw;
+    Tm = gw + mat;
+    M = gw + 2 * mat;
+  }
   // 0. stage G_B -> Lm, G_A -> M
-  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) {
+  for (int idx = tid; idx < K * K; idx += nt) {
     const int i = idx / K, k = idx % K;
     double gb, ga;
     if (GI) {
@@ -219,156 +381,156 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
       ga = GA[e * mat + i * rr + k];
       gb = GB[e * mat + i * rr + k];
     }
-    Lm[i * ld + k] = gb;
-    M[i * ld + k] = ga;
+    Lm[i * ldl + k] = gb;
+    M[i * ldm + k] = ga;
   }
   __syncthreads();
   // 1. semidefinite Cholesky of G_B (lower), columns with vanishing pivot dropped
   double dmax = 0.0;
-  for (int j = 0; j < K; ++j) dmax = fmax(dmax, Lm[j * ld + j]);
+  for (int j = 0; j < K; ++j) dmax = fmax(dmax, Lm[j * ldl + j]);
   const double floor_piv = 1e-14 * dmax;
   for (int j = 0; j < K; ++j) {
-    const double d = Lm[j * ld + j];
+    const double d = Lm[j * ldl + j];
     const bool keep = d > floor_piv && d > 0.0;
     const double ljj = keep ? sqrt(d) : 0.0;
     __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < K; i += blockDim.x)
-      Lm[i * ld + j] = keep ? Lm[i * ld + j] / ljj : 0.0;
-    if (threadIdx.x == 0) Lm[j * ld + j] = ljj;
+    for (int i = j + 1 + tid; i < K; i += nt) Lm[i * ldl + j] = keep ? Lm[i * ldl + j] / ljj : 0.0;
+    if (tid == 0) Lm[j * ldl + j] = ljj;
     __syncthreads();
     const int rem = K - j - 1;
-    for (int idx = threadIdx.x; idx < rem * rem; idx += blockDim.x) {
+    for (int idx = tid; idx < rem * rem; idx += nt) {
       const int i = j + 1 + idx / rem, k = j + 1 + idx % rem;
       if (k > i) continue;
-      Lm[i * ld + k] -= Lm[i * ld + j] * Lm[k * ld + j];
+      Lm[i * ldl + k] -= Lm[i * ldl + j] * Lm[k * ldl + j];
     }
     __syncthreads();
   }
-  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) {  // zero the strict upper part
+  for (int idx = tid; idx < K * K; idx += nt) {  // zero the strict upper part
     const int i = idx / K, k = idx % K;
-    if (k > i) Lm[i * ld + k] = 0.0;
+    if (k > i) Lm[i * ldl + k] = 0.0;
   }
   __syncthreads();
-  // 2. Tm = G_A L ; M = L^T Tm
-  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) {
+  // 2. Tm = G_A L ; M = L^T Tm (symmetrised)
+  for (int idx = tid; idx < K * K; idx += nt) {
     const int i = idx / K, j = idx % K;
     double s = 0.0;
-    for (int k = j; k < K; ++k) s = fma(M[i * ld + k], Lm[k * ld + j], s);
-    Tm[i * ld + j] = s;
+    for (int k = j; k < K; ++k) s = fma(M[i * ldm + k], Lm[k * ldl + j], s);
+    Tm[i * ldl + j] = s;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < n2 * n2; idx += blockDim.x) {
+  for (int idx = tid; idx < n2 * n2; idx += nt) {
     const int i = idx / n2, j = idx % n2;
     double s = 0.0;
     if (i < K && j < K)
-      for (int k = i; k < K; ++k) s = fma(Lm[k * ld + i], Tm[k * ld + j], s);
-    M[i * ld + j] = s;
+      for (int k = i; k < K; ++k) s = fma(Lm[k * ldl + i], Tm[k * ldl + j], s);
+    M[i * ldm + j] = s;
   }
   __syncthreads();
-  // symmetrise (rounding) and 3. parallel cyclic Jacobi (round-robin pairing)
-  for (int idx = threadIdx.x; idx < n2 * n2; idx += blockDim.x) {
+  for (int idx = tid; idx < n2 * n2; idx += nt) {
     const int i = idx / n2, j = idx % n2;
     if (j > i) {
-      const double v = 0.5 * (M[i * ld + j] + M[j * ld + i]);
-      M[i * ld + j] = v;
-      M[j * ld + i] = v;
+      const double v = 0.5 * (M[i * ldm + j] + M[j * ldm + i]);
+      M[i * ldm + j] = v;
+      M[j * ldm + i] = v;
     }
   }
   __syncthreads();
-  __shared__ double tri[4 * 64];  // V | A v / H | diagonal | squared off-diagonal
-  double* ev = in_smem ? tri : Tm;  // eigenvalues, descending
-  if (in_smem) {
-    // 3a. Householder tridiagonalisation (P = I - v v^T / H, A <- P A P) in shared memory
-    __shared__ double s_H, s_alpha, s_K;
-    double* V = tri;        // Householder vector
-    double* Pv = tri + 64;  // A v / H
-    const int n = n2;
-    const int tid = threadIdx.x;
-    for (int k = 0; k + 2 < n; ++k) {
-      if (tid < 32) {
-        double ss = 0.0;
-        for (int i = k + 1 + tid; i < n; i += 32) {
-          const double x = M[i * ld + k];
-          ss += x * x;
-        }
+  // 3a. Householder tridiagonalisation (P = I - v v^T / H, A <- P A P)
+  double* V = tri;
+  double* Pv = tri + kErMaxN;
+  const int n = n2;
+  for (int k = 0; k + 2 < n; ++k) {
+    if (tid < 32) {
+      double ss = 0.0;
+      for (int i = k + 1 + tid; i < n; i += 32) {
+        const double x = M[i * ldm + k];
+        ss += x * x;
+      }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (tid == 0) {
-          const double x0 = M[(k + 1) * ld + k];
-          const double nrm = sqrt(ss);
-          if (!(ss - x0 * x0 > 1e-300 * ss) || nrm == 0.0) {
-            s_H = 0.0;  // column already reduced
-            s_alpha = x0;
-          } else {
-            const double alpha = x0 > 0.0 ? -nrm : nrm;
-            s_alpha = alpha;
-            s_H = ss - x0 * alpha;  // ||v||^2 / 2
-          }
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (tid == 0) {
+        const double x0 = M[(k + 1) * ldm + k];
+        const double nrm = sqrt(ss);
+        if (!(ss - x0 * x0 > 1e-300 * ss) || nrm == 0.0) {
+          s_H = 0.0;  // column already reduced
+          s_alpha = x0;
+        } else {
+          const double alpha = x0 > 0.0 ? -nrm : nrm;
+          s_alpha = alpha;
+          s_H = ss - x0 * alpha;  // ||v||^2 / 2
         }
       }
+    }
+    __syncthreads();
+    const double H = s_H;
+    if (H == 0.0) {  // uniform
       __syncthreads();
-      const double H = s_H;
-      if (H == 0.0) {  // uniform
-        __syncthreads();
-        continue;
-      }
-      for (int i = k + 1 + tid; i < n; i += blockDim.x)
-        V[i] = i == k + 1 ? M[i * ld + k] - s_alpha : M[i * ld + k];
-      __syncthreads();
-      {
-        const int row = k + 1 + tid / 4, part = tid % 4;
+      continue;
+    }
+    for (int i = k + 1 + tid; i < n; i += nt) V[i] = i == k + 1 ? M[i * ldm + k] - s_alpha : M[i * ldm + k];
+    __syncthreads();
+    {
+      const int part = tid % 4, rows_per = nt / 4;
+      const int passes = (n - k - 1 + rows_per - 1) / rows_per;  // uniform: all lanes shuffle
+      for (int ps = 0; ps < passes; ++ps) {
+        const int row = k + 1 + tid / 4 + ps * rows_per;
         double acc = 0.0;
         if (row < n)
-          for (int j = k + 1 + part; j < n; j += 4) acc = fma(M[row * ld + j], V[j], acc);
+          for (int j = k + 1 + part; j < n; j += 4) acc = fma(M[row * ldm + j], V[j], acc);
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
         acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         if (row < n && part == 0) Pv[row] = acc / H;
       }
-      __syncthreads();
-      if (tid < 32) {
-        double acc = 0.0;
-        for (int i = k + 1 + tid; i < n; i += 32) acc = fma(V[i], Pv[i], acc);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (tid == 0) s_K = acc / (2.0 * H);
-      }
-      __syncthreads();
-      const double Kc = s_K;
-      const int mm = n - k - 1;
-      for (int idx = tid; idx < mm * mm; idx += blockDim.x) {
-        const int i = k + 1 + idx / mm, j = k + 1 + idx % mm;
-        const double wi = Pv[i] - Kc * V[i], wj = Pv[j] - Kc * V[j];
-        M[i * ld + j] -= V[i] * wj + wi * V[j];
-      }
-      if (tid == 0) M[(k + 1) * ld + k] = s_alpha;
-      __syncthreads();
-    }
-    // 3b. eigenvalues of the tridiagonal (d, e) by multisection on Sturm counts: a group of
-    // G lanes per eigenvalue evaluates G interior points per step (log2(G+1) bits / step)
-    double* Dg = Pv + 64;
-    double* E2 = Dg + 64;
-    for (int i = tid; i < n; i += blockDim.x) {
-      Dg[i] = M[i * ld + i];
-      E2[i] = i + 1 < n ? M[(i + 1) * ld + i] * M[(i + 1) * ld + i] : 0.0;
     }
     __syncthreads();
-    double lo = 0.0, hi = 0.0, amax = 0.0;
-    for (int i = 0; i < n; ++i) {  // Gershgorin (every thread, uniform)
-      const double r0 = i > 0 ? sqrt(E2[i - 1]) : 0.0, r1 = i + 1 < n ? sqrt(E2[i]) : 0.0;
-      lo = fmin(lo, Dg[i] - r0 - r1);
-      hi = fmax(hi, Dg[i] + r0 + r1);
-      amax = fmax(amax, fabs(Dg[i]) + r0 + r1);
+    if (tid < 32) {
+      double acc = 0.0;
+      for (int i = k + 1 + tid; i < n; i += 32) acc = fma(V[i], Pv[i], acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (tid == 0) s_K = acc / (2.0 * H);
     }
-    hi += 1e-14 * amax + 1e-300;
-    lo -= 1e-14 * amax + 1e-300;
-    const double pivmin = 1e-290 + 1e-30 * amax * amax;
-    int G = 1;
-    while (G * 2 <= 32 && G * 2 * n <= static_cast<int>(blockDim.x)) G *= 2;
-    const int idx = tid / G, l = tid % G;
+    __syncthreads();
+    const double Kc = s_K;
+    const int mm = n - k - 1;
+    for (int idx = tid; idx < mm * mm; idx += nt) {
+      const int i = k + 1 + idx / mm, j = k + 1 + idx % mm;
+      const double wi = Pv[i] - Kc * V[i], wj = Pv[j] - Kc * V[j];
+      M[i * ldm + j] -= V[i] * wj + wi * V[j];
+    }
+    if (tid == 0) M[(k + 1) * ldm + k] = s_alpha;
+    __syncthreads();
+  }
+  // 3b. eigenvalues of the tridiagonal (d, e) by multisection on Sturm counts: a group of G
+  // lanes per eigenvalue evaluates G interior points per step (log2(G+1) bits per step)
+  double* Dg = tri + 2 * kErMaxN;
+  double* E2 = tri + 3 * kErMaxN;
+  for (int i = tid; i < n; i += nt) {
+    Dg[i] = M[i * ldm + i];
+    E2[i] = i + 1 < n ? M[(i + 1) * ldm + i] * M[(i + 1) * ldm + i] : 0.0;
+  }
+  __syncthreads();
+  double lo = 0.0, hi = 0.0, amax = 0.0;
+  for (int i = 0; i < n; ++i) {  // Gershgorin (every thread, uniform)
+    const double r0 = i > 0 ? sqrt(E2[i - 1]) : 0.0, r1 = i + 1 < n ? sqrt(E2[i]) : 0.0;
+    lo = fmin(lo, Dg[i] - r0 - r1);
+    hi = fmax(hi, Dg[i] + r0 + r1);
+    amax = fmax(amax, fabs(Dg[i]) + r0 + r1);
+  }
+  hi += 1e-14 * amax + 1e-300;
+  lo -= 1e-14 * amax + 1e-300;
+  const double pivmin = 1e-290 + 1e-30 * amax * amax;
+  double* ev = V;  // eigenvalues, descending (V is free now)
+  int G = 1;
+  while (G * 2 <= 32 && G * 2 * n <= nt) G *= 2;
+  const int iters = G >= 16 ? 12 : G >= 8 ? 15 : G >= 4 ? 20 : G >= 2 ? 29 : 50;
+  const int lanes = (nt / G) * G;  // threads in whole groups
+  for (int base_idx = 0; base_idx < n; base_idx += nt / G) {
+    const int idx = base_idx + tid / G, l = tid % G;
+    double blo = lo, bhi = hi;
     const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((tid % 32) / G * G);
-    const int iters = G >= 16 ? 12 : G >= 8 ? 15 : G >= 4 ? 20 : G >= 2 ? 29 : 50;
     for (int it = 0; it < iters; ++it) {
-      const double sig = lo + (hi - lo) * (double)(l + 1) / (double)(G + 1);
+      const double sig = blo + (bhi - blo) * (double)(l + 1) / (double)(G + 1);
       int c = 0;
       {
         double q = Dg[0] - sig;
@@ -384,82 +546,20 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
       const int base = (tid % 32) / G * G;
       const double s_lo = __shfl_sync(0xffffffffu, sig, base + max(L - 1, 0));
       const double s_hi = __shfl_sync(0xffffffffu, sig, base + min(L, G - 1));
-      if (L > 0) lo = s_lo;
-      if (L < G) hi = s_hi;
+      if (L > 0) blo = s_lo;
+      if (L < G) bhi = s_hi;
     }
-    __syncthreads();
-    if (l == 0 && idx < n) ev[n - 1 - idx] = fmax(0.5 * (lo + hi), 0.0);
-  } else {
-    const int half = n2 / 2;
-    for (int sweep = 0; sweep < 40 && n2 > 1; ++sweep) {
-      double off = 0.0, dg = 0.0;
-      for (int idx = threadIdx.x; idx < n2 * n2; idx += blockDim.x) {
-        const int i = idx / n2, j = idx % n2;
-        const double v = M[i * ld + j];
-        if (i == j) dg += v * v; else off += v * v;
-      }
-      off = er_block_sum(off, red);
-      dg = er_block_sum(dg, red);
-      if (off <= 1e-30 * dg || off == 0.0) break;
-      for (int rd = 0; rd < n2 - 1; ++rd) {
-        for (int i = threadIdx.x; i < half; i += blockDim.x) {
-          int a = (rd + i) % (n2 - 1);
-          int b = i == 0 ? n2 - 1 : (rd - i + n2 - 1) % (n2 - 1);
-          const int p = min(a, b), q = max(a, b);
-          const double apq = M[p * ld + q];
-          double c = 1.0, s = 0.0;
-          if (apq != 0.0) {
-            const double theta = (M[q * ld + q] - M[p * ld + p]) / (2.0 * apq);
-            const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-            c = 1.0 / sqrt(t * t + 1.0);
-            s = t * c;
-          }
-          cs[i] = c;
-          sn[i] = s;
-          pp[i] = p;
-          qq[i] = q;
-        }
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < half * n2; idx += blockDim.x) {  // rows
-          const int i = idx / n2, k = idx % n2;
-          const int p = pp[i], q = qq[i];
-          const double c = cs[i], s = sn[i];
-          const double ap = M[p * ld + k], aq = M[q * ld + k];
-          M[p * ld + k] = c * ap - s * aq;
-          M[q * ld + k] = s * ap + c * aq;
-        }
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < half * n2; idx += blockDim.x) {  // columns
-          const int i = idx / n2, k = idx % n2;
-          const int p = pp[i], q = qq[i];
-          const double c = cs[i], s = sn[i];
-          const double ap = M[k * ld + p], aq = M[k * ld + q];
-          M[k * ld + p] = c * ap - s * aq;
-          M[k * ld + q] = s * ap + c * aq;
-        }
-        __syncthreads();
-      }
-    }
-    // 4. eigenvalues (clamped >= 0) sorted descending by rank counting; prefix energy
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-      const double v = fmax(M[i * ld + i], 0.0);
-      int rank = 0;
-      for (int j = 0; j < n2; ++j) {
-        const double w = fmax(M[j * ld + j], 0.0);
-        rank += (w > v) || (w == v && j < i);
-      }
-      ev[rank] = v;
-    }
-
+    if (l == 0 && idx < n && tid < lanes) ev[n - 1 - idx] = fmax(0.5 * (blo + bhi), 0.0);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  // 4. prefix energy
+  if (tid == 0) {
     double tot = 0.0;
-    for (int i = 0; i < n2; ++i) tot += ev[i];
+    for (int i = 0; i < n; ++i) tot += ev[i];
     int k = 1;
     if (tot > 0.0) {
       double pre = 0.0;
-      for (int i = 0; i < n2; ++i) {
+      for (int i = 0; i < n; ++i) {
         pre += ev[i];
         k = i + 1;
         if (pre >= tau * tot) break;
@@ -469,7 +569,7 @@ __global__ void __launch_bounds__(256) k_effrank(const DevT2* __restrict__ T, in
     s_tot = tot / ((double)D * (double)D);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     per[e] = s_k;
     energy[e] = s_tot;
   }
@@ -481,17 +581,25 @@ static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const
   static bool attr = false;
   if (!attr) {
     DLX_CUDA(cudaFuncSetAttribute(k_effrank, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kErSmemBytes + 1024 * 24)));
+                                  static_cast<int>(sizeof(double) * kErMSmem * (kErMSmem + 1))));
     attr = true;
   }
   int n2max = 0;
   for (const DevT2& t : P.t2) n2max = std::max(n2max, D * t.r + ((D * t.r) & 1));
-  const int sdim = n2max <= kErSmemDim ? n2max : 0;
-  const int hmax = std::max(1, n2max / 2);
-  const size_t smem = 3 * static_cast<size_t>(sdim) * (sdim + 1) * sizeof(double) +
-                      static_cast<size_t>(hmax) * (2 * sizeof(double) + 2 * sizeof(int));
-  k_effrank<<<P.t2.size(), 256, smem, s>>>(P.d_t2, D, rr, GA, GB, GI, gathered, P.payload_bytes,
-                                           sdim, hmax, W, tau, d_per, d_energy);
+  if (n2max > kErMaxN) raise(DLX_ERR_VALIDATION, "effective_rank: D * rank above 256 unsupported");
+  int sdim = 0, mdim = 0;
+  size_t smem = 0;
+  if (n2max <= kErAllSmem) {
+    sdim = n2max;
+    smem = 3 * static_cast<size_t>(sdim) * (sdim + 1) * sizeof(double);
+  } else if (n2max <= kErMSmem) {
+    mdim = n2max;
+    smem = static_cast<size_t>(mdim) * (mdim + 1) * sizeof(double);
+  }
+  const int threads = n2max <= 64 ? 256 : 512;
+  k_effrank<<<P.t2.size(), threads, smem, s>>>(P.d_t2, D, rr, GA, GB, GI, gathered,
+                                               P.payload_bytes, sdim, mdim, W, tau, d_per,
+                                               d_energy);
   DLX_LAUNCHED();
 }
 
@@ -500,11 +608,11 @@ void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* g
   if (P.t2.empty()) return;
   int K = 0;
   for (const DevT2& t : P.t2) K = std::max(K, D * t.r);
-  if (K > 2048) raise(DLX_ERR_VALIDATION, "effective_rank: D * rank above 2048 unsupported");
+  if (K > kErMaxN) raise(DLX_ERR_VALIDATION, "effective_rank: D * rank above 256 unsupported");
   const int64_t mat = static_cast<int64_t>(K) * K;
   const size_t ne = P.t2.size();
   auto* W = static_cast<double*>(ctx->scratch("er_W", sizeof(double) * mat * ne * 3));
-  if (K <= kCgMaxK) {
+  if (K <= kErMaxN) {
     // integer code Grams straight from the gathered payloads
     bool fresh = false;
     CodeGramJob& J = plan_ext<CodeGramJob>(P, "code_gram", &fresh);
@@ -520,9 +628,14 @@ void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* g
     }
     auto* GI = static_cast<double*>(ctx->scratch("er_GI", sizeof(double) * mat * ne * 2));
     DLX_CUDA(cudaMemsetAsync(GI, 0, sizeof(double) * mat * ne * 2, s));
-    k_code_gram<<<J.chunks.size(), 320, 0, s>>>(P.d_t2, J.d, gathered, P.payload_bytes, P.qbits,
-                                                D, K, GI);
-    DLX_LAUNCHED();
+    {
+      const int nt32 = (K + 31) / 32;
+      const int gy = (nt32 * (nt32 + 1) / 2 + kCgmWarps * kCgmTilesPerWarp - 1) /
+                     (kCgmWarps * kCgmTilesPerWarp);
+      k_code_gram_mma<<<dim3(J.chunks.size(), gy), 256, 0, s>>>(P.d_t2, J.d, gathered,
+                                                                P.payload_bytes, P.qbits, D, K, GI);
+      DLX_LAUNCHED();
+    }
     launch_effrank(P, D, K, nullptr, nullptr, GI, gathered,
                    W, tau, d_per, d_energy, s);
     return;

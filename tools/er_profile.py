@@ -1,0 +1,15 @@
+"""Effective rank at D workers on one GPU (payload replicated) — for an ncu launch list."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2506_21263_b200 import api, layouts
+ctx = api.Context(0)
+L = api.Layout(ctx, layouts.opt_1_3b())
+r, q = 32, 4
+delta = L.empty()
+api.fill_gaussian(L, delta, 1e-3, seed=1, tag=1, worker=0)
+pay = api.compress(L, delta, r, api.QuantSpec(q, 0), None, 0, 2, 12345).payload
+for D in [int(x) for x in os.environ.get("DS", "4,8").split(",")]:
+    g = pay.repeat(D)
+    api.effective_rank_device(L, g, D, r, q, 0.5)
+    torch.cuda.synchronize()
