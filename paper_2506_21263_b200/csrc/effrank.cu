@@ -9,6 +9,8 @@
 // eigenproblem (cyclic parallel Jacobi, one CTA per tensor). r' can differ from the dense
 // reference only where the prefix energy lands within rounding of tau (ties).
 #include <cuda_bf16.h>
+#include <cstdlib>
+#include <cstdio>
 
 #include "dlx_internal.cuh"
 #include "ptx.cuh"
@@ -317,6 +319,7 @@ __global__ void __launch_bounds__(256) k_code_gram_mma(const DevT2* __restrict__
 // and G_A L in the global work buffer, L2-resident); everything in the work buffer above.
 // Grams come either as fp64 matrices (GA, GB; row stride rr) or as integer code Grams (GI,
 // upper triangle, stride rr) scaled by the payload's column scales.
+__device__ long long g_er_prof[8];  // experiments (DLX_ER_PROF): phase cycles of block 0
 constexpr int kErAllSmem = 64;   // n <= 64: L, G_A L, M staged in shared memory
 constexpr int kErMSmem = 128;    // n <= 128: M staged in shared memory
 constexpr int kErMaxN = 256;     // tridiagonal scratch size
@@ -342,17 +345,33 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
   const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t mat = (int64_t)rr * rr;
   double* gw = work + 3 * e * mat;
+  // G_A / G_B entries from the integer code Grams (scaled) or the fp64 Grams
+  auto gram = [&](int which, int i, int k) -> double {
+    if (GI) {
+      const int lo = min(i, k), hi = max(i, k);
+      const double* gi = GI + (int64_t)e * 2 * mat + (which ? mat : 0);
+      const int wi = i / t.r, ji = i % t.r, wk = k / t.r, jk = k % t.r;
+      const int64_t so = which ? t.seg_qs : t.seg_ps;
+      const double si = *reinterpret_cast<const float*>(gathered + wi * pay_bytes + so + 4 * ji);
+      const double sk = *reinterpret_cast<const float*>(gathered + wk * pay_bytes + so + 4 * jk);
+      return gi[lo * rr + hi] * si * sk;
+    }
+    return (which ? GB : GA)[e * mat + i * rr + k];
+  };
+  // working set: all three in shared memory (n <= sdim); the Cholesky and M in shared memory
+  // one after the other with L and G_A L in the work buffer (n <= mdim); else all global
+  const bool all_s = n2 <= sdim, mid_s = !all_s && n2 <= mdim;
   double *Lm, *Tm, *M;
   int ldl, ldm;
-  if (n2 <= sdim) {  // all three in shared memory (launch sized for sdim)
+  if (all_s) {
     ldl = ldm = sdim + 1;
     Lm = er_sm;
     Tm = er_sm + (int64_t)sdim * ldl;
     M = er_sm + 2 * (int64_t)sdim * ldl;
-  } else if (n2 <= mdim) {  // M in shared memory (launch sized for mdim)
-    ldl = rr;
+  } else if (mid_s) {
+    ldl = mdim + 1;  // Cholesky staged in shared memory first
     ldm = mdim + 1;
-    Lm = gw;
+    Lm = er_sm;
     Tm = gw + mat;
     M = er_sm;
   } else {
@@ -361,70 +380,75 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
     Tm = gw + mat;
     M = gw + 2 * mat;
   }
-  // 0. stage G_B -> Lm, G_A -> M
+  long long pt0 = clock64();
+#define ER_MARK(i) do { if (blockIdx.x == 0 && tid == 0) { const long long c = clock64(); g_er_prof[i] = c - pt0; pt0 = c; } } while (0)
+  // 0. stage G_B -> Lm (lower), G_A -> GAs (M itself, or the work buffer in the mid mode)
+  double* GAs = mid_s ? gw + 2 * mat : M;
+  const int ldg = mid_s ? rr : ldm;
   for (int idx = tid; idx < K * K; idx += nt) {
     const int i = idx / K, k = idx % K;
-    double gb, ga;
-    if (GI) {
-      const int lo = min(i, k), hi = max(i, k);
-      const double* gi = GI + (int64_t)e * 2 * mat;
-      const int wi = i / t.r, ji = i % t.r, wk = k / t.r, jk = k % t.r;
-      const uint8_t* pi = gathered + wi * pay_bytes;
-      const uint8_t* pk = gathered + wk * pay_bytes;
-      const double sai = *reinterpret_cast<const float*>(pi + t.seg_ps + 4 * ji);
-      const double sak = *reinterpret_cast<const float*>(pk + t.seg_ps + 4 * jk);
-      const double sbi = *reinterpret_cast<const float*>(pi + t.seg_qs + 4 * ji);
-      const double sbk = *reinterpret_cast<const float*>(pk + t.seg_qs + 4 * jk);
-      ga = gi[lo * rr + hi] * sai * sak;
-      gb = gi[mat + lo * rr + hi] * sbi * sbk;
-    } else {
-      ga = GA[e * mat + i * rr + k];
-      gb = GB[e * mat + i * rr + k];
-    }
-    Lm[i * ldl + k] = gb;
-    M[i * ldm + k] = ga;
+    if (k <= i) Lm[i * ldl + k] = gram(1, i, k);
+    GAs[i * ldg + k] = gram(0, i, k);
   }
   __syncthreads();
+  ER_MARK(0);
   // 1. semidefinite Cholesky of G_B (lower), columns with vanishing pivot dropped
   double dmax = 0.0;
   for (int j = 0; j < K; ++j) dmax = fmax(dmax, Lm[j * ldl + j]);
   const double floor_piv = 1e-14 * dmax;
   for (int j = 0; j < K; ++j) {
-    const double d = Lm[j * ldl + j];
-    const bool keep = d > floor_piv && d > 0.0;
-    const double ljj = keep ? sqrt(d) : 0.0;
+    __shared__ double s_ljj, s_inv;
+    if (tid == 0) {  // one sqrt / division per step, broadcast
+      const double d = Lm[j * ldl + j];
+      const bool keep = d > floor_piv && d > 0.0;
+      s_ljj = keep ? sqrt(d) : 0.0;
+      s_inv = keep ? 1.0 / s_ljj : 0.0;
+    }
     __syncthreads();
-    for (int i = j + 1 + tid; i < K; i += nt) Lm[i * ldl + j] = keep ? Lm[i * ldl + j] / ljj : 0.0;
+    const double ljj = s_ljj, inv = s_inv;
+    for (int i = j + 1 + tid; i < K; i += nt) Lm[i * ldl + j] *= inv;
     if (tid == 0) Lm[j * ldl + j] = ljj;
     __syncthreads();
-    const int rem = K - j - 1;
-    for (int idx = tid; idx < rem * rem; idx += nt) {
-      const int i = j + 1 + idx / rem, k = j + 1 + idx % rem;
-      if (k > i) continue;
-      Lm[i * ldl + k] -= Lm[i * ldl + j] * Lm[k * ldl + j];
+    // trailing lower-triangle update: warp per row, lanes over columns
+    for (int i = j + 1 + tid / 32; i < K; i += nt / 32) {
+      const double lij = Lm[i * ldl + j];
+      for (int k = j + 1 + tid % 32; k <= i; k += 32) Lm[i * ldl + k] -= lij * Lm[k * ldl + j];
     }
     __syncthreads();
   }
-  for (int idx = tid; idx < K * K; idx += nt) {  // zero the strict upper part
-    const int i = idx / K, k = idx % K;
-    if (k > i) Lm[i * ldl + k] = 0.0;
+  if (mid_s) {  // move L to the work buffer; shared memory is needed for M next
+    for (int idx = tid; idx < K * K; idx += nt) {
+      const int i = idx / K, k = idx % K;
+      gw[i * rr + k] = k <= i ? Lm[i * ldl + k] : 0.0;
+    }
+    __syncthreads();
+    Lm = gw;
+    ldl = rr;
+  } else {
+    for (int idx = tid; idx < K * K; idx += nt) {  // zero the strict upper part
+      const int i = idx / K, k = idx % K;
+      if (k > i) Lm[i * ldl + k] = 0.0;
+    }
   }
   __syncthreads();
-  // 2. Tm = G_A L ; M = L^T Tm (symmetrised)
-  for (int idx = tid; idx < K * K; idx += nt) {
-    const int i = idx / K, j = idx % K;
-    double s = 0.0;
-    for (int k = j; k < K; ++k) s = fma(M[i * ldm + k], Lm[k * ldl + j], s);
-    Tm[i * ldl + j] = s;
-  }
+  ER_MARK(1);
+  // 2. Tm = G_A L ; M = L^T Tm (symmetrised). Warp per output row (broadcast operand), lanes
+  // over columns (coalesced operand).
+  const int nw = nt / 32, lane = tid % 32;
+  for (int i = tid / 32; i < K; i += nw)
+    for (int j = lane; j < K; j += 32) {
+      double s = 0.0;
+      for (int k = j; k < K; ++k) s = fma(GAs[i * ldg + k], Lm[k * ldl + j], s);
+      Tm[i * ldl + j] = s;
+    }
   __syncthreads();
-  for (int idx = tid; idx < n2 * n2; idx += nt) {
-    const int i = idx / n2, j = idx % n2;
-    double s = 0.0;
-    if (i < K && j < K)
-      for (int k = i; k < K; ++k) s = fma(Lm[k * ldl + i], Tm[k * ldl + j], s);
-    M[i * ldm + j] = s;
-  }
+  for (int i = tid / 32; i < n2; i += nw)
+    for (int j = lane; j < n2; j += 32) {
+      double s = 0.0;
+      if (i < K && j < K)
+        for (int k = i; k < K; ++k) s = fma(Lm[k * ldl + i], Tm[k * ldl + j], s);
+      M[i * ldm + j] = s;
+    }
   __syncthreads();
   for (int idx = tid; idx < n2 * n2; idx += nt) {
     const int i = idx / n2, j = idx % n2;
@@ -435,6 +459,7 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
     }
   }
   __syncthreads();
+  ER_MARK(2);
   // 3a. Householder tridiagonalisation (P = I - v v^T / H, A <- P A P)
   double* V = tri;
   double* Pv = tri + kErMaxN;
@@ -492,15 +517,17 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
     }
     __syncthreads();
     const double Kc = s_K;
-    const int mm = n - k - 1;
-    for (int idx = tid; idx < mm * mm; idx += nt) {
-      const int i = k + 1 + idx / mm, j = k + 1 + idx % mm;
-      const double wi = Pv[i] - Kc * V[i], wj = Pv[j] - Kc * V[j];
-      M[i * ldm + j] -= V[i] * wj + wi * V[j];
+    for (int i = k + 1 + tid / 32; i < n; i += nt / 32) {
+      const double vi = V[i], wi = Pv[i] - Kc * vi;
+      for (int j = k + 1 + tid % 32; j < n; j += 32) {
+        const double wj = Pv[j] - Kc * V[j];
+        M[i * ldm + j] -= vi * wj + wi * V[j];
+      }
     }
     if (tid == 0) M[(k + 1) * ldm + k] = s_alpha;
     __syncthreads();
   }
+  ER_MARK(3);
   // 3b. eigenvalues of the tridiagonal (d, e) by multisection on Sturm counts: a group of G
   // lanes per eigenvalue evaluates G interior points per step (log2(G+1) bits per step)
   double* Dg = tri + 2 * kErMaxN;
@@ -531,14 +558,32 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
     const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((tid % 32) / G * G);
     for (int it = 0; it < iters; ++it) {
       const double sig = blo + (bhi - blo) * (double)(l + 1) / (double)(G + 1);
+      // Sturm count = sign changes of the characteristic-polynomial sequence
+      // p_j = (d_j - sig) p_{j-1} - e_{j-1}^2 p_{j-2} (division-free; exact power-of-two
+      // rescaling keeps it in range; a zero takes the sign opposite to its predecessor, as
+      // the LDL^T recurrence with a -pivmin pivot does)
       int c = 0;
       {
-        double q = Dg[0] - sig;
-        c += q < 0.0;
+        double pm = 1.0, p = Dg[0] - sig;
+        bool neg_prev = false;  // sign of p_0 = +
+        bool neg = p < 0.0 || p == 0.0;
+        c += neg != neg_prev;
+        neg_prev = neg;
         for (int j = 1; j < n; ++j) {
-          if (fabs(q) < pivmin) q = -pivmin;
-          q = (Dg[j] - sig) - E2[j - 1] / q;
-          c += q < 0.0;
+          const double pn = fma(Dg[j] - sig, p, -E2[j - 1] * pm);
+          neg = pn == 0.0 ? !neg_prev : pn < 0.0;
+          c += neg != neg_prev;
+          neg_prev = neg;
+          pm = p;
+          p = pn;
+          const double ap = fabs(p) + fabs(pm);
+          if (ap > 0x1p+600) {
+            p = scalbn(p, -600);
+            pm = scalbn(pm, -600);
+          } else if (ap < 0x1p-600) {
+            p = scalbn(p, 600);
+            pm = scalbn(pm, 600);
+          }
         }
       }
       const unsigned below = __ballot_sync(0xffffffffu, c <= idx) & gmask;
@@ -552,6 +597,7 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
     if (l == 0 && idx < n && tid < lanes) ev[n - 1 - idx] = fmax(0.5 * (blo + bhi), 0.0);
   }
   __syncthreads();
+  ER_MARK(4);
   // 4. prefix energy
   if (tid == 0) {
     double tot = 0.0;
@@ -601,6 +647,13 @@ static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const
                                                P.payload_bytes, sdim, mdim, W, tau, d_per,
                                                d_energy);
   DLX_LAUNCHED();
+  if (getenv("DLX_ER_PROF")) {
+    long long h[8];
+    DLX_CUDA(cudaStreamSynchronize(s));
+    DLX_CUDA(cudaMemcpyFromSymbol(h, g_er_prof, sizeof(h)));
+    fprintf(stderr, "[k_effrank n=%d] cycles: stage %lld chol %lld products %lld tridiag %lld sturm %lld\n",
+            n2max, h[0], h[1], h[2], h[3], h[4]);
+  }
 }
 
 void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
