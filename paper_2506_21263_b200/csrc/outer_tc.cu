@@ -152,7 +152,10 @@ __global__ void __launch_bounds__(kO5Threads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(o5smem) + 1023) & ~uintptr_t(1023));
   const int nkc = KA / KD::AK;                             // 128-B K chunks
   const uint32_t stage_bytes = 4 * kO5StreamBox + KD::NBP * nkc * kO5BBox;
-  const uint32_t aband_bytes = nkc * kO5ABox;              // 128 rows x KA
+  // bf16 path: A moves through a ring of nab 16-KB boxes into TMEM (tcgen05.cp) and the MMAs
+  // read it from there; tf32 path: nab whole A bands stay in shared memory
+  constexpr bool TA = BF;
+  const uint32_t aband_bytes = TA ? kO5ABox : nkc * kO5ABox;
   uint8_t* abuf = smem + nst * stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(abuf + nab * aband_bytes);
   uint64_t* sfull = bars;                // [nst]
@@ -182,10 +185,11 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  constexpr uint32_t kTmemCols = TA ? 512 : 64;  // acc [0, 64); TMEM A slots from column 128
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
-                 "r"(64));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -195,8 +199,8 @@ __global__ void __launch_bounds__(kO5Threads, 1)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
-    int s = 0, a = -1;
-    uint32_t sph = 0, aph[2] = {0, 0};
+    int s = 0, a = -1, ar = 0;
+    uint32_t sph = 0, aph[2] = {0, 0}, arph = 0;
     // (L2 eviction hints on these loads / the stores measured 10 % slower: none)
     // Work is claimed dynamically (one atomic per chunk of 128 columns of a row band) in the
     // global band-major order, so concurrently active CTAs stream ADJACENT column chunks of
@@ -211,6 +215,45 @@ __global__ void __launch_bounds__(kO5Threads, 1)
       const int4 bd = bands[band];  // (slot, m0, first column, columns)
       const O5Maps* mp = maps + bd.x;
       const int ntile = (bd.w + kO5TileN - 1) / kO5TileN;
+      auto push_tile = [&](int n) {
+        mbar_wait(&sempty[s], sph ^ 1);
+        if (elect_one()) {
+          const int n0 = bd.z + kO5TileN * n;
+          sinfo[s] = make_int4(bd.x, bd.y, n0, (a < 0 ? 0 : a) | (n == 0 ? 2 : 0) | (n == ntile - 1 ? 4 : 0));
+          uint8_t* st = smem + s * stage_bytes;
+          mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox + KD::NBP * nkc * kO5BBox);
+          for (int q = 0; q < nstreams; ++q)
+            tma_load_2d(st + q * kO5StreamBox, &mp->s[q], &sfull[s], n0, bd.y);
+          uint8_t* bb = st + 4 * kO5StreamBox;
+          for (int pl = 0; pl < KD::NBP; ++pl)
+            for (int kc = 0; kc < nkc; ++kc)
+              tma_load_2d(bb + (pl * nkc + kc) * kO5BBox, &mp->b[pl], &sfull[s], KD::AK * kc, n0);
+        }
+        __syncwarp();
+        if (++s == nst) {
+          s = 0;
+          sph ^= 1;
+        }
+      };
+      if (TA) {
+        // first tile, then the A boxes through the ring (the MMA warp drains them into TMEM
+        // when it reaches that tile), then the rest of the chunk
+        push_tile(0);
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(&aempty[ar], arph ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(&afull[ar], kO5ABox);
+            tma_load_2d(abuf + ar * kO5ABox, &mp->a, &afull[ar], KD::AK * kc, bd.y);
+          }
+          __syncwarp();
+          if (++ar == nab) {
+            ar = 0;
+            arph ^= 1;
+          }
+        }
+        for (int n = 1; n < ntile; ++n) push_tile(n);
+        continue;
+      }
       a = nab == 2 ? (a + 1) & 1 : 0;
       mbar_wait(&aempty[a], aph[a] ^ 1);
       aph[a] ^= 1;
@@ -253,13 +296,37 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     const uint32_t idesc = BF ? idesc_bf16(kO5TileN) : idesc_tf32(kO5TileN, false, false);
     int s = 0, a = 0, c = 0;
     uint32_t sph = 0, cph = 0, aph[2] = {0, 0};
+    int ar = 0, ta = 1;
+    uint32_t arph = 0;
+    const uint32_t a_tmem0 = tmem + 128u;
+    const uint32_t a_slot_cols = static_cast<uint32_t>(KA / 2);  // bf16: 2 per 32-bit column
     for (;;) {
       mbar_wait(&sfull[s], sph);
       const int4 tl = sinfo[s];
       if (tl.x < 0) break;
       const DevT2 t = T[tl.x];
       const bool last_in_band = tl.w & 4;
-      if (tl.w & 2) {
+      if (TA && (tl.w & 2)) {
+        // new chunk: copy its A band (nkc boxes of 128 rows x 128 B) into the other TMEM slot;
+        // tcgen05.cp and tcgen05.mma execute in issue order, so the MMAs below see it
+        ta ^= 1;
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(&afull[ar], arph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t d0 = sdesc(su32(abuf + ar * kO5ABox), 16u, 1024u);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              tmem_cp_128x256b(a_tmem0 + ta * a_slot_cols + 8u * (4 * kc + kk), d0 + 2u * kk);
+            mma_commit(&aempty[ar]);
+          }
+          __syncwarp();
+          if (++ar == nab) {
+            ar = 0;
+            arph ^= 1;
+          }
+        }
+      } else if (!TA && (tl.w & 2)) {
         a = tl.w & 1;
         mbar_wait(&afull[a], aph[a]);
         aph[a] ^= 1;
@@ -275,8 +342,11 @@ __global__ void __launch_bounds__(kO5Threads, 1)
       const uint32_t dacc = tmem + 32u * c, sacc = dacc + 16u;
       const int K = D * t.r;
       const int s_lo = self_index * t.r, s_hi = s_lo + t.r;
-      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc) {
-        if (BF)
+      const uint32_t a_t = a_tmem0 + ta * a_slot_cols;
+      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc, int kstep) {
+        if (TA)
+          mma_bf16_ts(d, a_t + 8u * kstep, bd, idesc, acc);
+        else if (BF)
           mma_bf16(d, ad, bd, idesc, acc);
         else
           mma_tf32(d, ad, bd, idesc, acc);
@@ -291,16 +361,16 @@ __global__ void __launch_bounds__(kO5Threads, 1)
             const uint64_t boff = (uint64_t)((kc * kO5BBox + kk * 32) >> 4);
             const uint32_t first = (kc == 0 && kk == 0) ? 0u : 1u;
 #pragma unroll
-            for (int pl = 0; pl < KD::NBP; ++pl) mma(dacc, ad, b0[pl] + boff, pl == 0 ? first : 1u);
+            for (int pl = 0; pl < KD::NBP; ++pl) mma(dacc, ad, b0[pl] + boff, pl == 0 ? first : 1u, 4 * kc + kk);
             if (SELF && D > 1 && k >= s_lo && k < s_hi) {
               const uint32_t sfirst = k == s_lo ? 0u : 1u;
 #pragma unroll
-              for (int pl = 0; pl < KD::NBP; ++pl) mma(sacc, ad, b0[pl] + boff, pl == 0 ? sfirst : 1u);
+              for (int pl = 0; pl < KD::NBP; ++pl) mma(sacc, ad, b0[pl] + boff, pl == 0 ? sfirst : 1u, 4 * kc + kk);
             }
           }
         }
         mma_commit(&accfull[c]);
-        if (last_in_band) mma_commit(&aempty[a]);
+        if (!TA && last_in_band) mma_commit(&aempty[a]);
       }
       __syncwarp();
       if (++s == nst) {
@@ -418,7 +488,7 @@ __global__ void __launch_bounds__(kO5Threads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
@@ -504,19 +574,20 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   }();
   const int nkc = S.KA / ak;
   const size_t stage = 4 * kO5StreamBox + nbp * nkc * kO5BBox + 2 * 8 + 16;
-  const size_t aband = static_cast<size_t>(nkc) * kO5ABox;
+  // tf32: whole A bands in shared memory; bf16: a 2-box ring feeding A into TMEM
+  const size_t aband = S.bf ? kO5ABox : static_cast<size_t>(nkc) * kO5ABox;
   auto stages = [&](int nab) {
     const size_t fixed = 1024 + nab * aband + 16 + 8 * 8;
     return budget > fixed ? static_cast<int>(std::min<size_t>(kO5MaxStages, (budget - fixed) / stage)) : 0;
   };
-  S.nab = stages(2) >= 3 ? 2 : 1;
+  S.nab = S.bf ? 2 : (stages(2) >= 3 ? 2 : 1);
   S.nst = stages(S.nab);
   if (S.nst < 2) raise(DLX_ERR_VALIDATION, "outer update: K too large for the tensor-core path");
   S.smem = 1024 + S.nab * aband + 16 + 8 * 8 + S.nst * stage;
   // A / B staging offsets cover every slot (shared buffers); bands and rows only the range.
   // Work unit = a chunk of a row band (128 rows x chunk columns); chunks are claimed in
   // band-major order so concurrently active CTAs read adjacent columns of the same rows.
-  const int64_t chunk = S.nab == 2 ? 128 : 256;  // single A buffer: amortise its reload
+  const int64_t chunk = (S.bf || S.nab == 2) ? 128 : 256;  // single smem A band: amortise reloads
   for (size_t k = 0; k < P.t2.size(); ++k) {
     const DevT2& t = P.t2[k];
     const bool in = static_cast<int>(k) >= R.s0 && static_cast<int>(k) < R.s1;
