@@ -432,23 +432,41 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
   }
   __syncthreads();
   ER_MARK(1);
-  // 2. Tm = G_A L ; M = L^T Tm (symmetrised). Warp per output row (broadcast operand), lanes
-  // over columns (coalesced operand).
+  // 2. Tm = G_A L ; M = L^T Tm (symmetrised), on the fp64 tensor cores: warp = 8x8 output
+  // block, DMMA m8n8k4 over the triangular K range (operands zero-padded to whole blocks)
   const int nw = nt / 32, lane = tid % 32;
-  for (int i = tid / 32; i < K; i += nw)
-    for (int j = lane; j < K; j += 32) {
-      double s = 0.0;
-      for (int k = j; k < K; ++k) s = fma(GAs[i * ldg + k], Lm[k * ldl + j], s);
-      Tm[i * ldl + j] = s;
+  const int KB = (K + 7) / 8;
+  auto ldz = [](const double* X, int ld, int r, int c, int lim) -> double {
+    return (r < lim && c < lim) ? X[r * ld + c] : 0.0;
+  };
+  for (int blk = tid / 32; blk < KB * KB; blk += nw) {
+    const int bi = blk / KB, bj = blk % KB;
+    double acc[2] = {0.0, 0.0};
+    for (int k0 = 8 * bj; k0 < K; k0 += 4)  // L[k][j] = 0 for k < j
+      dmma_8x8x4(acc, ldz(GAs, ldg, 8 * bi + lane / 4, k0 + lane % 4, K),
+                 ldz(Lm, ldl, k0 + lane % 4, 8 * bj + lane / 4, K));
+    const int i = 8 * bi + lane / 4;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = 8 * bj + 2 * (lane % 4) + q;
+      if (i < K && j < K) Tm[i * ldl + j] = acc[q];
     }
+  }
   __syncthreads();
-  for (int i = tid / 32; i < n2; i += nw)
-    for (int j = lane; j < n2; j += 32) {
-      double s = 0.0;
-      if (i < K && j < K)
-        for (int k = i; k < K; ++k) s = fma(Lm[k * ldl + i], Tm[k * ldl + j], s);
-      M[i * ldm + j] = s;
+  const int NB2 = (n2 + 7) / 8;
+  for (int blk = tid / 32; blk < NB2 * NB2; blk += nw) {
+    const int bi = blk / NB2, bj = blk % NB2;
+    double acc[2] = {0.0, 0.0};
+    for (int k0 = 8 * bi; k0 < K; k0 += 4)  // L[k][i] = 0 for k < i
+      dmma_8x8x4(acc, ldz(Lm, ldl, k0 + lane % 4, 8 * bi + lane / 4, K),
+                 ldz(Tm, ldl, k0 + lane % 4, 8 * bj + lane / 4, K));
+    const int i = 8 * bi + lane / 4;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = 8 * bj + 2 * (lane % 4) + q;
+      if (i < n2 && j < n2) M[i * ldm + j] = (i < K && j < K) ? acc[q] : 0.0;
     }
+  }
   __syncthreads();
   for (int idx = tid; idx < n2 * n2; idx += nt) {
     const int i = idx / n2, j = idx % n2;
