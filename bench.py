@@ -33,7 +33,7 @@ METRIC = "outer-sync ms/round & params/s (compress→allreduce→Nesterov), 1/2/
 # plus its 2048 bias (1 050 624 params), full reference round with the adaptive SVD
 CPU_SAMPLE = [(512, 2048), (2048,)]
 # dominant kernels timed with per-launch CUDA events (dlx_kernel_time)
-KERNELS = ("k_o5", "k_tc_sweep_k1", "k_tc_sweep_k2")
+KERNELS = ("k_o5", "k_tc_sweep_k1", "k_tc_sweep_k2", "k_outer_raw")
 
 
 def parse():
@@ -51,6 +51,8 @@ def parse():
                          "controller every round but time at rank1 = 32, the configured rank)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compress", action="store_true",
+                    help="dilocox-no-compress ablation: raw fp32 exchange (compress_raw)")
     ap.add_argument("--side-stream", action="store_true",
                     help="run the effective-rank measurement on a side stream")
     return ap.parse_args()
@@ -211,7 +213,9 @@ def main():
     api.fill_gaussian(L, local, -1e-3, seed=1, tag=0xDA7A, worker=rank, base=anchor)
     torch.cuda.synchronize()
 
-    cfg = OuterConfig(rank1=args.rank, qbits=args.qbits, adaptive=not args.no_adaptive,
+    cfg = OuterConfig(rank1=args.rank, qbits=args.qbits,
+                      adaptive=not (args.no_adaptive or args.no_compress),
+                      compress=not args.no_compress,
                       H1=125, window_c=5, tau=0.5, power_iters=2, seed=1, overlap=True,
                       hold_rank=not args.follow_controller)
     eng = OuterSync(L, cfg, anchor, world=world, rank=rank, side_stream=args.side_stream)
@@ -350,7 +354,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_round,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Tensor::gaussian-identical device generator)",
-            "config": {"workload": f"{args.config} outer-sync round (configs[1])",
+            "config": {"workload": f"{args.config} outer-sync round (configs[1])" +
+                                   (", dilocox-no-compress ablation" if args.no_compress else ""),
                        "params_per_worker": P, "workers": world, "rank1": args.rank,
                        "qbits": args.qbits, "rounding": "stochastic", "power_iters": iters,
                        "adaptive": cfg.adaptive, "tau": cfg.tau, "window_c": cfg.window_c,

@@ -151,6 +151,17 @@ dlx_status dlx_outer_update_range(dlx_ctx* ctx, const dlx_layout* layout, int ra
                                   dlx_round_stats* d_stats, int t_begin, int t_end,
                                   void* stream);
 
+/* dilocox-no-compress ablation (compress_raw compress.cpp:185-199, engine.cpp:231-233): the
+ * exchanged payload is each worker's raw fp32 pending slab; d_gathered holds D slabs back to
+ * back (worker order). Delta = float(sum_w double(x_w) * (1/D)) exactly as allreduce_avg,
+ * then the same fused error feedback / staging / Nesterov as dlx_outer_update. measure_error
+ * of a raw payload is 0 (exact reconstruction). */
+dlx_status dlx_outer_update_raw(dlx_ctx* ctx, const dlx_layout* layout, int D,
+                                const float* d_gathered, int self_index, int mode,
+                                float* d_pending, float* d_anchor, const float* d_local,
+                                float* d_velocity, float gamma, float beta, int classical,
+                                dlx_round_stats* d_stats, void* stream);
+
 /* stage_deltas (engine.cpp:266-276): pending <- (anchor - local) + (d_err ? d_err : 0).
  * d_err may alias d_pending. d_norm_sq (nullable device double) gets ||pending||^2. */
 dlx_status dlx_stage_deltas(dlx_ctx* ctx, const dlx_layout* layout, const float* d_anchor,

@@ -310,6 +310,28 @@ def outer_update(layout: Layout, gathered: torch.Tensor, D: int, rank: int, qbit
                                            int(tensors[1]), _stream(stream)))
 
 
+def compress_raw(layout: Layout, delta: torch.Tensor) -> torch.Tensor:
+    """compress_raw (compress.cpp:185-199): the payload of the no-compress ablation is the
+    raw fp32 slab itself (32 bits per parameter)."""
+    return delta
+
+
+def payload_bits_raw(layout: Layout) -> int:
+    """payload_bits_formula for RawDense payloads (compress.cpp:92-114): 32 n per tensor."""
+    return 32 * int(layout.total_params)
+
+
+def outer_update_raw(layout: Layout, gathered: torch.Tensor, D: int, pending: torch.Tensor,
+                     anchor: torch.Tensor, local: torch.Tensor | None, velocity: torch.Tensor,
+                     gamma: float, beta: float, classical: bool = False, mode: int = OVERLAPPED,
+                     self_index: int = -1, stats: torch.Tensor | None = None, stream=None):
+    """dilocox-no-compress: reference-exact allreduce_avg of D raw slabs (gathered back to
+    back) fused with error feedback, staging and Nesterov."""
+    check(lib().dlx_outer_update_raw(layout.ctx.h, layout.h, D, _ptr(gathered), self_index, mode,
+                                     _ptr(pending), _ptr(anchor), _ptr(local), _ptr(velocity),
+                                     gamma, beta, int(classical), _ptr(stats), _stream(stream)))
+
+
 def stage_deltas(layout: Layout, anchor, local, err, pending, norm_sq=None, stream=None):
     """stage_deltas (engine.cpp:266-276): pending = (anchor - local) + err."""
     check(lib().dlx_stage_deltas(layout.ctx.h, layout.h, _ptr(anchor), _ptr(local), _ptr(err),

@@ -649,6 +649,26 @@ dlx_status dlx_outer_update_range(dlx_ctx* ctx, const dlx_layout* layout, int ra
   });
 }
 
+dlx_status dlx_outer_update_raw(dlx_ctx* ctx, const dlx_layout* layout, int D,
+                                const float* d_gathered, int self_index, int mode,
+                                float* d_pending, float* d_anchor, const float* d_local,
+                                float* d_velocity, float gamma, float beta, int classical,
+                                dlx_round_stats* d_stats, void* stream) {
+  return guard([&] {
+    set_device(ctx);
+    if (D < 1) raise(DLX_ERR_VALIDATION, "allreduce_avg: no payloads");
+    if (mode != DLX_MODE_OVERLAPPED && mode != DLX_MODE_SYNC)
+      raise(DLX_ERR_VALIDATION, "unknown outer-update mode");
+    if (self_index >= D) raise(DLX_ERR_VALIDATION, "self_index out of range");
+    if (mode == DLX_MODE_OVERLAPPED && !d_local)
+      raise(DLX_ERR_VALIDATION, "overlapped mode needs the local parameters");
+    cudaStream_t s = as_stream(stream);
+    if (d_stats) DLX_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(dlx_round_stats), s));
+    launch_outer_raw(*layout, D, d_gathered, self_index, mode, d_pending, d_anchor, d_local,
+                     d_velocity, gamma, beta, classical, d_stats, s);
+  });
+}
+
 dlx_status dlx_outer_update(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits, int D,
                             const uint8_t* d_gathered, int self_index, int mode,
                             float* d_pending, float* d_anchor, const float* d_local,

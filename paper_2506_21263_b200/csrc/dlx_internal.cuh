@@ -270,6 +270,10 @@ void launch_outer_1d(const Plan& P, int D, const uint8_t* gathered, int self_ind
                      const SlotRange& R, cudaStream_t s);
 void launch_reconstruct_dense(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                               float* out, cudaStream_t s);
+void launch_outer_raw(const dlx_layout& L, int D, const float* gathered, int self_index, int mode,
+                      float* pending, float* anchor, const float* local, float* velocity,
+                      float gamma, float beta, int classical, dlx_round_stats* stats,
+                      cudaStream_t s);
 void launch_stage(const dlx_layout& L, const float* anchor, const float* local,
                   const float* err, float* pending, double* norm_sq, cudaStream_t s);
 void launch_nesterov(int64_t n, float gamma, float beta, int classical, float* anchor,

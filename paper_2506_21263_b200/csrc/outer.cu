@@ -717,6 +717,78 @@ void launch_outer_1d(const Plan& P, int D, const uint8_t* gathered, int self_ind
   DLX_LAUNCHED();
 }
 
+// ------------------------------------------------------------------ no-compress ablation
+// dilocox-no-compress (compress_raw compress.cpp:185-199): the payload is the raw fp32 delta,
+// allreduce_avg = float(sum over workers ascending of double(x_w) * (1/D)) — reference-exact
+// — then the same fused epilogue. Elementwise over the whole slab (padding is zero).
+__global__ void __launch_bounds__(256) k_outer_raw(int64_t n, const float* __restrict__ gathered,
+                                                   int64_t slab, int D, int self_index, int mode,
+                                                   float* pending, float* anchor,
+                                                   const float* local, float* velocity,
+                                                   float gamma, float beta, int classical,
+                                                   dlx_round_stats* stats) {
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const double inv = 1.0 / (double)D;
+  const bool ovl = mode == DLX_MODE_OVERLAPPED;
+  // float4 lanes (the slab is a multiple of 64 elements, 256-B aligned)
+  for (int64_t i4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i4 < n / 4;
+       i4 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 4 * i4;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int w = 0; w < D; ++w) {
+      const float4 g = __ldcs(reinterpret_cast<const float4*>(gathered + w * slab + i));
+      acc[0] = __dadd_rn(acc[0], (double)g.x);
+      acc[1] = __dadd_rn(acc[1], (double)g.y);
+      acc[2] = __dadd_rn(acc[2], (double)g.z);
+      acc[3] = __dadd_rn(acc[3], (double)g.w);
+    }
+    const float4 p4 = *reinterpret_cast<const float4*>(pending + i);
+    const float4 a4 = *reinterpret_cast<const float4*>(anchor + i);
+    const float4 v4 = *reinterpret_cast<const float4*>(velocity + i);
+    const float4 l4 = ovl ? __ldcs(reinterpret_cast<const float4*>(local + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float pd[4] = {p4.x, p4.y, p4.z, p4.w}, an[4] = {a4.x, a4.y, a4.z, a4.w};
+    const float ve[4] = {v4.x, v4.y, v4.z, v4.w}, lo[4] = {l4.x, l4.y, l4.z, l4.w};
+    float op[4], oa[4], ov[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float delta = (float)__dmul_rn(acc[j], inv);
+      const EpiOut o = epilogue(delta, pd[j], an[j], lo[j], ve[j], mode, gamma, beta, classical);
+      if (self_index >= 0) {  // measure_error: the raw payload reconstructs exactly
+        const double df = (double)gathered[self_index * slab + i + j] - (double)pd[j];
+        v[0] += df * df;
+        v[1] += (double)pd[j] * (double)pd[j];
+      }
+      v[3] += (double)o.e * (double)o.e;
+      if (ovl) v[2] += (double)o.pend * (double)o.pend;
+      if (!isfinite(o.anchor)) v[4] += 1.0;
+      op[j] = o.pend;
+      oa[j] = o.anchor;
+      ov[j] = o.v;
+    }
+    *reinterpret_cast<float4*>(pending + i) = make_float4(op[0], op[1], op[2], op[3]);
+    *reinterpret_cast<float4*>(anchor + i) = make_float4(oa[0], oa[1], oa[2], oa[3]);
+    *reinterpret_cast<float4*>(velocity + i) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+  }
+  stats_add(stats, v[0], v[1], v[2], v[3], v[4], nullptr);
+}
+
+void launch_outer_raw(const dlx_layout& L, int D, const float* gathered, int self_index, int mode,
+                      float* pending, float* anchor, const float* local, float* velocity,
+                      float gamma, float beta, int classical, dlx_round_stats* stats,
+                      cudaStream_t s) {
+  int dev = 0, sms = 0;
+  DLX_CUDA(cudaGetDevice(&dev));
+  DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (L.slab % 4 != 0) raise(DLX_ERR_VALIDATION, "outer_update_raw: slab not a multiple of 4");
+  // algorithmic bytes: D gathered slabs + pending, anchor, velocity, local read; 3 written
+  // (at D = 1 the single gathered slab is usually the pending buffer itself: read once)
+  const int reads = D + (mode == DLX_MODE_OVERLAPPED ? 4 : 3) - (gathered == pending ? 1 : 0);
+  KernelTimer timer("k_outer_raw", 4.0 * L.slab * (reads + 3), s);
+  k_outer_raw<<<sms * 8, 256, 0, s>>>(L.slab, gathered, L.slab, D, self_index, mode, pending,
+                                      anchor, local, velocity, gamma, beta, classical, stats);
+  DLX_LAUNCHED();
+}
+
 // ------------------------------------------------------------------ dense reconstruction
 // Reference-exact decompress / allreduce_avg (fp64 accumulation over ascending k per
 // worker, float per worker, double sum over workers, * 1/D, float): bit-identical output.

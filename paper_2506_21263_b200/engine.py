@@ -61,6 +61,7 @@ class OuterConfig:
     outer_classical: bool = False
     seed: int = 1
     overlap: bool = True      # dilocox (overlapped) vs dilocox-no-overlap (sync)
+    compress: bool = True     # False: dilocox-no-compress ablation (raw fp32 exchange)
     measure_error: bool = True
     # benchmarking aid: run the adaptive measurement + controller every round but keep
     # operating at rank1 (the controller's choice is recorded in RoundRecord.r_next)
@@ -199,9 +200,40 @@ class OuterSync:
         return exchange(self.payload[:pb], self.gathered, self.warm_q[:qel] if qel > 0 else None,
                         self.world, self.group)
 
+    def _collective_average_raw(self, local: torch.Tensor | None, mode: int) -> RoundRecord:
+        """dilocox-no-compress (engine.cpp:231-233): compress_raw payloads, reference-exact
+        average (all-gather of the raw slabs, fp64 sum in worker order), fused epilogue;
+        no measurement (adaptive needs compression, engine.cpp:50)."""
+        L, cfg = self.L, self.cfg
+        self._ev("compress")
+        payload = api.compress_raw(L, self.pending)
+        self._ev("exchange")
+        if self.world > 1:
+            import torch.distributed as dist
+            if getattr(self, "_gathered_raw", None) is None:
+                self._gathered_raw = torch.empty(self.world * L.slab_elems, dtype=torch.float32,
+                                                 device=self.anchor.device)
+            dist.all_gather_into_tensor(self._gathered_raw, payload, group=self.group)
+            gathered = self._gathered_raw
+        else:
+            gathered = payload
+        cur = torch.cuda.current_stream()
+        self._ev("outer_update")
+        self._wait_pre_update()
+        api.outer_update_raw(L, gathered, self.world, self.pending, self.anchor, local,
+                             self.velocity, cfg.outer_lr, cfg.outer_momentum, cfg.outer_classical,
+                             mode=mode, self_index=self.rank if cfg.measure_error else -1,
+                             stats=self.stats, stream=cur)
+        self._ev("end")
+        self.stats_host[self.round % 2].copy_(self.stats, non_blocking=True)
+        return RoundRecord(round=self.round, r_t=0, H_t=self.H_t, averaged=True,
+                           payload_bytes=api.payload_bits_raw(L) / 8.0, omega_sq=0.0)
+
     def collective_average(self, local: torch.Tensor | None, mode: int) -> RoundRecord:
         """Compress (shared stream per round), exchange, measure, fused outer update."""
         cfg, L = self.cfg, self.L
+        if not cfg.compress:
+            return self._collective_average_raw(local, mode)
         r, q = self.r_t, cfg.qbits
         pb = L.payload_bytes(r, q)
         qel = L.q_factor_elems(r)
@@ -295,7 +327,7 @@ class OuterSync:
 
     def _adapt(self):
         cfg = self.cfg
-        if not cfg.adaptive:
+        if not cfg.adaptive or not cfg.compress:
             return self.r_t, self.H_t
         return api.adapt_compression(self.window, cfg.rank1, cfg.H1, cfg.window_c,
                                      cfg.resolved_H_min())
@@ -318,7 +350,7 @@ class OuterSync:
         self.round += 1
         if self.has_pending:
             rec = self.collective_average(local, OVERLAPPED)
-            if self.cfg.adaptive:
+            if self.cfg.adaptive and self.cfg.compress:
                 self._push_window(rec.r_prime)
         else:
             rec = RoundRecord(round=self.round, r_t=self.r_t, H_t=self.H_t)
@@ -340,7 +372,7 @@ class OuterSync:
         self.has_pending = True
         rec = self.collective_average(None, SYNC)
         r_next, h_next = self.r_t, self.H_t
-        if self.cfg.adaptive:
+        if self.cfg.adaptive and self.cfg.compress:
             self._push_window(rec.r_prime)
             r_next, h_next = self._adapt()
         rec = self._finish(rec, SYNC)
@@ -393,7 +425,7 @@ class OuterSync:
         prev = [self._d2h_ev] if self._d2h_ev is not None else []
         self._pre_update = evs + prev  # for the un-chunked paths (staging round, sync mode)
         job = {"h2d": evs, "prev": prev, "out": h_anchor_out, "done": False}
-        self._host_job = job if self.cfg.overlap else None
+        self._host_job = job if (self.cfg.overlap and self.cfg.compress) else None
         try:
             rec = self.step(self._dev_local)
         finally:

@@ -455,3 +455,34 @@ def test_layouts_recreated_after_close(ctx, oracle):
         ca, _ = decode_payload(L, res.payload, rank, q)
         assert (ca == ref["codes"]).mean() >= 0.99, it
         L.close()
+
+
+@pytest.mark.parametrize("D", [1, 3])
+def test_outer_update_raw_bitexact(ctx, oracle, D):
+    """dilocox-no-compress: allreduce_avg of raw payloads (fp64 sum in worker order, * 1/D,
+    one rounding) and the fused epilogue, bit-exact; measure_error of a raw payload is 0."""
+    from paper_2506_21263_b200 import api
+    import torch
+    shapes = [(40, 36), (36,), (7, 5)]
+    L = mk(ctx, shapes)
+    n = L.total_params
+    xs = [(np.float32(1e-3) * oracle.gaussian(oracle.stream(w, 21), n)[0]).astype(np.float32)
+          for w in range(D)]
+    anchor, local, vel, _ = _rand_state(oracle, L, 5)
+    pend = xs[0]
+    gathered = torch.cat([L.pack(x) for x in xs])
+    dP, dA, dL, dV = L.pack(pend), L.pack(anchor), L.pack(local), L.pack(vel)
+    stats = torch.zeros(8, dtype=torch.float64, device="cuda")
+    api.outer_update_raw(L, gathered, D, dP, dA, dL, dV, 0.7, 0.9, False, mode=api.OVERLAPPED,
+                         self_index=0, stats=stats)
+    f = np.float32
+    delta = (np.sum(np.stack(xs).astype(np.float64), axis=0) * (1.0 / D)).astype(np.float32)
+    e = (pend - delta).astype(f)
+    want_p = ((anchor - local).astype(f) + e).astype(f)
+    want_v = ((f(0.9) * vel).astype(f) + delta).astype(f)
+    want_a = (anchor - (f(0.7) * (delta + (f(0.9) * want_v).astype(f)).astype(f)).astype(f)).astype(f)
+    assert np.array_equal(L.unpack(dP), want_p)
+    assert np.array_equal(L.unpack(dV), want_v)
+    assert np.array_equal(L.unpack(dA), want_a)
+    st = stats.cpu().numpy()
+    assert st[0] == 0.0 and st[1] > 0
