@@ -323,6 +323,77 @@ __device__ long long g_er_prof[8];  // experiments (DLX_ER_PROF): phase cycles o
 constexpr int kErAllSmem = 64;   // n <= 64: L, G_A L, M staged in shared memory
 constexpr int kErMSmem = 128;    // n <= 128: M staged in shared memory
 constexpr int kErMaxN = 256;     // tridiagonal scratch size
+constexpr int kErSwitch = 160;   // global mode: trailing block moves to smem at this size
+
+// Steps k in [k0, k1) of the one-stage Householder tridiagonalisation (P = I - v v^T / H,
+// A <- P A P) of the n x n symmetric matrix M (row stride ldm); sh = shared (H, alpha, K).
+__device__ __noinline__ void hh_steps(double* M, int ldm, int n, int k0, int k1, double* V,
+                                      double* Pv, double* sh) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = k0; k < k1; ++k) {
+    if (tid < 32) {
+      double ss = 0.0;
+      for (int i = k + 1 + tid; i < n; i += 32) {
+        const double x = M[i * ldm + k];
+        ss += x * x;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (tid == 0) {
+        const double x0 = M[(k + 1) * ldm + k];
+        const double nrm = sqrt(ss);
+        if (!(ss - x0 * x0 > 1e-300 * ss) || nrm == 0.0) {
+          sh[0] = 0.0;  // column already reduced
+          sh[1] = x0;
+        } else {
+          const double alpha = x0 > 0.0 ? -nrm : nrm;
+          sh[1] = alpha;
+          sh[0] = ss - x0 * alpha;  // ||v||^2 / 2
+        }
+      }
+    }
+    __syncthreads();
+    const double H = sh[0];
+    if (H == 0.0) {  // uniform
+      __syncthreads();
+      continue;
+    }
+    for (int i = k + 1 + tid; i < n; i += nt) V[i] = i == k + 1 ? M[i * ldm + k] - sh[1] : M[i * ldm + k];
+    __syncthreads();
+    {
+      const int part = tid % 4, rows_per = nt / 4;
+      const int passes = (n - k - 1 + rows_per - 1) / rows_per;  // uniform: all lanes shuffle
+      for (int ps = 0; ps < passes; ++ps) {
+        const int row = k + 1 + tid / 4 + ps * rows_per;
+        double acc = 0.0;
+        if (row < n)
+          for (int j = k + 1 + part; j < n; j += 4) acc = fma(M[row * ldm + j], V[j], acc);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (row < n && part == 0) Pv[row] = acc / H;
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double acc = 0.0;
+      for (int i = k + 1 + tid; i < n; i += 32) acc = fma(V[i], Pv[i], acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (tid == 0) sh[2] = acc / (2.0 * H);
+    }
+    __syncthreads();
+    const double Kc = sh[2];
+    for (int i = k + 1 + tid / 32; i < n; i += nt / 32) {
+      const double vi = V[i], wi = Pv[i] - Kc * vi;
+      for (int j = k + 1 + tid % 32; j < n; j += 32) {
+        const double wj = Pv[j] - Kc * V[j];
+        M[i * ldm + j] -= vi * wj + wi * V[j];
+      }
+    }
+    if (tid == 0) M[(k + 1) * ldm + k] = sh[1];
+    __syncthreads();
+  }
+}
 
 __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, int D, int rr,
                                                  const double* __restrict__ GA,
@@ -478,72 +549,26 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
   }
   __syncthreads();
   ER_MARK(2);
-  // 3a. Householder tridiagonalisation (P = I - v v^T / H, A <- P A P)
+  // 3a. Householder tridiagonalisation. In the global-memory mode the trailing block moves
+  // into shared memory once it fits (kErSwitch rows) and is copied back afterwards.
   double* V = tri;
   double* Pv = tri + kErMaxN;
   const int n = n2;
-  for (int k = 0; k + 2 < n; ++k) {
-    if (tid < 32) {
-      double ss = 0.0;
-      for (int i = k + 1 + tid; i < n; i += 32) {
-        const double x = M[i * ldm + k];
-        ss += x * x;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (tid == 0) {
-        const double x0 = M[(k + 1) * ldm + k];
-        const double nrm = sqrt(ss);
-        if (!(ss - x0 * x0 > 1e-300 * ss) || nrm == 0.0) {
-          s_H = 0.0;  // column already reduced
-          s_alpha = x0;
-        } else {
-          const double alpha = x0 > 0.0 ? -nrm : nrm;
-          s_alpha = alpha;
-          s_H = ss - x0 * alpha;  // ||v||^2 / 2
-        }
-      }
-    }
-    __syncthreads();
-    const double H = s_H;
-    if (H == 0.0) {  // uniform
+  __shared__ double s_hak[3];
+  {
+    const int k_end = max(n - 2, 0);
+    const int k_sw = (all_s || mid_s) ? k_end : max(0, min(k_end, n - kErSwitch));
+    hh_steps(M, ldm, n, 0, k_sw, V, Pv, s_hak);
+    if (k_sw < k_end) {
+      const int ls = kErSwitch + 1;
+      for (int i = k_sw + tid / 32; i < n; i += nt / 32)
+        for (int j = k_sw + tid % 32; j < n; j += 32) er_sm[(i - k_sw) * ls + (j - k_sw)] = M[i * ldm + j];
       __syncthreads();
-      continue;
+      hh_steps(er_sm - (int64_t)k_sw * ls - k_sw, ls, n, k_sw, k_end, V, Pv, s_hak);
+      for (int i = k_sw + tid / 32; i < n; i += nt / 32)
+        for (int j = k_sw + tid % 32; j < n; j += 32) M[i * ldm + j] = er_sm[(i - k_sw) * ls + (j - k_sw)];
+      __syncthreads();
     }
-    for (int i = k + 1 + tid; i < n; i += nt) V[i] = i == k + 1 ? M[i * ldm + k] - s_alpha : M[i * ldm + k];
-    __syncthreads();
-    {
-      const int part = tid % 4, rows_per = nt / 4;
-      const int passes = (n - k - 1 + rows_per - 1) / rows_per;  // uniform: all lanes shuffle
-      for (int ps = 0; ps < passes; ++ps) {
-        const int row = k + 1 + tid / 4 + ps * rows_per;
-        double acc = 0.0;
-        if (row < n)
-          for (int j = k + 1 + part; j < n; j += 4) acc = fma(M[row * ldm + j], V[j], acc);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        if (row < n && part == 0) Pv[row] = acc / H;
-      }
-    }
-    __syncthreads();
-    if (tid < 32) {
-      double acc = 0.0;
-      for (int i = k + 1 + tid; i < n; i += 32) acc = fma(V[i], Pv[i], acc);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (tid == 0) s_K = acc / (2.0 * H);
-    }
-    __syncthreads();
-    const double Kc = s_K;
-    for (int i = k + 1 + tid / 32; i < n; i += nt / 32) {
-      const double vi = V[i], wi = Pv[i] - Kc * vi;
-      for (int j = k + 1 + tid % 32; j < n; j += 32) {
-        const double wj = Pv[j] - Kc * V[j];
-        M[i * ldm + j] -= vi * wj + wi * V[j];
-      }
-    }
-    if (tid == 0) M[(k + 1) * ldm + k] = s_alpha;
-    __syncthreads();
   }
   ER_MARK(3);
   // 3b. eigenvalues of the tridiagonal (d, e) by multisection on Sturm counts: a group of G
@@ -645,7 +670,7 @@ static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const
   static bool attr = false;
   if (!attr) {
     DLX_CUDA(cudaFuncSetAttribute(k_effrank, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(double) * kErMSmem * (kErMSmem + 1))));
+                                  static_cast<int>(sizeof(double) * kErSwitch * (kErSwitch + 1))));
     attr = true;
   }
   int n2max = 0;
@@ -659,6 +684,8 @@ static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const
   } else if (n2max <= kErMSmem) {
     mdim = n2max;
     smem = static_cast<size_t>(mdim) * (mdim + 1) * sizeof(double);
+  } else {
+    smem = static_cast<size_t>(kErSwitch) * (kErSwitch + 1) * sizeof(double);
   }
   const int threads = n2max <= 64 ? 256 : 512;
   k_effrank<<<P.t2.size(), threads, smem, s>>>(P.d_t2, D, rr, GA, GB, GI, gathered,

@@ -31,3 +31,15 @@ for D in [int(x) for x in os.environ.get("DS", "1,2,4,8").split(",")]:
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
     print(f"r={r} D={D} K={D*r}: outer_update {ms:.3f} ms  {28 * L.total_params / ms / 1e6:.0f} GB/s", flush=True)
+
+# effective rank at the same D
+for D in [int(x) for x in os.environ.get("DS", "1,2,4,8").split(",")]:
+    g = pay.repeat(D)
+    for _ in range(2):
+        api.effective_rank_device(L, g, D, r, q, 0.5)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    api.effective_rank_device(L, g, D, r, q, 0.5)
+    e1.record(); torch.cuda.synchronize()
+    print(f"r={r} D={D} K={D*r}: effective_rank {e0.elapsed_time(e1):.3f} ms", flush=True)
