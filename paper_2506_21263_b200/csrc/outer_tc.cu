@@ -78,49 +78,72 @@ __global__ void __launch_bounds__(256) k_o5_prep(
   __shared__ float tile[kPrepRows][BF ? 257 : 65];
   const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kPrepRows;
   const float invD = __fdiv_rn(1.0f, (float)D);
-  {
-    const int rl = threadIdx.x % kPrepRows;
-    const int64_t g = g0 + rl;
+  // phase 1, task = (K column k, 8-row group): the group's 8 codes are one <= 64-bit field of
+  // the column-major factor (segments are 32-row aligned, so groups never straddle one)
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(gathered);
+  const int64_t nwords = D * pay_bytes / 4;
+  const uint32_t mask = (1u << qbits) - 1u;
+  const int sh = 32 - qbits;
+  constexpr int kGroups = kPrepRows / 8;
+  __shared__ int64_t dst_off[kPrepRows];  // element offset of each row's [KA] run; side in bit 62
+  if (threadIdx.x < kPrepRows) {
+    const int64_t g = g0 + threadIdx.x;
+    int64_t o = -1;
     if (g < nrows) {
-      const int4 rw = rows[g];  // (slot, side, row, -)
-      const DevT2& t = T[rw.x];
-      const int side = rw.y, row = rw.z;
-      const int64_t n = side == 0 ? t.a : t.b;
-      for (int k = threadIdx.x / kPrepRows; k < KA; k += 256 / kPrepRows) {
-        const int w = k / t.r, j = k % t.r;
-        float v = 0.f;
-        if (w < D && row < n) {
-          const uint8_t* pay = gathered + w * pay_bytes;
-          const int64_t idx = (int64_t)j * n + row;  // column-major code index within the factor
-          const uint8_t* seg = pay + (side == 0 ? t.seg_pc : t.seg_qc);
-          const int64_t bit = idx * qbits;
-          const uint32_t word = static_cast<uint32_t>(seg[bit >> 3]) |
-                                (static_cast<uint32_t>(seg[(bit >> 3) + 1]) << 8);
-          int c = static_cast<int>((word >> (bit & 7)) & ((1u << qbits) - 1u));
-          if (c & (1 << (qbits - 1))) c -= 1 << qbits;
-          if (side == 0) {
-            v = static_cast<float>(c);
-          } else {
-            const float sp = *reinterpret_cast<const float*>(pay + t.seg_ps + 4 * j);
-            const float sq = *reinterpret_cast<const float*>(pay + t.seg_qs + 4 * j);
-            v = __fmul_rn(static_cast<float>(c), __fmul_rn(__fmul_rn(sp, sq), invD));
-          }
-        }
-        tile[rl][k] = v;
+      const int4 rw = rows[g];
+      o = (rw.y == 0 ? aoff[rw.x] : boff[rw.x]) + static_cast<int64_t>(rw.z) * KA;
+      if (rw.y != 0) o |= int64_t(1) << 62;
+    }
+    dst_off[threadIdx.x] = o;
+  }
+  for (int task = threadIdx.x; task < KA * kGroups; task += 256) {
+    const int k = task / kGroups, grp = task % kGroups;
+    const int64_t g = g0 + 8 * grp;
+    float* dst = &tile[8 * grp][k];
+    if (g >= nrows) continue;
+    const int4 rw = rows[g];  // (slot, side, row, -) of the group's first row
+    const DevT2& t = T[rw.x];
+    const int side = rw.y, row0 = rw.z;
+    const int64_t n = side == 0 ? t.a : t.b;
+    const int w = k / t.r, j = k % t.r;
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (w < D && row0 < n) {
+      const uint8_t* pay = gathered + w * pay_bytes;
+      const int64_t bit = (w * pay_bytes + (side == 0 ? t.seg_pc : t.seg_qc)) * 8 +
+                          ((int64_t)j * n + row0) * qbits;
+      const int64_t wi = bit >> 5;
+      const uint32_t w0 = words[wi];
+      const uint32_t w1 = wi + 1 < nwords ? words[wi + 1] : 0u;
+      const uint32_t w2 = wi + 2 < nwords ? words[wi + 2] : 0u;
+      const int s = static_cast<int>(bit & 31);
+      const uint64_t lo = static_cast<uint64_t>(w0) | (static_cast<uint64_t>(w1) << 32);
+      const uint64_t f = (lo >> s) | (s ? (static_cast<uint64_t>(w2) << (64 - s)) : 0ull);
+      float scale = 1.f;
+      if (side != 0) {
+        const float sp = *reinterpret_cast<const float*>(pay + t.seg_ps + 4 * j);
+        const float sq = *reinterpret_cast<const float*>(pay + t.seg_qs + 4 * j);
+        scale = __fmul_rn(__fmul_rn(sp, sq), invD);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (row0 + i >= n) break;
+        const int c = static_cast<int>((static_cast<uint32_t>(f >> (i * qbits)) & mask) << sh) >> sh;
+        v[i] = side == 0 ? static_cast<float>(c) : __fmul_rn(static_cast<float>(c), scale);
       }
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[i * (BF ? 257 : 65)] = v[i];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < kPrepRows * KA; e += 256) {
     const int rl = e / KA, k = e - rl * KA;
-    const int64_t g = g0 + rl;
-    if (g >= nrows) break;
-    const int4 rw = rows[g];
+    const int64_t dof = dst_off[rl];
+    if (dof < 0) break;
     const float v = tile[rl][k];
-    if (rw.y == 0) {
-      o5_store(&A[aoff[rw.x] + static_cast<int64_t>(rw.z) * KA + k], v);
+    if (!(dof >> 62)) {
+      o5_store(&A[dof + k], v);
     } else {
-      const int64_t o = boff[rw.x] + static_cast<int64_t>(rw.z) * KA + k;
+      const int64_t o = (dof & ((int64_t(1) << 62) - 1)) + k;
       if (!BF) {
         const float h = tf32_hi(v);
         o5_store(&Bp[0][o], h);

@@ -138,12 +138,20 @@ __global__ void __launch_bounds__(256) k_quant_pack(const DevStream* __restrict_
   const uint64_t mask = (1ull << qbits) - 1ull;
   uint64_t bits = 0;
   int valid = 0;
+  // (column, row) of the group's first code: one 32-bit division per group, then stepped
+  const uint32_t clen = static_cast<uint32_t>(st.col_len);
+  const uint32_t idx0 = static_cast<uint32_t>(lg * 8);
+  uint32_t colw = idx0 / clen, roww = idx0 - colw * clen;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int64_t idx = lg * 8 + t;
     if (idx >= total) break;
     ++valid;
-    const int64_t col = idx / st.col_len, row = idx - col * st.col_len;
+    const int64_t col = colw, row = roww;
+    if (++roww == clen) {
+      roww = 0;
+      ++colw;
+    }
     const int64_t c = st.chunk0 + col;
     int code = 0;
     if (cmax[c] != 0.f) {
