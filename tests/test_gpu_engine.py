@@ -87,3 +87,59 @@ def test_step_host_matches_step(ctx, oracle):
         assert torch.equal(e1.velocity, e2.velocity)
         assert torch.equal(e1.pending, e2.pending)
         assert torch.equal(h_anchor, e2.anchor.cpu())
+
+
+def _lowrank_drift(shapes, rank, seed):
+    """Pseudo-gradient with a realistic spectrum (bench-compress's lowrank+noise generator,
+    tools/dilocox.cpp:183-192): a decaying rank-`rank` component plus small noise per 2-D
+    tensor, small noise on 1-D tensors."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for s in shapes:
+        if len(s) == 2:
+            a, b = s
+            u = rng.standard_normal((a, rank)).astype(np.float32)
+            v = rng.standard_normal((b, rank)).astype(np.float32)
+            sv = (1e-3 * 0.7 ** np.arange(rank)).astype(np.float32)
+            d = (u * sv) @ v.T + np.float32(1e-6) * rng.standard_normal((a, b)).astype(np.float32)
+            parts.append(d.astype(np.float32).reshape(-1))
+        else:
+            parts.append((np.float32(1e-4) * rng.standard_normal(s)).astype(np.float32))
+    return np.concatenate(parts)
+
+
+def test_engine_mini_opt_c1(ctx, oracle):
+    """SURVEY C1 (mini-OPT, 10.76 M params, r = 8, q = 8): three overlapped rounds of the
+    engine against the reference round (orc_outer_round) on the full named layout, with a
+    low-rank-plus-noise drift (a flat Gaussian spectrum leaves the rank-8 subspace
+    ill-determined, which amplifies fp32-vs-fp64 rounding in either implementation)."""
+    from paper_2506_21263_b200 import layouts
+    shapes = [s for _, s in layouts.mini_opt()]
+    t = Table(shapes)
+    n = t.numel()
+    rank, q = 8, 8
+    anchor0 = (np.float32(0.02) * oracle.gaussian(oracle.stream(7, 0), n)[0]).astype(np.float32)
+    local = (anchor0 - _lowrank_drift(shapes, rank, 3)).astype(np.float32)
+    from paper_2506_21263_b200 import api
+    from paper_2506_21263_b200.engine import OuterConfig, OuterSync
+    L = api.Layout(ctx, layouts.mini_opt())
+    cfg = OuterConfig(rank1=rank, qbits=q, power_iters=2, adaptive=False, seed=1, overlap=True)
+    eng = OuterSync(L, cfg, L.pack(anchor0))
+    dlocal = L.pack(local)
+    eng.step(dlocal)
+    a = anchor0.copy()
+    v = np.zeros(n, np.float32)
+    pend = (anchor0 - local).astype(np.float32)[None].copy()
+    loc = local[None].copy()
+    wq = np.zeros(max(1, sum(s[1] * min(rank, *s) for s in shapes if len(s) == 2)), np.float32)
+    wr = 0
+    for rnd in (2, 3, 4):
+        rec = eng.step(dlocal)
+        out = oracle.outer_round(t, 1, 1, rnd, rank, q, 0, 2, False, 0.5, rank, 0.7, 0.9, False, 1,
+                                 a, v, pend, loc, wr, wq)
+        wr = out["warm_rank"]
+        assert abs(rec.comp_error - out["comp_error"]) <= 1e-2 * out["comp_error"], rnd
+        assert rec.payload_bytes == out["payload_bits"] / 8.0
+    assert rel_fro(L.unpack(eng.anchor) - anchor0, a - anchor0) <= TOL_STATE
+    assert rel_fro(L.unpack(eng.velocity), v) <= TOL_STATE
+    assert rel_fro(L.unpack(eng.pending), pend[0]) <= TOL_STATE
