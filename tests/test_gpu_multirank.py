@@ -1,0 +1,86 @@
+"""N>1 on real GPUs (skipped with fewer than 2 devices): two ranks (torchrun, NCCL over
+NVLink) run overlapped rounds through OuterSync; every rank must end with bitwise-identical
+anchors and velocities (SPEC anchor consistency: the all-gathered payloads are reconstructed
+with a self_index-independent summation order), and the result must match a single-process
+D=2 reference round (orc_outer_round) within the state tolerance."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+WORKER = r'''
+import json, os, sys
+sys.path.insert(0, os.environ["DLX_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+from oracle.oracle import Oracle, Table
+from paper_2506_21263_b200 import api
+from paper_2506_21263_b200.engine import OuterConfig, OuterSync
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("nccl", device_id=torch.device(f"cuda:{rank}"))
+shapes = [(96, 64), (64,), (64, 200), (200,), (130, 48)]
+R = Oracle("restatement")
+t = Table(shapes)
+n = t.numel()
+anchor0 = (np.float32(0.02) * R.gaussian(R.stream(7, 0), n)[0]).astype(np.float32)
+locs = [(anchor0 - np.float32(1e-3) * R.gaussian(R.stream(1, 10 + w), n)[0]).astype(np.float32)
+        for w in range(world)]
+ctx = api.Context(rank)
+L = api.Layout(ctx, [(f"t{i}", s) for i, s in enumerate(shapes)])
+cfg = OuterConfig(rank1=8, qbits=4, power_iters=2, adaptive=True, seed=1, overlap=True,
+                  hold_rank=True)
+eng = OuterSync(L, cfg, L.pack(anchor0), world=world, rank=rank)
+dl = L.pack(locs[rank])
+recs = [eng.step(dl) for _ in range(4)]
+torch.cuda.synchronize()
+out = {"anchor": L.unpack(eng.anchor).tolist(), "vel": L.unpack(eng.velocity).tolist(),
+       "pend": L.unpack(eng.pending).tolist(), "rprime": [r.r_prime for r in recs]}
+json.dump(out, open(os.path.join(os.environ["DLX_OUT"], f"rank{rank}.json"), "w"))
+dist.barrier()
+dist.destroy_process_group()
+'''
+
+
+def test_two_ranks_nccl_identical_state(tmp_path, oracle):
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    script = tmp_path / "worker.py"
+    script.write_text(WORKER)
+    env = dict(os.environ, DLX_ROOT=ROOT, DLX_OUT=str(tmp_path))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = [json.load(open(tmp_path / f"rank{k}.json")) for k in range(2)]
+    a0, a1 = np.array(res[0]["anchor"], np.float32), np.array(res[1]["anchor"], np.float32)
+    assert np.array_equal(a0, a1), "anchors differ across ranks"
+    assert np.array_equal(np.array(res[0]["vel"]), np.array(res[1]["vel"]))
+    assert res[0]["rprime"] == res[1]["rprime"]
+    # single-process D=2 reference rounds (rounds 2..4; round 1 stages only)
+    from oracle.oracle import Table
+    shapes = [(96, 64), (64,), (64, 200), (200,), (130, 48)]
+    t = Table(shapes)
+    n = t.numel()
+    anchor0 = (np.float32(0.02) * oracle.gaussian(oracle.stream(7, 0), n)[0]).astype(np.float32)
+    locs = np.stack([(anchor0 - np.float32(1e-3) * oracle.gaussian(oracle.stream(1, 10 + w), n)[0])
+                     for w in range(2)]).astype(np.float32)
+    a = anchor0.copy()
+    v = np.zeros(n, np.float32)
+    pend = np.stack([anchor0 - locs[w] for w in range(2)]).astype(np.float32)
+    wq = np.zeros(max(1, sum(s[1] * min(8, *s) for s in shapes if len(s) == 2)), np.float32)
+    wr = 0
+    for rnd in (2, 3, 4):
+        out = oracle.outer_round(t, 2, 1, rnd, 8, 4, 0, 2, False, 0.5, 8, 0.7, 0.9, False, 1,
+                                 a, v, pend, locs.copy(), wr, wq)
+        wr = out["warm_rank"]
+    from tests._util import rel_fro
+    assert rel_fro(a0 - anchor0, a - anchor0) <= 1e-2
+    for k in range(2):
+        assert rel_fro(np.array(res[k]["pend"], np.float32), pend[k]) <= 1e-2
