@@ -151,6 +151,17 @@ dlx_status dlx_outer_update_range(dlx_ctx* ctx, const dlx_layout* layout, int ra
                                   dlx_round_stats* d_stats, int t_begin, int t_end,
                                   void* stream);
 
+/* ---- inner optimiser (the overlap partner) ----------------------------
+ * adamw_step (optim.cpp:15-47) over n contiguous fp32 parameters (16-B aligned buffers):
+ * *step is the caller's persistent step counter and is incremented as in the reference; the
+ * bias corrections and warm-up LR are computed on the host exactly as optim.cpp does, so the
+ * update is bit-exact. A non-finite gradient sets *d_nonfinite (nullable device int) — the
+ * caller raises NumericError after synchronising (the reference throws after the update). */
+dlx_status dlx_adamw_step(dlx_ctx* ctx, int64_t n, float lr, float beta1, float beta2, float eps,
+                          float weight_decay, int64_t warmup_steps, int64_t* step, float* d_p,
+                          const float* d_g, float* d_m, float* d_v, int* d_nonfinite,
+                          void* stream);
+
 /* dilocox-no-compress ablation (compress_raw compress.cpp:185-199, engine.cpp:231-233): the
  * exchanged payload is each worker's raw fp32 pending slab; d_gathered holds D slabs back to
  * back (worker order). Delta = float(sum_w double(x_w) * (1/D)) exactly as allreduce_avg,

@@ -504,6 +504,38 @@ int orc_measure_error(int nt, const int* ndim, const int64_t* dims, const float*
 
 /* ------------------------------------------------------------- Nesterov (optim.cpp:56-78) */
 
+/* ----------------------------------------------------------------- adamw (optim.cpp:15-47) */
+
+int orc_adamw_step(int64_t n, float lr, float beta1, float beta2, float eps, float weight_decay,
+                   int64_t warmup_steps, int64_t* step, float* p, const float* g, float* m,
+                   float* v) {
+  *step += 1;
+  const float bc1 = 1.0f - powf(beta1, (float)(*step));
+  const float bc2 = 1.0f - powf(beta2, (float)(*step));
+  float lr_t = lr;
+  if (warmup_steps > 0 && *step < warmup_steps) lr_t = lr * (float)(*step) / (float)warmup_steps;
+  const float inv_bc1 = 1.0f / bc1;
+  const float inv_bc2 = 1.0f / bc2;
+  float probe = 0.0f;
+  for (int64_t k = 0; k < n; ++k) {
+    const float gk = g[k];
+    probe += gk * 0.0f;
+    const float m1 = beta1 * m[k];
+    const float m2 = (1.0f - beta1) * gk;
+    m[k] = m1 + m2;
+    const float v1 = beta2 * v[k];
+    const float v2 = ((1.0f - beta2) * gk) * gk;
+    v[k] = v1 + v2;
+    const float mhat = m[k] * inv_bc1;
+    const float vhat = v[k] * inv_bc2;
+    const float den = sqrtf(vhat) + eps;
+    const float upd = mhat / den + weight_decay * p[k];
+    p[k] = p[k] - lr_t * upd;
+  }
+  if (!isfinite(probe)) return fail(4, "adamw_step: non-finite gradient");
+  return 0;
+}
+
 int orc_nesterov(int64_t n, float gamma, float beta, int classical, float* anchor, float* v,
                  const float* delta) {
   for (int64_t k = 0; k < n; ++k) {

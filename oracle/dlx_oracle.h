@@ -69,6 +69,11 @@ int orc_allreduce_avg(int D, int nt, const int* ndim, const int64_t* dims, const
                       const int8_t* const* codes, const float* const* scales, float* out);
 int orc_measure_error(int nt, const int* ndim, const int64_t* dims, const float* delta,
                       const int* ranks, const int8_t* codes, const float* scales, double* err);
+/* adamw_step (optim.cpp:15-47) on one flat tensor; *step is the persistent step counter
+ * (incremented). Returns 4 (NumericError) on a non-finite gradient, like the reference. */
+int orc_adamw_step(int64_t n, float lr, float beta1, float beta2, float eps, float weight_decay,
+                   int64_t warmup_steps, int64_t* step, float* p, const float* g, float* m,
+                   float* v);
 int orc_nesterov(int64_t n, float gamma, float beta, int classical, float* anchor, float* v,
                  const float* delta);
 int orc_effective_rank(int nt, const int* ndim, const int64_t* dims, const float* data,

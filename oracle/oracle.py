@@ -252,6 +252,19 @@ class Oracle:
                                                   C.c_float), C.byref(err)))
         return err.value
 
+    def adamw_step(self, p, g, m, v, step, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8,
+                   weight_decay=0.01, warmup_steps=0):
+        """adamw_step (optim.cpp:15-47); returns (p, m, v, step) (inputs untouched)."""
+        p = np.array(p, np.float32, copy=True); m = np.array(m, np.float32, copy=True)
+        v = np.array(v, np.float32, copy=True); g = np.ascontiguousarray(g, np.float32)
+        st = C.c_int64(step)
+        self._check(self.lib.orc_adamw_step(C.c_int64(p.size), C.c_float(lr), C.c_float(beta1),
+                                            C.c_float(beta2), C.c_float(eps),
+                                            C.c_float(weight_decay), C.c_int64(warmup_steps),
+                                            C.byref(st), _p(p, C.c_float), _p(g, C.c_float),
+                                            _p(m, C.c_float), _p(v, C.c_float)))
+        return p, m, v, st.value
+
     def nesterov(self, anchor, v, delta, gamma=0.7, beta=0.9, classical=False):
         anchor = np.array(anchor, np.float32, copy=True); v = np.array(v, np.float32, copy=True)
         delta = np.ascontiguousarray(delta, np.float32)

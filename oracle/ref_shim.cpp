@@ -397,6 +397,35 @@ int orc_measure_error(int nt, const int* ndim, const int64_t* dims, const float*
   });
 }
 
+int orc_adamw_step(int64_t n, float lr, float beta1, float beta2, float eps, float weight_decay,
+                   int64_t warmup_steps, int64_t* step, float* p, const float* g, float* m,
+                   float* v) {
+  return guarded([&] {
+    ParamSet ps, gs;
+    Tensor tp({n}), tg({n});
+    std::memcpy(tp.data(), p, sizeof(float) * static_cast<size_t>(n));
+    std::memcpy(tg.data(), g, sizeof(float) * static_cast<size_t>(n));
+    ps.add("x", std::move(tp));
+    gs.add("x", std::move(tg));
+    AdamWHyper h;
+    h.lr = lr;
+    h.beta1 = beta1;
+    h.beta2 = beta2;
+    h.eps = eps;
+    h.weight_decay = weight_decay;
+    h.warmup_steps = warmup_steps;
+    AdamWState st = make_adamw_state(ps, h);
+    st.step = *step;
+    std::memcpy(st.m.tensor(0).data(), m, sizeof(float) * static_cast<size_t>(n));
+    std::memcpy(st.v.tensor(0).data(), v, sizeof(float) * static_cast<size_t>(n));
+    adamw_step(st, ps, gs);
+    *step = st.step;
+    std::memcpy(p, ps.tensor(0).data(), sizeof(float) * static_cast<size_t>(n));
+    std::memcpy(m, st.m.tensor(0).data(), sizeof(float) * static_cast<size_t>(n));
+    std::memcpy(v, st.v.tensor(0).data(), sizeof(float) * static_cast<size_t>(n));
+  });
+}
+
 int orc_nesterov(int64_t n, float gamma, float beta, int classical, float* anchor, float* v,
                  const float* delta) {
   return guarded([&] {

@@ -79,6 +79,8 @@ PROTOS = {
                                       _vp, _f, _f, _i32, _vp, _i32, _i32, _vp]),
     "dlx_outer_update_raw": (_i32, [_vp, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _f, _f,
                                     _i32, _vp, _vp]),
+    "dlx_adamw_step": (_i32, [_vp, _i64, _f, _f, _f, _f, _f, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                              _vp]),
     "dlx_stage_deltas": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "dlx_nesterov": (_i32, [_vp, _i64, _f, _f, _i32, _vp, _vp, _vp, _vp]),
     "dlx_effective_rank": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _d, _vp, _vp, _vp]),

@@ -310,6 +310,46 @@ def outer_update(layout: Layout, gathered: torch.Tensor, D: int, rank: int, qbit
                                            int(tensors[1]), _stream(stream)))
 
 
+@dataclass
+class AdamWHyper:
+    """optim.hpp:10-19."""
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.95
+    eps: float = 1e-8
+    weight_decay: float = 0.01
+    warmup_steps: int = 0
+
+
+class AdamWState:
+    """make_adamw_state (optim.cpp:7-13): device m, v like the parameters, host step."""
+
+    def __init__(self, params: torch.Tensor, hyper: AdamWHyper | None = None):
+        self.m = torch.zeros_like(params)
+        self.v = torch.zeros_like(params)
+        self.step = 0
+        self.hyper = hyper or AdamWHyper()
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=params.device)
+
+
+def adamw_step(ctx: Context, state: AdamWState, params: torch.Tensor, grads: torch.Tensor,
+               stream=None, raise_nonfinite: bool = False):
+    """adamw_step (optim.cpp:15-47), in place on params / state (bit-exact).
+    raise_nonfinite=True synchronises and raises NumericError on a non-finite gradient, as
+    the reference does (otherwise the flag stays in state.nonfinite)."""
+    h = state.hyper
+    st = C.c_int64(state.step)
+    check(lib().dlx_adamw_step(ctx.h, params.numel(), h.lr, h.beta1, h.beta2, h.eps,
+                               h.weight_decay, h.warmup_steps, C.byref(st),
+                               _ptr(params), _ptr(grads), _ptr(state.m), _ptr(state.v),
+                               _ptr(state.nonfinite), _stream(stream)))
+    state.step = st.value
+    if raise_nonfinite and int(state.nonfinite.item()):
+        state.nonfinite.zero_()
+        from ._lib import NumericError
+        raise NumericError("adamw_step: non-finite gradient")
+
+
 def compress_raw(layout: Layout, delta: torch.Tensor) -> torch.Tensor:
     """compress_raw (compress.cpp:185-199): the payload of the no-compress ablation is the
     raw fp32 slab itself (32 bits per parameter)."""

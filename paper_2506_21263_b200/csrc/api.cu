@@ -649,6 +649,20 @@ dlx_status dlx_outer_update_range(dlx_ctx* ctx, const dlx_layout* layout, int ra
   });
 }
 
+dlx_status dlx_adamw_step(dlx_ctx* ctx, int64_t n, float lr, float beta1, float beta2, float eps,
+                          float weight_decay, int64_t warmup_steps, int64_t* step, float* d_p,
+                          const float* d_g, float* d_m, float* d_v, int* d_nonfinite,
+                          void* stream) {
+  return guard([&] {
+    set_device(ctx);
+    if (n < 0 || !step) raise(DLX_ERR_VALIDATION, "adamw_step: bad arguments");
+    *step += 1;  // optim.cpp:20
+    if (n == 0) return;
+    launch_adamw(n, lr, beta1, beta2, eps, weight_decay, warmup_steps, *step, d_p, d_g, d_m, d_v,
+                 d_nonfinite, as_stream(stream));
+  });
+}
+
 dlx_status dlx_outer_update_raw(dlx_ctx* ctx, const dlx_layout* layout, int D,
                                 const float* d_gathered, int self_index, int mode,
                                 float* d_pending, float* d_anchor, const float* d_local,

@@ -274,6 +274,9 @@ void launch_outer_raw(const dlx_layout& L, int D, const float* gathered, int sel
                       float* pending, float* anchor, const float* local, float* velocity,
                       float gamma, float beta, int classical, dlx_round_stats* stats,
                       cudaStream_t s);
+void launch_adamw(int64_t n, float lr, float beta1, float beta2, float eps, float wd,
+                  int64_t warmup_steps, int64_t step, float* p, const float* g, float* m,
+                  float* v, int* nonfinite, cudaStream_t s);
 void launch_stage(const dlx_layout& L, const float* anchor, const float* local,
                   const float* err, float* pending, double* norm_sq, cudaStream_t s);
 void launch_nesterov(int64_t n, float gamma, float beta, int classical, float* anchor,

@@ -486,3 +486,29 @@ def test_outer_update_raw_bitexact(ctx, oracle, D):
     assert np.array_equal(L.unpack(dA), want_a)
     st = stats.cpu().numpy()
     assert st[0] == 0.0 and st[1] > 0
+
+
+def test_adamw_step_bitexact(ctx, oracle):
+    """Inner optimiser (the overlap partner): adamw_step bit-exact with the oracle over
+    several steps (with warm-up), odd length (vector body + scalar tail), NumericError on a
+    non-finite gradient."""
+    from paper_2506_21263_b200 import NumericError, api
+    import torch
+    n = 10007
+    p = (np.float32(0.02) * oracle.gaussian(oracle.stream(3, 1), n)[0]).astype(np.float32)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    step = 0
+    dp = torch.from_numpy(p.copy()).cuda()
+    st = api.AdamWState(dp, api.AdamWHyper(warmup_steps=3))
+    for k in range(5):
+        g = (np.float32(1e-2) * oracle.gaussian(oracle.stream(4, k), n)[0]).astype(np.float32)
+        p, m, v, step = oracle.adamw_step(p, g, m, v, step, warmup_steps=3)
+        api.adamw_step(ctx, st, dp, torch.from_numpy(g).cuda(), raise_nonfinite=True)
+        assert st.step == step
+        assert np.array_equal(dp.cpu().numpy(), p)
+        assert np.array_equal(st.m.cpu().numpy(), m)
+        assert np.array_equal(st.v.cpu().numpy(), v)
+    g[5] = np.inf
+    with pytest.raises(NumericError):
+        api.adamw_step(ctx, st, dp, torch.from_numpy(g).cuda(), raise_nonfinite=True)

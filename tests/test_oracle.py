@@ -186,3 +186,26 @@ def test_measure_error_under_omega_bound(oracle):
         d = oracle.gaussian(oracle.stream(seed, 0x6A), t.numel())[0]
         c = oracle.compress(t, d, 8, 4, 0, 2, oracle.stream(seed, 1))
         assert oracle.measure_error(t, d, c["ranks"], c["codes"], c["scales"]) <= bound
+
+
+def test_adamw_restatement_matches_reference(oracle, reference):
+    """adamw_step (optim.cpp:15-47): the plain-C restatement is bit-identical to the
+    reference library over several steps, with and without LR warm-up, and both raise
+    NumericError on a non-finite gradient."""
+    n = 4097
+    p = (np.float32(0.02) * oracle.gaussian(oracle.stream(3, 1), n)[0]).astype(np.float32)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    pr, mr, vr, step, stepr = p.copy(), m.copy(), v.copy(), 0, 0
+    for k in range(5):
+        g = (np.float32(1e-2) * oracle.gaussian(oracle.stream(4, k), n)[0]).astype(np.float32)
+        warm = 3 if k % 2 else 0
+        p, m, v, step = oracle.adamw_step(p, g, m, v, step, warmup_steps=warm)
+        pr, mr, vr, stepr = reference.adamw_step(pr, g, mr, vr, stepr, warmup_steps=warm)
+        assert step == stepr
+        assert np.array_equal(p, pr) and np.array_equal(m, mr) and np.array_equal(v, vr)
+    from oracle.oracle import OracleError
+    g[7] = np.nan
+    for backend in (oracle, reference):
+        with pytest.raises(OracleError):
+            backend.adamw_step(p, g, m, v, step)
