@@ -36,7 +36,7 @@ static void make_job(const Plan& P, GramJob* J, const std::vector<DevMat>& mats)
   for (size_t e = 0; e < mats.size(); ++e) {
     const DevMat& m = mats[e];
     J->rmax = std::max(J->rmax, m.r);
-    const int64_t ns = std::max<int64_t>(1, ceil_div(m.n, 1024));
+    const int64_t ns = std::max<int64_t>(1, ceil_div(m.n, 512));
     const int64_t rows = round_up(ceil_div(m.n, ns), 32);
     J->part0.push_back(J->total_parts);
     int cnt = 0;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(320) k_gram_dmma(const DevMat* __restrict__ ma
     cj = ci + rem;
   }
   const bool active = warp < nblk;
-  double acc[2] = {0.0, 0.0};
+  double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};  // two independent DMMA chains
   const float* Y = buf + m.off;
   const int cols = nb * 8;
   const int per = (cols * kGdRows + 319) / 320;  // staged elements per thread (<= 7)
@@ -222,10 +222,15 @@ __global__ void __launch_bounds__(320) k_gram_dmma(const DevMat* __restrict__ ma
       const double* pa = Ys + (ci * 8 + lane / 4) * kGdLd + lane % 4;
       const double* pb = Ys + (cj * 8 + lane / 4) * kGdLd + lane % 4;
 #pragma unroll 4
-      for (int k = 0; k < kGdRows; k += 4) dmma_8x8x4(acc, pa[k], pb[k]);
+      for (int k = 0; k < kGdRows; k += 8) {
+        dmma_8x8x4(acc, pa[k], pb[k]);
+        dmma_8x8x4(acc2, pa[k + 4], pb[k + 4]);
+      }
     }
   }
   if (active) {
+    acc[0] += acc2[0];
+    acc[1] += acc2[1];
     double* out = partial + (int64_t)sp.w * rr * rr;
     const int gj = ci * 8 + lane / 4;
 #pragma unroll
@@ -604,18 +609,25 @@ __global__ void __launch_bounds__(128) k_apply_dmma(const DevMat* __restrict__ m
     for (int rb = 0; rb < 4; ++rb) {
       const int rl = warp * 32 + rb * 8;  // first tile row of this 8-row block
       const double* pa = Ys + (rl + lane / 4) * kAdLdY + lane % 4;
-      for (int cj = 0; cj < nb; ++cj) {
-        double acc[2] = {0.0, 0.0};
-        const double* pb = Rs + (lane % 4) * kAdLdR + cj * 8 + lane / 4;
-        for (int k = 0; k < 8 * (cj + 1); k += 4) dmma_8x8x4(acc, pa[k], pb[k * kAdLdR]);
-        const int64_t row = jb.y + rl + lane / 4;
-        if (row < m.n) {
+      // the four column blocks as independent DMMA chains (block cj needs k < 8 (cj + 1))
+      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      const double* pb = Rs + (lane % 4) * kAdLdR + lane / 4;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        const double a = pa[k];
+#pragma unroll
+        for (int cj = 0; cj < 4; ++cj)
+          if (cj < nb && k < 8 * (cj + 1)) dmma_8x8x4(acc[cj], a, pb[k * kAdLdR + cj * 8]);
+      }
+      const int64_t row = jb.y + rl + lane / 4;
+      if (row < m.n) {
+#pragma unroll
+        for (int cj = 0; cj < 4; ++cj)
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int col = cj * 8 + 2 * (lane % 4) + q;
-            if (col < r) Y[(int64_t)col * m.ld + row] = (float)acc[q];
+            if (cj < nb && col < r) Y[(int64_t)col * m.ld + row] = (float)acc[cj][q];
           }
-        }
       }
     }
     j = jn;
