@@ -53,8 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compress", action="store_true",
                     help="dilocox-no-compress ablation: raw fp32 exchange (compress_raw)")
-    ap.add_argument("--side-stream", action="store_true",
-                    help="run the effective-rank measurement on a side stream")
+    ap.add_argument("--side-stream", type=int, default=None,
+                    help="1/0: run the effective-rank measurement on a side stream (default: "
+                         "on when N > 1, where the ranks split the eigenproblems)")
     return ap.parse_args()
 
 
@@ -218,7 +219,7 @@ def main():
                       compress=not args.no_compress,
                       H1=125, window_c=5, tau=0.5, power_iters=2, seed=1, overlap=True,
                       hold_rank=not args.follow_controller)
-    eng = OuterSync(L, cfg, anchor, world=world, rank=rank, side_stream=args.side_stream)
+    eng = OuterSync(L, cfg, anchor, world=world, rank=rank, side_stream=None if args.side_stream is None else bool(args.side_stream))
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -271,7 +272,7 @@ def main():
         phases[n0] = phases.get(n0, 0.0) + e0.elapsed_time(e1)
     phases = {k: v / args.steps for k, v in phases.items()}
     if eng.side_events:
-        phases["effective_rank (" + ("side stream" if args.side_stream else "inside outer_update") + ")"] = \
+        phases["effective_rank (" + ("side stream" if eng.side is not None else "inside outer_update") + ")"] = \
             sum(a.elapsed_time(b) for a, b in eng.side_events) / args.steps
     eng.phase_events = None
 

@@ -193,6 +193,14 @@ dlx_status dlx_nesterov(dlx_ctx* ctx, int64_t n, float gamma, float beta, int cl
 dlx_status dlx_effective_rank(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
                               int D, const uint8_t* d_gathered, double tau, int* d_per_tensor,
                               double* d_energy, void* stream);
+/* dlx_effective_rank restricted to the 2-D tensors with (index among 2-D tensors) % nshards
+ * == shard; the entries of the other tensors are set to 0. Every rank of a D-worker group
+ * holds the same all-gather buffer, so the group splits the eigenproblems (shard = rank,
+ * nshards = world) and sums the per-tensor arrays (exact: one nonzero term each). */
+dlx_status dlx_effective_rank_shard(dlx_ctx* ctx, const dlx_layout* layout, int rank,
+                                    int qbits, int D, const uint8_t* d_gathered, double tau,
+                                    int shard, int nshards, int* d_per_tensor, double* d_energy,
+                                    void* stream);
 dlx_status dlx_effective_rank_reduce(const dlx_layout* layout, const int* per_tensor,
                                      const double* energy, int r_max, int* aggregate,
                                      int* all_zero);

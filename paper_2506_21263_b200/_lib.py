@@ -84,6 +84,8 @@ PROTOS = {
     "dlx_stage_deltas": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "dlx_nesterov": (_i32, [_vp, _i64, _f, _f, _i32, _vp, _vp, _vp, _vp]),
     "dlx_effective_rank": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _d, _vp, _vp, _vp]),
+    "dlx_effective_rank_shard": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _d, _i32, _i32, _vp, _vp,
+                                        _vp]),
     "dlx_effective_rank_reduce": (_i32, [_vp, _ip, _dp, _i32, _ip, _ip]),
     "dlx_adapt_compression": (_i32, [_ip, _i32, _i32, _i32, _i32, _i32, _ip, _ip]),
     "dlx_omega_bound": (_d, [_i32, _i32, _i32]),

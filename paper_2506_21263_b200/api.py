@@ -395,13 +395,19 @@ class EffectiveRank:
 
 
 def effective_rank_device(layout: Layout, gathered: torch.Tensor, D: int, rank: int,
-                          qbits: int, tau: float, stream=None):
-    """Launch the factor-space effective rank; returns device (per_tensor, energy)."""
+                          qbits: int, tau: float, stream=None, shard: int = 0, nshards: int = 1,
+                          per: torch.Tensor | None = None, energy: torch.Tensor | None = None):
+    """Launch the factor-space effective rank; returns device (per_tensor, energy). With
+    nshards > 1 only the 2-D tensors whose index % nshards == shard are measured and the
+    other entries are zero (dlx_effective_rank_shard)."""
     n2 = sum(1 for s in layout.shapes if len(s) == 2)
-    per = torch.zeros(max(n2, 1), dtype=torch.int32, device=gathered.device)
-    energy = torch.zeros(max(n2, 1), dtype=torch.float64, device=gathered.device)
-    check(lib().dlx_effective_rank(layout.ctx.h, layout.h, rank, qbits, D, _ptr(gathered), tau,
-                                   _ptr(per), _ptr(energy), _stream(stream)))
+    if per is None:
+        per = torch.zeros(max(n2, 1), dtype=torch.int32, device=gathered.device)
+    if energy is None:
+        energy = torch.zeros(max(n2, 1), dtype=torch.float64, device=gathered.device)
+    check(lib().dlx_effective_rank_shard(layout.ctx.h, layout.h, rank, qbits, D, _ptr(gathered),
+                                         tau, shard, nshards, _ptr(per), _ptr(energy),
+                                         _stream(stream)))
     return per, energy
 
 

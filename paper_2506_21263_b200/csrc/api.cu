@@ -712,17 +712,26 @@ dlx_status dlx_nesterov(dlx_ctx* ctx, int64_t n, float gamma, float beta, int cl
   });
 }
 
-dlx_status dlx_effective_rank(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
-                              int D, const uint8_t* d_gathered, double tau, int* d_per_tensor,
-                              double* d_energy, void* stream) {
+dlx_status dlx_effective_rank_shard(dlx_ctx* ctx, const dlx_layout* layout, int rank,
+                                    int qbits, int D, const uint8_t* d_gathered, double tau,
+                                    int shard, int nshards, int* d_per_tensor, double* d_energy,
+                                    void* stream) {
   return guard([&] {
     set_device(ctx);
     validate_quant(rank, qbits);
     if (!(tau > 0.0) || !(tau < 1.0)) raise(DLX_ERR_VALIDATION, "effective_rank: need 0 < tau < 1");
     if (D < 1) raise(DLX_ERR_VALIDATION, "effective_rank: no payloads");
     Plan& P = const_cast<dlx_layout*>(layout)->plan(rank, qbits);
-    effective_rank_factors(ctx, P, D, d_gathered, tau, d_per_tensor, d_energy, as_stream(stream));
+    effective_rank_factors(ctx, P, D, d_gathered, tau, d_per_tensor, d_energy, shard, nshards,
+                           as_stream(stream));
   });
+}
+
+dlx_status dlx_effective_rank(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
+                              int D, const uint8_t* d_gathered, double tau, int* d_per_tensor,
+                              double* d_energy, void* stream) {
+  return dlx_effective_rank_shard(ctx, layout, rank, qbits, D, d_gathered, tau, 0, 1,
+                                  d_per_tensor, d_energy, stream);
 }
 
 dlx_status dlx_effective_rank_reduce(const dlx_layout* layout, const int* per_tensor,

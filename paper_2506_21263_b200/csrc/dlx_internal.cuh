@@ -282,6 +282,7 @@ void launch_stage(const dlx_layout& L, const float* anchor, const float* local,
 void launch_nesterov(int64_t n, float gamma, float beta, int classical, float* anchor,
                      float* v, const float* delta, cudaStream_t s);
 void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
-                            double tau, int* d_per, double* d_energy, cudaStream_t s);
+                            double tau, int* d_per, double* d_energy, int shard, int nshards,
+                            cudaStream_t s);
 
 }  // namespace dlx

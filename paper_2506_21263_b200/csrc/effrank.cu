@@ -403,19 +403,20 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
                                                  int64_t pay_bytes, int sdim, int mdim,
                                                  double* __restrict__ work, double tau,
                                                  int* __restrict__ per,
-                                                 double* __restrict__ energy) {
+                                                 double* __restrict__ energy, int shard,
+                                                 int nshards) {
   extern __shared__ double er_sm[];
   __shared__ double red[32];
   __shared__ double tri[4 * kErMaxN];  // V | A v / H | diagonal | squared off-diagonal
   __shared__ double s_H, s_alpha, s_K, s_tot;
   __shared__ int s_k;
-  const int e = blockIdx.x;
+  const int e = shard + blockIdx.x * nshards;  // this shard's tensors: e % nshards == shard
   const DevT2& t = T[e];
   const int K = D * t.r;
   const int n2 = K + (K & 1);
   const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t mat = (int64_t)rr * rr;
-  double* gw = work + 3 * e * mat;
+  double* gw = work + 3 * (int64_t)blockIdx.x * mat;
   // G_A / G_B entries from the integer code Grams (scaled) or the fp64 Grams
   auto gram = [&](int which, int i, int k) -> double {
     if (GI) {
@@ -666,7 +667,8 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
 
 static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const double* GB,
                            const double* GI, const uint8_t* gathered, double* W, double tau,
-                           int* d_per, double* d_energy, cudaStream_t s) {
+                           int* d_per, double* d_energy, int shard, int nshards,
+                           cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     DLX_CUDA(cudaFuncSetAttribute(k_effrank, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -688,9 +690,11 @@ static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const
     smem = static_cast<size_t>(kErSwitch) * (kErSwitch + 1) * sizeof(double);
   }
   const int threads = n2max <= 64 ? 256 : 512;
-  k_effrank<<<P.t2.size(), threads, smem, s>>>(P.d_t2, D, rr, GA, GB, GI, gathered,
-                                               P.payload_bytes, sdim, mdim, W, tau, d_per,
-                                               d_energy);
+  const int ne = static_cast<int>(P.t2.size());
+  const int nb = (ne - shard + nshards - 1) / nshards;
+  if (nb <= 0) return;
+  k_effrank<<<nb, threads, smem, s>>>(P.d_t2, D, rr, GA, GB, GI, gathered, P.payload_bytes,
+                                      sdim, mdim, W, tau, d_per, d_energy, shard, nshards);
   DLX_LAUNCHED();
   if (getenv("DLX_ER_PROF")) {
     long long h[8];
@@ -702,20 +706,30 @@ static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const
 }
 
 void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
-                            double tau, int* d_per, double* d_energy, cudaStream_t s) {
+                            double tau, int* d_per, double* d_energy, int shard, int nshards,
+                            cudaStream_t s) {
   if (P.t2.empty()) return;
+  if (nshards < 1 || shard < 0 || shard >= nshards)
+    raise(DLX_ERR_VALIDATION, "effective_rank: need 0 <= shard < nshards");
+  if (nshards > 1) {  // tensors of other shards report (0, 0)
+    DLX_CUDA(cudaMemsetAsync(d_per, 0, sizeof(int) * P.t2.size(), s));
+    DLX_CUDA(cudaMemsetAsync(d_energy, 0, sizeof(double) * P.t2.size(), s));
+  }
   int K = 0;
   for (const DevT2& t : P.t2) K = std::max(K, D * t.r);
   if (K > kErMaxN) raise(DLX_ERR_VALIDATION, "effective_rank: D * rank above 256 unsupported");
   const int64_t mat = static_cast<int64_t>(K) * K;
   const size_t ne = P.t2.size();
-  auto* W = static_cast<double*>(ctx->scratch("er_W", sizeof(double) * mat * ne * 3));
+  const int nown = (static_cast<int>(ne) - shard + nshards - 1) / nshards;
+  if (nown <= 0) return;
+  auto* W = static_cast<double*>(ctx->scratch("er_W", sizeof(double) * mat * nown * 3));
   if (K <= kErMaxN) {
     // integer code Grams straight from the gathered payloads
     bool fresh = false;
-    CodeGramJob& J = plan_ext<CodeGramJob>(P, "code_gram", &fresh);
+    CodeGramJob& J = plan_ext<CodeGramJob>(
+        P, "code_gram/" + std::to_string(shard) + "/" + std::to_string(nshards), &fresh);
     if (fresh) {
-      for (size_t k = 0; k < ne; ++k)
+      for (size_t k = shard; k < ne; k += static_cast<size_t>(nshards))
         for (int side = 0; side < 2; ++side) {
           const int64_t n = side == 0 ? P.t2[k].a : P.t2[k].b;
           for (int64_t r0 = 0; r0 < n; r0 += kCgChunk)
@@ -726,6 +740,7 @@ void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* g
     }
     auto* GI = static_cast<double*>(ctx->scratch("er_GI", sizeof(double) * mat * ne * 2));
     DLX_CUDA(cudaMemsetAsync(GI, 0, sizeof(double) * mat * ne * 2, s));
+    if (J.chunks.empty()) return;
     {
       const int nt32 = (K + 31) / 32;
       const int gy = (nt32 * (nt32 + 1) / 2 + kCgmWarps * kCgmTilesPerWarp - 1) /
@@ -735,7 +750,7 @@ void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* g
       DLX_LAUNCHED();
     }
     launch_effrank(P, D, K, nullptr, nullptr, GI, gathered,
-                   W, tau, d_per, d_energy, s);
+                   W, tau, d_per, d_energy, shard, nshards, s);
     return;
   }
   float* phat = static_cast<float*>(ctx->scratch("er_phat", sizeof(float) * P.pelems * D));
@@ -752,7 +767,7 @@ void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* g
   const std::string tag = std::to_string(D);
   gram_batched(ctx, P, "erA" + tag, A, phat, GA, s);
   gram_batched(ctx, P, "erB" + tag, B, qhat, GB, s);
-  launch_effrank(P, D, K, GA, GB, nullptr, nullptr, W, tau, d_per, d_energy, s);
+  launch_effrank(P, D, K, GA, GB, nullptr, nullptr, W, tau, d_per, d_energy, shard, nshards, s);
 }
 
 }  // namespace dlx

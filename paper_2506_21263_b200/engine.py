@@ -125,7 +125,8 @@ class RoundRecord:
 
 class OuterSync:
     def __init__(self, layout: api.Layout, cfg: OuterConfig, anchor: torch.Tensor,
-                 world: int = 1, rank: int = 0, group=None, side_stream: bool = False):
+                 world: int = 1, rank: int = 0, group=None, side_stream: bool | None = None,
+                 shard_effective_rank: bool = True):
         self.L = layout
         self.cfg = cfg
         self.world, self.rank, self.group = world, rank, group
@@ -145,16 +146,25 @@ class OuterSync:
         self.payload = torch.zeros(pb, dtype=torch.uint8, device=dev)
         self.gathered = torch.zeros(world * pb, dtype=torch.uint8, device=dev)
         self.stats = torch.zeros(8, dtype=torch.float64, device=dev)
-        # Optional side stream for the effective-rank measurement. Off by default: the fused
+        # Side stream for the effective-rank measurement. Default off at world == 1: the fused
         # outer update is a persistent grid with ~215 KB of shared memory per SM, so side
         # kernels cannot co-reside and only serialise behind it (measured 0.1-0.2 ms slower).
-        self.side = torch.cuda.Stream(device=dev) if side_stream else None
+        # At world > 1 the eigenproblems are split across the ranks (every rank holds the same
+        # all-gather buffer) and each rank's share runs on a few SMs beside the outer update.
+        if side_stream is None:
+            side_stream = world > 1
+        # high priority: the measurement's few CTAs are dispatched ahead of the outer update's
+        # persistent grid, so the host learns r' (next round's rank) early in the round
+        self.side = torch.cuda.Stream(device=dev, priority=-1) if side_stream else None
+        self.er_shards = world if (shard_effective_rank and world > 1) else 1
         # per-round host copies of the device stats, double-buffered (records resolve lazily)
         self.stats_host = torch.zeros((2, 8), dtype=torch.float64, pin_memory=True)
         n2 = sum(1 for s in layout.shapes if len(s) == 2)
         self._n2 = n2
-        self.per_host = torch.zeros(max(n2, 1), dtype=torch.int32, pin_memory=True)
-        self.energy_host = torch.zeros(max(n2, 1), dtype=torch.float64, pin_memory=True)
+        # per-tensor effective ranks (as doubles) | energies: device results and host copy
+        self.er_dev = torch.zeros(2 * max(n2, 1), dtype=torch.float64, device=dev)
+        self.er_per = torch.zeros(max(n2, 1), dtype=torch.int32, device=dev)
+        self.er_host = torch.zeros(2 * max(n2, 1), dtype=torch.float64, pin_memory=True)
         self.last = RoundRecord()
         self.phase_events = None  # optional: list collecting (name, event) on the main stream
         self.side_events: list = []  # (start, end) of the effective rank on the side stream
@@ -256,14 +266,21 @@ class OuterSync:
                 if self.phase_events is not None:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(side)
-                per, energy = api.effective_rank_device(L, gathered, self.world, r, q, cfg.tau,
-                                                        stream=side)
+                nb = max(self._n2, 1)
+                api.effective_rank_device(L, gathered, self.world, r, q, cfg.tau, stream=side,
+                                          shard=self.rank if self.er_shards > 1 else 0,
+                                          nshards=self.er_shards, per=self.er_per,
+                                          energy=self.er_dev[nb:])
+                self.er_dev[:nb].copy_(self.er_per)
+                if self.er_shards > 1:
+                    # one nonzero term per entry: the sum is exact and identical on every rank
+                    import torch.distributed as dist
+                    dist.all_reduce(self.er_dev, group=self.group)
                 if self.phase_events is not None:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(side)
                     self.side_events.append((e0, e1))
-                self.per_host.copy_(per, non_blocking=True)
-                self.energy_host.copy_(energy, non_blocking=True)
+                self.er_host.copy_(self.er_dev, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(side)
         self._outer_update(gathered, r, q, local, mode, cur)
@@ -273,8 +290,10 @@ class OuterSync:
                           payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
         if cfg.adaptive and self._n2:
             ev.synchronize()
-            er = api.effective_rank_reduce(L, self.per_host.numpy()[:self._n2],
-                                           self.energy_host.numpy()[:self._n2], cfg.rank1)
+            h = self.er_host.numpy()
+            nb = max(self._n2, 1)
+            er = api.effective_rank_reduce(L, h[:self._n2].astype(np.int32),
+                                           h[nb:nb + self._n2], cfg.rank1)
             rec.r_prime = er.aggregate
             cur.wait_stream(self.side or cur)
         self.warm_rank = r

@@ -289,6 +289,15 @@ def test_effective_rank_factor_space(ctx, oracle, rank, q, D):
         assert [k for _, k in er.per_tensor] == per.tolist()
         assert er.aggregate == agg and er.all_zero == allz
     per_d, energy_d = api.effective_rank_device(L, torch.cat(pays), D, rank, q, 0.5)
+    # split across S "ranks" (dlx_effective_rank_shard): the sum of the shards is exact
+    for S in (2, 3, 7):
+        ps = [api.effective_rank_device(L, torch.cat(pays), D, rank, q, 0.5, shard=k, nshards=S)
+              for k in range(S)]
+        assert torch.equal(sum(p for p, _ in ps), per_d)
+        assert torch.equal(sum(e for _, e in ps), energy_d)
+        for k, (p, _) in enumerate(ps):
+            own = [i % S == k for i in range(per_d.numel())]
+            assert all((int(x) != 0) == o for x, o in zip(p.tolist(), own))
     en = energy_d.cpu().numpy()
     for x, e in zip(dense, en):
         f = float(np.sum(x.astype(np.float64) ** 2))
