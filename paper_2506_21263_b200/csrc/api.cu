@@ -329,6 +329,8 @@ dlx_status dlx_set_option(const char* key, int value) {
       option_tensor_cores() = value != 0;
     } else if (k == "outer_tensor_cores") {
       option_outer_tc() = value != 0;
+    } else if (k == "effrank_big_from") {
+      option_effrank_big_from() = value;
     } else if (k == "kernel_events") {
       g_kernel_events = value != 0;
     } else {

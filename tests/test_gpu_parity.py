@@ -304,6 +304,45 @@ def test_effective_rank_factor_space(ctx, oracle, rank, q, D):
         assert abs(e - f) <= 1e-5 * f
 
 
+@pytest.mark.parametrize("D,rank,big_from", [(8, 32, 128), (5, 32, 128), (3, 32, 0), (2, 8, 0),
+                                           (1, 8, 0)])
+def test_effective_rank_large_k(ctx, oracle, D, rank, big_from):
+    """The large-K eigen kernel (blocked Cholesky, tiled DMMA products, packed fused
+    Householder, certified multisection; K = D r up to 256) vs the reference's dense SVD of
+    the averaged Delta, per tensor; big_from = 0 forces it on small K too."""
+    from paper_2506_21263_b200 import api
+    import torch
+    shapes = [(300, 280), (280,), (260, 400), (40, 300)]
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    ranks = t.ranks(rank)
+    codes, scales, pays = [], [], []
+    for w in range(D):
+        d = oracle.gaussian(oracle.stream(w, 19), t.numel())[0]
+        c = oracle.compress(t, d, rank, 4, 0, 1, oracle.stream(3, 3))
+        codes.append(c["codes"]); scales.append(c["scales"])
+        pays.append(_payload_from_oracle(L, oracle, t, ranks, rank, 4, c["codes"], c["scales"]))
+    avg = oracle.allreduce_avg(t, ranks, codes, scales)
+    dense = [x for x, s in zip(split_dense(shapes, avg), shapes) if len(s) == 2]
+    api.set_option("effrank_big_from", big_from)
+    try:
+        for tau in (0.3, 0.5, 0.9):
+            per, agg, allz = oracle.effective_rank(t, avg, tau, rank)
+            er = api.effective_rank(L, torch.cat(pays), D, rank, 4, tau, rank)
+            assert [k for _, k in er.per_tensor] == per.tolist()
+            assert er.aggregate == agg and er.all_zero == allz
+        _, energy_d = api.effective_rank_device(L, torch.cat(pays), D, rank, 4, 0.5)
+        for x, e in zip(dense, energy_d.cpu().numpy()):
+            f = float(np.sum(x.astype(np.float64) ** 2))
+            assert abs(e - f) <= 1e-5 * f
+        # an all-zero exchange: k = 1 per tensor, zero energy, all_zero flagged
+        z = torch.zeros_like(torch.cat(pays))
+        er = api.effective_rank(L, z, D, rank, 4, 0.5, rank)
+        assert er.all_zero and er.aggregate == 1 and all(k == 1 for _, k in er.per_tensor)
+    finally:
+        api.set_option("effrank_big_from", 128)
+
+
 def test_errors_are_typed(ctx):
     from paper_2506_21263_b200 import ShapeError, ValidationError, api
     L = mk(ctx, [(8, 8)])
