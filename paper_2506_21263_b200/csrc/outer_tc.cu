@@ -29,7 +29,9 @@
 
 namespace dlx {
 
-constexpr int kO5Threads = 320;
+constexpr int kO5Threads = 320;     // tf32 path: producer, MMA, 8 epilogue warps
+constexpr int kO5ThreadsTA = 352;   // bf16 / TMEM-A path: + a B-operand producer warp
+constexpr int kO5MaxBRing = 4;
 constexpr int kO5MaxStages = 6;
 constexpr int kO5TileN = 16;                          // tile = 128 rows x 16 columns
 constexpr uint32_t kO5StreamBox = 128 * kO5TileN * 4;  // 8 KB per streamed operand (SW64)
@@ -164,22 +166,29 @@ __global__ void __launch_bounds__(256) k_o5_prep(
 // ------------------------------------------------------------------ the kernel
 // 16-column tiles keep 4-5 stages (36 KB each at K = 32) in flight per SM while one is in
 // the epilogue, so the HBM stream does not stall behind a stage that is being written back.
+// bf16 path: the B tile (16 columns x K x 3 planes: 24 KB at K = 256) moves through its own
+// ring, filled by a dedicated warp that follows the stage descriptors; the stream stages then
+// carry only the four 8-KB parameter boxes, so more of them fit (the HBM stream runs further
+// ahead) and the MMA of a tile no longer waits for that tile's stream data.
 template <bool SELF, bool BF>
-__global__ void __launch_bounds__(kO5Threads, 1)
+__global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
     k_o5(const DevT2* __restrict__ T, const O5Maps* __restrict__ maps,
          const int4* __restrict__ bands, int nbands, int* __restrict__ band_ctr, int D, int KA,
-         int nst, int nab, int self_index, int mode, float gamma, float beta, int classical,
-         dlx_round_stats* stats) {
+         int nst, int nab, int nbr, int self_index, int mode, float gamma, float beta,
+         int classical, dlx_round_stats* stats) {
   using KD = O5Kind<BF>;
   extern __shared__ __align__(1024) uint8_t o5smem[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(o5smem) + 1023) & ~uintptr_t(1023));
   const int nkc = KA / KD::AK;                             // 128-B K chunks
-  const uint32_t stage_bytes = 4 * kO5StreamBox + KD::NBP * nkc * kO5BBox;
   // bf16 path: A moves through a ring of nab 16-KB boxes into TMEM (tcgen05.cp) and the MMAs
-  // read it from there; tf32 path: nab whole A bands stay in shared memory
+  // read it from there, B through its own ring of nbr slots; tf32 path: nab whole A bands
+  // stay in shared memory and B rides in the stream stage
   constexpr bool TA = BF;
+  const uint32_t bslot_bytes = KD::NBP * nkc * kO5BBox;
+  const uint32_t stage_bytes = 4 * kO5StreamBox + (TA ? 0u : bslot_bytes);
   const uint32_t aband_bytes = TA ? kO5ABox : nkc * kO5ABox;
-  uint8_t* abuf = smem + nst * stage_bytes;
+  uint8_t* bring = smem + nst * stage_bytes;
+  uint8_t* abuf = bring + (TA ? nbr * bslot_bytes : 0u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(abuf + nab * aband_bytes);
   uint64_t* sfull = bars;                // [nst]
   uint64_t* sempty = sfull + nst;        // [nst]
@@ -187,7 +196,10 @@ __global__ void __launch_bounds__(kO5Threads, 1)
   uint64_t* aempty = afull + 2;          // [2]
   uint64_t* accfull = aempty + 2;        // [2]
   uint64_t* accempty = accfull + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+  uint64_t* tinfo = accempty + 2;        // [nst] stage descriptor written (TA)
+  uint64_t* bfull = tinfo + kO5MaxStages;     // [nbr] (TA)
+  uint64_t* bempty = bfull + kO5MaxBRing;     // [nbr] (TA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + kO5MaxBRing);
   // per-stage tile descriptor written by the producer before the stage's arrive:
   // (t2 slot or -1 = end, row m0, column n0, A slot | 2 first-of-band | 4 last-of-band)
   int4* sinfo = reinterpret_cast<int4*>(tmem_slot + 4);
@@ -199,6 +211,11 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     for (int i = 0; i < nst; ++i) {
       mbar_init(&sfull[i], 1);
       mbar_init(&sempty[i], 1);
+      mbar_init(&tinfo[i], 1);
+    }
+    for (int i = 0; i < nbr; ++i) {
+      mbar_init(&bfull[i], 1);
+      mbar_init(&bempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&afull[i], 1);
@@ -238,19 +255,16 @@ __global__ void __launch_bounds__(kO5Threads, 1)
       const int4 bd = bands[band];  // (slot, m0, first column, columns)
       const O5Maps* mp = maps + bd.x;
       const int ntile = (bd.w + kO5TileN - 1) / kO5TileN;
-      auto push_tile = [&](int n) {
+      auto push_tile = [&](int n) {  // TA: stream boxes only (B: warp 10)
         mbar_wait(&sempty[s], sph ^ 1);
         if (elect_one()) {
           const int n0 = bd.z + kO5TileN * n;
           sinfo[s] = make_int4(bd.x, bd.y, n0, (a < 0 ? 0 : a) | (n == 0 ? 2 : 0) | (n == ntile - 1 ? 4 : 0));
+          mbar_arrive(&tinfo[s]);
           uint8_t* st = smem + s * stage_bytes;
-          mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox + KD::NBP * nkc * kO5BBox);
+          mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox);
           for (int q = 0; q < nstreams; ++q)
             tma_load_2d(st + q * kO5StreamBox, &mp->s[q], &sfull[s], n0, bd.y);
-          uint8_t* bb = st + 4 * kO5StreamBox;
-          for (int pl = 0; pl < KD::NBP; ++pl)
-            for (int kc = 0; kc < nkc; ++kc)
-              tma_load_2d(bb + (pl * nkc + kc) * kO5BBox, &mp->b[pl], &sfull[s], KD::AK * kc, n0);
         }
         __syncwarp();
         if (++s == nst) {
@@ -260,7 +274,8 @@ __global__ void __launch_bounds__(kO5Threads, 1)
       };
       if (TA) {
         // first tile, then the A boxes through the ring (the MMA warp drains them into TMEM
-        // when it reaches that tile), then the rest of the chunk
+        // when it reaches that tile), then the rest of the chunk. (Moving the A boxes to the
+        // B producer warp, or draining them into TMEM ahead of the chunk, measured slower.)
         push_tile(0);
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait(&aempty[ar], arph ^ 1);
@@ -311,6 +326,7 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     mbar_wait(&sempty[s], sph ^ 1);
     if (elect_one()) {
       sinfo[s] = make_int4(-1, 0, 0, 0);
+      if (TA) mbar_arrive(&tinfo[s]);
       mbar_arrive(&sfull[s]);
     }
     __syncwarp();
@@ -319,45 +335,51 @@ __global__ void __launch_bounds__(kO5Threads, 1)
     const uint32_t idesc = BF ? idesc_bf16(kO5TileN) : idesc_tf32(kO5TileN, false, false);
     int s = 0, a = 0, c = 0;
     uint32_t sph = 0, cph = 0, aph[2] = {0, 0};
-    int ar = 0, ta = 1;
-    uint32_t arph = 0;
+    int ar = 0, ta = 1, bs = 0;
+    uint32_t arph = 0, bph = 0;
+
     const uint32_t a_tmem0 = tmem + 128u;
     const uint32_t a_slot_cols = static_cast<uint32_t>(KA / 2);  // bf16: 2 per 32-bit column
     for (;;) {
-      mbar_wait(&sfull[s], sph);
+      mbar_wait(TA ? &tinfo[s] : &sfull[s], sph);  // TA: the descriptor, not the stream data
       const int4 tl = sinfo[s];
       if (tl.x < 0) break;
       const DevT2 t = T[tl.x];
       const bool last_in_band = tl.w & 4;
-      if (TA && (tl.w & 2)) {
-        // new chunk: copy its A band (nkc boxes of 128 rows x 128 B) into the other TMEM slot;
-        // tcgen05.cp and tcgen05.mma execute in issue order, so the MMAs below see it
+      // copy A box `kc` of the next chunk (128 rows x 128 B) from the ring into TMEM slot `sl`;
+      // tcgen05.cp and tcgen05.mma execute in issue order, so later MMAs see it
+      auto drain_box = [&](int sl, int kc) {
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t d0 = sdesc(su32(abuf + ar * kO5ABox), 16u, 1024u);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tmem_cp_128x256b(a_tmem0 + sl * a_slot_cols + 8u * (4 * kc + kk), d0 + 2u * kk);
+          mma_commit(&aempty[ar]);
+        }
+        __syncwarp();
+        if (++ar == nab) {
+          ar = 0;
+          arph ^= 1;
+        }
+      };
+      if (TA && (tl.w & 2)) {  // new chunk: its A band into the other TMEM slot
         ta ^= 1;
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait(&afull[ar], arph);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint64_t d0 = sdesc(su32(abuf + ar * kO5ABox), 16u, 1024u);
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              tmem_cp_128x256b(a_tmem0 + ta * a_slot_cols + 8u * (4 * kc + kk), d0 + 2u * kk);
-            mma_commit(&aempty[ar]);
-          }
-          __syncwarp();
-          if (++ar == nab) {
-            ar = 0;
-            arph ^= 1;
-          }
+          drain_box(ta, kc);
         }
       } else if (!TA && (tl.w & 2)) {
         a = tl.w & 1;
         mbar_wait(&afull[a], aph[a]);
         aph[a] ^= 1;
       }
+      if (TA) mbar_wait(&bfull[bs], bph);
       mbar_wait(&accempty[c], cph ^ 1);
       tc_fence_after();
       const uint32_t abase = su32(abuf + a * aband_bytes);
-      const uint32_t bbase = su32(smem + s * stage_bytes + 4 * kO5StreamBox);
+      const uint32_t bbase = TA ? su32(bring + bs * bslot_bytes)
+                                : su32(smem + s * stage_bytes + 4 * kO5StreamBox);
       const uint64_t a0 = sdesc(abase, 16u, 1024u);
       uint64_t b0[KD::NBP];
 #pragma unroll
@@ -393,15 +415,48 @@ __global__ void __launch_bounds__(kO5Threads, 1)
           }
         }
         mma_commit(&accfull[c]);
+        if (TA) mma_commit(&bempty[bs]);
         if (!TA && last_in_band) mma_commit(&aempty[a]);
+      }
+      __syncwarp();
+
+      if (++s == nst) {
+        s = 0;
+        sph ^= 1;
+      }
+      if (TA && ++bs == nbr) {
+        bs = 0;
+        bph ^= 1;
+      }
+      c ^= 1;
+      if (c == 0) cph ^= 1;
+    }
+  } else if (TA && warp == 10) {
+    // ---------------------------------------------------------------- B producer (TA)
+    int s = 0, bs = 0;
+    uint32_t sph = 0, bph = 0;
+    for (;;) {
+      mbar_wait(&tinfo[s], sph);
+      const int4 tl = sinfo[s];
+      if (tl.x < 0) break;
+      const O5Maps* mp = maps + tl.x;
+      mbar_wait(&bempty[bs], bph ^ 1);
+      if (elect_one()) {
+        uint8_t* bb = bring + bs * bslot_bytes;
+        mbar_expect_tx(&bfull[bs], bslot_bytes);
+        for (int pl = 0; pl < KD::NBP; ++pl)
+          for (int kc = 0; kc < nkc; ++kc)
+            tma_load_2d(bb + (pl * nkc + kc) * kO5BBox, &mp->b[pl], &bfull[bs], KD::AK * kc, tl.z);
       }
       __syncwarp();
       if (++s == nst) {
         s = 0;
         sph ^= 1;
       }
-      c ^= 1;
-      if (c == 0) cph ^= 1;
+      if (++bs == nbr) {
+        bs = 0;
+        bph ^= 1;
+      }
     }
   } else {
     // ---------------------------------------------------------------- epilogue (8 warps)
@@ -548,6 +603,7 @@ struct O5State : PlanExt {
   int D = 0, KA = 0;
   bool bf = false;         // bf16 x 3 operands (K > 32) vs tf32 x 2
   int nab = 2, nst = 0;    // A-band buffers, stream stages
+  int nbr = 0;             // B ring slots (bf16 path)
   size_t smem = 0;
   std::vector<int4> rows;
   int4* d_rows = nullptr;
@@ -591,26 +647,41 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   S.s0 = R.s0;
   S.s1 = R.s1;
   // shared-memory plan: A band buffers (double if 3+ stream stages still fit) + stages
-  static const size_t budget = [] {  // experiments: DLX_O5_SMEM_KB
+  // tf32: 215 KB measured best; bf16 (stream-only stages): the whole 227 KB
+  static const int budget_kb = [] {  // experiments: DLX_O5_SMEM_KB
     const char* e = getenv("DLX_O5_SMEM_KB");
-    return static_cast<size_t>(e ? atoi(e) : 215) * 1024;
+    return e ? atoi(e) : 0;
   }();
+  const size_t budget = static_cast<size_t>(budget_kb ? budget_kb : (S.bf ? 227 : 215)) * 1024;
   const int nkc = S.KA / ak;
-  const size_t stage = 4 * kO5StreamBox + nbp * nkc * kO5BBox + 2 * 8 + 16;
+  // bf16: B moves through its own ring (nbr slots), the stages carry the stream boxes only
+  const size_t bslot = static_cast<size_t>(nbp) * nkc * kO5BBox;
+  const size_t stage = 4 * kO5StreamBox + (S.bf ? 0 : bslot) + 2 * 8 + 16;
   // tf32: whole A bands in shared memory; bf16: a 2-box ring feeding A into TMEM
   const size_t aband = S.bf ? kO5ABox : static_cast<size_t>(nkc) * kO5ABox;
-  auto stages = [&](int nab) {
-    const size_t fixed = 1024 + nab * aband + 16 + 8 * 8;
+  constexpr size_t kBars = 1024;  // barriers, TMEM slot, stage descriptors
+  auto stages = [&](int nab, int nbr) {
+    const size_t fixed = 1024 + nab * aband + nbr * bslot + kBars;
     return budget > fixed ? static_cast<int>(std::min<size_t>(kO5MaxStages, (budget - fixed) / stage)) : 0;
   };
-  S.nab = S.bf ? 2 : (stages(2) >= 3 ? 2 : 1);
-  S.nst = stages(S.nab);
+  if (S.bf) {  // two A boxes (one serialises the band loads: D=8 7.7 -> 8.6 ms), then B slots
+    S.nab = 2;
+    S.nbr = stages(S.nab, 3) >= stages(S.nab, 2) ? 3 : 2;
+  } else {
+    S.nab = stages(2, 0) >= 3 ? 2 : 1;
+    S.nbr = 0;
+  }
+  S.nst = stages(S.nab, S.nbr);
   if (S.nst < 2) raise(DLX_ERR_VALIDATION, "outer update: K too large for the tensor-core path");
-  S.smem = 1024 + S.nab * aband + 16 + 8 * 8 + S.nst * stage;
+  S.smem = 1024 + S.nab * aband + S.nbr * bslot + kBars + S.nst * stage;
   // A / B staging offsets cover every slot (shared buffers); bands and rows only the range.
   // Work unit = a chunk of a row band (128 rows x chunk columns); chunks are claimed in
   // band-major order so concurrently active CTAs read adjacent columns of the same rows.
-  const int64_t chunk = (S.bf || S.nab == 2) ? 128 : 256;  // single smem A band: amortise reloads
+  static const int chunk_env = [] {  // experiments: DLX_O5_CHUNK (columns per claimed chunk)
+    const char* e = getenv("DLX_O5_CHUNK");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t chunk = chunk_env ? chunk_env : (S.bf || S.nab == 2) ? 128 : 256;  // single smem A band: amortise reloads
   for (size_t k = 0; k < P.t2.size(); ++k) {
     const DevT2& t = P.t2[k];
     const bool in = static_cast<int>(k) >= R.s0 && static_cast<int>(k) < R.s1;
@@ -649,9 +720,9 @@ static void launch_o5(const Plan& P, const O5State& S, int grid, int nbands, int
     DLX_CUDA(cudaFuncSetAttribute(k_o5<SELF, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  k_o5<SELF, BF><<<grid, kO5Threads, S.smem, s>>>(P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D,
-                                                  S.KA, S.nst, S.nab, self_index, mode, gamma,
-                                                  beta, classical, stats);
+  k_o5<SELF, BF><<<grid, BF ? kO5ThreadsTA : kO5Threads, S.smem, s>>>(
+      P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, S.KA, S.nst, S.nab, S.nbr, self_index,
+      mode, gamma, beta, classical, stats);
 }
 
 void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,

@@ -18,9 +18,9 @@ for l in sass:
         break
     if not inside:
         continue
-    mm = re.search(r'line (\d+)', l)
+    mm = re.search(r'File "([^"]+)", line (\d+)', l)
     if "//##" in l and mm:
-        cur = int(mm.group(1))
+        cur = (mm.group(1), int(mm.group(2)))
         continue
     r = re.match(r'\s+/\*([0-9a-f]+)\*/', l)
     if r:
@@ -36,8 +36,13 @@ for k, r in enumerate(rows[2:]):
     st[m.get(k)] += int(r[si] or 0)
     ex[m.get(k)] += int(r[ei] or 0)
 tot = sum(st.values())
-fname = next(re.search(r'File "([^"]+)"', l).group(1) for l in sass if 'File "' in l)
-src = open(fname).read().splitlines()
-for line, s in st.most_common(top):
-    txt = src[line - 1].strip()[:80] if line else "?"
-    print(f"{100 * s / tot:5.1f}%  exec {ex[line]:>11}  L{line}: {txt}")
+srcs = {}
+for key, s in st.most_common(top):
+    if key is None:
+        print(f"{100 * s / tot:5.1f}%  ?")
+        continue
+    f, line = key
+    if f not in srcs:
+        srcs[f] = open(f).read().splitlines()
+    txt = srcs[f][line - 1].strip()[:80]
+    print(f"{100 * s / tot:5.1f}%  exec {ex[key]:>11}  {f.split('/')[-1]}:{line}: {txt}")
