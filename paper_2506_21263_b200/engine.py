@@ -157,6 +157,14 @@ class OuterSync:
         # persistent grid, so the host learns r' (next round's rank) early in the round
         self.side = torch.cuda.Stream(device=dev, priority=-1) if side_stream else None
         self.er_shards = world if (shard_effective_rank and world > 1) else 1
+        # the shards' per-tensor results are summed on the host over a CPU (gloo) group: the
+        # host waits for r' anyway, and an NCCL kernel would queue behind the outer update's
+        # persistent grid for SMs
+        self._cpu_group = None
+        if self.er_shards > 1:
+            import torch.distributed as dist
+            self._cpu_group = dist.new_group(backend="gloo")
+        self._bcast_work = None  # in-flight warm-start broadcast (waited before next compress)
         # per-round host copies of the device stats, double-buffered (records resolve lazily)
         self.stats_host = torch.zeros((2, 8), dtype=torch.float64, pin_memory=True)
         n2 = sum(1 for s in layout.shapes if len(s) == 2)
@@ -206,9 +214,21 @@ class OuterSync:
         return s / w if w > 0 else 0.0
 
     def _exchange(self, pb: int, qel: int):
-        """All-gather payloads; broadcast worker-0 Q (warm start) — NCCL over NVLink."""
-        return exchange(self.payload[:pb], self.gathered, self.warm_q[:qel] if qel > 0 else None,
-                        self.world, self.group)
+        """All-gather payloads (the outer update waits for it); broadcast worker-0 Q (warm
+        start) asynchronously — only the next round's compress needs it. NCCL over NVLink."""
+        if self.world == 1:
+            return self.payload[:pb]
+        g = exchange(self.payload[:pb], self.gathered, None, self.world, self.group)
+        if qel > 0:
+            import torch.distributed as dist
+            self._bcast_work = dist.broadcast(self.warm_q[:qel], src=0, group=self.group,
+                                              async_op=True)
+        return g
+
+    def _wait_bcast(self):
+        if self._bcast_work is not None:
+            self._bcast_work.wait()  # the current stream waits; the host does not
+            self._bcast_work = None
 
     def _collective_average_raw(self, local: torch.Tensor | None, mode: int) -> RoundRecord:
         """dilocox-no-compress (engine.cpp:231-233): compress_raw payloads, reference-exact
@@ -248,6 +268,7 @@ class OuterSync:
         pb = L.payload_bytes(r, q)
         qel = L.q_factor_elems(r)
         s0 = api.rng_stream(cfg.seed, api.stream_key(0xC09C, self.round))  # engine.cpp:226
+        self._wait_bcast()
         self._ev("compress")
         # compress in place over the warm buffer: each rank overwrites it with its own Q,
         # then rank 0's copy is broadcast (engine.cpp:498-501)
@@ -272,10 +293,6 @@ class OuterSync:
                                           nshards=self.er_shards, per=self.er_per,
                                           energy=self.er_dev[nb:])
                 self.er_dev[:nb].copy_(self.er_per)
-                if self.er_shards > 1:
-                    # one nonzero term per entry: the sum is exact and identical on every rank
-                    import torch.distributed as dist
-                    dist.all_reduce(self.er_dev, group=self.group)
                 if self.phase_events is not None:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(side)
@@ -290,6 +307,10 @@ class OuterSync:
                           payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
         if cfg.adaptive and self._n2:
             ev.synchronize()
+            if self.er_shards > 1:
+                # one nonzero term per entry: the sum is exact and identical on every rank
+                import torch.distributed as dist
+                dist.all_reduce(self.er_host, group=self._cpu_group)
             h = self.er_host.numpy()
             nb = max(self._n2, 1)
             er = api.effective_rank_reduce(L, h[:self._n2].astype(np.int32),
