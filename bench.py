@@ -275,6 +275,15 @@ def main():
         phases["effective_rank (" + ("side stream" if eng.side is not None else "inside outer_update") + ")"] = \
             sum(a.elapsed_time(b) for a, b in eng.side_events) / args.steps
     eng.phase_events = None
+    phases_per_rank = None
+    if world > 1:  # every rank's phase times (rank skew shows up as exchange time)
+        names = sorted(phases)
+        t = torch.tensor([phases[k] for k in names] + [ms / args.steps], dtype=torch.float64,
+                         device=dev)
+        allp = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allp, t)
+        phases_per_rank = [{**{k: float(v) for k, v in zip(names, x.tolist())},
+                            "round": float(x[-1])} for x in allp]
 
     # ---------------- roofline of the dominant kernel (CUDA events around each launch)
     peaks = {}
@@ -367,7 +376,8 @@ def main():
                        "mode": "overlapped (one-step delay)", "parallelism": f"dp{world}",
                        "payload_bytes": recs[-1].payload_bytes if recs else None,
                        "l2": "inputs (>=5 GB slabs) larger than L2; no flush",
-                       "phase_ms": phases},
+                       "phase_ms": phases,
+                       **({"phase_ms_per_rank": phases_per_rank} if phases_per_rank else {})},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "params/s", "steps": ke,

@@ -137,27 +137,63 @@ __global__ void __launch_bounds__(256) k_o5_prep(
     for (int i = 0; i < 8; ++i) dst[i * (BF ? 257 : 65)] = v[i];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < kPrepRows * KA; e += 256) {
-    const int rl = e / KA, k = e - rl * KA;
-    const int64_t dof = dst_off[rl];
-    if (dof < 0) break;
-    const float v = tile[rl][k];
-    if (!(dof >> 62)) {
-      o5_store(&A[dof + k], v);
-    } else {
-      const int64_t o = (dof & ((int64_t(1) << 62) - 1)) + k;
-      if (!BF) {
+  if constexpr (BF) {
+    // 8 consecutive k of one row per thread -> one 16-B store per plane; the 8 reads of a
+    // lane are rotated by (lane / 4) so a warp's reads of one step hit 32 distinct banks
+    const int kg_n = KA / 8;
+    for (int e = threadIdx.x; e < kPrepRows * kg_n; e += 256) {
+      const int rl = e / kg_n, kg = e - rl * kg_n;
+      const int64_t dof = dst_off[rl];
+      if (dof < 0) break;
+      const int rot = (threadIdx.x & 31) >> 2;
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int ii = (i + rot) & 7;
+        v[ii] = tile[rl][8 * kg + ii];
+      }
+      if (!(dof >> 62)) {
+        uint4 pk;
+        uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+          w[i] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(A_) + dof + 8 * kg) = pk;
+      } else {
+        const int64_t o = (dof & ((int64_t(1) << 62) - 1)) + 8 * kg;
+        float rem[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rem[i] = v[i];
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl) {
+          uint4 pk;
+          uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(rem[2 * i], rem[2 * i + 1]);
+            w[i] = *reinterpret_cast<const uint32_t*>(&b2);
+            rem[2 * i] = rem[2 * i] - __low2float(b2);  // exact
+            rem[2 * i + 1] = rem[2 * i + 1] - __high2float(b2);
+          }
+          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(Bp[pl]) + o) = pk;
+        }
+      }
+    }
+  } else {  // tf32: A exact, B = hi + lo
+    for (int e = threadIdx.x; e < kPrepRows * KA; e += 256) {
+      const int rl = e / KA, k = e - rl * KA;
+      const int64_t dof = dst_off[rl];
+      if (dof < 0) break;
+      const float v = tile[rl][k];
+      if (!(dof >> 62)) {
+        o5_store(&A[dof + k], v);
+      } else {
+        const int64_t o = (dof & ((int64_t(1) << 62) - 1)) + k;
         const float h = tf32_hi(v);
         o5_store(&Bp[0][o], h);
         o5_store(&Bp[1][o], v - h);
-      } else {
-        float rem = v;
-#pragma unroll
-        for (int pl = 0; pl < 3; ++pl) {
-          const __nv_bfloat16 b = __float2bfloat16_rn(rem);
-          reinterpret_cast<__nv_bfloat16*>(Bp[pl])[o] = b;
-          rem = rem - __bfloat162float(b);  // exact
-        }
       }
     }
   }

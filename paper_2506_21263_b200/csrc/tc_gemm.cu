@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                const int4* __restrict__ tiles, const int* __restrict__ cta_off, int N,
                int lr, int cr,
                const int* __restrict__ splits, const int64_t* __restrict__ part_off,
-               float* __restrict__ out, float* __restrict__ part) {
+               float* __restrict__ out, float* __restrict__ part, int hints) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t kA = KB * kAStage;          // raw A bytes per stage
@@ -198,14 +198,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (j < nb) {
               const int kj = static_cast<int>(k) + 32 * j;
               if (!A_MN) {
-                tma_load_2d_hint(st + j * kAStage, &mp->a, &lfull[s], kj, tl.y, pol_stream);  // {k, m0}
+                if (hints)
+                  tma_load_2d_hint(st + j * kAStage, &mp->a, &lfull[s], kj, tl.y, pol_stream);  // {k, m0}
+                else
+                  tma_load_2d(st + j * kAStage, &mp->a, &lfull[s], kj, tl.y);
               } else {
 #pragma unroll
                 for (int q = 0; q < 4; ++q)  // raw [k][m] tile: 4 boxes of 32 rows x 32 columns
-                  tma_load_2d_hint(st + j * kAStage + q * 4096, &mp->a, &lfull[s], tl.y + 32 * q, kj,
-                                   pol_stream);
+                  if (hints)
+                    tma_load_2d_hint(st + j * kAStage + q * 4096, &mp->a, &lfull[s], tl.y + 32 * q, kj,
+                                     pol_stream);
+                  else
+                    tma_load_2d(st + j * kAStage + q * 4096, &mp->a, &lfull[s], tl.y + 32 * q, kj);
               }
-              tma_load_2d_hint(st + kA + j * b_box, &mp->b, &lfull[s], kj, 0, pol_keep);  // {k, n}
+              if (hints)
+                tma_load_2d_hint(st + kA + j * b_box, &mp->b, &lfull[s], kj, 0, pol_keep);  // {k, n}
+              else
+                tma_load_2d(st + kA + j * b_box, &mp->b, &lfull[s], kj, 0);
             }
           }
         }
@@ -545,8 +554,13 @@ static void launch_sweep_kb(const Plan& P, const TcMaps* maps, const int4* d_til
                                   227 * 1024));
     attr = true;
   }
+  static const int hints = [] {  // experiments: DLX_SWEEP_HINTS=0 drops the L2 cache hints
+    const char* e = getenv("DLX_SWEEP_HINTS");
+    return e ? atoi(e) : 1;
+  }();
   k_tc_sweep<A_MN, KB><<<grid, kTcThreads, sm, s>>>(P.d_t2, maps, d_tiles, d_off, N, lr, cr,
-                                                    P.d_k2_splits, P.d_k2_part_off, out, part);
+                                                    P.d_k2_splits, P.d_k2_part_off, out, part,
+                                                    hints);
 }
 
 template <bool A_MN>
