@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -30,7 +31,7 @@
 namespace dlx {
 
 constexpr int kO5Threads = 320;     // tf32 path: producer, MMA, 8 epilogue warps
-constexpr int kO5ThreadsTA = 352;   // bf16 / TMEM-A path: + a B-operand producer warp
+constexpr int kO5ThreadsTA = 352;   // fp16 / TMEM-A path: + a B-operand producer warp
 constexpr int kO5MaxBRing = 4;
 constexpr int kO5MaxStages = 6;
 constexpr int kO5TileN = 16;                          // tile = 128 rows x 16 columns
@@ -39,29 +40,59 @@ constexpr uint32_t kO5ABox = 128 * 128;               // 16 KB: 128 rows x 128 B
 constexpr uint32_t kO5BBox = kO5TileN * 128;          // 2 KB: 16 rows x 128 B of K (SW128)
 
 // Operand kinds of the factor GEMM. K = D r <= 32: tf32, A exact, B = hi + lo (2 MMAs per
-// k-step of 8). K > 32 (more workers): bf16, A exact (|code| <= 127), B = b1 + b2 + b3 with
-// each term the bf16 rounding of the remainder (24 significant bits, 3 MMAs per k-step of
-// 16) — half the operand bytes per K, so K = 256 (D = 8 at r = 32) still fits the stages.
+// k-step of 8). K > 32 (more workers): fp16 (kind::f16), A exact (|code| <= 127), B
+// prescaled per tensor by a power of two (k_o5_escale) and split hi + lo (22 significant
+// bits, as the tf32 pair; 2 MMAs per k-step of 16) — half the operand bytes per K of tf32,
+// and two planes instead of three bf16 ones, so K = 256 (D = 8 at r = 32) keeps 5 stages.
 template <bool BF>
 struct O5Kind {
   static constexpr int ES = BF ? 2 : 4;    // bytes per operand element
   static constexpr int AK = 128 / ES;      // K elements per 128-B swizzle atom row
   static constexpr int KS = BF ? 16 : 8;   // MMA K per instruction (32 B)
-  static constexpr int NBP = BF ? 3 : 2;   // B planes
+  static constexpr int NBP = 2;            // B planes (hi + lo)
 };
 
 struct O5Maps {
   CUtensorMap s[4];  // pending, anchor, velocity, local: dims {b, a}, box {16, 128}, SW64
   CUtensorMap a;     // A (codes of P): dims {KA, lda}, box {AK, 128}, SW128
-  CUtensorMap b[3];  // B planes: dims {KA, ldb}, box {AK, 16}, SW128
+  CUtensorMap b[2];  // B planes: dims {KA, ldb}, box {AK, 16}, SW128
 };
 
 // ------------------------------------------------------------------ prep: A and B operands
 template <bool BF>
 constexpr int prep_rows() { return BF ? 32 : 64; }  // factor rows per k_o5_prep block
 
-__device__ __forceinline__ void o5_store(float* p, float v) { *p = v; }
-__device__ __forceinline__ void o5_store(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+// fp16 path: per-tensor power-of-two prescale of B = code_Q s_P s_Q / D, chosen so that
+// max |B| 2^e lies in [2^14, 2^15): both fp16 planes stay in range and the scaling is exact
+// (undone on the fp32 accumulator in the epilogue). pre = 2^e, post = 2^-e per 2-D slot.
+__global__ void __launch_bounds__(256) k_o5_escale(const DevT2* __restrict__ T,
+                                                   const uint8_t* __restrict__ gathered,
+                                                   int64_t pay_bytes, int qbits, int D,
+                                                   float* __restrict__ pre,
+                                                   float* __restrict__ post) {
+  const DevT2& t = T[blockIdx.x];
+  __shared__ float red[8];
+  float m = 0.f;
+  for (int i = threadIdx.x; i < D * t.r; i += 256) {
+    const int w = i / t.r, j = i % t.r;
+    const uint8_t* pay = gathered + w * pay_bytes;
+    const float sp = *reinterpret_cast<const float*>(pay + t.seg_ps + 4 * j);
+    const float sq = *reinterpret_cast<const float*>(pay + t.seg_qs + 4 * j);
+    m = fmaxf(m, fabsf(sp * sq));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i]);
+    const float mb = m * static_cast<float>((1 << (qbits - 1)) - 1) / static_cast<float>(D);
+    int e = 0;
+    if (mb > 0.f && isfinite(mb)) e = min(max(14 - ilogbf(mb), -120), 120);
+    pre[blockIdx.x] = ldexpf(1.f, e);
+    post[blockIdx.x] = ldexpf(1.f, -e);
+  }
+}
 
 // Block = 64 consecutive factor rows: codes are decoded column by column (coalesced over
 // rows), staged in shared memory, and written row-major [row][KA] with coalesced stores.
@@ -71,11 +102,10 @@ __global__ void __launch_bounds__(256) k_o5_prep(
     const DevT2* __restrict__ T, const int4* __restrict__ rows, int nrows,
     const int64_t* __restrict__ aoff, const int64_t* __restrict__ boff,
     const uint8_t* __restrict__ gathered, int64_t pay_bytes, int qbits, int D, int KA,
-    void* __restrict__ A_, void* __restrict__ B0_, void* __restrict__ B1_,
-    void* __restrict__ B2_) {
-  using E = typename std::conditional<BF, __nv_bfloat16, float>::type;
-  E* A = static_cast<E*>(A_);
-  E* Bp[3] = {static_cast<E*>(B0_), static_cast<E*>(B1_), static_cast<E*>(B2_)};
+    const float* __restrict__ pre, void* __restrict__ A_, void* __restrict__ B0_,
+    void* __restrict__ B1_) {
+  float* A = static_cast<float*>(A_);
+  float* Bp[2] = {static_cast<float*>(B0_), static_cast<float*>(B1_)};
   constexpr int kPrepRows = prep_rows<BF>();
   __shared__ float tile[kPrepRows][BF ? 257 : 65];
   const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kPrepRows;
@@ -120,17 +150,19 @@ __global__ void __launch_bounds__(256) k_o5_prep(
       const int s = static_cast<int>(bit & 31);
       const uint64_t lo = static_cast<uint64_t>(w0) | (static_cast<uint64_t>(w1) << 32);
       const uint64_t f = (lo >> s) | (s ? (static_cast<uint64_t>(w2) << (64 - s)) : 0ull);
-      float scale = 1.f;
+      float scale = 1.f, ps = 1.f;
       if (side != 0) {
         const float sp = *reinterpret_cast<const float*>(pay + t.seg_ps + 4 * j);
         const float sq = *reinterpret_cast<const float*>(pay + t.seg_qs + 4 * j);
         scale = __fmul_rn(__fmul_rn(sp, sq), invD);
+        if (BF) ps = pre[rw.x];  // power of two: exact
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         if (row0 + i >= n) break;
         const int c = static_cast<int>((static_cast<uint32_t>(f >> (i * qbits)) & mask) << sh) >> sh;
-        v[i] = side == 0 ? static_cast<float>(c) : __fmul_rn(static_cast<float>(c), scale);
+        v[i] = side == 0 ? static_cast<float>(c)
+                         : __fmul_rn(__fmul_rn(static_cast<float>(c), scale), ps);
       }
     }
 #pragma unroll
@@ -152,33 +184,30 @@ __global__ void __launch_bounds__(256) k_o5_prep(
         const int ii = (i + rot) & 7;
         v[ii] = tile[rl][8 * kg + ii];
       }
-      if (!(dof >> 62)) {
+      if (!(dof >> 62)) {  // A: codes, exact in fp16
         uint4 pk;
         uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-          w[i] = *reinterpret_cast<const uint32_t*>(&b2);
+          const __half2 h2 = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+          w[i] = *reinterpret_cast<const uint32_t*>(&h2);
         }
-        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(A_) + dof + 8 * kg) = pk;
-      } else {
+        *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(A_) + dof + 8 * kg) = pk;
+      } else {  // B (prescaled): hi = fp16(v), lo = fp16(v - hi) (v - hi exact in fp32)
         const int64_t o = (dof & ((int64_t(1) << 62) - 1)) + 8 * kg;
-        float rem[8];
+        uint4 ph, pl;
+        uint32_t* wh = reinterpret_cast<uint32_t*>(&ph);
+        uint32_t* wl = reinterpret_cast<uint32_t*>(&pl);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) rem[i] = v[i];
-#pragma unroll
-        for (int pl = 0; pl < 3; ++pl) {
-          uint4 pk;
-          uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const __nv_bfloat162 b2 = __floats2bfloat162_rn(rem[2 * i], rem[2 * i + 1]);
-            w[i] = *reinterpret_cast<const uint32_t*>(&b2);
-            rem[2 * i] = rem[2 * i] - __low2float(b2);  // exact
-            rem[2 * i + 1] = rem[2 * i + 1] - __high2float(b2);
-          }
-          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(Bp[pl]) + o) = pk;
+        for (int i = 0; i < 4; ++i) {
+          const __half2 h2 = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+          const __half2 l2 = __floats2half2_rn(v[2 * i] - __low2float(h2),
+                                               v[2 * i + 1] - __high2float(h2));
+          wh[i] = *reinterpret_cast<const uint32_t*>(&h2);
+          wl[i] = *reinterpret_cast<const uint32_t*>(&l2);
         }
+        *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(Bp[0]) + o) = ph;
+        *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(Bp[1]) + o) = pl;
       }
     }
   } else {  // tf32: A exact, B = hi + lo
@@ -188,12 +217,12 @@ __global__ void __launch_bounds__(256) k_o5_prep(
       if (dof < 0) break;
       const float v = tile[rl][k];
       if (!(dof >> 62)) {
-        o5_store(&A[dof + k], v);
+        A[dof + k] = v;
       } else {
         const int64_t o = (dof & ((int64_t(1) << 62) - 1)) + k;
         const float h = tf32_hi(v);
-        o5_store(&Bp[0][o], h);
-        o5_store(&Bp[1][o], v - h);
+        Bp[0][o] = h;
+        Bp[1][o] = v - h;
       }
     }
   }
@@ -202,7 +231,7 @@ __global__ void __launch_bounds__(256) k_o5_prep(
 // ------------------------------------------------------------------ the kernel
 // 16-column tiles keep 4-5 stages (36 KB each at K = 32) in flight per SM while one is in
 // the epilogue, so the HBM stream does not stall behind a stage that is being written back.
-// bf16 path: the B tile (16 columns x K x 3 planes: 24 KB at K = 256) moves through its own
+// fp16 path: the B tile (16 columns x K x 2 planes: 16 KB at K = 256) moves through its own
 // ring, filled by a dedicated warp that follows the stage descriptors; the stream stages then
 // carry only the four 8-KB parameter boxes, so more of them fit (the HBM stream runs further
 // ahead) and the MMA of a tile no longer waits for that tile's stream data.
@@ -210,8 +239,8 @@ template <bool SELF, bool BF>
 __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
     k_o5(const DevT2* __restrict__ T, const O5Maps* __restrict__ maps,
          const int4* __restrict__ bands, int nbands, int* __restrict__ band_ctr, int D, int KA,
-         int nst, int nab, int nbr, int self_index, int mode, float gamma, float beta,
-         int classical, dlx_round_stats* stats) {
+         int nst, int nab, int nbr, int a_bw, int self_index, int mode, float gamma,
+         float beta, int classical, const float* __restrict__ post, dlx_round_stats* stats) {
   using KD = O5Kind<BF>;
   extern __shared__ __align__(1024) uint8_t o5smem[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(o5smem) + 1023) & ~uintptr_t(1023));
@@ -228,9 +257,9 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(abuf + nab * aband_bytes);
   uint64_t* sfull = bars;                // [nst]
   uint64_t* sempty = sfull + nst;        // [nst]
-  uint64_t* afull = sempty + nst;        // [2]
-  uint64_t* aempty = afull + 2;          // [2]
-  uint64_t* accfull = aempty + 2;        // [2]
+  uint64_t* afull = sempty + nst;        // [nab <= 4]
+  uint64_t* aempty = afull + 4;          // [nab <= 4]
+  uint64_t* accfull = aempty + 4;        // [2]
   uint64_t* accempty = accfull + 2;      // [2]
   uint64_t* tinfo = accempty + 2;        // [nst] stage descriptor written (TA)
   uint64_t* bfull = tinfo + kO5MaxStages;     // [nbr] (TA)
@@ -253,9 +282,11 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       mbar_init(&bfull[i], 1);
       mbar_init(&bempty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < nab; ++i) {
       mbar_init(&afull[i], 1);
       mbar_init(&aempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&accfull[i], 1);
       mbar_init(&accempty[i], 256);
     }
@@ -313,7 +344,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
         // when it reaches that tile), then the rest of the chunk. (Moving the A boxes to the
         // B producer warp, or draining them into TMEM ahead of the chunk, measured slower.)
         push_tile(0);
-        for (int kc = 0; kc < nkc; ++kc) {
+        for (int kc = 0; kc < nkc && !a_bw; ++kc) {
           mbar_wait(&aempty[ar], arph ^ 1);
           if (elect_one()) {
             mbar_expect_tx(&afull[ar], kO5ABox);
@@ -368,7 +399,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    const uint32_t idesc = BF ? idesc_bf16(kO5TileN) : idesc_tf32(kO5TileN, false, false);
+    const uint32_t idesc = BF ? idesc_f16(kO5TileN) : idesc_tf32(kO5TileN, false, false);
     int s = 0, a = 0, c = 0;
     uint32_t sph = 0, cph = 0, aph[2] = {0, 0};
     int ar = 0, ta = 1, bs = 0;
@@ -469,13 +500,28 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
     }
   } else if (TA && warp == 10) {
     // ---------------------------------------------------------------- B producer (TA)
-    int s = 0, bs = 0;
-    uint32_t sph = 0, bph = 0;
+    int s = 0, bs = 0, ar = 0;
+    uint32_t sph = 0, bph = 0, arph = 0;
     for (;;) {
       mbar_wait(&tinfo[s], sph);
       const int4 tl = sinfo[s];
       if (tl.x < 0) break;
       const O5Maps* mp = maps + tl.x;
+      if (a_bw && (tl.w & 2)) {
+        // the whole A band fits the box ring: issue it as soon as the chunk is scheduled
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(&aempty[ar], arph ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(&afull[ar], kO5ABox);
+            tma_load_2d(abuf + ar * kO5ABox, &mp->a, &afull[ar], KD::AK * kc, tl.y);
+          }
+          __syncwarp();
+          if (++ar == nab) {
+            ar = 0;
+            arph ^= 1;
+          }
+        }
+      }
       mbar_wait(&bempty[bs], bph ^ 1);
       if (elect_one()) {
         uint8_t* bb = bring + bs * bslot_bytes;
@@ -515,6 +561,14 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       if (SELF && D > 1) tmem_ld8(tmem + lane_base + 32u * c + 16u + 8u * half, sv);
       tc_fence_before();
       mbar_arrive(&accempty[c]);
+      if (BF) {  // undo the B prescale (power of two: exact)
+        const float ps = post[tl.x];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          dv[i] = __fmul_rn(dv[i], ps);
+          if (SELF && D > 1) sv[i] = __fmul_rn(sv[i], ps);
+        }
+      }
       uint8_t* st = smem + s * stage_bytes;
       const int64_t grow = tl.y + row;
       const int64_t col0 = tl.z + 8 * half;
@@ -640,6 +694,7 @@ struct O5State : PlanExt {
   bool bf = false;         // bf16 x 3 operands (K > 32) vs tf32 x 2
   int nab = 2, nst = 0;    // A-band buffers, stream stages
   int nbr = 0;             // B ring slots (bf16 path)
+  int a_bw = 0;            // bf16: A boxes issued by the B warp (whole band fits the ring)
   size_t smem = 0;
   std::vector<int4> rows;
   int4* d_rows = nullptr;
@@ -700,8 +755,18 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
     const size_t fixed = 1024 + nab * aband + nbr * bslot + kBars;
     return budget > fixed ? static_cast<int>(std::min<size_t>(kO5MaxStages, (budget - fixed) / stage)) : 0;
   };
-  if (S.bf) {  // two A boxes (one serialises the band loads: D=8 7.7 -> 8.6 ms), then B slots
-    S.nab = 2;
+  if (S.bf) {
+    // A box ring: the whole band when that costs no stream stage (its loads are then issued
+    // ahead by the B warp and never stall the stream producer), else two boxes (one
+    // serialises the band loads: D=8 7.7 -> 8.6 ms; four at the cost of two stages: 7.3 ->
+    // 8.0 ms); then B slots
+    static const int nab_env = [] {  // experiments: DLX_O5_NAB
+      const char* e = getenv("DLX_O5_NAB");
+      return e ? atoi(e) : 0;
+    }();
+    S.nab = nab_env ? nab_env : (nkc <= 4 && stages(nkc, 2) >= stages(2, 2) ? std::max(nkc, 2) : 2);
+    S.nab = std::min(S.nab, 4);
+    S.a_bw = S.nab >= nkc ? 1 : 0;
     S.nbr = stages(S.nab, 3) >= stages(S.nab, 2) ? 3 : 2;
   } else {
     S.nab = stages(2, 0) >= 3 ? 2 : 1;
@@ -749,16 +814,16 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
 
 template <bool SELF, bool BF>
 static void launch_o5(const Plan& P, const O5State& S, int grid, int nbands, int D, int self_index,
-                      int mode, float gamma, float beta, int classical, dlx_round_stats* stats,
-                      cudaStream_t s) {
+                      int mode, float gamma, float beta, int classical, const float* post,
+                      dlx_round_stats* stats, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     DLX_CUDA(cudaFuncSetAttribute(k_o5<SELF, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
   k_o5<SELF, BF><<<grid, BF ? kO5ThreadsTA : kO5Threads, S.smem, s>>>(
-      P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, S.KA, S.nst, S.nab, S.nbr, self_index,
-      mode, gamma, beta, classical, stats);
+      P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, S.KA, S.nst, S.nab, S.nbr, S.a_bw,
+      self_index, mode, gamma, beta, classical, post, stats);
 }
 
 void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
@@ -771,22 +836,30 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   const int KA = S.KA;
   const size_t es = S.bf ? 2 : 4;
   void* A = ctx->scratch("o5_A", es * (S.a_elems + 1024));
-  void* B[3] = {ctx->scratch("o5_B0", es * (S.b_elems + 1024)),
-                ctx->scratch("o5_B1", es * (S.b_elems + 1024)),
-                S.bf ? ctx->scratch("o5_B2", es * (S.b_elems + 1024)) : nullptr};
+  void* B[2] = {ctx->scratch("o5_B0", es * (S.b_elems + 1024)),
+                ctx->scratch("o5_B1", es * (S.b_elems + 1024))};
+  float* pre = nullptr;
+  float* post = nullptr;
+  if (S.bf) {  // per-tensor B prescale for the fp16 planes
+    pre = static_cast<float*>(ctx->scratch("o5_escale", sizeof(float) * 2 * (P.t2.size() + 1)));
+    post = pre + P.t2.size() + 1;
+    k_o5_escale<<<static_cast<unsigned>(P.t2.size()), 256, 0, s>>>(P.d_t2, gathered, P.payload_bytes,
+                                                                   P.qbits, D, pre, post);
+    DLX_LAUNCHED();
+  }
   if (S.bf)
     k_o5_prep<true><<<static_cast<unsigned>(ceil_div(S.rows.size(), prep_rows<true>())), 256, 0, s>>>(
         P.d_t2, S.d_rows, static_cast<int>(S.rows.size()), S.d_aoff, S.d_boff, gathered,
-        P.payload_bytes, P.qbits, D, KA, A, B[0], B[1], B[2]);
+        P.payload_bytes, P.qbits, D, KA, pre, A, B[0], B[1]);
   else
     k_o5_prep<false><<<static_cast<unsigned>(ceil_div(S.rows.size(), prep_rows<false>())), 256, 0, s>>>(
         P.d_t2, S.d_rows, static_cast<int>(S.rows.size()), S.d_aoff, S.d_boff, gathered,
-        P.payload_bytes, P.qbits, D, KA, A, B[0], B[1], B[2]);
+        P.payload_bytes, P.qbits, D, KA, pre, A, B[0], B[1]);
   DLX_LAUNCHED();
   const void* key[8] = {pending, anchor, velocity, mode == DLX_MODE_OVERLAPPED ? local : nullptr,
-                        A, B[0], B[1], B[2]};
+                        A, B[0], B[1], nullptr};
   if (!std::equal(key, key + 8, S.key)) {
-    const CUtensorMapDataType dt = S.bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const CUtensorMapDataType dt = S.bf ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const uint32_t ak = S.bf ? O5Kind<true>::AK : O5Kind<false>::AK;
     for (size_t k = S.s0; k < static_cast<size_t>(S.s1); ++k) {
       const DevT2& t = P.t2[k];
@@ -799,7 +872,7 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
                         CU_TENSOR_MAP_SWIZZLE_64B);
       o5_encode_map(&m.a, static_cast<uint8_t*>(A) + es * S.aoff[k], KA, t.lda, KA * es, ak, 128,
                     CU_TENSOR_MAP_SWIZZLE_128B, dt);
-      for (int pl = 0; pl < (S.bf ? 3 : 2); ++pl)
+      for (int pl = 0; pl < 2; ++pl)
         o5_encode_map(&m.b[pl], static_cast<uint8_t*>(B[pl]) + es * S.boff[k], KA, t.ldb, KA * es, ak,
                       kO5TileN, CU_TENSOR_MAP_SWIZZLE_128B, dt);
     }
@@ -819,14 +892,14 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   KernelTimer timer("k_o5", (mode == DLX_MODE_OVERLAPPED ? 28.0 : 24.0) * S.params, s);
   if (self_index >= 0) {
     if (S.bf)
-      launch_o5<true, true>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, stats, s);
+      launch_o5<true, true>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
     else
-      launch_o5<true, false>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, stats, s);
+      launch_o5<true, false>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
   } else {
     if (S.bf)
-      launch_o5<false, true>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, stats, s);
+      launch_o5<false, true>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
     else
-      launch_o5<false, false>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, stats, s);
+      launch_o5<false, false>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
   }
   DLX_LAUNCHED();
 }
