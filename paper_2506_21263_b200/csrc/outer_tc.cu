@@ -31,7 +31,7 @@
 namespace dlx {
 
 constexpr int kO5Threads = 320;     // tf32 path: producer, MMA, 8 epilogue warps
-constexpr int kO5ThreadsTA = 352;   // fp16 / TMEM-A path: + a B-operand producer warp
+constexpr int kO5ThreadsTA = 384;   // fp16 / TMEM-A path: + B-operand and A-band loader warps
 constexpr int kO5MaxBRing = 4;
 constexpr int kO5MaxStages = 6;
 constexpr int kO5TileN = 16;                          // tile = 128 rows x 16 columns
@@ -239,7 +239,7 @@ template <bool SELF, bool BF>
 __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
     k_o5(const DevT2* __restrict__ T, const O5Maps* __restrict__ maps,
          const int4* __restrict__ bands, int nbands, int* __restrict__ band_ctr, int D, int KA,
-         int nst, int nab, int nbr, int a_bw, int self_index, int mode, float gamma,
+         int nst, int nab, int nbr, int a_mode, int self_index, int mode, float gamma,
          float beta, int classical, const float* __restrict__ post, dlx_round_stats* stats) {
   using KD = O5Kind<BF>;
   extern __shared__ __align__(1024) uint8_t o5smem[];
@@ -264,7 +264,13 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
   uint64_t* tinfo = accempty + 2;        // [nst] stage descriptor written (TA)
   uint64_t* bfull = tinfo + kO5MaxStages;     // [nbr] (TA)
   uint64_t* bempty = bfull + kO5MaxBRing;     // [nbr] (TA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + kO5MaxBRing);
+  uint64_t* adone = bempty + kO5MaxBRing;     // [2] MMAs reading a TMEM A slot done (TA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(adone + 2);
+  // TA: who issues the A boxes — 0 the stream producer (after a chunk's first tile), 1 the B
+  // warp, 2 a dedicated warp (11); bit 2: the MMA warp drains the next chunk's boxes into
+  // the other TMEM slot as they land instead of at the chunk's first tile
+  const int a_src = a_mode & 3;
+  const bool a_early = (a_mode & 4) != 0;
   // per-stage tile descriptor written by the producer before the stage's arrive:
   // (t2 slot or -1 = end, row m0, column n0, A slot | 2 first-of-band | 4 last-of-band)
   int4* sinfo = reinterpret_cast<int4*>(tmem_slot + 4);
@@ -289,6 +295,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&accfull[i], 1);
       mbar_init(&accempty[i], 256);
+      mbar_init(&adone[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -344,7 +351,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
         // when it reaches that tile), then the rest of the chunk. (Moving the A boxes to the
         // B producer warp, or draining them into TMEM ahead of the chunk, measured slower.)
         push_tile(0);
-        for (int kc = 0; kc < nkc && !a_bw; ++kc) {
+        for (int kc = 0; kc < nkc && a_src == 0; ++kc) {
           mbar_wait(&aempty[ar], arph ^ 1);
           if (elect_one()) {
             mbar_expect_tx(&afull[ar], kO5ABox);
@@ -404,6 +411,10 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
     uint32_t sph = 0, cph = 0, aph[2] = {0, 0};
     int ar = 0, ta = 1, bs = 0;
     uint32_t arph = 0, bph = 0;
+    int pend = 0;             // early mode: boxes of the next chunk already in TMEM
+    bool nt_ready = false;    // early mode: the other slot's MMAs are done
+    bool aused[2] = {false, false};
+    uint32_t adph[2] = {0, 0};
 
     const uint32_t a_tmem0 = tmem + 128u;
     const uint32_t a_slot_cols = static_cast<uint32_t>(KA / 2);  // bf16: 2 per 32-bit column
@@ -430,12 +441,22 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
           arph ^= 1;
         }
       };
-      if (TA && (tl.w & 2)) {  // new chunk: its A band into the other TMEM slot
-        ta ^= 1;
-        for (int kc = 0; kc < nkc; ++kc) {
-          mbar_wait(&afull[ar], arph);
-          drain_box(ta, kc);
+      if (TA && (tl.w & 2)) {  // new chunk: (the rest of) its A band into the other TMEM slot
+        const int nt = ta ^ 1;
+        if (a_early && !nt_ready) {
+          if (aused[nt]) {
+            mbar_wait(&adone[nt], adph[nt]);
+            adph[nt] ^= 1;
+          }
+          nt_ready = true;
         }
+        for (; pend < nkc; ++pend) {
+          mbar_wait(&afull[ar], arph);
+          drain_box(nt, pend);
+        }
+        ta = nt;
+        pend = 0;
+        nt_ready = false;
       } else if (!TA && (tl.w & 2)) {
         a = tl.w & 1;
         mbar_wait(&afull[a], aph[a]);
@@ -483,10 +504,22 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
         }
         mma_commit(&accfull[c]);
         if (TA) mma_commit(&bempty[bs]);
+        if (TA && a_early && last_in_band) mma_commit(&adone[ta]);
         if (!TA && last_in_band) mma_commit(&aempty[a]);
       }
       __syncwarp();
-
+      if (TA && a_early) {
+        if (last_in_band) aused[ta] = true;
+        const int nt = ta ^ 1;
+        if (!nt_ready && (!aused[nt] || mbar_test(&adone[nt], adph[nt]))) {
+          if (aused[nt]) adph[nt] ^= 1;
+          nt_ready = true;
+        }
+        while (nt_ready && pend < nkc && mbar_test(&afull[ar], arph)) {
+          drain_box(nt, pend);
+          ++pend;
+        }
+      }
       if (++s == nst) {
         s = 0;
         sph ^= 1;
@@ -507,7 +540,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       const int4 tl = sinfo[s];
       if (tl.x < 0) break;
       const O5Maps* mp = maps + tl.x;
-      if (a_bw && (tl.w & 2)) {
+      if (a_src == 1 && (tl.w & 2)) {
         // the whole A band fits the box ring: issue it as soon as the chunk is scheduled
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait(&aempty[ar], arph ^ 1);
@@ -538,6 +571,34 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       if (++bs == nbr) {
         bs = 0;
         bph ^= 1;
+      }
+    }
+  } else if (TA && warp == 11) {
+    // ---------------------------------------------------------------- A loader (TA, a_src 2)
+    int s = 0, ar = 0;
+    uint32_t sph = 0, arph = 0;
+    for (; a_src == 2;) {
+      mbar_wait(&tinfo[s], sph);
+      const int4 tl = sinfo[s];
+      if (tl.x < 0) break;
+      if (tl.w & 2) {
+        const O5Maps* mp = maps + tl.x;
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(&aempty[ar], arph ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(&afull[ar], kO5ABox);
+            tma_load_2d(abuf + ar * kO5ABox, &mp->a, &afull[ar], KD::AK * kc, tl.y);
+          }
+          __syncwarp();
+          if (++ar == nab) {
+            ar = 0;
+            arph ^= 1;
+          }
+        }
+      }
+      if (++s == nst) {
+        s = 0;
+        sph ^= 1;
       }
     }
   } else {
@@ -694,7 +755,7 @@ struct O5State : PlanExt {
   bool bf = false;         // bf16 x 3 operands (K > 32) vs tf32 x 2
   int nab = 2, nst = 0;    // A-band buffers, stream stages
   int nbr = 0;             // B ring slots (bf16 path)
-  int a_bw = 0;            // bf16: A boxes issued by the B warp (whole band fits the ring)
+  int a_mode = 0;          // fp16 path: A-box issuer / early drain (see k_o5)
   size_t smem = 0;
   std::vector<int4> rows;
   int4* d_rows = nullptr;
@@ -766,7 +827,11 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
     }();
     S.nab = nab_env ? nab_env : (nkc <= 4 && stages(nkc, 2) >= stages(2, 2) ? std::max(nkc, 2) : 2);
     S.nab = std::min(S.nab, 4);
-    S.a_bw = S.nab >= nkc ? 1 : 0;
+    static const int amode_env = [] {  // experiments: DLX_O5_AMODE
+      const char* e = getenv("DLX_O5_AMODE");
+      return e ? atoi(e) : -1;
+    }();
+    S.a_mode = amode_env >= 0 ? amode_env : (S.nab >= nkc ? 1 : 0);
     S.nbr = stages(S.nab, 3) >= stages(S.nab, 2) ? 3 : 2;
   } else {
     S.nab = stages(2, 0) >= 3 ? 2 : 1;
@@ -822,7 +887,7 @@ static void launch_o5(const Plan& P, const O5State& S, int grid, int nbands, int
     attr = true;
   }
   k_o5<SELF, BF><<<grid, BF ? kO5ThreadsTA : kO5Threads, S.smem, s>>>(
-      P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, S.KA, S.nst, S.nab, S.nbr, S.a_bw,
+      P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, S.KA, S.nst, S.nab, S.nbr, S.a_mode,
       self_index, mode, gamma, beta, classical, post, stats);
 }
 
