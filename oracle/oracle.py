@@ -334,5 +334,37 @@ class Oracle:
                     payload_bits=bits.value, err_norm0=en.value, max_delta_norm=mx.value)
 
 
+def ref_mlp_overlapped_run(widths, activation, samples, teacher_hidden, seed, D, H1,
+                           total_steps, batch, rank1, qbits, rounding, power_iters, adaptive,
+                           eval_fraction=0.05):
+    """The reference's own overlapped training run (test_support.hpp:114-218) on the mlp /
+    synthetic-regression workload — reference backend only (oracle/_ref). Returns the initial
+    model (flat, ParamSet order), final anchor, per-round losses and the train split."""
+    if not available("reference"):
+        raise OracleError(1, "reference library not built")
+    lib = C.CDLL(LIBS["reference"])
+    widths = np.ascontiguousarray(widths, np.int32)
+    nparams = sum(int(widths[i]) * int(widths[i + 1]) + int(widths[i + 1])
+                  for i in range(len(widths) - 1))
+    a0 = np.zeros(nparams, np.float32)
+    a1 = np.zeros(nparams, np.float32)
+    losses = np.zeros(total_steps + 1, np.float64)
+    nr = C.c_int(0)
+    tx = np.zeros((samples, int(widths[0])), np.float32)
+    ty = np.zeros((samples, int(widths[-1])), np.float32)
+    nt = C.c_int64(0)
+    rc = lib.orc_ref_mlp_overlapped_run(
+        _p(widths, C.c_int), len(widths), int(activation == "tanh"), C.c_int64(samples),
+        teacher_hidden, C.c_uint64(seed), D, H1, C.c_int64(total_steps), batch, rank1, qbits,
+        rounding, power_iters, int(adaptive), C.c_double(eval_fraction), _p(a0, C.c_float),
+        _p(a1, C.c_float), _p(losses, C.c_double), C.byref(nr), _p(tx, C.c_float),
+        _p(ty, C.c_float), C.byref(nt))
+    if rc != 0:
+        lib.orc_last_error.restype = C.c_char_p
+        raise OracleError(rc, lib.orc_last_error().decode())
+    n = nt.value
+    return dict(anchor0=a0, anchor=a1, losses=losses[:nr.value], train_x=tx[:n], train_y=ty[:n])
+
+
 def available(backend: str) -> bool:
     return os.path.exists(LIBS[backend])

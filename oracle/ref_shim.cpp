@@ -14,6 +14,8 @@
 #include <vector>
 
 #include "dilocox/collective.hpp"
+#include "dilocox/data.hpp"
+#include "dilocox/model.hpp"
 #include "dilocox/compress.hpp"
 #include "dilocox/engine.hpp"
 #include "dilocox/optim.hpp"
@@ -21,6 +23,7 @@
 #include "dilocox/rng.hpp"
 #include "dilocox/tensor.hpp"
 #include "dlx_oracle.h"
+#include "test_support.hpp"  // proj/tests: reference_overlapped_run (the reference's own oracle)
 
 using namespace dilocox;
 
@@ -566,6 +569,58 @@ int orc_outer_round(int D, int nt, const int* ndim, const int64_t* dims, uint64_
       std::memcpy(warm_q + off, q.data(), sizeof(float) * static_cast<size_t>(q.size()));
       off += q.size();
     }
+  });
+}
+
+// The reference's full overlapped training run (test_support.hpp:114-218) on the mlp /
+// synthetic-regression workload (mode dilocox, M = 1): returns the initial model, the final
+// anchor, the per-round mean last-step losses and the train split it trained on.
+int orc_ref_mlp_overlapped_run(const int* widths, int nw, int tanh_act, int64_t samples,
+                               int teacher_hidden, uint64_t seed, int D, int H1,
+                               int64_t total_steps, int batch, int rank1, int qbits,
+                               int rounding, int power_iters, int adaptive,
+                               double eval_fraction, float* anchor0, float* anchor_out,
+                               double* losses, int* nrounds, float* train_x, float* train_y,
+                               int64_t* ntrain) {
+  return guarded([&] {
+    EngineConfig cfg;
+    cfg.mode = Mode::Dilocox;
+    cfg.D = D;
+    cfg.M = 1;
+    cfg.total_inner_steps = total_steps;
+    cfg.batch = batch;
+    cfg.seed = seed;
+    cfg.model = mlp_spec(std::vector<int>(widths, widths + nw),
+                         tanh_act ? Activation::Tanh : Activation::Relu);
+    cfg.schedule.H1 = H1;
+    cfg.schedule.adaptive = adaptive != 0;
+    cfg.compression.rank1 = rank1;
+    cfg.compression.quant.qbits = qbits;
+    cfg.compression.quant.rounding = rounding ? Rounding::Nearest : Rounding::Stochastic;
+    cfg.compression.power_iters = power_iters;
+    Dataset full = make_synthetic_regression(samples, widths[0], widths[nw - 1], teacher_hidden,
+                                             seed);
+    ParamSet a0 = build_model(cfg.model, cfg.seed);
+    int64_t off = 0;
+    for (int i = 0; i < a0.count(); ++i) {
+      const Tensor& t = a0.tensor(i);
+      std::memcpy(anchor0 + off, t.data(), sizeof(float) * static_cast<size_t>(t.size()));
+      off += t.size();
+    }
+    auto split = split_train_eval(full, eval_fraction);
+    const Dataset& train = split.first;
+    *ntrain = train.features.rows();
+    std::memcpy(train_x, train.features.data(), sizeof(float) * static_cast<size_t>(train.features.size()));
+    std::memcpy(train_y, train.targets.data(), sizeof(float) * static_cast<size_t>(train.targets.size()));
+    testsup::ReferenceResult res = testsup::reference_overlapped_run(cfg, full, eval_fraction);
+    off = 0;
+    for (int i = 0; i < res.anchor.count(); ++i) {
+      const Tensor& t = res.anchor.tensor(i);
+      std::memcpy(anchor_out + off, t.data(), sizeof(float) * static_cast<size_t>(t.size()));
+      off += t.size();
+    }
+    *nrounds = static_cast<int>(res.train_losses.size());
+    for (size_t i = 0; i < res.train_losses.size(); ++i) losses[i] = res.train_losses[i];
   });
 }
 

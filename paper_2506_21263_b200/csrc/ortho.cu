@@ -413,11 +413,22 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
   const int np = nparts[e];
   // fold; columns >= r are padded with the identity so the factorisation below runs all 32
   // steps without data-dependent branches
+  // (8 independent partial sums per element: the row-split partials are L2 reads, and a
+  // single dependent chain over ~100 of them made this fold the kernel's whole cost)
   for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
     const int j = idx / 32, k = idx % 32;
     double g = (j == k && j >= r) ? 1.0 : 0.0;
-    if (j < r && k < r && k >= j)
-      for (int p = 0; p < np; ++p) g += src[(int64_t)p * rr * rr + j * rr + k];
+    if (j < r && k < r && k >= j) {
+      const double* sp = src + j * rr + k;
+      const int64_t st = (int64_t)rr * rr;
+      double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      int p = 0;
+      for (; p + 8 <= np; p += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += sp[(p + u) * st];
+      for (; p < np; ++p) a[p & 7] += sp[p * st];
+      g += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    }
     G[j][k] = g;
   }
   __syncthreads();

@@ -1,0 +1,42 @@
+"""§8f row 3: a full overlapped DiLoCoX training run on the GPU — mlp / synthetic-regression
+inner training (torch fp64 GEMMs + the fused dlx_adamw_step), compressed one-step-delayed
+outer sync (OuterSync) — against the reference's own reference_overlapped_run
+(test_support.hpp:114-218) compiled from /root/reference (oracle/_ref), same data, same model
+init, same seeds. The inner trajectories agree to fp32 rounding per step, so the final
+anchor and the per-round losses are compared within tolerance."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("act,qbits,rounding,adaptive", [("tanh", 4, 0, True),
+                                                          ("relu", 8, 1, False)])
+def test_overlapped_training_run_matches_reference(ctx, act, qbits, rounding, adaptive):
+    import torch
+    from oracle.oracle import available, ref_mlp_overlapped_run
+    from paper_2506_21263_b200 import api
+    from paper_2506_21263_b200.engine import OuterConfig
+    from paper_2506_21263_b200.training import MLP, Replica, mlp_table, shard, train_overlapped
+    if not available("reference"):
+        pytest.skip("reference library (oracle/_ref) not built")
+    widths, seed, H1, steps, batch, rank1 = [16, 64, 64, 8], 5, 5, 40, 8, 8
+    ref = ref_mlp_overlapped_run(widths, act, 2000, 32, seed, 1, H1, steps, batch, rank1, qbits,
+                                 rounding, 2, adaptive)
+    L = api.Layout(ctx, mlp_table(widths))
+    mlp = MLP(L, widths, act)
+    xs, ys = shard(ref["train_x"], ref["train_y"], 1, 0)
+    dev = f"cuda:{ctx.device}"
+    rep = Replica(mlp, torch.from_numpy(np.ascontiguousarray(xs)).to(dev),
+                  torch.from_numpy(np.ascontiguousarray(ys)).to(dev), seed, 0)
+    cfg = OuterConfig(rank1=rank1, qbits=qbits, rounding=rounding, power_iters=2, H1=H1,
+                      adaptive=adaptive, seed=seed)
+    a0 = L.pack(ref["anchor0"])
+    anchor, losses, recs = train_overlapped(L, mlp, a0.clone(), rep, cfg, steps, batch)
+    got = L.unpack(anchor)
+    assert len(losses) == len(ref["losses"])
+    np.testing.assert_allclose(losses, ref["losses"], rtol=2e-3)
+    moved_ref = ref["anchor"] - ref["anchor0"]
+    rel = np.linalg.norm(got - ref["anchor"]) / np.linalg.norm(moved_ref)
+    assert rel <= 1e-2, rel
+    assert all(np.isfinite(r.comp_error) for r in recs if r.averaged)
