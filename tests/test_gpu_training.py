@@ -44,3 +44,67 @@ def test_overlapped_training_run_matches_reference(ctx, act, qbits, rounding, ad
     print(f"anchor rel diff {rel:.2e}, losses {losses}")
     assert rel <= tol, rel
     assert all(np.isfinite(r.comp_error) for r in recs if r.averaged)
+
+
+WORKER = r'''
+import json, os, sys
+sys.path.insert(0, os.environ["DLX_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+from oracle.oracle import ref_mlp_overlapped_run
+from paper_2506_21263_b200 import api
+from paper_2506_21263_b200.engine import OuterConfig
+from paper_2506_21263_b200.training import MLP, Replica, mlp_table, shard, train_overlapped
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("nccl", device_id=torch.device(f"cuda:{rank}"))
+widths, seed, H1, steps, batch = [16, 64, 64, 8], 9, 4, 24, 8
+ref = ref_mlp_overlapped_run(widths, "tanh", 2000, 32, seed, world, H1, steps, batch, 8, 8, 0,
+                             2, True)
+ctx = api.Context(rank)
+L = api.Layout(ctx, mlp_table(widths))
+mlp = MLP(L, widths, "tanh")
+xs, ys = shard(ref["train_x"], ref["train_y"], world, rank)
+dev = f"cuda:{rank}"
+rep = Replica(mlp, torch.from_numpy(np.ascontiguousarray(xs)).to(dev),
+              torch.from_numpy(np.ascontiguousarray(ys)).to(dev), seed, rank)
+cfg = OuterConfig(rank1=8, qbits=8, rounding=0, power_iters=2, H1=H1, adaptive=True, seed=seed)
+anchor, losses, recs = train_overlapped(L, mlp, L.pack(ref["anchor0"]), rep, cfg, steps, batch,
+                                        world=world, rank=rank)
+out = {"anchor": L.unpack(anchor).tolist(), "losses": losses,
+       "ref_anchor": ref["anchor"].tolist(), "ref_anchor0": ref["anchor0"].tolist(),
+       "ref_losses": ref["losses"].tolist()}
+json.dump(out, open(os.path.join(os.environ["DLX_OUT"], f"rank{rank}.json"), "w"))
+dist.barrier()
+dist.destroy_process_group()
+'''
+
+
+def test_two_rank_training_run_matches_reference(tmp_path):
+    """D = 2 workers, one per GPU (NCCL): both ranks end with bitwise-identical anchors, the
+    mean of their per-round losses tracks the reference's D = 2 run, and the anchor matches."""
+    import json
+    import os
+    import subprocess
+    import sys
+    import torch
+    from oracle.oracle import available
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    if not available("reference"):
+        pytest.skip("reference library (oracle/_ref) not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "worker.py"
+    script.write_text(WORKER)
+    env = dict(os.environ, DLX_ROOT=root, DLX_OUT=str(tmp_path))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29537", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = [json.load(open(tmp_path / f"rank{k}.json")) for k in range(2)]
+    a0, a1 = np.array(res[0]["anchor"], np.float32), np.array(res[1]["anchor"], np.float32)
+    assert np.array_equal(a0, a1), "anchors differ across ranks"
+    mean_losses = (np.array(res[0]["losses"]) + np.array(res[1]["losses"])) / 2
+    np.testing.assert_allclose(mean_losses, res[0]["ref_losses"], rtol=2e-3)
+    ra, ra0 = np.array(res[0]["ref_anchor"], np.float32), np.array(res[0]["ref_anchor0"], np.float32)
+    rel = np.linalg.norm(a0 - ra) / np.linalg.norm(ra - ra0)
+    assert rel <= 1e-2, rel
