@@ -10,6 +10,8 @@
 // MGS2 kernel with the reference's seeded column replacement (RngStream(0x5eedc01,
 // stream_key({n, r, j, attempt}))). That path only triggers on (near) rank-deficient
 // inputs such as all-zero tensors.
+#include <cstdlib>
+
 #include "dlx_internal.cuh"
 #include "ptx.cuh"
 
@@ -36,7 +38,11 @@ static void make_job(const Plan& P, GramJob* J, const std::vector<DevMat>& mats)
   for (size_t e = 0; e < mats.size(); ++e) {
     const DevMat& m = mats[e];
     J->rmax = std::max(J->rmax, m.r);
-    const int64_t ns = std::max<int64_t>(1, ceil_div(m.n, 512));
+    static const int64_t split_rows = [] {  // experiments: DLX_GRAM_SPLIT
+      const char* e = getenv("DLX_GRAM_SPLIT");
+      return static_cast<int64_t>(e ? atoi(e) : 512);
+    }();
+    const int64_t ns = std::max<int64_t>(1, ceil_div(m.n, split_rows));
     const int64_t rows = round_up(ceil_div(m.n, ns), 32);
     J->part0.push_back(J->total_parts);
     int cnt = 0;

@@ -20,14 +20,14 @@ for D in [int(x) for x in os.environ.get("DS", "1,2,4,8").split(",")]:
     g = pay.repeat(D)
     for _ in range(2):
         api.outer_update(L, g, D, r, q, delta, anchor, local, vel, 0.7, 0.9, False,
-                         mode=api.OVERLAPPED, self_index=0, stats=stats)
+                         mode=api.OVERLAPPED, self_index=int(os.environ.get('SELF', '0')), stats=stats)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     n = 3
     for _ in range(n):
         api.outer_update(L, g, D, r, q, delta, anchor, local, vel, 0.7, 0.9, False,
-                         mode=api.OVERLAPPED, self_index=0, stats=stats)
+                         mode=api.OVERLAPPED, self_index=int(os.environ.get('SELF', '0')), stats=stats)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
     print(f"r={r} D={D} K={D*r}: outer_update {ms:.3f} ms  {28 * L.total_params / ms / 1e6:.0f} GB/s", flush=True)
