@@ -847,7 +847,12 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
     const char* e = getenv("DLX_O5_CHUNK");
     return e ? atoi(e) : 0;
   }();
-  const int64_t chunk = chunk_env ? chunk_env : (S.bf || S.nab == 2) ? 128 : 256;  // single smem A band: amortise reloads
+  // 128-column chunks (DRAM row locality across concurrently active CTAs); K = 256 (four
+  // A boxes per band): 192, the A band's TMEM refill amortised over 12 tiles (7.37 -> 7.05
+  // ms at D = 8; 256 measured 7.47); single smem A band (tf32): 256
+  const int64_t chunk = chunk_env ? chunk_env
+                        : S.bf ? (nkc >= 4 ? 192 : 128)
+                               : (S.nab == 2 ? 128 : 256);
   for (size_t k = 0; k < P.t2.size(); ++k) {
     const DevT2& t = P.t2[k];
     const bool in = static_cast<int>(k) >= R.s0 && static_cast<int>(k) < R.s1;
