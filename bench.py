@@ -67,16 +67,21 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
-        self.device = device
+    def __init__(self, devices):
+        # every rank samples its own GPU by index (-i <uuid> queries measured 100+ ms host
+        # stalls of the CUDA process on that GPU)
+        self.devices = devices
         self.proc = None
         self.lines = []  # (monotonic time, csv line)
         self.window = (0.0, float("inf"))
 
     def __enter__(self):
+        if not self.devices:
+            return self
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", ",".join(str(d) for d in self.devices),
+                 f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -240,8 +245,11 @@ def main():
     api.set_option("kernel_events", 1)  # per-launch CUDA events on the launching stream
     for k in KERNELS:
         api.kernel_time(k)
+    import gc
+    gc.collect()
+    gc.disable()  # a collector pause on one rank's host stalls every rank at the all-gather
     barrier()
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler([str(local_rank)]) as clocks:
         clocks.wait_first()
         clocks.start()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -252,6 +260,7 @@ def main():
         t1.record(stream)
         barrier()
         clocks.stop()
+    gc.enable()
     launches = api.take_launch_count()
     ktimes = {k: api.kernel_time(k) for k in KERNELS}
     api.set_option("kernel_events", 0)
@@ -266,11 +275,23 @@ def main():
     # per-phase device time (main stream) + effective rank (side stream)
     phases = {}
     ev = eng.phase_events
-    for (n0, e0), (_, e1) in zip(ev, ev[1:]):
+    exch = []  # per-round exchange time (all-gather incl. waiting for the other ranks)
+    gaps = []  # device idle between one round's end and the next round's compress
+    for (n0, e0), (n1, e1) in zip(ev, ev[1:]):
         if n0 == "end":
+            if n1 == "compress":
+                gaps.append(e0.elapsed_time(e1))
             continue
-        phases[n0] = phases.get(n0, 0.0) + e0.elapsed_time(e1)
+        t = e0.elapsed_time(e1)
+        phases[n0] = phases.get(n0, 0.0) + t
+        if n0 == "exchange":
+            exch.append(t)
     phases = {k: v / args.steps for k, v in phases.items()}
+    if exch:
+        phases["exchange_max"] = max(exch)
+    if gaps:
+        phases["inter_round_gap"] = sum(gaps) / args.steps
+        phases["inter_round_gap_max"] = max(gaps)
     if eng.side_events:
         phases["effective_rank (" + ("side stream" if eng.side is not None else "inside outer_update") + ")"] = \
             sum(a.elapsed_time(b) for a, b in eng.side_events) / args.steps

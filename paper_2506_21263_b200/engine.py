@@ -15,6 +15,7 @@ the effective-rank measurement run on a side stream.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -156,15 +157,25 @@ class OuterSync:
         # high priority: the measurement's few CTAs are dispatched ahead of the outer update's
         # persistent grid, so the host learns r' (next round's rank) early in the round
         self.side = torch.cuda.Stream(device=dev, priority=-1) if side_stream else None
+        if os.environ.get("DLX_ER_SHARD") == "0":  # experiments
+            shard_effective_rank = False
         self.er_shards = world if (shard_effective_rank and world > 1) else 1
-        # the shards' per-tensor results are summed on the host over a CPU (gloo) group: the
-        # host waits for r' anyway, and an NCCL kernel would queue behind the outer update's
-        # persistent grid for SMs
-        self._cpu_group = None
+        # the shards' per-tensor results are summed over a dedicated NCCL group whose stream
+        # has high priority: its kernel takes the SMs the measurement frees ahead of the outer
+        # update's pending CTAs (on the default-priority stream it would wait for the whole
+        # outer update; a CPU gloo all-reduce measured occasional 20 ms stalls)
+        self._er_group = None
+        self._er_gloo = os.environ.get("DLX_ER_GLOO") == "1"  # experiments
         if self.er_shards > 1:
             import torch.distributed as dist
-            self._cpu_group = dist.new_group(backend="gloo")
+            if self._er_gloo:
+                self._er_group = dist.new_group(backend="gloo")
+            else:
+                opts = dist.ProcessGroupNCCL.Options()
+                opts.is_high_priority_stream = True
+                self._er_group = dist.new_group(backend="nccl", pg_options=opts)
         self._bcast_work = None  # in-flight warm-start broadcast (waited before next compress)
+        self.bcast_sync = os.environ.get("DLX_BCAST_SYNC", "0") == "1"
         # per-round host copies of the device stats, double-buffered (records resolve lazily)
         self.stats_host = torch.zeros((2, 8), dtype=torch.float64, pin_memory=True)
         n2 = sum(1 for s in layout.shapes if len(s) == 2)
@@ -218,6 +229,9 @@ class OuterSync:
         start) asynchronously — only the next round's compress needs it. NCCL over NVLink."""
         if self.world == 1:
             return self.payload[:pb]
+        if self.bcast_sync:
+            return exchange(self.payload[:pb], self.gathered, self.warm_q[:qel] if qel else None,
+                            self.world, self.group)
         g = exchange(self.payload[:pb], self.gathered, None, self.world, self.group)
         if qel > 0:
             import torch.distributed as dist
@@ -293,6 +307,10 @@ class OuterSync:
                                           nshards=self.er_shards, per=self.er_per,
                                           energy=self.er_dev[nb:])
                 self.er_dev[:nb].copy_(self.er_per)
+                if self.er_shards > 1 and not self._er_gloo:
+                    # one nonzero term per entry: the sum is exact and identical on every rank
+                    import torch.distributed as dist
+                    dist.all_reduce(self.er_dev, group=self._er_group)
                 if self.phase_events is not None:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(side)
@@ -307,10 +325,9 @@ class OuterSync:
                           payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
         if cfg.adaptive and self._n2:
             ev.synchronize()
-            if self.er_shards > 1:
-                # one nonzero term per entry: the sum is exact and identical on every rank
+            if self.er_shards > 1 and self._er_gloo:
                 import torch.distributed as dist
-                dist.all_reduce(self.er_host, group=self._cpu_group)
+                dist.all_reduce(self.er_host, group=self._er_group)
             h = self.er_host.numpy()
             nb = max(self._n2, 1)
             er = api.effective_rank_reduce(L, h[:self._n2].astype(np.int32),
