@@ -60,6 +60,75 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- clocks
+class NvmlClockSampler:
+    """SM clocks / throttle reasons sampled in-process through NVML (the fields of the
+    profiling recipe's nvidia-smi clocks line) every 50 ms during the timed region, on rank 0
+    only. Any clock query of a GPU measured a one-off stall of the rank driving it (NVML:
+    ~15-25 ms per run; an nvidia-smi subprocess: 20-100 ms, on whichever rank it sampled);
+    with every rank sampling, the slowest stall sets everyone's round at the next all-gather.
+    DLX_CLOCKS=off disables sampling (the line then carries no clocks)."""
+
+    BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+            "sw_power_cap": 0x4}
+
+    def __init__(self, index: int | None):
+        self.index = index
+        self.samples = []  # (monotonic time, sm MHz, max MHz, reason bits)
+        self.window = (0.0, float("inf"))
+        self._stop = threading.Event()
+        self.t = None
+
+    def __enter__(self):
+        if self.index is None:
+            return self
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        except Exception:
+            return self
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                rb = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+                self.samples.append((time.monotonic(), sm, rb))
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def wait_first(self, timeout=5.0):
+        t = time.monotonic() + timeout
+        while self.t is not None and not self.samples and time.monotonic() < t:
+            time.sleep(0.01)
+
+    def start(self):
+        self.window = (time.monotonic(), float("inf"))
+
+    def stop(self):
+        self.window = (self.window[0], time.monotonic())
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.t is not None:
+            self.t.join(timeout=1.0)
+
+    def summary(self):
+        inside = [x for x in self.samples if self.window[0] <= x[0] <= self.window[1]]
+        reasons = sorted(n for n, b in self.BITS.items() if any(x[2] & b for x in inside))
+        sm = [x[1] for x in inside]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": getattr(self, "mx", None), "reasons": reasons,
+                "samples": len(sm), "source": "nvml"}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -249,7 +318,13 @@ def main():
     gc.collect()
     gc.disable()  # a collector pause on one rank's host stalls every rank at the all-gather
     barrier()
-    with ClockSampler([str(local_rank)]) as clocks:
+    smi = os.environ.get("DLX_CLOCKS", "nvml0")  # nvml0 | nvml | smi | smi0 | off
+    if smi.startswith("nvml"):
+        sampler = NvmlClockSampler(local_rank if (smi == "nvml" or local_rank == 0) else None)
+    else:
+        sampler = ClockSampler([str(local_rank)] if smi == "smi" or
+                               (smi == "smi0" and local_rank == 0) else None)
+    with sampler as clocks:
         clocks.wait_first()
         clocks.start()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -261,6 +336,7 @@ def main():
         barrier()
         clocks.stop()
     gc.enable()
+    eng.flush()  # held rank: the rounds' r' / controller suggestions were read back lazily
     launches = api.take_launch_count()
     ktimes = {k: api.kernel_time(k) for k in KERNELS}
     api.set_option("kernel_events", 0)

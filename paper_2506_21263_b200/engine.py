@@ -87,14 +87,28 @@ class RoundRecord:
     round: int = 0
     r_t: int = 0
     H_t: int = 0
-    r_prime: int = 0
     payload_bytes: float = 0.0
     omega_sq: float = 0.0
     averaged: bool = False
-    r_next: int = 0
-    H_next: int = 0
     _stats: dict = field(default_factory=dict, repr=False)
     _pending: object = field(default=None, repr=False)  # (event, host stats view, mode)
+    # r', r_next, H_next: with the rank held (OuterConfig.hold_rank) the effective rank is
+    # merged after the outer update and read back lazily; reading one of them drains it
+    _ctl: dict = field(default_factory=lambda: {"r_prime": 0, "r_next": 0, "H_next": 0},
+                       repr=False)
+    _drain: object = field(default=None, repr=False)
+
+    def _ctl_get(self, name):
+        if self._drain is not None:
+            self._drain()
+        return self._ctl[name]
+
+    r_prime = property(lambda self: self._ctl_get("r_prime"),
+                       lambda self, v: self._ctl.__setitem__("r_prime", v))
+    r_next = property(lambda self: self._ctl_get("r_next"),
+                      lambda self, v: self._ctl.__setitem__("r_next", v))
+    H_next = property(lambda self: self._ctl_get("H_next"),
+                      lambda self, v: self._ctl.__setitem__("H_next", v))
 
     def resolve(self) -> "RoundRecord":
         if self._pending is not None:
@@ -125,6 +139,12 @@ class RoundRecord:
 
 
 class OuterSync:
+    ER_SLOTS = 8  # effective-rank results in flight (rank held: read back lazily)
+    # per-round statistics in flight: the host may run this many rounds minus two ahead of
+    # the device, so a host stall (a clock query, a scheduler hiccup) is absorbed by queued
+    # rounds instead of idling the GPU and, at N > 1, every other rank at the next all-gather
+    STATS_SLOTS = 8
+
     def __init__(self, layout: api.Layout, cfg: OuterConfig, anchor: torch.Tensor,
                  world: int = 1, rank: int = 0, group=None, side_stream: bool | None = None,
                  shard_effective_rank: bool = True):
@@ -160,30 +180,24 @@ class OuterSync:
         if os.environ.get("DLX_ER_SHARD") == "0":  # experiments
             shard_effective_rank = False
         self.er_shards = world if (shard_effective_rank and world > 1) else 1
-        # the shards' per-tensor results are summed over a dedicated NCCL group whose stream
-        # has high priority: its kernel takes the SMs the measurement frees ahead of the outer
-        # update's pending CTAs (on the default-priority stream it would wait for the whole
-        # outer update; a CPU gloo all-reduce measured occasional 20 ms stalls)
-        self._er_group = None
-        self._er_gloo = os.environ.get("DLX_ER_GLOO") == "1"  # experiments
-        if self.er_shards > 1:
-            import torch.distributed as dist
-            if self._er_gloo:
-                self._er_group = dist.new_group(backend="gloo")
-            else:
-                opts = dist.ProcessGroupNCCL.Options()
-                opts.is_high_priority_stream = True
-                self._er_group = dist.new_group(backend="nccl", pg_options=opts)
         self._bcast_work = None  # in-flight warm-start broadcast (waited before next compress)
-        self.bcast_sync = os.environ.get("DLX_BCAST_SYNC", "0") == "1"
+        # warm-start broadcast right after the all-gather, before the outer update: 57 MB at
+        # OPT-1.3B r=32 (~0.1 ms over NVLink); issued asynchronously it ran beside the outer
+        # update's persistent grid and was the other source of multi-ms rank stalls
+        self.bcast_sync = os.environ.get("DLX_BCAST_SYNC", "1") == "1"
         # per-round host copies of the device stats, double-buffered (records resolve lazily)
-        self.stats_host = torch.zeros((2, 8), dtype=torch.float64, pin_memory=True)
+        self.stats_host = torch.zeros((self.STATS_SLOTS, 8), dtype=torch.float64,
+                                      pin_memory=True)
+        self._unresolved: list = []  # records whose device statistics are not read yet
         n2 = sum(1 for s in layout.shapes if len(s) == 2)
         self._n2 = n2
         # per-tensor effective ranks (as doubles) | energies: device results and host copy
         self.er_dev = torch.zeros(2 * max(n2, 1), dtype=torch.float64, device=dev)
         self.er_per = torch.zeros(max(n2, 1), dtype=torch.int32, device=dev)
-        self.er_host = torch.zeros(2 * max(n2, 1), dtype=torch.float64, pin_memory=True)
+        self.er_host = torch.zeros((self.ER_SLOTS, 2 * max(n2, 1)), dtype=torch.float64,
+                                   pin_memory=True)
+        self._er_fifo: list = []  # (record, event, host slot) awaiting their r'
+        self._er_slot = 0
         self.last = RoundRecord()
         self.phase_events = None  # optional: list collecting (name, event) on the main stream
         self.side_events: list = []  # (start, end) of the effective rank on the side stream
@@ -269,7 +283,7 @@ class OuterSync:
                              mode=mode, self_index=self.rank if cfg.measure_error else -1,
                              stats=self.stats, stream=cur)
         self._ev("end")
-        self.stats_host[self.round % 2].copy_(self.stats, non_blocking=True)
+        self.stats_host[self.round % self.STATS_SLOTS].copy_(self.stats, non_blocking=True)
         return RoundRecord(round=self.round, r_t=0, H_t=self.H_t, averaged=True,
                            payload_bytes=api.payload_bits_raw(L) / 8.0, omega_sq=0.0)
 
@@ -307,35 +321,59 @@ class OuterSync:
                                           nshards=self.er_shards, per=self.er_per,
                                           energy=self.er_dev[nb:])
                 self.er_dev[:nb].copy_(self.er_per)
-                if self.er_shards > 1 and not self._er_gloo:
-                    # one nonzero term per entry: the sum is exact and identical on every rank
-                    import torch.distributed as dist
-                    dist.all_reduce(self.er_dev, group=self._er_group)
                 if self.phase_events is not None:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(side)
                     self.side_events.append((e0, e1))
-                self.er_host.copy_(self.er_dev, non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(side)
         self._outer_update(gathered, r, q, local, mode, cur)
         self._ev("end")
-        self.stats_host[self.round % 2].copy_(self.stats, non_blocking=True)
+        self.stats_host[self.round % self.STATS_SLOTS].copy_(self.stats, non_blocking=True)
         rec = RoundRecord(round=self.round, r_t=r, H_t=self.H_t, averaged=True,
                           payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
         if cfg.adaptive and self._n2:
-            ev.synchronize()
-            if self.er_shards > 1 and self._er_gloo:
-                import torch.distributed as dist
-                dist.all_reduce(self.er_host, group=self._er_group)
-            h = self.er_host.numpy()
-            nb = max(self._n2, 1)
-            er = api.effective_rank_reduce(L, h[:self._n2].astype(np.int32),
-                                           h[nb:nb + self._n2], cfg.rank1)
-            rec.r_prime = er.aggregate
+            # the shards' per-tensor (k, energy) are summed AFTER the outer update, on the main
+            # stream: no collective runs beside its persistent grid (an NCCL all-reduce there,
+            # or a per-round CPU/gloo one, measured 20-260 ms rank stalls)
             cur.wait_stream(self.side or cur)
+            if self.er_shards > 1:
+                import torch.distributed as dist
+                # one nonzero term per entry: the sum is exact and identical on every rank
+                dist.all_reduce(self.er_dev, group=self.group)
+            if len(self._er_fifo) >= self.ER_SLOTS:
+                self._drain_er(block=True, upto=1)
+            slot = self._er_slot
+            self._er_slot = (slot + 1) % self.ER_SLOTS
+            self.er_host[slot].copy_(self.er_dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self._er_fifo.append((rec, ev, slot))
+            rec._drain = lambda: self._drain_er(block=True)
         self.warm_rank = r
         return rec
+
+    def _drain_er(self, block: bool, upto: int | None = None):
+        """Resolve pending effective ranks in round order: r' into the window, then the
+        controller's (r_next, H_next) for that round (engine.cpp:278-308)."""
+        n = 0
+        while self._er_fifo and (upto is None or n < upto):
+            rec, ev, slot = self._er_fifo[0]
+            if not block and not ev.query():
+                break
+            ev.synchronize()
+            self._er_fifo.pop(0)
+            h = self.er_host[slot].numpy()
+            nb = max(self._n2, 1)
+            er = api.effective_rank_reduce(self.L, h[:self._n2].astype(np.int32),
+                                           h[nb:nb + self._n2], self.cfg.rank1)
+            rec._drain = None
+            rec.r_prime = er.aggregate
+            self._push_window(er.aggregate)
+            rec.r_next, rec.H_next = self._adapt()
+            n += 1
+
+    def flush(self):
+        """Wait for every pending effective rank (RoundRecord r' / r_next / H_next)."""
+        self._drain_er(block=True)
 
     def _outer_update(self, gathered, r: int, q: int, local, mode: int, cur):
         cfg, L = self.cfg, self.L
@@ -371,14 +409,14 @@ class OuterSync:
 
     def _finish(self, rec: RoundRecord, mode: int) -> RoundRecord:
         # no host wait on the main stream: the record resolves its device statistics when
-        # read. The previous round's record is resolved first (its stats buffer is reused
-        # two rounds later, and a non-finite update surfaces no later than the next round).
-        prev = self.last
-        if prev is not None and prev._pending is not None and prev.round == rec.round - 1:
-            prev.resolve()
+        # read. Records older than STATS_SLOTS - 2 rounds are resolved here (their host stats
+        # slot is about to be reused; a non-finite update surfaces within that many rounds).
+        while self._unresolved and self._unresolved[0].round <= rec.round - (self.STATS_SLOTS - 2):
+            self._unresolved.pop(0).resolve()
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream())
-        rec._pending = (ev, self.stats_host[rec.round % 2].numpy(), mode)
+        rec._pending = (ev, self.stats_host[rec.round % self.STATS_SLOTS].numpy(), mode)
+        self._unresolved.append(rec)
         self.last = rec
         return rec
 
@@ -407,8 +445,8 @@ class OuterSync:
         self.round += 1
         if self.has_pending:
             rec = self.collective_average(local, OVERLAPPED)
-            if self.cfg.adaptive and self.cfg.compress:
-                self._push_window(rec.r_prime)
+            # rank held: r' is not needed before the next round (read lazily); else wait
+            self._drain_er(block=not self.cfg.hold_rank)
         else:
             rec = RoundRecord(round=self.round, r_t=self.r_t, H_t=self.H_t)
             self._wait_pre_update()
@@ -430,7 +468,7 @@ class OuterSync:
         rec = self.collective_average(None, SYNC)
         r_next, h_next = self.r_t, self.H_t
         if self.cfg.adaptive and self.cfg.compress:
-            self._push_window(rec.r_prime)
+            self._drain_er(block=not self.cfg.hold_rank)
             r_next, h_next = self._adapt()
         rec = self._finish(rec, SYNC)
         self._apply_next(rec, r_next, h_next)
