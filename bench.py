@@ -301,6 +301,17 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # clock sampling starts before the warm-up rounds (the summary keeps only the samples
+    # inside the timed region): the first queries under load are where the sampled rank
+    # stalls
+    smi = os.environ.get("DLX_CLOCKS", "nvml0")  # nvml0 | nvml | smi | smi0 | off
+    if smi.startswith("nvml"):
+        sampler = NvmlClockSampler(local_rank if (smi == "nvml" or local_rank == 0) else None)
+    else:
+        sampler = ClockSampler([str(local_rank)] if smi == "smi" or
+                               (smi == "smi0" and local_rank == 0) else None)
+    sampler.__enter__()
+    sampler.wait_first()
     # round 1 stages delta (no exchange, engine.cpp:473); then W warm-up rounds
     eng.step(local)
     for _ in range(args.warmup):
@@ -318,23 +329,17 @@ def main():
     gc.collect()
     gc.disable()  # a collector pause on one rank's host stalls every rank at the all-gather
     barrier()
-    smi = os.environ.get("DLX_CLOCKS", "nvml0")  # nvml0 | nvml | smi | smi0 | off
-    if smi.startswith("nvml"):
-        sampler = NvmlClockSampler(local_rank if (smi == "nvml" or local_rank == 0) else None)
-    else:
-        sampler = ClockSampler([str(local_rank)] if smi == "smi" or
-                               (smi == "smi0" and local_rank == 0) else None)
-    with sampler as clocks:
-        clocks.wait_first()
-        clocks.start()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(args.steps):
-            recs.append(eng.step(local))
-        t1.record(stream)
-        barrier()
-        clocks.stop()
+    clocks = sampler
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        recs.append(eng.step(local))
+    t1.record(stream)
+    barrier()
+    clocks.stop()
+    sampler.__exit__(None, None, None)
     gc.enable()
     eng.flush()  # held rank: the rounds' r' / controller suggestions were read back lazily
     launches = api.take_launch_count()
