@@ -46,9 +46,10 @@ def parse():
     ap.add_argument("--rank", type=int, default=32)
     ap.add_argument("--qbits", type=int, default=4)
     ap.add_argument("--no-adaptive", action="store_true")
-    ap.add_argument("--follow-controller", action="store_true",
-                    help="apply the adaptive controller's rank (default: measure r' and run the "
-                         "controller every round but time at rank1 = 32, the configured rank)")
+    ap.add_argument("--hold-rank", action="store_true",
+                    help="measure r' and run the controller every round but keep operating at "
+                         "rank1 (default: the controller's rank is applied from the next round "
+                         "on, engine.cpp:476-487, 506-507 — configs[1]'s adaptive schedule)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compress", action="store_true",
@@ -292,7 +293,7 @@ def main():
                       adaptive=not (args.no_adaptive or args.no_compress),
                       compress=not args.no_compress,
                       H1=125, window_c=5, tau=0.5, power_iters=2, seed=1, overlap=True,
-                      hold_rank=not args.follow_controller)
+                      hold_rank=args.hold_rank)
     eng = OuterSync(L, cfg, anchor, world=world, rank=rank, side_stream=None if args.side_stream is None else bool(args.side_stream))
     stream = torch.cuda.current_stream()
 
@@ -373,8 +374,8 @@ def main():
     if gaps:
         phases["inter_round_gap"] = sum(gaps) / args.steps
         phases["inter_round_gap_max"] = max(gaps)
-    if eng.side_events:
-        phases["effective_rank (" + ("side stream" if eng.side is not None else "inside outer_update") + ")"] = \
+    if eng.side_events and eng.side is not None:
+        phases["effective_rank (side stream, sharded)"] = \
             sum(a.elapsed_time(b) for a, b in eng.side_events) / args.steps
     eng.phase_events = None
     phases_per_rank = None
@@ -472,9 +473,11 @@ def main():
                        "qbits": args.qbits, "rounding": "stochastic", "power_iters": iters,
                        "adaptive": cfg.adaptive, "tau": cfg.tau, "window_c": cfg.window_c,
                        "r_t_timed": rts, "r_prime_timed": [r.r_prime for r in recs],
-                       "controller": ("applied" if args.follow_controller else
-                                      "evaluated every round, rank held at rank1 (r_next "
-                                      f"suggested: {[r.r_next for r in recs]})"),
+                       "controller": ("evaluated every round, rank held at rank1 (r_next "
+                                      f"suggested: {[r.r_next for r in recs]})" if args.hold_rank
+                                      else "applied (r_t of round t+1 = adapt_compression of "
+                                           "the r' window, engine.cpp:476-487)"),
+                       "r_t_per_round": [r.r_t for r in recs],
                        "mode": "overlapped (one-step delay)", "parallelism": f"dp{world}",
                        "payload_bytes": recs[-1].payload_bytes if recs else None,
                        "l2": "inputs (>=5 GB slabs) larger than L2; no flush",

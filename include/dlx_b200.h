@@ -65,6 +65,47 @@ const char* dlx_last_error(void); /* thread-local message of the last failing ca
 dlx_status dlx_ctx_create(int device, dlx_ctx** out);
 dlx_status dlx_ctx_destroy(dlx_ctx* ctx);
 
+/* ---- worker sync (one process per GPU = one DiLoCoX worker) ---------------------------
+ * Replaces the reference's in-process collective: allreduce_avg (collective.hpp:23,
+ * collective.cpp:17-46) is a mean of per-worker reconstructions, so the exchange of a round
+ * is an all-gather of every worker's compressed payload (worker order = rank order) plus the
+ * broadcast of worker 0's float Q factors as everyone's next warm start (collective_average,
+ * engine.cpp:215-263, 241, 498-501). NCCL over NVLink / NVSwitch, resolved at run time
+ * (libnccl.so.2; DLX_ERR_NCCL if absent). The collectives run on a library-owned
+ * high-priority side stream, joined to the caller's stream by events.
+ *
+ * Bootstrap: rank 0 calls dlx_comm_unique_id and ships the 128 bytes to the other ranks by
+ * any means (file, TCP, MPI, torch.distributed); every rank then calls dlx_comm_init (a
+ * collective: blocks until all ranks have joined). dlx_ctx_create_dist does both steps'
+ * second half in one call. */
+#define DLX_UNIQUE_ID_BYTES 128
+enum { DLX_EXCHANGE_BCAST_DEFERRED = 1 }; /* dlx_exchange flags */
+dlx_status dlx_comm_unique_id(void* out /* DLX_UNIQUE_ID_BYTES */);
+dlx_status dlx_comm_init(dlx_ctx* ctx, int rank, int world, const void* unique_id);
+dlx_status dlx_ctx_create_dist(int device, int rank, int world, const void* unique_id,
+                               dlx_ctx** out);
+dlx_status dlx_comm_info(const dlx_ctx* ctx, int* rank, int* world);
+/* All-gather d_payload (payload_bytes, this worker's) into d_gathered (world * payload_bytes,
+ * worker w at offset w * payload_bytes) and broadcast worker 0's d_warm_q (warm_elems floats,
+ * in place) to every worker. `stream` is ordered after the all-gather; after the broadcast
+ * too unless flags has DLX_EXCHANGE_BCAST_DEFERRED, in which case dlx_exchange_wait_warm
+ * joins it later (it is only needed by the next round's compress). world == 1: copies the
+ * payload into d_gathered (if distinct) and returns. */
+dlx_status dlx_exchange(dlx_ctx* ctx, const uint8_t* d_payload, int64_t payload_bytes,
+                        uint8_t* d_gathered, float* d_warm_q, int64_t warm_elems, int flags,
+                        void* stream);
+dlx_status dlx_exchange_wait_warm(dlx_ctx* ctx, void* stream);
+/* Generic pieces of the same communicator: byte all-gather (the no-compress ablation's raw
+ * slabs, compress_raw compress.cpp:185-199) and an fp64 sum (the per-tensor effective-rank
+ * shards: one nonzero term per entry, so the sum is exact on every rank). */
+dlx_status dlx_comm_allgather(dlx_ctx* ctx, const void* d_send, int64_t bytes, void* d_recv,
+                              void* stream);
+dlx_status dlx_comm_allreduce_sum_f64(dlx_ctx* ctx, double* d_buf, int64_t n, void* stream);
+/* Poll the communicator for an asynchronous NCCL failure (ncclCommGetAsyncError): DLX_OK or
+ * DLX_ERR_NCCL. Cheap; the engine polls once per round. */
+dlx_status dlx_comm_check(dlx_ctx* ctx);
+dlx_status dlx_comm_destroy(dlx_ctx* ctx);
+
 /* ---- tensor table (ParamSet layout) ---------------------------------------------------
  * ndim[i] in {1,2}; dims[2i], dims[2i+1] = (rows, cols) or (n, 1). Mirrors
  * ParamSet::add / same_layout (params.hpp:12-33). */
@@ -178,6 +219,24 @@ dlx_status dlx_outer_update_raw(dlx_ctx* ctx, const dlx_layout* layout, int D,
 dlx_status dlx_stage_deltas(dlx_ctx* ctx, const dlx_layout* layout, const float* d_anchor,
                             const float* d_local, const float* d_err, float* d_pending,
                             double* d_norm_sq, void* stream);
+
+/* measure_error (compress.cpp:246-262) of one payload against the dense delta it compressed:
+ * d_out[0] = sum (decompress(payload) - delta)^2, d_out[1] = sum delta^2 (device doubles;
+ * comp_error = d_out[0] / d_out[1], 0 when d_out[1] == 0). */
+dlx_status dlx_measure_error(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
+                             const uint8_t* d_payload, const float* d_delta, double* d_out,
+                             void* stream);
+
+/* The same reduction for a dense reconstruction already in a slab (RawDense payloads). */
+dlx_status dlx_sqdiff_slabs(dlx_ctx* ctx, const dlx_layout* layout, const float* d_rec,
+                            const float* d_delta, double* d_out, void* stream);
+
+/* Worker-order mean of D fp32 slabs of n elements stored ld apart (d_in[w * ld + i]):
+ * out = float((sum_w double(x_w)) * (1.0 / D)) — allreduce_avg over compress_raw payloads
+ * (collective.cpp:17-46, compress.cpp:185-199) and the per-step gradient mean of the
+ * all-reduce baseline (engine.cpp:559-570). Bit-exact. */
+dlx_status dlx_mean_slabs(dlx_ctx* ctx, int64_t n, int64_t ld, int D, const float* d_in,
+                          float* d_out, void* stream);
 
 /* nesterov_outer_step (optim.cpp:56-78) on a dense averaged delta. */
 dlx_status dlx_nesterov(dlx_ctx* ctx, int64_t n, float gamma, float beta, int classical,

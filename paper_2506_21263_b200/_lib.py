@@ -95,6 +95,20 @@ PROTOS = {
     "dlx_set_option": (_i32, [C.c_char_p, _i32]),
     "dlx_kernel_time": (_i32, [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dlx_debug_sweep": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
+    "dlx_measure_error": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "dlx_sqdiff_slabs": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "dlx_mean_slabs": (_i32, [_vp, _i64, _i64, _i32, _vp, _vp, _vp]),
+    # worker sync (NCCL inside the library)
+    "dlx_comm_unique_id": (_i32, [_vp]),
+    "dlx_comm_init": (_i32, [_vp, _i32, _i32, _vp]),
+    "dlx_ctx_create_dist": (_i32, [_i32, _i32, _i32, _vp, C.POINTER(_vp)]),
+    "dlx_comm_info": (_i32, [_vp, _ip, _ip]),
+    "dlx_exchange": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _i32, _vp]),
+    "dlx_exchange_wait_warm": (_i32, [_vp, _vp]),
+    "dlx_comm_allgather": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "dlx_comm_allreduce_sum_f64": (_i32, [_vp, _vp, _i64, _vp]),
+    "dlx_comm_check": (_i32, [_vp]),
+    "dlx_comm_destroy": (_i32, [_vp]),
 }
 
 _lib = None

@@ -72,6 +72,53 @@ class Context:
             lib().dlx_ctx_destroy(self.h)
             self.h = None
 
+    # -- worker sync (dlx_comm_*; NCCL inside the library)
+    def init_comm(self, rank: int, world: int, unique_id: bytes) -> None:
+        """Join the D-worker communicator (collective: every rank calls it with rank 0's
+        unique id)."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(lib().dlx_comm_init(self.h, rank, world, buf))
+        self.rank, self.world = rank, world
+
+    def comm_check(self) -> None:
+        """Raise NcclError if the communicator reported an asynchronous failure."""
+        check(lib().dlx_comm_check(self.h))
+
+    def wait_warm(self, stream=None) -> None:
+        check(lib().dlx_exchange_wait_warm(self.h, _stream(stream)))
+
+
+def comm_unique_id() -> bytes:
+    """dlx_comm_unique_id: 128 opaque bytes rank 0 ships to every rank."""
+    buf = C.create_string_buffer(128)
+    check(lib().dlx_comm_unique_id(buf))
+    return buf.raw
+
+
+def exchange(ctx: Context, payload: torch.Tensor, gathered: torch.Tensor,
+             warm_q: torch.Tensor | None, defer_warm: bool = False, stream=None) -> torch.Tensor:
+    """dlx_exchange: all-gather of the payloads (worker order = rank order) + broadcast of
+    worker 0's warm Q, on the library's side stream joined to `stream`."""
+    pb = payload.numel()
+    nw = gathered.numel() // max(pb, 1)
+    wq = warm_q if (warm_q is not None and warm_q.numel() > 0) else None
+    check(lib().dlx_exchange(ctx.h, _ptr(payload), pb, _ptr(gathered), _ptr(wq),
+                             0 if wq is None else wq.numel(), 1 if defer_warm else 0,
+                             _stream(stream)))
+    return gathered[:nw * pb]
+
+
+def comm_allgather(ctx: Context, send: torch.Tensor, recv: torch.Tensor, stream=None):
+    check(lib().dlx_comm_allgather(ctx.h, _ptr(send), send.numel() * send.element_size(),
+                                   _ptr(recv), _stream(stream)))
+    return recv
+
+
+def comm_allreduce_sum_f64(ctx: Context, buf: torch.Tensor, stream=None):
+    assert buf.dtype == torch.float64
+    check(lib().dlx_comm_allreduce_sum_f64(ctx.h, _ptr(buf), buf.numel(), _stream(stream)))
+    return buf
+
 
 @dataclass
 class QuantSpec:
@@ -370,6 +417,26 @@ def outer_update_raw(layout: Layout, gathered: torch.Tensor, D: int, pending: to
     check(lib().dlx_outer_update_raw(layout.ctx.h, layout.h, D, _ptr(gathered), self_index, mode,
                                      _ptr(pending), _ptr(anchor), _ptr(local), _ptr(velocity),
                                      gamma, beta, int(classical), _ptr(stats), _stream(stream)))
+
+
+def measure_error(layout: Layout, payload: torch.Tensor, rank: int, qbits: int,
+                  delta: torch.Tensor, stream=None) -> float:
+    """measure_error (compress.cpp:246-262) on the device (synchronises for the result)."""
+    out = torch.zeros(2, dtype=torch.float64, device=delta.device)
+    check(lib().dlx_measure_error(layout.ctx.h, layout.h, rank, qbits, _ptr(payload), _ptr(delta),
+                                  _ptr(out), _stream(stream)))
+    num, den = out.tolist()
+    return num / den if den > 0 else 0.0
+
+
+def mean_slabs(ctx: Context, gathered: torch.Tensor, D: int, n: int, ld: int | None = None,
+               out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Worker-order fp64 mean of D slabs (dlx_mean_slabs), bit-exact with the reference."""
+    ld = n if ld is None else ld
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=gathered.device)
+    check(lib().dlx_mean_slabs(ctx.h, n, ld, D, _ptr(gathered), _ptr(out), _stream(stream)))
+    return out
 
 
 def stage_deltas(layout: Layout, anchor, local, err, pending, norm_sq=None, stream=None):

@@ -1,7 +1,13 @@
 // api.cu — C-ABI entry points (include/dlx_b200.h): validation, plans, orchestration.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <string>
 
 #include "dlx_internal.cuh"
@@ -18,6 +24,79 @@ void check_cuda(cudaError_t e, const char* what) {
 }
 
 void count_launch(int n) { g_launches += static_cast<uint64_t>(n); }
+
+namespace {
+struct ProfEntry {
+  int64_t calls = 0;
+  double total = 0.0, max = 0.0;
+};
+std::mutex g_prof_mu;
+std::map<std::string, ProfEntry>* g_prof = nullptr;
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+bool prof_on() {
+  static const bool on = [] {
+    const char* e = getenv("DLX_HOST_PROF");
+    if (!(e && e[0] == '1')) return false;
+    g_prof = new std::map<std::string, ProfEntry>();
+    atexit([] {
+      for (auto& kv : *g_prof)
+        fprintf(stderr, "[dlx host] %-28s calls %6lld total %9.2f ms max %8.3f ms\n",
+                kv.first.c_str(), static_cast<long long>(kv.second.calls), kv.second.total,
+                kv.second.max);
+    });
+    return true;
+  }();
+  return on;
+}
+}  // namespace
+
+HostProf::HostProf(const char* n) : name(n), t0(0.0), on(prof_on()) {
+  if (on) t0 = now_ms();
+}
+HostProf::~HostProf() {
+  if (!on) return;
+  const double dt = now_ms() - t0;
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  ProfEntry& e = (*g_prof)[name];
+  ++e.calls;
+  e.total += dt;
+  e.max = std::max(e.max, dt);
+}
+
+void upload_now(void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  int dev = 0;
+  DLX_CUDA(cudaGetDevice(&dev));
+  cudaStream_t s = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = streams.find(dev);
+    if (it == streams.end()) {
+      DLX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      streams[dev] = s;
+    } else {
+      s = it->second;
+    }
+  }
+  DLX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  DLX_CUDA(cudaStreamSynchronize(s));
+}
+
+void smem_optin(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  DLX_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, func, bytes})) return;
+  DLX_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({dev, func, bytes});
+}
 
 namespace {
 struct TimedLaunch {
@@ -43,26 +122,14 @@ KernelTimer::~KernelTimer() {
   if (slot >= 0) cudaEventRecord(g_timed[slot].b, stream);
 }
 
-template <class F>
-static dlx_status guard(F&& f) {
-  try {
-    f();
-    return DLX_OK;
-  } catch (const Error& e) {
-    g_last_error = e.msg;
-    return e.code;
-  } catch (const std::exception& e) {
-    g_last_error = e.what();
-    return DLX_ERR_VALIDATION;
-  }
-}
+void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 template <class T>
 static T* upload(const std::vector<T>& v) {
   if (v.empty()) return nullptr;
   T* d = nullptr;
   DLX_CUDA(cudaMalloc(&d, sizeof(T) * v.size()));
-  DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  upload_now(d, v.data(), sizeof(T) * v.size());
   return d;
 }
 
@@ -88,6 +155,7 @@ static void validate_quant(int rank, int qbits) {
 }
 
 static std::unique_ptr<Plan> build_plan(const dlx_layout& L, int rank, int qbits) {
+  HostProf hp("build_plan");
   auto P = std::make_unique<Plan>();
   P->rank = rank;
   P->qbits = qbits;
@@ -300,6 +368,7 @@ void* dlx_ctx::scratch(const std::string& name, size_t bytes, bool zero) {
 }
 
 dlx_ctx::~dlx_ctx() {
+  if (comm) dlx::destroy_comm(comm);
   for (auto& kv : arenas) cudaFree(kv.second.first);
   if (internal) cudaStreamDestroy(internal);
 }
@@ -403,6 +472,22 @@ dlx_status dlx_ctx_create(int device, dlx_ctx** out) {
     DLX_CUDA(cudaStreamCreateWithFlags(&c->internal, cudaStreamNonBlocking));
     *out = c;
   });
+}
+
+dlx_status dlx_ctx_create_dist(int device, int rank, int world, const void* unique_id,
+                               dlx_ctx** out) {
+  dlx_ctx* c = nullptr;
+  dlx_status st = dlx_ctx_create(device, &c);
+  if (st != DLX_OK) return st;
+  st = dlx_comm_init(c, rank, world, unique_id);
+  if (st != DLX_OK) {
+    const std::string msg = g_last_error;
+    dlx_ctx_destroy(c);
+    g_last_error = msg;
+    return st;
+  }
+  *out = c;
+  return DLX_OK;
 }
 
 dlx_status dlx_ctx_destroy(dlx_ctx* ctx) {
@@ -524,6 +609,7 @@ static void run_compress(dlx_ctx* ctx, dlx_layout* L, const float* d_delta, int 
                          int rounding, int iters, uint64_t s0, const float* d_warm_q,
                          int warm_rank, uint8_t* d_payload, float* d_q_out, uint64_t* d_draws,
                          cudaStream_t s) {
+  HostProf hp("compress");
   validate_quant(rank, qbits);
   if (iters < 1) raise(DLX_ERR_VALIDATION, "lowrank_approx: iters must be >= 1");
   if (rounding != 0 && rounding != 1) raise(DLX_ERR_VALIDATION, "unknown rounding mode");
@@ -563,6 +649,7 @@ static void run_compress(dlx_ctx* ctx, dlx_layout* L, const float* d_delta, int 
     // all-zero tensors). Bases converge tensor by tensor.
     if (!(cold && rounding == 0) || P.t2.empty()) break;
     int h_mis = 0;
+    HostProf hw("compress.cold_verify_wait");
     DLX_CUDA(cudaMemcpyAsync(&h_mis, mismatch, sizeof(int), cudaMemcpyDeviceToHost, s));
     DLX_CUDA(cudaStreamSynchronize(s));
     if (!h_mis) break;
@@ -703,6 +790,43 @@ dlx_status dlx_stage_deltas(dlx_ctx* ctx, const dlx_layout* layout, const float*
     cudaStream_t s = as_stream(stream);
     if (d_norm_sq) DLX_CUDA(cudaMemsetAsync(d_norm_sq, 0, sizeof(double), s));
     launch_stage(*layout, d_anchor, d_local, d_err, d_pending, d_norm_sq, s);
+  });
+}
+
+dlx_status dlx_measure_error(dlx_ctx* ctx, const dlx_layout* layout, int rank, int qbits,
+                             const uint8_t* d_payload, const float* d_delta, double* d_out,
+                             void* stream) {
+  return guard([&] {
+    set_device(ctx);
+    validate_quant(rank, qbits);
+    if (!d_payload || !d_delta || !d_out) raise(DLX_ERR_VALIDATION, "null buffer");
+    Plan& P = const_cast<dlx_layout*>(layout)->plan(rank, qbits);
+    cudaStream_t s = as_stream(stream);
+    float* rec = static_cast<float*>(ctx->scratch("measure_rec", sizeof(float) * layout->slab));
+    launch_reconstruct_dense(ctx, P, 1, d_payload, rec, s);
+    DLX_CUDA(cudaMemsetAsync(d_out, 0, 2 * sizeof(double), s));
+    launch_sqdiff(*layout, rec, d_delta, d_out, s);
+  });
+}
+
+dlx_status dlx_sqdiff_slabs(dlx_ctx* ctx, const dlx_layout* layout, const float* d_rec,
+                            const float* d_delta, double* d_out, void* stream) {
+  return guard([&] {
+    set_device(ctx);
+    if (!d_rec || !d_delta || !d_out) raise(DLX_ERR_VALIDATION, "null buffer");
+    cudaStream_t s = as_stream(stream);
+    DLX_CUDA(cudaMemsetAsync(d_out, 0, 2 * sizeof(double), s));
+    launch_sqdiff(*layout, d_rec, d_delta, d_out, s);
+  });
+}
+
+dlx_status dlx_mean_slabs(dlx_ctx* ctx, int64_t n, int64_t ld, int D, const float* d_in,
+                          float* d_out, void* stream) {
+  return guard([&] {
+    set_device(ctx);
+    if (D < 1) raise(DLX_ERR_VALIDATION, "allreduce_avg: no payloads");
+    if (n < 0 || ld < n) raise(DLX_ERR_VALIDATION, "mean_slabs: bad sizes");
+    launch_mean_slabs(n, ld, d_in, D, d_out, as_stream(stream));
   });
 }
 

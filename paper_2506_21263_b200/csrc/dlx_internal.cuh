@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <cstring>
+#include <exception>
 #include <stdint.h>
 
 #include <map>
@@ -19,9 +21,44 @@ struct Error {
   dlx_status code;
   std::string msg;
 };
+struct Comm;  // comm.cu: NCCL communicator + exchange stream of a context
+void destroy_comm(Comm* c);
 [[noreturn]] void raise(dlx_status code, const std::string& msg);
+void set_last_error(const std::string& msg);  // dlx_last_error() of the calling thread
+// Runs f, mapping a thrown Error to its status code (and the message to dlx_last_error).
+template <class F>
+dlx_status guard(F&& f) {
+  try {
+    f();
+    return DLX_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return DLX_ERR_VALIDATION;
+  }
+}
 void check_cuda(cudaError_t e, const char* what);
 void count_launch(int n = 1);
+// Opt kernel `func` into `bytes` of dynamic shared memory on the CURRENT device. The
+// attribute is per device, so the opt-in is cached per (device, kernel, bytes): a second
+// context on another device in the same process gets its own.
+void smem_optin(const void* func, int bytes);
+// Host-side wall time per scope, reported at exit when DLX_HOST_PROF=1 (where the host
+// spends its time between launches: plan / state builds on a rank change, waits).
+struct HostProf {
+  explicit HostProf(const char* name);
+  ~HostProf();
+  const char* name;
+  double t0;
+  bool on;
+};
+// Host -> device copy of a small table that returns once the bytes have landed, issued on a
+// per-device non-blocking stream: unlike cudaMemcpy it does not wait for the work queued on
+// the legacy default stream (a plan built while the previous round's outer update still
+// runs — a rank change under the adaptive schedule — must not drain the GPU).
+void upload_now(void* dst, const void* src, size_t bytes);
 #define DLX_CUDA(x) ::dlx::check_cuda((x), #x)
 #define DLX_LAUNCHED() do { ::dlx::check_cuda(cudaGetLastError(), "kernel launch"); ::dlx::count_launch(); } while (0)
 
@@ -115,6 +152,7 @@ struct Plan;
 struct dlx_ctx {
   int device = 0;
   cudaStream_t internal = nullptr;
+  dlx::Comm* comm = nullptr;  // dlx_comm_init (worker sync); null = single worker
   // grow-only scratch arenas
   std::map<std::string, std::pair<void*, size_t>> arenas;
   void* scratch(const std::string& name, size_t bytes, bool zero = false);
@@ -202,13 +240,68 @@ T& plan_ext(const Plan& P, const std::string& key, bool* fresh = nullptr) {
   return *static_cast<T*>(e.get());
 }
 
+// Device copies of per-tensor TMA descriptor tables, keyed by the buffer addresses they were
+// encoded for. A caller that alternates buffers (ping-pong local / anchor slabs) hits the
+// cache instead of re-encoding. Each entry's host side is pinned and never rewritten while
+// the entry lives, so the upload is a plain stream-ordered copy with no host
+// synchronisation; only evicting an entry (more than kEntries distinct keys) waits for the
+// device, since in-flight kernels may still read the evicted table.
+template <class T, int NK>
+struct MapTableCache : PlanExt {
+  static constexpr int kEntries = 4;
+  struct Entry {
+    const void* key[NK];
+    T* host = nullptr;  // pinned
+    T* dev = nullptr;
+    uint64_t used = 0;
+  };
+  std::vector<Entry> entries;
+  uint64_t tick = 0;
+  ~MapTableCache() override {
+    for (Entry& e : entries) {
+      if (e.host) cudaFreeHost(e.host);
+      if (e.dev) cudaFree(e.dev);
+    }
+  }
+  // Returns the device table for `key`; `encode(T* host)` fills a new table of n entries.
+  template <class F>
+  const T* get(const void* const* key, size_t n, cudaStream_t s, F&& encode) {
+    ++tick;
+    for (Entry& e : entries)
+      if (std::equal(key, key + NK, e.key)) {
+        e.used = tick;
+        return e.dev;
+      }
+    if (static_cast<int>(entries.size()) >= kEntries) {
+      auto victim = std::min_element(entries.begin(), entries.end(),
+                                     [](const Entry& x, const Entry& y) { return x.used < y.used; });
+      DLX_CUDA(cudaDeviceSynchronize());
+      cudaFreeHost(victim->host);
+      cudaFree(victim->dev);
+      entries.erase(victim);
+    }
+    HostProf hp("map_table (new)");
+    Entry e{};
+    std::copy(key, key + NK, e.key);
+    const size_t bytes = sizeof(T) * std::max<size_t>(n, 1);
+    DLX_CUDA(cudaMallocHost(&e.host, bytes));
+    DLX_CUDA(cudaMalloc(&e.dev, bytes));
+    std::memset(static_cast<void*>(e.host), 0, bytes);
+    encode(e.host);
+    DLX_CUDA(cudaMemcpyAsync(e.dev, e.host, bytes, cudaMemcpyHostToDevice, s));
+    e.used = tick;
+    entries.push_back(e);
+    return entries.back().dev;
+  }
+};
+
 // Upload a host vector into a plan-owned device buffer (at least min_elems elements).
 template <class T>
 T* plan_upload(const Plan& P, const std::vector<T>& v, size_t min_elems = 0) {
   const size_t n = std::max(v.size(), min_elems);
   if (n == 0) return nullptr;
   T* d = static_cast<T*>(P.dev_alloc(sizeof(T) * n));
-  if (!v.empty()) DLX_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  if (!v.empty()) upload_now(d, v.data(), sizeof(T) * v.size());
   return d;
 }
 
@@ -280,6 +373,9 @@ void launch_adamw(int64_t n, float lr, float beta1, float beta2, float eps, floa
                   float* v, int* nonfinite, cudaStream_t s);
 void launch_stage(const dlx_layout& L, const float* anchor, const float* local,
                   const float* err, float* pending, double* norm_sq, cudaStream_t s);
+void launch_sqdiff(const dlx_layout& L, const float* rec, const float* delta, double* out,
+                   cudaStream_t s);
+void launch_mean_slabs(int64_t n, int64_t ld, const float* x, int D, float* out, cudaStream_t s);
 void launch_nesterov(int64_t n, float gamma, float beta, int classical, float* anchor,
                      float* v, const float* delta, cudaStream_t s);
 void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,

@@ -1192,12 +1192,8 @@ static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const
                            const double* GI, const uint8_t* gathered, double* W, double tau,
                            int* d_per, double* d_energy, int shard, int nshards,
                            cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    DLX_CUDA(cudaFuncSetAttribute(k_effrank, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(double) * kErSwitch * (kErSwitch + 1))));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_effrank),
+             static_cast<int>(sizeof(double) * kErSwitch * (kErSwitch + 1)));
   int n2max = 0;
   for (const DevT2& t : P.t2) n2max = std::max(n2max, D * t.r + ((D * t.r) & 1));
   if (n2max > kErMaxN) raise(DLX_ERR_VALIDATION, "effective_rank: D * rank above 256 unsupported");
@@ -1205,12 +1201,7 @@ static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const
   const int nb = (ne - shard + nshards - 1) / nshards;
   if (nb <= 0) return;
   if (GI && n2max > option_effrank_big_from()) {
-    static bool battr = false;
-    if (!battr) {
-      DLX_CUDA(cudaFuncSetAttribute(k_effrank_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kEbSmem)));
-      battr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(k_effrank_big), static_cast<int>(kEbSmem));
     k_effrank_big<<<nb, kEbThreads, kEbSmem, s>>>(P.d_t2, D, rr, GI, gathered, P.payload_bytes,
                                                   W, tau, d_per, d_energy, shard, nshards);
     DLX_LAUNCHED();
@@ -1256,6 +1247,7 @@ static void launch_effrank(const Plan& P, int D, int rr, const double* GA, const
 void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                             double tau, int* d_per, double* d_energy, int shard, int nshards,
                             cudaStream_t s) {
+  HostProf hp_("effective_rank_factors");
   if (P.t2.empty()) return;
   if (nshards < 1 || shard < 0 || shard >= nshards)
     raise(DLX_ERR_VALIDATION, "effective_rank: need 0 <= shard < nshards");

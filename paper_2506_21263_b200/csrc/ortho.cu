@@ -262,11 +262,7 @@ static void launch_gram(const GramJob& J, const float* buf, double* partial, cud
   const int nb = (J.rmax + 3) / 4, nblk = nb * (nb + 1) / 2;
   const int gy = nblk >= 256 ? (nblk + 255) / 256 : 1;
   const size_t sm = gram_smem(J.rmax);
-  static bool attr = false;
-  if (!attr) {
-    DLX_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_gram), 64 * 1024);
   k_gram<<<dim3(J.splits.size(), gy), 256, sm, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial,
                                                      only);
   DLX_LAUNCHED();
@@ -746,12 +742,8 @@ static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* /*tmp*/, const 
   auto* flags1 = static_cast<int*>(ctx->scratch("ortho_flags1" + tag, sizeof(int) * ne));
   auto* need2 = static_cast<int*>(ctx->scratch("ortho_need2" + tag, sizeof(int) * ne));
   auto* flags2 = static_cast<int*>(ctx->scratch("ortho_flags2" + tag, sizeof(int) * ne));
-  static bool attr = false;
-  if (!attr) {
-    DLX_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    DLX_CUDA(cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_apply), 160 * 1024);
+  smem_optin(reinterpret_cast<const void*>(k_chol), 80 * 1024);
   const size_t csm = rr <= 64 ? 2 * sizeof(double) * rr * rr : 0;
   const size_t asm_ = apply_smem(rr);
   // pass 1 (every factor), in place
@@ -770,6 +762,7 @@ static void cholqr2(dlx_ctx* ctx, GramJob& J, float* buf, float* /*tmp*/, const 
 
 void orthonormalize_batched(dlx_ctx* ctx, const Plan& P, int side, float* buf, float* tmp,
                             cudaStream_t s) {
+  HostProf hp_("orthonormalize_batched");
   if (P.mats[side].empty()) return;
   GramJob& J = job_for(P, side == 0 ? "P" : "Q", P.mats[side]);
   cholqr2(ctx, J, buf, tmp, side == 0 ? "P" : "Q", side == 0 ? P.pelems : P.qelems, s);

@@ -442,20 +442,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 k5_encode_fn() {
   return fn;
 }
 
-struct K5MapCache : PlanExt {
-  const void* key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  K5Maps* d = nullptr;
-  std::vector<K5Maps> h;
-};
+using K5MapCache = MapTableCache<K5Maps, 6>;
 
 static const K5Maps* k5_maps(const Plan& P, int D, const float* pending, const float* anchor,
                              const float* velocity, const float* local, const float* phat,
                              cudaStream_t s) {
   K5MapCache& c = plan_ext<K5MapCache>(P, "k5_maps");
   const void* key[6] = {pending, anchor, velocity, local, phat, reinterpret_cast<const void*>(static_cast<intptr_t>(D))};
-  if (c.d && std::equal(key, key + 6, c.key)) return c.d;
-  if (!c.d) c.d = static_cast<K5Maps*>(P.dev_alloc(sizeof(K5Maps) * std::max<size_t>(P.t2.size(), 1)));
-  c.h.assign(P.t2.size(), K5Maps{});
+  return c.get(key, P.t2.size(), s, [&](K5Maps* h) {
   for (size_t k = 0; k < P.t2.size(); ++k) {
     const DevT2& t = P.t2[k];
     if (t.b % 4 != 0) continue;
@@ -465,7 +459,7 @@ static const K5Maps* k5_maps(const Plan& P, int D, const float* pending, const f
       const cuuint64_t strides[1] = {static_cast<cuuint64_t>(t.b) * 4};
       const cuuint32_t box[2] = {128, 16};
       const cuuint32_t estr[2] = {1, 1};
-      CUresult r = k5_encode_fn()(&c.h[k].m[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+      CUresult r = k5_encode_fn()(&h[k].m[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                                   const_cast<float*>(static_cast<const float*>(key[q])) + t.off,
                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -477,7 +471,7 @@ static const K5Maps* k5_maps(const Plan& P, int D, const float* pending, const f
       const cuuint64_t strides[1] = {static_cast<cuuint64_t>(t.lda) * 4};
       const cuuint32_t box[2] = {16, 32};
       const cuuint32_t estr[2] = {1, 1};
-      CUresult r = k5_encode_fn()(&c.h[k].m[4], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+      CUresult r = k5_encode_fn()(&h[k].m[4], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                                   const_cast<float*>(phat) + D * t.poff, dims, strides, box, estr,
                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -485,10 +479,7 @@ static const K5Maps* k5_maps(const Plan& P, int D, const float* pending, const f
       if (r != CUDA_SUCCESS) raise(DLX_ERR_CUDA, "cuTensorMapEncodeTiled (K5 Phat) failed");
     }
   }
-  DLX_CUDA(cudaMemcpyAsync(c.d, c.h.data(), sizeof(K5Maps) * P.t2.size(), cudaMemcpyHostToDevice, s));
-  DLX_CUDA(cudaStreamSynchronize(s));
-  std::copy(key, key + 6, c.key);
-  return c.d;
+  });
 }
 
 static size_t k5s_smem() {
@@ -536,7 +527,20 @@ bool& option_outer_tc() {
   return on;
 }
 
+void launch_outer_2d_impl(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
+                          int self_index, int mode, float* pending, float* anchor,
+                          const float* local, float* velocity, float gamma, float beta,
+                          int classical, dlx_round_stats* stats, const SlotRange& R,
+                          cudaStream_t s);
 void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
+                     int self_index, int mode, float* pending, float* anchor,
+                     const float* local, float* velocity, float gamma, float beta,
+                     int classical, dlx_round_stats* stats, const SlotRange& R, cudaStream_t s) {
+  HostProf hp("outer_update_2d");
+  launch_outer_2d_impl(ctx, P, D, gathered, self_index, mode, pending, anchor, local, velocity,
+                       gamma, beta, classical, stats, R, s);
+}
+void launch_outer_2d_impl(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered,
                      int self_index, int mode, float* pending, float* anchor,
                      const float* local, float* velocity, float gamma, float beta,
                      int classical, dlx_round_stats* stats, const SlotRange& R,
@@ -571,12 +575,8 @@ void launch_outer_2d(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathered
   float* qhat = static_cast<float*>(ctx->scratch("qhat", sizeof(float) * P.qelems * D));
   dequant_factors(P, D, gathered, P.payload_bytes, phat, qhat, 0, s);
   if (!k5s_tiles->empty()) {
-    static bool attr = false;
-    if (!attr) {
-      DLX_CUDA(cudaFuncSetAttribute(k5s_outer<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5s_smem()));
-      DLX_CUDA(cudaFuncSetAttribute(k5s_outer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5s_smem()));
-      attr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(k5s_outer<true>), (int)k5s_smem());
+    smem_optin(reinterpret_cast<const void*>(k5s_outer<false>), (int)k5s_smem());
     int sms = 0, dev = 0;
     DLX_CUDA(cudaGetDevice(&dev));
     DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -870,9 +870,9 @@ __global__ void __launch_bounds__(256) k_stage(const Span* __restrict__ spans,
   if ((threadIdx.x & 31) == 0 && norm_sq && ss != 0.0) atomicAdd(norm_sq, ss);
 }
 
-void launch_stage(const dlx_layout& L, const float* anchor, const float* local,
-                  const float* err, float* pending, double* norm_sq, cudaStream_t s) {
-  if (L.nt == 0) return;
+// Device table of the layout's tensor spans (slab offset, element count), built once per
+// layout; returns it and the longest span.
+static const Span* layout_spans(const dlx_layout& L, int64_t* longest) {
   std::vector<Span> spans(L.nt);
   int64_t mx = 1;
   for (int i = 0; i < L.nt; ++i) {
@@ -882,11 +882,92 @@ void launch_stage(const dlx_layout& L, const float* anchor, const float* local,
   Span* d = static_cast<Span*>(L.d_spans);
   if (!d) {
     DLX_CUDA(cudaMalloc(&d, sizeof(Span) * L.nt));
-    DLX_CUDA(cudaMemcpy(d, spans.data(), sizeof(Span) * L.nt, cudaMemcpyHostToDevice));
+    upload_now(d, spans.data(), sizeof(Span) * L.nt);
     const_cast<dlx_layout&>(L).d_spans = d;
   }
+  *longest = mx;
+  return d;
+}
+
+void launch_stage(const dlx_layout& L, const float* anchor, const float* local,
+                  const float* err, float* pending, double* norm_sq, cudaStream_t s) {
+  if (L.nt == 0) return;
+  int64_t mx = 1;
+  const Span* d = layout_spans(L, &mx);
   const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 1024));
   k_stage<<<dim3(gx, L.nt), 256, 0, s>>>(d, anchor, local, err, pending, norm_sq);
+  DLX_LAUNCHED();
+}
+
+// measure_error (compress.cpp:246-262): out[0] += sum (rec - delta)^2, out[1] += sum delta^2
+// over the layout's tensor elements, in fp64 (block partial sums; the summation order is not
+// the reference's serial one, so the ratio agrees to ~1e-15 relative, not bit for bit).
+__global__ void __launch_bounds__(256) k_sqdiff(const Span* __restrict__ spans,
+                                                const float* __restrict__ rec,
+                                                const float* __restrict__ delta,
+                                                double* out) {
+  const Span sp = spans[blockIdx.y];
+  double num = 0.0, den = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < sp.n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)delta[sp.off + k];
+    const double diff = (double)rec[sp.off + k] - d;
+    num += diff * diff;
+    den += d * d;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
+  }
+  __shared__ double sn[8], sd[8];
+  if ((threadIdx.x & 31) == 0) {
+    sn[threadIdx.x >> 5] = num;
+    sd[threadIdx.x >> 5] = den;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      a += sn[w];
+      b += sd[w];
+    }
+    if (a != 0.0) atomicAdd(out, a);
+    if (b != 0.0) atomicAdd(out + 1, b);
+  }
+}
+
+void launch_sqdiff(const dlx_layout& L, const float* rec, const float* delta, double* out,
+                   cudaStream_t s) {
+  if (L.nt == 0) return;
+  int64_t mx = 1;
+  const Span* d = layout_spans(L, &mx);
+  const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 512));
+  k_sqdiff<<<dim3(gx, L.nt), 256, 0, s>>>(d, rec, delta, out);
+  DLX_LAUNCHED();
+}
+
+// Worker-order fp64 mean of D slabs (leading dimension ld): allreduce_avg of RawDense
+// payloads (collective.cpp:17-46 over compress_raw, compress.cpp:185-199) and the per-step
+// gradient mean of the all-reduce baseline (engine.cpp:559-570): double sum in worker order,
+// times the double 1/D, rounded to float once — bit-identical to the reference.
+__global__ void __launch_bounds__(256) k_mean_slabs(int64_t n, int64_t ld,
+                                                    const float* __restrict__ x, int D,
+                                                    float* __restrict__ out) {
+  const double inv = 1.0 / (double)D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = (double)x[i];
+    for (int w = 1; w < D; ++w) acc = __dadd_rn(acc, (double)x[(int64_t)w * ld + i]);
+    out[i] = (float)__dmul_rn(acc, inv);
+  }
+}
+
+void launch_mean_slabs(int64_t n, int64_t ld, const float* x, int D, float* out,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  const int g = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 148 * 16));
+  k_mean_slabs<<<g, 256, 0, s>>>(n, ld, x, D, out);
   DLX_LAUNCHED();
 }
 

@@ -768,9 +768,7 @@ struct O5State : PlanExt {
   int* d_ctr = nullptr;
   int64_t* d_aoff = nullptr;
   int64_t* d_boff = nullptr;
-  O5Maps* d_maps = nullptr;
-  std::vector<O5Maps> h_maps;
-  const void* key[8] = {};
+  MapTableCache<O5Maps, 8> maps;  // descriptor tables keyed by the state / operand buffers
 };
 
 bool o5_eligible(const Plan& P, int D, int self_index) {
@@ -790,6 +788,7 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   bool fresh = false;
   O5State& S = plan_ext<O5State>(P, "o5:" + std::to_string(D) + ":" + R.key(), &fresh);
   if (!fresh) return S;
+  HostProf hp("o5_state (new)");
   S.D = D;
   const int K = D * P.rmax;
   S.bf = K > 32;
@@ -877,22 +876,17 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   S.d_rows = plan_upload(P, S.rows, 1);
   S.d_aoff = plan_upload(P, S.aoff, 1);
   S.d_boff = plan_upload(P, S.boff, 1);
-  S.d_maps = static_cast<O5Maps*>(P.dev_alloc(sizeof(O5Maps) * P.t2.size()));
-  S.h_maps.resize(P.t2.size());
   return S;
 }
 
 template <bool SELF, bool BF>
-static void launch_o5(const Plan& P, const O5State& S, int grid, int nbands, int D, int self_index,
+static void launch_o5(const Plan& P, const O5State& S, const O5Maps* maps, int grid, int nbands,
+                      int D, int self_index,
                       int mode, float gamma, float beta, int classical, const float* post,
                       dlx_round_stats* stats, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    DLX_CUDA(cudaFuncSetAttribute(k_o5<SELF, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_o5<SELF, BF>), 227 * 1024);
   k_o5<SELF, BF><<<grid, BF ? kO5ThreadsTA : kO5Threads, S.smem, s>>>(
-      P.d_t2, S.d_maps, S.d_bands, nbands, S.d_ctr, D, S.KA, S.nst, S.nab, S.nbr, S.a_mode,
+      P.d_t2, maps, S.d_bands, nbands, S.d_ctr, D, S.KA, S.nst, S.nab, S.nbr, S.a_mode,
       self_index, mode, gamma, beta, classical, post, stats);
 }
 
@@ -928,13 +922,12 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   DLX_LAUNCHED();
   const void* key[8] = {pending, anchor, velocity, mode == DLX_MODE_OVERLAPPED ? local : nullptr,
                         A, B[0], B[1], nullptr};
-  if (!std::equal(key, key + 8, S.key)) {
+  const O5Maps* maps = S.maps.get(key, P.t2.size(), s, [&](O5Maps* h) {
     const CUtensorMapDataType dt = S.bf ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const uint32_t ak = S.bf ? O5Kind<true>::AK : O5Kind<false>::AK;
     for (size_t k = S.s0; k < static_cast<size_t>(S.s1); ++k) {
       const DevT2& t = P.t2[k];
-      O5Maps& m = S.h_maps[k];
-      std::memset(&m, 0, sizeof(m));
+      O5Maps& m = h[k];
       const float* srcs[4] = {pending, anchor, velocity, local};
       for (int q = 0; q < 4; ++q)
         if (srcs[q] && (q < 3 || mode == DLX_MODE_OVERLAPPED))
@@ -946,11 +939,7 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
         o5_encode_map(&m.b[pl], static_cast<uint8_t*>(B[pl]) + es * S.boff[k], KA, t.ldb, KA * es, ak,
                       kO5TileN, CU_TENSOR_MAP_SWIZZLE_128B, dt);
     }
-    DLX_CUDA(cudaMemcpyAsync(S.d_maps, S.h_maps.data(), sizeof(O5Maps) * P.t2.size(),
-                             cudaMemcpyHostToDevice, s));
-    DLX_CUDA(cudaStreamSynchronize(s));
-    std::copy(key, key + 8, S.key);
-  }
+  });
   int dev = 0, sms = 0;
   DLX_CUDA(cudaGetDevice(&dev));
   DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -962,14 +951,14 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   KernelTimer timer("k_o5", (mode == DLX_MODE_OVERLAPPED ? 28.0 : 24.0) * S.params, s);
   if (self_index >= 0) {
     if (S.bf)
-      launch_o5<true, true>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
+      launch_o5<true, true>(P, S, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
     else
-      launch_o5<true, false>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
+      launch_o5<true, false>(P, S, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
   } else {
     if (S.bf)
-      launch_o5<false, true>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
+      launch_o5<false, true>(P, S, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
     else
-      launch_o5<false, false>(P, S, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
+      launch_o5<false, false>(P, S, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
   }
   DLX_LAUNCHED();
 }

@@ -190,6 +190,7 @@ bool& option_tensor_cores() {
 static bool use_tc(const Plan& P) { return option_tensor_cores() && tc_supported(P); }
 
 void launch_k1(const Plan& P, const float* slab, const float* q, float* y, cudaStream_t s) {
+  HostProf hp_("launch_k1");
   const bool tc = use_tc(P);
   if (tc) launch_k1_tc(P, slab, q, y, s);
   const std::vector<int4>& tiles = tc ? P.k1_rest : P.k1_tiles;
@@ -321,6 +322,7 @@ __global__ void k2_reduce(const DevT2* __restrict__ T, const int* __restrict__ s
 
 void launch_k2(const Plan& P, const float* slab, const float* p, float* z, float* part,
                cudaStream_t s) {
+  HostProf hp_("launch_k2");
   if (P.k2_tiles.empty()) return;
   const bool tc = use_tc(P);
   if (tc) launch_k2_tc(P, slab, p, z, part, s);

@@ -183,6 +183,7 @@ void quantize_all(dlx_ctx* ctx, const Plan& P, const float* pbuf, const float* q
                   const float* slab, int rounding, uint64_t s0, int cold,
                   const int64_t* d_cold_base_used, uint8_t* payload, uint64_t* d_draws,
                   int* d_mismatch, int64_t* d_cold_base_actual, cudaStream_t s) {
+  HostProf hp_("quantize_all");
   const int nc = static_cast<int>(P.chunks.size());
   if (nc == 0) {
     DLX_CUDA(cudaMemsetAsync(d_draws, 0, 8, s));

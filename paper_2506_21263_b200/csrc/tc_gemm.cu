@@ -432,15 +432,14 @@ struct TcState : PlanExt {
   int4* d_k2 = nullptr;
   int* d_off1 = nullptr;
   int* d_off2 = nullptr;
-  TcMaps* d_maps[2] = {nullptr, nullptr};
-  const void* key[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-  std::vector<TcMaps> host[2];
+  MapTableCache<TcMaps, 2> maps[2];  // K1 / K2 descriptor tables keyed by (slab, factors)
 };
 
 static TcState& tc_state(const Plan& P) {
   bool fresh = false;
   TcState* s = &plan_ext<TcState>(P, "tc_sweep", &fresh);
   if (fresh) {
+    HostProf hp("tc_state (new)");
     constexpr int64_t KC = 2048;
     for (size_t k = 0; k < P.t2.size(); ++k) {
       const DevT2& t = P.t2[k];
@@ -483,10 +482,6 @@ static TcState& tc_state(const Plan& P) {
     s->d_k2 = plan_upload(P, s->k2);
     s->d_off1 = plan_upload(P, s->off1);
     s->d_off2 = plan_upload(P, s->off2);
-    for (int w = 0; w < 2; ++w) {
-      s->d_maps[w] = static_cast<TcMaps*>(P.dev_alloc(sizeof(TcMaps) * std::max<size_t>(P.t2.size(), 1)));
-      s->host[w].resize(P.t2.size());
-    }
   }
   return *s;
 }
@@ -495,28 +490,23 @@ static TcState& tc_state(const Plan& P) {
 static const TcMaps* tc_maps(const Plan& P, int which, const float* slab, const float* fac,
                              cudaStream_t s) {
   TcState& S = tc_state(P);
-  if (S.key[which][0] == slab && S.key[which][1] == fac) return S.d_maps[which];
+  const void* key[2] = {slab, fac};
   const int N = tc_n(P);
-  for (size_t k = 0; k < P.t2.size(); ++k) {
-    const DevT2& t = P.t2[k];
-    TcMaps& m = S.host[which][k];
-    std::memset(&m, 0, sizeof(m));
-    if (!tc_eligible(t)) continue;
-    const float* A = slab + t.off;
-    if (which == 0) {
-      encode(&m.a, A, t.b, t.a, t.b * 4, 32, 128);
-      encode(&m.b, fac + t.qoff, t.b, t.r, t.ldb * 4, 32, N);
-    } else {
-      encode(&m.a, A, t.b, t.a, t.b * 4, 32, 32, /*swizzle=*/false);
-      encode(&m.b, fac + t.poff, t.a, t.r, t.lda * 4, 32, N);
+  return S.maps[which].get(key, P.t2.size(), s, [&](TcMaps* host) {
+    for (size_t k = 0; k < P.t2.size(); ++k) {
+      const DevT2& t = P.t2[k];
+      TcMaps& m = host[k];
+      if (!tc_eligible(t)) continue;
+      const float* A = slab + t.off;
+      if (which == 0) {
+        encode(&m.a, A, t.b, t.a, t.b * 4, 32, 128);
+        encode(&m.b, fac + t.qoff, t.b, t.r, t.ldb * 4, 32, N);
+      } else {
+        encode(&m.a, A, t.b, t.a, t.b * 4, 32, 32, /*swizzle=*/false);
+        encode(&m.b, fac + t.poff, t.a, t.r, t.lda * 4, 32, N);
+      }
     }
-  }
-  DLX_CUDA(cudaMemcpyAsync(S.d_maps[which], S.host[which].data(), sizeof(TcMaps) * P.t2.size(),
-                           cudaMemcpyHostToDevice, s));
-  DLX_CUDA(cudaStreamSynchronize(s));  // host staging buffer reused on the next re-encode
-  S.key[which][0] = slab;
-  S.key[which][1] = fac;
-  return S.d_maps[which];
+  });
 }
 
 // Boxes per stage: 2 (32 KB of delta per stage) while the rings still fit; 1 for wide N.
@@ -548,12 +538,7 @@ static void launch_sweep_kb(const Plan& P, const TcMaps* maps, const int4* d_til
   int lr = 0, cr = 0;
   tc_rings(N, KB, lr, cr);
   const size_t sm = tc_smem(N, KB, lr, cr);
-  static bool attr = false;
-  if (!attr) {
-    DLX_CUDA(cudaFuncSetAttribute(k_tc_sweep<A_MN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_tc_sweep<A_MN, KB>), 227 * 1024);
   static const int hints = [] {  // experiments: DLX_SWEEP_HINTS=0 drops the L2 cache hints
     const char* e = getenv("DLX_SWEEP_HINTS");
     return e ? atoi(e) : 1;

@@ -79,6 +79,10 @@ _STAT_FIELDS = ("comp_error", "bound_violated", "err_buf_norm", "max_delta_norm"
 class RoundRecord:
     """Hot-path fields of RoundRecord (engine.hpp:74-95).
 
+    comp_error / err_buf_norm describe THIS rank's worker (its own payload and error buffer);
+    the reference's record reports worker 0 (engine.cpp:239, finish_record), so rank 0's
+    records are the ones that follow reference semantics.
+
     The statistics the fused outer update reduces on the device (comp_error, bound_violated,
     err_buf_norm, max_delta_norm, nonfinite) are read back lazily: the engine does not wait
     for the round's main stream, so the host enqueues round t+1 while round t's outer update
@@ -181,6 +185,16 @@ class OuterSync:
             shard_effective_rank = False
         self.er_shards = world if (shard_effective_rank and world > 1) else 1
         self._bcast_work = None  # in-flight warm-start broadcast (waited before next compress)
+        # worker sync through the library's own NCCL communicator (dlx_exchange: all-gather +
+        # warm-Q broadcast on its side stream). torch.distributed only bootstraps it (ships
+        # rank 0's unique id); DLX_LIB_NCCL=0 keeps the exchange in torch.distributed.
+        self.lib_comm = (world > 1 and anchor.is_cuda and
+                         os.environ.get("DLX_LIB_NCCL", "1") == "1")
+        if self.lib_comm and getattr(layout.ctx, "world", 1) != world:
+            import torch.distributed as dist
+            uid = [api.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0, group=group)
+            layout.ctx.init_comm(rank, world, uid[0])
         # warm-start broadcast right after the all-gather, before the outer update: 57 MB at
         # OPT-1.3B r=32 (~0.1 ms over NVLink); issued asynchronously it ran beside the outer
         # update's persistent grid and was the other source of multi-ms rank stalls
@@ -205,6 +219,7 @@ class OuterSync:
         self._h2d = self._d2h = None
         self._dev_local = None
         self._d2h_ev = None
+        self._host_h2d_last = None
         self._pre_update: list = []  # events the next read of local / write of anchor waits on
         self._host_job = None        # per-step chunk schedule while step_host runs
         self.host_chunks = 8         # tensor groups of the chunked host pipeline
@@ -243,6 +258,10 @@ class OuterSync:
         start) asynchronously — only the next round's compress needs it. NCCL over NVLink."""
         if self.world == 1:
             return self.payload[:pb]
+        if self.lib_comm:
+            return api.exchange(self.L.ctx, self.payload[:pb], self.gathered,
+                                self.warm_q[:qel] if qel else None,
+                                defer_warm=not self.bcast_sync)
         if self.bcast_sync:
             return exchange(self.payload[:pb], self.gathered, self.warm_q[:qel] if qel else None,
                             self.world, self.group)
@@ -254,6 +273,9 @@ class OuterSync:
         return g
 
     def _wait_bcast(self):
+        if self.lib_comm:
+            self.L.ctx.wait_warm()
+            return
         if self._bcast_work is not None:
             self._bcast_work.wait()  # the current stream waits; the host does not
             self._bcast_work = None
@@ -271,7 +293,10 @@ class OuterSync:
             if getattr(self, "_gathered_raw", None) is None:
                 self._gathered_raw = torch.empty(self.world * L.slab_elems, dtype=torch.float32,
                                                  device=self.anchor.device)
-            dist.all_gather_into_tensor(self._gathered_raw, payload, group=self.group)
+            if self.lib_comm:
+                api.comm_allgather(L.ctx, payload, self._gathered_raw)
+            else:
+                dist.all_gather_into_tensor(self._gathered_raw, payload, group=self.group)
             gathered = self._gathered_raw
         else:
             gathered = payload
@@ -306,50 +331,80 @@ class OuterSync:
         self._ev("exchange")
         gathered = self._exchange(pb, qel)
         cur = torch.cuda.current_stream()
-        self._ev("outer_update")
-        if cfg.adaptive and self._n2:
-            # factor-space effective rank on the side stream, overlapping the outer update
-            side = self.side or cur
+        rec = RoundRecord(round=self.round, r_t=r, H_t=self.H_t, averaged=True,
+                          payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
+        measure = cfg.adaptive and self._n2 > 0
+        side = self.side if self.side is not None else None
+        if measure and side is None:
+            # Unsharded measurement on the main stream BEFORE the outer update: r' (and so the
+            # controller's next rank, engine.cpp:476-487) is on the host while the outer update
+            # still runs, so applying the controller costs no host round trip on the device
+            # timeline. (The persistent outer-update grid holds every SM, so a side stream
+            # would only serialise behind it.)
+            self._ev("effective_rank")
+            self._effective_rank(gathered, r, q, cur)
+            self._queue_er(rec, cur)
+        elif measure:
+            # sharded across the ranks, on a high-priority side stream beside the outer update
             side.wait_stream(cur)
             with torch.cuda.stream(side):
-                if self.phase_events is not None:
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e0.record(side)
-                nb = max(self._n2, 1)
-                api.effective_rank_device(L, gathered, self.world, r, q, cfg.tau, stream=side,
-                                          shard=self.rank if self.er_shards > 1 else 0,
-                                          nshards=self.er_shards, per=self.er_per,
-                                          energy=self.er_dev[nb:])
-                self.er_dev[:nb].copy_(self.er_per)
-                if self.phase_events is not None:
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e1.record(side)
-                    self.side_events.append((e0, e1))
+                self._effective_rank(gathered, r, q, side)
+        self._ev("outer_update")
         self._outer_update(gathered, r, q, local, mode, cur)
         self._ev("end")
         self.stats_host[self.round % self.STATS_SLOTS].copy_(self.stats, non_blocking=True)
-        rec = RoundRecord(round=self.round, r_t=r, H_t=self.H_t, averaged=True,
-                          payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
-        if cfg.adaptive and self._n2:
+        if measure and side is not None:
             # the shards' per-tensor (k, energy) are summed AFTER the outer update, on the main
             # stream: no collective runs beside its persistent grid (an NCCL all-reduce there,
             # or a per-round CPU/gloo one, measured 20-260 ms rank stalls)
-            cur.wait_stream(self.side or cur)
+            cur.wait_stream(side)
             if self.er_shards > 1:
-                import torch.distributed as dist
                 # one nonzero term per entry: the sum is exact and identical on every rank
-                dist.all_reduce(self.er_dev, group=self.group)
-            if len(self._er_fifo) >= self.ER_SLOTS:
-                self._drain_er(block=True, upto=1)
-            slot = self._er_slot
-            self._er_slot = (slot + 1) % self.ER_SLOTS
-            self.er_host[slot].copy_(self.er_dev, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(cur)
-            self._er_fifo.append((rec, ev, slot))
-            rec._drain = lambda: self._drain_er(block=True)
+                if self.lib_comm:
+                    api.comm_allreduce_sum_f64(self.L.ctx, self.er_dev)
+                else:
+                    import torch.distributed as dist
+                    dist.all_reduce(self.er_dev, group=self.group)
+            self._queue_er(rec, cur)
+        elif cfg.adaptive and cfg.compress and self._n2 == 0:
+            # no 2-D tensor: effective_rank's aggregate is 1 (compress.cpp:333-339), pushed
+            # every averaged round (engine.cpp:258-261, 480-482)
+            rec.r_prime = 1
+            self._push_window(1)
+            rec.r_next, rec.H_next = self._adapt()
         self.warm_rank = r
         return rec
+
+    def _effective_rank(self, gathered, r: int, q: int, stream):
+        """Factor-space effective rank (dlx_effective_rank_shard) into er_dev."""
+        cfg, L = self.cfg, self.L
+        e0 = e1 = None
+        if self.phase_events is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        nb = max(self._n2, 1)
+        api.effective_rank_device(L, gathered, self.world, r, q, cfg.tau, stream=stream,
+                                  shard=self.rank if self.er_shards > 1 else 0,
+                                  nshards=self.er_shards, per=self.er_per,
+                                  energy=self.er_dev[nb:])
+        self.er_dev[:nb].copy_(self.er_per)
+        if e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+            self.side_events.append((e0, e1))
+
+    def _queue_er(self, rec: RoundRecord, stream):
+        """Copy the round's per-tensor (k, energy) to pinned host memory behind an event;
+        the host resolves r' from it (lazily while the rank is held)."""
+        if len(self._er_fifo) >= self.ER_SLOTS:
+            self._drain_er(block=True, upto=1)
+        slot = self._er_slot
+        self._er_slot = (slot + 1) % self.ER_SLOTS
+        self.er_host[slot].copy_(self.er_dev, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self._er_fifo.append((rec, ev, slot))
+        rec._drain = lambda: self._drain_er(block=True)
 
     def _drain_er(self, block: bool, upto: int | None = None):
         """Resolve pending effective ranks in round order: r' into the window, then the
@@ -413,6 +468,8 @@ class OuterSync:
         # slot is about to be reused; a non-finite update surfaces within that many rounds).
         while self._unresolved and self._unresolved[0].round <= rec.round - (self.STATS_SLOTS - 2):
             self._unresolved.pop(0).resolve()
+        if self.lib_comm:
+            self.L.ctx.comm_check()  # surfaces an asynchronous NCCL failure (NcclError)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream())
         rec._pending = (ev, self.stats_host[rec.round % self.STATS_SLOTS].numpy(), mode)
@@ -517,6 +574,7 @@ class OuterSync:
                 ev = torch.cuda.Event()
                 ev.record(self._h2d)
                 evs.append(ev)
+        self._host_h2d_last = evs[-1] if evs else None
         prev = [self._d2h_ev] if self._d2h_ev is not None else []
         self._pre_update = evs + prev  # for the un-chunked paths (staging round, sync mode)
         job = {"h2d": evs, "prev": prev, "out": h_anchor_out, "done": False}
@@ -534,6 +592,18 @@ class OuterSync:
         return rec
 
     def host_wait(self, stream=None):
-        """Make `stream` (default: current) wait for the last step_host D2H."""
+        """Make `stream` (default: current) wait for the last step_host D2H (device-side
+        ordering only; the host does not block)."""
         if self._d2h_ev is not None:
             (stream or torch.cuda.current_stream()).wait_event(self._d2h_ev)
+
+    def host_sync(self):
+        """Block the host until the last step_host call's copies are done: afterwards the
+        caller may overwrite the `h_local` it passed and read `h_anchor_out`. (step_host
+        returns as soon as the work is enqueued; both host buffers are in use until then.)"""
+        for e in self._pre_update:
+            e.synchronize()
+        if self._d2h_ev is not None:
+            self._d2h_ev.synchronize()
+        if self._host_h2d_last is not None:
+            self._host_h2d_last.synchronize()

@@ -1,0 +1,355 @@
+"""Parity at the benchmarked shapes (BASELINE configs[1], OPT-1.3B) and with the adaptive
+controller APPLIED, against the compiled reference (oracle/_ref, built from
+/root/reference sources) — not only the plain-C restatement.
+
+Shapes: the OPT-1.3B embedding (50272 x 2048: K2 split-K over 25 row partitions), the
+position table (2050 x 2048), one full decoder layer (4 x 2048^2, 2048 x 8192, 8192 x 2048 and
+its 1-D tensors) and, device-only, the whole 146 + 242 tensor layout (k_o5 chunk claiming
+across every tensor, the fp16 B-prescale at D = 8).
+
+Bars (the parity contract):
+  * compress: draws consumed exact; >= 99.9 % identical codes; |Q_gpu - Q_ref| <= 1e-4 and
+    scales within 1e-4 relative;
+    decompressed payloads within 1e-3 relative Frobenius (fp32 tensor-core power iteration
+    vs the reference's fp64 loops);
+  * reconstruction inside the fused outer update: per tensor ||D_gpu - D_ref||_F <= 1e-5
+    ||D_ref||_F and max|D_gpu - D_ref| <= 1e-5 max|D_ref|; 1-D tensors bit-exact;
+  * the device fp64 allreduce_avg / decompress path: bit-exact;
+  * epilogue (error feedback, staging, Nesterov): bit-exact given the reconstructed Delta;
+  * effective rank r' equal to the reference's dense SVD;
+  * controller-applied rounds: identical rank schedule (r_t, r', r_next, H_next) every round;
+    each round's map (from the engine's own state) within 1e-2 of the reference's.
+Low-rank-plus-noise inputs (bench-compress's generator, tools/dilocox.cpp:183-192) give the
+rank-32 subspace a defined spectrum; a flat Gaussian spectrum makes the subspace itself
+ill-conditioned in either implementation.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import Table
+from tests._util import decode_payload, draws_between, rel_fro, split_dense, split_q
+
+pytestmark = pytest.mark.gpu
+
+RANK, Q = 32, 4
+TOL_RECON = 1e-5
+TOL_Q = 1e-4
+TOL_COMPRESS = 1e-3
+
+
+def _head_table():
+    from paper_2506_21263_b200 import layouts
+    tbl = layouts.opt_1_3b()
+    # embed_tokens, embed_positions, then layer 0 (16 tensors)
+    return tbl[:2] + [x for x in tbl if x[0].startswith("layers.0.")]
+
+
+def _lowrank_noise(shapes, seed, k=48, decay=0.8, amp=1e-3, noise=2e-6):
+    rng = np.random.default_rng(seed)
+    parts = []
+    for s in shapes:
+        if len(s) == 2:
+            a, b = s
+            u = rng.standard_normal((a, k), dtype=np.float32)
+            v = rng.standard_normal((b, k), dtype=np.float32)
+            sv = (amp * decay ** np.arange(k)).astype(np.float32)
+            d = (u * sv) @ v.T
+            d += np.float32(noise) * rng.standard_normal((a, b), dtype=np.float32)
+            parts.append(d.reshape(-1))
+        else:
+            parts.append((np.float32(1e-4) * rng.standard_normal(s[0], dtype=np.float32)))
+    return np.concatenate(parts).astype(np.float32)
+
+
+@pytest.fixture(scope="module")
+def head(ctx, reference):
+    """Layout + input + the reference's own compress of it (cold, then warm)."""
+    from paper_2506_21263_b200 import api
+    tbl = _head_table()
+    shapes = [s for _, s in tbl]
+    t = Table(shapes)
+    L = api.Layout(ctx, tbl)
+    flat = _lowrank_noise(shapes, 2026)
+    st0 = reference.stream(1, reference.stream_key(0xC09C, 2))
+    ref = reference.compress(t, flat, RANK, Q, 0, 2, st0)
+    st1 = reference.stream(1, reference.stream_key(0xC09C, 3))
+    ref_w = reference.compress(t, flat, RANK, Q, 0, 2, st1, warm_rank=RANK, warm_q=ref["q"])
+    return dict(L=L, t=t, shapes=shapes, flat=flat, delta=L.pack(flat), st0=st0, st1=st1,
+                ref=ref, ref_w=ref_w, R=reference)
+
+
+def _payload(L, reference, t, ranks, codes, scales):
+    return L.parse(reference.serialize(t, ranks, RANK, Q, codes, scales), RANK, Q)
+
+
+def _check(h, ref, res, st):
+    from paper_2506_21263_b200 import api
+    import torch
+    L, t = h["L"], h["t"]
+    assert int(res.draws.item()) == draws_between(st, ref["state"])
+    codes, scales = decode_payload(L, res.payload, RANK, Q)
+    same = (codes == ref["codes"]).mean()
+    assert same >= 0.999, same
+    # scales = max|column| / L of factors that carry the fp32-vs-fp64 power-iteration
+    # difference (a 50272-term contraction): same bar as the factors, 1e-4 relative
+    assert np.allclose(scales, ref["scales"], rtol=TOL_Q, atol=0)
+    for got, want in zip(L.factors_from_device(res.q_factors, RANK, 1),
+                         split_q(h["shapes"], RANK, ref["q"])):
+        assert np.abs(got - want).max() <= TOL_Q
+    # decompressed payloads compared on the device (the fp64 path is reference-exact)
+    d_gpu = api.decompress(L, res.payload, RANK, Q)
+    d_ref = api.decompress(L, _payload(L, h["R"], t, ref["ranks"], ref["codes"], ref["scales"]),
+                           RANK, Q)
+    num = torch.linalg.vector_norm((d_gpu - d_ref).double())
+    den = torch.linalg.vector_norm(d_ref.double())
+    assert float(num / den) <= TOL_COMPRESS
+
+
+def test_headline_compress_vs_reference(ctx, reference, head):
+    """dlx_compress on the benchmarked tensors, cold start then warm start (the bench's
+    steady state, power_iters = 2), against the reference's compress."""
+    from paper_2506_21263_b200 import api
+    h = head
+    L = h["L"]
+    res = api.compress(L, h["delta"], RANK, api.QuantSpec(Q, api.STOCHASTIC), None, 0, 2, h["st0"])
+    _check(h, h["ref"], res, h["st0"])
+    warm = L.factors_to_device(split_q(h["shapes"], RANK, h["ref"]["q"]), RANK, 1)
+    res_w = api.compress(L, h["delta"], RANK, api.QuantSpec(Q, api.STOCHASTIC), warm, RANK, 2,
+                         h["st1"])
+    _check(h, h["ref_w"], res_w, h["st1"])
+
+
+def _sync_delta(L, gathered, D):
+    """Delta from the fused outer update in sync mode on a zero pending buffer
+    (pending' = 0 - Delta exactly)."""
+    from paper_2506_21263_b200 import api
+    z, a0, v0 = L.empty(), L.empty(), L.empty()
+    api.outer_update(L, gathered, D, RANK, Q, z, a0, None, v0, 0.7, 0.9, False, mode=api.SYNC)
+    return -z
+
+
+def _check_recon(L, dg, dref):
+    """Per-tensor reconstruction bars on device slabs."""
+    for i, s in enumerate(L.shapes):
+        o, n = int(L.offsets[i]), L.numels[i]
+        x, y = dg[o:o + n].double(), dref[o:o + n].double()
+        if len(s) == 1:
+            assert bool((dg[o:o + n] == dref[o:o + n]).all()), (i, "1-D must be exact")
+            continue
+        den = float(y.norm())
+        assert float((x - y).norm()) <= TOL_RECON * den, (i, s)
+        assert float((x - y).abs().max()) <= TOL_RECON * float(y.abs().max()), (i, s)
+
+
+def _check_epilogue(L, dg, anchor, local, vel, pend, gathered, D, classical=False):
+    """Overlapped fused update vs the reference's op order (engine.cpp:254-276,
+    optim.cpp:56-78; separate fp32 roundings), given the reconstructed Delta: bit-exact."""
+    from paper_2506_21263_b200 import api
+    import torch
+    dP, dA, dV = pend.clone(), anchor.clone(), vel.clone()
+    stats = torch.zeros(8, dtype=torch.float64, device=dg.device)
+    api.outer_update(L, gathered, D, RANK, Q, dP, dA, local, dV, 0.7, 0.9, classical,
+                     mode=api.OVERLAPPED, self_index=0, stats=stats)
+    g, b = torch.tensor(0.7, dtype=torch.float32, device=dg.device), \
+        torch.tensor(0.9, dtype=torch.float32, device=dg.device)
+    m = _valid(L)  # tensor elements only (the slab's alignment padding is never touched)
+    e = pend - dg
+    want_p = (anchor - local) + e
+    want_v = (b * vel) + dg
+    want_a = anchor - g * want_v if classical else anchor - g * (dg + b * want_v)
+    assert torch.equal(dP[m], want_p[m])
+    assert torch.equal(dV[m], want_v[m])
+    assert torch.equal(dA[m], want_a[m])
+    return stats
+
+
+def _valid(L):
+    import torch
+    m = torch.zeros(L.slab_elems, dtype=torch.bool, device=f"cuda:{L.ctx.device}")
+    for o, n in zip(L.offsets[:L.nt], L.numels):
+        m[int(o):int(o) + n] = True
+    return m
+
+
+def _rand_state(L, seed):
+    import torch
+    g = torch.Generator(device=f"cuda:{L.ctx.device}").manual_seed(seed)
+    n, dev = L.slab_elems, f"cuda:{L.ctx.device}"
+    anchor = 0.02 * torch.randn(n, device=dev, generator=g)
+    local = anchor - 1e-3 * torch.randn(n, device=dev, generator=g)
+    vel = 1e-4 * torch.randn(n, device=dev, generator=g)
+    pend = 1e-3 * torch.randn(n, device=dev, generator=g)
+    return anchor, local, vel, pend
+
+
+def test_headline_outer_update_d1_vs_reference(ctx, reference, head):
+    """D = 1 (tf32 x2 operand path): the reference's allreduce_avg of the reference's own
+    payload vs the fused reconstruction; the device fp64 path bit-exact; the epilogue
+    bit-exact; measure_error vs the reference's."""
+    from paper_2506_21263_b200 import api
+    import torch
+    L, t, ref = head["L"], head["t"], head["ref"]
+    pay = _payload(L, reference, t, ref["ranks"], ref["codes"], ref["scales"])
+    avg_ref = reference.allreduce_avg(t, ref["ranks"], [ref["codes"]], [ref["scales"]])
+    avg_ref_dev = L.pack(avg_ref)
+    avg_dev = api.allreduce_avg(L, pay, 1, RANK, Q)
+    assert torch.equal(avg_dev, avg_ref_dev), "device fp64 allreduce_avg must be reference-exact"
+    dg = _sync_delta(L, pay, 1)
+    _check_recon(L, dg, avg_ref_dev)
+    anchor, local, vel, pend = _rand_state(L, 5)
+    pend = head["delta"].clone()  # measure_error of the compressed delta itself
+    stats = _check_epilogue(L, dg, anchor, local, vel, pend, pay, 1)
+    ce_ref = reference.measure_error(t, head["flat"], ref["ranks"], ref["codes"], ref["scales"])
+    st = stats.cpu().numpy()
+    assert abs(st[0] / st[1] - ce_ref) <= 1e-4 * ce_ref
+
+
+def _random_codes(t, ranks, seed, q=Q):
+    """Random codes in [-L, L] and scales spanning five decades (the fp16 B prescale must
+    keep every tensor's product range)."""
+    rng = np.random.default_rng(seed)
+    lv = (1 << (q - 1)) - 1
+    codes, scales = [], []
+    for s, r in zip(t.shapes, ranks):
+        if len(s) == 2:
+            a, b = s
+            codes.append(rng.integers(-lv, lv + 1, size=(a + b) * r, dtype=np.int8))
+            scales.append((10.0 ** rng.uniform(-6, -1, size=2 * r)).astype(np.float32))
+        else:
+            codes.append(rng.integers(-lv, lv + 1, size=s[0], dtype=np.int8))
+            scales.append((10.0 ** rng.uniform(-6, -1, size=1)).astype(np.float32))
+    return np.concatenate(codes), np.concatenate(scales)
+
+
+def test_headline_outer_update_d8_layer_vs_reference(ctx, reference):
+    """D = 8 (K = 256: fp16 operands, A through TMEM, B prescaled) on one full OPT-1.3B
+    decoder layer against the reference's allreduce_avg of the eight payloads."""
+    from paper_2506_21263_b200 import api, layouts
+    import torch
+    tbl = [x for x in _head_table() if x[0].startswith("layers.0.")]
+    shapes = [s for _, s in tbl]
+    t = Table(shapes)
+    L = api.Layout(ctx, tbl)
+    ranks = t.ranks(RANK)
+    cs = [_random_codes(t, ranks, 100 + w) for w in range(8)]
+    gathered = torch.cat([_payload(L, reference, t, ranks, c, s) for c, s in cs])
+    avg_ref = L.pack(reference.allreduce_avg(t, ranks, [c for c, _ in cs], [s for _, s in cs]))
+    assert torch.equal(api.allreduce_avg(L, gathered, 8, RANK, Q), avg_ref)
+    dg = _sync_delta(L, gathered, 8)
+    _check_recon(L, dg, avg_ref)
+    anchor, local, vel, pend = _rand_state(L, 7)
+    for classical in (False, True):
+        _check_epilogue(L, dg, anchor, local, vel, pend, gathered, 8, classical)
+
+
+@pytest.mark.parametrize("D", [1, 8])
+def test_full_opt13b_layout_outer_update(ctx, D):
+    """The whole OPT-1.3B layout (146 2-D + 242 1-D tensors, 1.316 G params): the fused
+    outer update (k_o5 chunk claiming over every tensor) vs the device fp64 allreduce_avg
+    (bit-exact with the reference above and in test_gpu_parity), per tensor; the epilogue
+    bit-exact at full scale."""
+    from paper_2506_21263_b200 import api, layouts
+    import torch
+    L = api.Layout(ctx, layouts.opt_1_3b())
+    pb = L.payload_bytes(RANK, Q)
+    seg = L.segments(RANK, Q)
+    g = torch.Generator(device="cuda").manual_seed(D)
+    pays = []
+    for w in range(D):
+        p = torch.randint(0, 256, (pb,), dtype=torch.uint8, device="cuda", generator=g)
+        host = p.cpu().numpy()
+        rng = np.random.default_rng(w)
+        for i, s in enumerate(L.shapes):
+            r = min(RANK, *s) if len(s) == 2 else 1
+            for col in ((2, 3) if len(s) == 2 else (2,)):
+                sc = (10.0 ** rng.uniform(-6, -1, size=r)).astype(np.float32)
+                host[seg[i, col]:seg[i, col] + 4 * r] = sc.view(np.uint8)
+        pays.append(torch.from_numpy(host).cuda())
+    gathered = torch.cat(pays)
+    avg = api.allreduce_avg(L, gathered, D, RANK, Q)
+    dg = _sync_delta(L, gathered, D)
+    _check_recon(L, dg, avg)
+    anchor, local, vel, pend = _rand_state(L, 11)
+    _check_epilogue(L, dg, anchor, local, vel, pend, gathered, D)
+    del anchor, local, vel, pend, avg, dg
+    torch.cuda.empty_cache()
+
+
+def test_headline_effective_rank_vs_reference(ctx, reference):
+    """r' of one 2048 x 2048 tensor (D = 4 gathered payloads, r = 32) vs the reference's
+    dense fp64 SVD (Gram -> Householder -> QL) of the averaged Delta, for three tau."""
+    from paper_2506_21263_b200 import api
+    import torch
+    shapes = [(2048, 2048)]
+    t = Table(shapes)
+    L = api.Layout(ctx, [("w", (2048, 2048))])
+    ranks = t.ranks(RANK)
+    D = 4
+    codes, scales, pays = [], [], []
+    for w in range(D):
+        # reference compress of low-rank + noise deltas (shared spectrum, worker noise)
+        d = _lowrank_noise(shapes, 40 + w, k=24, decay=0.85)
+        c = reference.compress(t, d, RANK, Q, 0, 2, reference.stream(1, 77))
+        codes.append(c["codes"]); scales.append(c["scales"])
+        pays.append(_payload(L, reference, t, ranks, c["codes"], c["scales"]))
+    avg = reference.allreduce_avg(t, ranks, codes, scales)
+    gathered = torch.cat(pays)
+    for tau in (0.3, 0.5, 0.9):
+        per, agg, allz = reference.effective_rank(t, avg, tau, RANK)
+        er = api.effective_rank(L, gathered, D, RANK, Q, tau, RANK)
+        assert [k for _, k in er.per_tensor] == per.tolist(), tau
+        assert er.aggregate == agg and er.all_zero == allz
+
+
+def test_engine_controller_applied_vs_reference(ctx, reference):
+    """OuterSync with the adaptive controller APPLIED (hold_rank=False) for 9 rounds against
+    the reference's round (orc_outer_round = collective_average + stage_deltas + Nesterov +
+    warm refresh, engine.cpp:215-276, 494-501) and the reference's own controller
+    (push_rank_window + adapt_compression, engine.cpp:476-487, 278-308). The schedule drops
+    r_t from r1 = 12 once the window fills, which forces a stochastic cold restart
+    (compress.cpp:161-164) with the speculative draw bases verified on the device. Each round
+    the reference starts from the engine's own state (anchor, velocity, pending delta, warm Q),
+    so the per-round map is compared at the tight bar and the schedule must match exactly."""
+    from paper_2506_21263_b200 import api
+    from paper_2506_21263_b200.engine import OuterConfig, OuterSync
+    shapes = [(96, 80), (80,), (128, 64), (64, 40), (40,), (48, 96)]
+    t = Table(shapes)
+    n = t.numel()
+    r1, c, H1 = 12, 3, 20
+    h_min = (H1 + 9) // 10
+    anchor0 = (np.float32(0.02) * reference.gaussian(reference.stream(7, 0), n)[0]).astype(np.float32)
+    local = (anchor0 - _lowrank_noise(shapes, 9, k=3, decay=0.5, noise=1e-6)).astype(np.float32)
+    L = api.Layout(ctx, [(f"t{i}", s) for i, s in enumerate(shapes)])
+    cfg = OuterConfig(rank1=r1, qbits=Q, power_iters=2, adaptive=True, window_c=c, tau=0.5,
+                      H1=H1, seed=1, overlap=True, hold_rank=False)
+    eng = OuterSync(L, cfg, L.pack(anchor0))
+    dlocal = L.pack(local)
+    rec = eng.step(dlocal)  # round 1: staging only (engine.cpp:473)
+    assert rec.r_t == r1
+    qmax = max(1, sum(s[1] * min(r1, *s) for s in shapes if len(s) == 2))
+    rank_t, window, ranks_seen = r1, [], []
+    for rnd in range(2, 11):
+        # the reference round starts from the engine's state
+        a0 = L.unpack(eng.anchor)
+        a, v = a0.copy(), L.unpack(eng.velocity)
+        pend = L.unpack(eng.pending)[None].copy()
+        wr = eng.warm_rank
+        wq = np.zeros(qmax, np.float32)
+        if wr:
+            flat = np.concatenate([f.reshape(-1) for f in
+                                   L.factors_from_device(eng.warm_q, wr, 1)]).astype(np.float32)
+            wq[:flat.size] = flat
+        rec = eng.step(dlocal)
+        out = reference.outer_round(t, 1, 1, rnd, rank_t, Q, 0, 2, True, 0.5, r1, 0.7, 0.9,
+                                    False, 1, a, v, pend, local[None].copy(), wr, wq)
+        assert rec.r_t == rank_t, (rnd, rec.r_t, rank_t)
+        assert rec.r_prime == out["r_prime"], (rnd, rec.r_prime, out["r_prime"])
+        assert abs(rec.comp_error - out["comp_error"]) <= 1e-2 * out["comp_error"], rnd
+        window = (window + [out["r_prime"]])[-c:]
+        rank_t, h_t = reference.adapt_compression(window, r1, H1, c, h_min)
+        assert (rec.r_next, rec.H_next) == (rank_t, h_t), rnd
+        ranks_seen.append(rec.r_t)
+        assert rel_fro(L.unpack(eng.anchor) - a0, a - a0) <= 1e-2, rnd
+        assert rel_fro(L.unpack(eng.velocity), v) <= 1e-2, rnd
+        assert rel_fro(L.unpack(eng.pending), pend[0]) <= 1e-2, rnd
+    assert ranks_seen[0] == r1 and ranks_seen[-1] < r1, ranks_seen  # a rank change happened

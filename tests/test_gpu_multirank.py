@@ -47,15 +47,19 @@ dist.destroy_process_group()
 '''
 
 
-def test_two_ranks_nccl_identical_state(tmp_path, oracle):
+@pytest.mark.parametrize("lib_nccl", ["1", "0"])
+def test_two_ranks_nccl_identical_state(tmp_path, oracle, lib_nccl):
+    """lib_nccl = 1: the exchange through the C-ABI (dlx_exchange, the library's own NCCL
+    communicator); 0: through torch.distributed."""
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     script = tmp_path / "worker.py"
     script.write_text(WORKER)
-    env = dict(os.environ, DLX_ROOT=ROOT, DLX_OUT=str(tmp_path))
+    env = dict(os.environ, DLX_ROOT=ROOT, DLX_OUT=str(tmp_path), DLX_LIB_NCCL=lib_nccl)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29531", str(script)]
+           "--master-addr", "127.0.0.1", "--master-port", str(29531 + int(lib_nccl)),
+           str(script)]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     res = [json.load(open(tmp_path / f"rank{k}.json")) for k in range(2)]
