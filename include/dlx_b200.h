@@ -142,7 +142,10 @@ dlx_status dlx_fill_gaussian(dlx_ctx* ctx, const dlx_layout* layout, float* d_ou
  * for warm_rank; used iff warm_rank == rank (compress.cpp:161). Writes the payload and
  * the float Q factors (next warm start, compress.hpp:86-90). *d_draws (nullable, device
  * uint64) receives the number of draws consumed (the reference advances its RngStream&
- * by exactly that). */
+ * by exactly that). Fully asynchronous: a cold start under stochastic rounding verifies its
+ * speculative draw offsets on the device (a CUDA-graph WHILE node redoes the compress body
+ * from the observed offsets; all-zero chunks draw nothing, compress.cpp:28-30); the
+ * (pathological) failure to converge is reported as *d_draws == UINT64_MAX. */
 dlx_status dlx_compress(dlx_ctx* ctx, const dlx_layout* layout, const float* d_delta, int rank,
                         int qbits, int rounding, int power_iters, uint64_t rng_state,
                         const float* d_warm_q, int warm_rank, uint8_t* d_payload,

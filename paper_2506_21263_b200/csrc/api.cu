@@ -110,6 +110,8 @@ std::vector<TimedLaunch> g_timed;  // recorded launches (events owned, destroyed
 
 KernelTimer::KernelTimer(const char* name, double bytes, cudaStream_t s) : stream(s) {
   if (!g_kernel_events) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) return;
   TimedLaunch t{name, bytes, nullptr, nullptr};
   DLX_CUDA(cudaEventCreate(&t.a));
   DLX_CUDA(cudaEventCreate(&t.b));
@@ -143,8 +145,8 @@ void* Plan::dev_alloc(size_t bytes) const {
 Plan::~Plan() {
   for (void* p : owned) cudaFree(p);
   void* ptrs[] = {d_t2, d_t1, d_chunks, d_streams, d_mats[0], d_mats[1], d_k1_tiles,
-                  d_k2_tiles, d_k2_part_off, d_k2_splits, d_k5_tiles, d_cold_base_spec[0],
-                  d_cold_base_spec[1], d_k1_rest, d_k2_rest, d_k5s_tiles};
+                  d_k2_tiles, d_k2_part_off, d_k2_splits, d_cold_base_spec[0],
+                  d_cold_base_spec[1], d_k1_rest, d_k2_rest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -157,6 +159,7 @@ static void validate_quant(int rank, int qbits) {
 static std::unique_ptr<Plan> build_plan(const dlx_layout& L, int rank, int qbits) {
   HostProf hp("build_plan");
   auto P = std::make_unique<Plan>();
+  P->layout = &L;
   P->rank = rank;
   P->qbits = qbits;
   int64_t cur = 0, poff = 0, qoff = 0;
@@ -311,17 +314,6 @@ static std::unique_ptr<Plan> build_plan(const dlx_layout& L, int rank, int qbits
           P->k2_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(j0), c0, s));
           if (!tc) P->k2_rest.push_back(P->k2_tiles.back());
         }
-    if (t.b % 4 == 0) {
-      for (int64_t n0 = 0; n0 < t.b; n0 += 128)
-        for (int64_t m0 = 0; m0 < t.a; m0 += 16)
-          P->k5s_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0),
-                                           static_cast<int>(n0), 0));
-    } else {
-      for (int64_t m0 = 0; m0 < t.a; m0 += 16)
-        for (int64_t n0 = 0; n0 < t.b; n0 += 128)
-          P->k5_tiles.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0),
-                                          static_cast<int>(n0), 0));
-    }
   }
   P->k2_part_elems = std::max<int64_t>(part, 32);
 
@@ -335,8 +327,6 @@ static std::unique_ptr<Plan> build_plan(const dlx_layout& L, int rank, int qbits
   P->d_k2_tiles = upload(P->k2_tiles);
   P->d_k2_part_off = upload(P->k2_part_off);
   P->d_k2_splits = upload(P->k2_splits);
-  P->d_k5_tiles = upload(P->k5_tiles);
-  P->d_k5s_tiles = upload(P->k5s_tiles);
   P->d_k1_rest = upload(P->k1_rest);
   P->d_k2_rest = upload(P->k2_rest);
   P->d_cold_base_spec[0] = upload(P->cold_base_spec[0]);
@@ -369,6 +359,7 @@ void* dlx_ctx::scratch(const std::string& name, size_t bytes, bool zero) {
 
 dlx_ctx::~dlx_ctx() {
   if (comm) dlx::destroy_comm(comm);
+  if (capture) cudaStreamDestroy(capture);
   for (auto& kv : arenas) cudaFree(kv.second.first);
   if (internal) cudaStreamDestroy(internal);
 }
@@ -605,6 +596,139 @@ dlx_status dlx_fill_gaussian(dlx_ctx* ctx, const dlx_layout* L, float* d_out,
   });
 }
 
+// ---- device-side verification of the speculative cold-start draw bases
+// A cold start (no usable warm Q, compress.cpp:161-164) draws each 2-D tensor's b*r initial
+// values right before its quantisation draws, so its offset depends on how many draws every
+// earlier chunk consumed — and all-zero chunks consume none (compress.cpp:28-30), which is
+// only known after the power iteration. The first pass speculates "no all-zero chunk"; the
+// quantiser's scan records the actual bases and a mismatch flag. A CUDA graph with a WHILE
+// node re-runs the compress body from the actual bases until they agree, entirely on the
+// device: no host synchronisation, so the round stays asynchronous across a rank change.
+// Non-convergence (more redo passes than 2-D tensors) sets *draws = UINT64_MAX.
+__global__ void k_cold_cond_init(cudaGraphConditionalHandle h, const int* mismatch, int* attempts) {
+  *attempts = 0;
+  cudaGraphSetConditional(h, *mismatch ? 1u : 0u);
+}
+__global__ void k_cold_cond(cudaGraphConditionalHandle h, const int* mismatch, int* attempts,
+                            int max_attempts, uint64_t* draws) {
+  unsigned again = *mismatch ? 1u : 0u;
+  if (again && ++*attempts > max_attempts) {
+    *draws = ~0ull;
+    again = 0u;
+  }
+  cudaGraphSetConditional(h, again);
+}
+__global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
+
+namespace {
+struct CompressBufs {
+  const float* delta;
+  float *pbuf, *ptmp, *qbuf, *qtmp, *part;
+  uint8_t* payload;
+  uint64_t* draws;
+  int* mismatch;
+  int64_t *base_actual, *base_try;
+  uint64_t* s0dev;
+  int* attempts;
+};
+
+// the compress body from the cold init on: cold-start Q0 at `bases`, power iteration,
+// quantise (writes mismatch / base_actual when cold)
+void compress_body(dlx_ctx* ctx, const Plan& P, const CompressBufs& B, int rounding, int iters,
+                   uint64_t s0, const uint64_t* s0p, bool cold, const int64_t* bases,
+                   cudaStream_t s) {
+  if (cold && !P.t2.empty()) {
+    launch_cold_init(P, B.qbuf, bases, s0, s, s0p);
+    orthonormalize_batched(ctx, P, 1, B.qbuf, B.qtmp, s);
+  }
+  for (int it = 0; it < iters; ++it) {
+    launch_k1(P, B.delta, B.qbuf, B.pbuf, s);
+    orthonormalize_batched(ctx, P, 0, B.pbuf, B.ptmp, s);
+    launch_k2(P, B.delta, B.pbuf, B.qbuf, B.part, s);
+    orthonormalize_batched(ctx, P, 1, B.qbuf, B.qtmp, s);
+  }
+  launch_k1(P, B.delta, B.qbuf, B.pbuf, s);
+  DLX_CUDA(cudaMemsetAsync(B.mismatch, 0, sizeof(int), s));
+  quantize_all(ctx, P, B.pbuf, B.qbuf, B.delta, rounding, s0, cold ? 1 : 0, bases, B.payload,
+               B.draws, B.mismatch, B.base_actual, s, s0p);
+}
+
+struct ColdRedo : PlanExt {
+  struct Entry {
+    std::vector<const void*> key;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<Entry> entries;
+  ~ColdRedo() override {
+    for (Entry& e : entries) {
+      if (e.exec) cudaGraphExecDestroy(e.exec);
+      if (e.graph) cudaGraphDestroy(e.graph);
+    }
+  }
+};
+
+cudaGraphExec_t cold_redo_graph(dlx_ctx* ctx, const Plan& P, const CompressBufs& B, int iters) {
+  ColdRedo& R = plan_ext<ColdRedo>(P, "cold_redo");
+  const std::vector<const void*> key = {B.delta, B.pbuf, B.ptmp, B.qbuf, B.qtmp, B.part,
+                                        B.payload, B.draws, B.mismatch, B.base_actual,
+                                        B.base_try, B.s0dev, B.attempts,
+                                        reinterpret_cast<const void*>(static_cast<intptr_t>(iters))};
+  for (auto& e : R.entries)
+    if (e.key == key) return e.exec;
+  HostProf hp("cold_redo_graph (new)");
+  if (R.entries.size() >= 4) {  // bounded: evict the oldest (wait for in-flight replays)
+    DLX_CUDA(cudaDeviceSynchronize());
+    cudaGraphExecDestroy(R.entries.front().exec);
+    cudaGraphDestroy(R.entries.front().graph);
+    R.entries.erase(R.entries.begin());
+  }
+  if (!ctx->capture) DLX_CUDA(cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking));
+  cudaStream_t cs = ctx->capture;
+  ColdRedo::Entry e;
+  e.key = key;
+  DLX_CUDA(cudaGraphCreate(&e.graph, 0));
+  cudaGraphConditionalHandle h;
+  DLX_CUDA(cudaGraphConditionalHandleCreate(&h, e.graph, 0, cudaGraphCondAssignDefault));
+  const uint64_t saved = dlx_take_launch_count();  // captured launches are not launches
+  // head: condition = first pass's mismatch
+  DLX_CUDA(cudaStreamBeginCaptureToGraph(cs, e.graph, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed));
+  k_cold_cond_init<<<1, 1, 0, cs>>>(h, B.mismatch, B.attempts);
+  DLX_CUDA(cudaGetLastError());
+  cudaGraph_t g2 = nullptr;
+  DLX_CUDA(cudaStreamEndCapture(cs, &g2));
+  size_t n = 0;
+  DLX_CUDA(cudaGraphGetNodes(e.graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  DLX_CUDA(cudaGraphGetNodes(e.graph, nodes.data(), &n));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  DLX_CUDA(cudaGraphAddNode(&wnode, e.graph, nodes.data(), n, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  // body: redo from the observed bases, then re-evaluate
+  DLX_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed));
+  DLX_CUDA(cudaMemcpyAsync(B.base_try, B.base_actual, sizeof(int64_t) * P.t2.size(),
+                           cudaMemcpyDeviceToDevice, cs));
+  compress_body(ctx, P, B, 0, iters, 0, B.s0dev, true, B.base_try, cs);
+  k_cold_cond<<<1, 1, 0, cs>>>(h, B.mismatch, B.attempts, static_cast<int>(P.t2.size()) + 2,
+                               B.draws);
+  DLX_CUDA(cudaGetLastError());
+  cudaGraph_t b2 = nullptr;
+  DLX_CUDA(cudaStreamEndCapture(cs, &b2));
+  DLX_CUDA(cudaGraphInstantiate(&e.exec, e.graph, 0));
+  dlx_take_launch_count();
+  count_launch(static_cast<int>(saved));
+  R.entries.push_back(e);
+  return R.entries.back().exec;
+}
+}  // namespace
+
 static void run_compress(dlx_ctx* ctx, dlx_layout* L, const float* d_delta, int rank, int qbits,
                          int rounding, int iters, uint64_t s0, const float* d_warm_q,
                          int warm_rank, uint8_t* d_payload, float* d_q_out, uint64_t* d_draws,
@@ -615,49 +739,38 @@ static void run_compress(dlx_ctx* ctx, dlx_layout* L, const float* d_delta, int 
   if (rounding != 0 && rounding != 1) raise(DLX_ERR_VALIDATION, "unknown rounding mode");
   if (!d_delta || !d_payload) raise(DLX_ERR_VALIDATION, "null buffer");
   Plan& P = L->plan(rank, qbits);
-  float* pbuf = static_cast<float*>(ctx->scratch("pbuf", sizeof(float) * P.pelems));
-  float* ptmp = static_cast<float*>(ctx->scratch("ptmp", sizeof(float) * P.pelems));
-  float* qtmp = static_cast<float*>(ctx->scratch("qtmp", sizeof(float) * P.qelems));
-  float* qbuf = d_q_out ? d_q_out : static_cast<float*>(ctx->scratch("qbuf", sizeof(float) * P.qelems));
-  float* part = static_cast<float*>(ctx->scratch("k2part", sizeof(float) * P.k2_part_elems));
-  uint64_t* draws = d_draws ? d_draws : static_cast<uint64_t*>(ctx->scratch("draws", 8));
-  int* mismatch = static_cast<int*>(ctx->scratch("mismatch", sizeof(int)));
+  CompressBufs B{};
+  B.delta = d_delta;
+  B.pbuf = static_cast<float*>(ctx->scratch("pbuf", sizeof(float) * P.pelems));
+  B.ptmp = static_cast<float*>(ctx->scratch("ptmp", sizeof(float) * P.pelems));
+  B.qtmp = static_cast<float*>(ctx->scratch("qtmp", sizeof(float) * P.qelems));
+  B.qbuf = d_q_out ? d_q_out : static_cast<float*>(ctx->scratch("qbuf", sizeof(float) * P.qelems));
+  B.part = static_cast<float*>(ctx->scratch("k2part", sizeof(float) * P.k2_part_elems));
+  B.payload = d_payload;
+  // the draw count lands in a context buffer (a stable address for the redo graph) and is
+  // copied out to the caller's at the end
+  B.draws = static_cast<uint64_t*>(ctx->scratch("draws", 8));
+  B.mismatch = static_cast<int*>(ctx->scratch("mismatch", sizeof(int)));
   const size_t nb = std::max<size_t>(P.t2.size(), 1);
-  int64_t* base_actual = static_cast<int64_t*>(ctx->scratch("cold_actual", 8 * nb));
-  int64_t* base_try = static_cast<int64_t*>(ctx->scratch("cold_try", 8 * nb));
+  B.base_actual = static_cast<int64_t*>(ctx->scratch("cold_actual", 8 * nb));
+  B.base_try = static_cast<int64_t*>(ctx->scratch("cold_try", 8 * nb));
+  B.s0dev = static_cast<uint64_t*>(ctx->scratch("cold_s0", 8));
+  B.attempts = static_cast<int*>(ctx->scratch("cold_attempts", sizeof(int)));
   const bool cold = !(d_warm_q && warm_rank == rank);
-  if (!cold && d_warm_q != qbuf)
-    DLX_CUDA(cudaMemcpyAsync(qbuf, d_warm_q, sizeof(float) * P.qelems, cudaMemcpyDeviceToDevice, s));
-  const int64_t* bases = P.d_cold_base_spec[rounding == 0 ? 0 : 1];
-  for (int attempt = 0;; ++attempt) {
-    if (cold && !P.t2.empty()) {
-      launch_cold_init(P, qbuf, bases, s0, s);
-      orthonormalize_batched(ctx, P, 1, qbuf, qtmp, s);
-    }
-    for (int it = 0; it < iters; ++it) {
-      launch_k1(P, d_delta, qbuf, pbuf, s);
-      orthonormalize_batched(ctx, P, 0, pbuf, ptmp, s);
-      launch_k2(P, d_delta, pbuf, qbuf, part, s);
-      orthonormalize_batched(ctx, P, 1, qbuf, qtmp, s);
-    }
-    launch_k1(P, d_delta, qbuf, pbuf, s);
-    DLX_CUDA(cudaMemsetAsync(mismatch, 0, sizeof(int), s));
-    quantize_all(ctx, P, pbuf, qbuf, d_delta, rounding, s0, cold ? 1 : 0, bases, d_payload,
-                 draws, mismatch, base_actual, s);
-    // Cold start under stochastic rounding assumed no all-zero chunk before each tensor's
-    // init draws; verify and redo with the observed bases if that was wrong (rare:
-    // all-zero tensors). Bases converge tensor by tensor.
-    if (!(cold && rounding == 0) || P.t2.empty()) break;
-    int h_mis = 0;
-    HostProf hw("compress.cold_verify_wait");
-    DLX_CUDA(cudaMemcpyAsync(&h_mis, mismatch, sizeof(int), cudaMemcpyDeviceToHost, s));
-    DLX_CUDA(cudaStreamSynchronize(s));
-    if (!h_mis) break;
-    if (attempt > static_cast<int>(P.t2.size()) + 1)
-      raise(DLX_ERR_NUMERIC, "compress: cold-start draw offsets did not converge");
-    DLX_CUDA(cudaMemcpyAsync(base_try, base_actual, 8 * P.t2.size(), cudaMemcpyDeviceToDevice, s));
-    bases = base_try;
+  if (!cold && d_warm_q != B.qbuf)
+    DLX_CUDA(cudaMemcpyAsync(B.qbuf, d_warm_q, sizeof(float) * P.qelems, cudaMemcpyDeviceToDevice, s));
+  compress_body(ctx, P, B, rounding, iters, s0, nullptr, cold,
+                P.d_cold_base_spec[rounding == 0 ? 0 : 1], s);
+  // Nearest rounding draws nothing while quantising, so its cold bases are exact; the
+  // stochastic bases are verified (and the body redone) on the device
+  if (cold && rounding == 0 && !P.t2.empty()) {
+    cudaGraphExec_t g = cold_redo_graph(ctx, P, B, iters);
+    k_set_u64<<<1, 1, 0, s>>>(B.s0dev, s0);
+    DLX_LAUNCHED();
+    DLX_CUDA(cudaGraphLaunch(g, s));
+    count_launch(2);
   }
+  if (d_draws) DLX_CUDA(cudaMemcpyAsync(d_draws, B.draws, 8, cudaMemcpyDeviceToDevice, s));
 }
 
 dlx_status dlx_compress(dlx_ctx* ctx, const dlx_layout* layout, const float* d_delta, int rank,

@@ -23,6 +23,11 @@ struct Error {
 };
 struct Comm;  // comm.cu: NCCL communicator + exchange stream of a context
 void destroy_comm(Comm* c);
+// Derived state owned by a Plan (per rank) or by a layout (rank-independent tables), freed
+// with its owner (no address-keyed global caches).
+struct PlanExt {
+  virtual ~PlanExt() = default;
+};
 [[noreturn]] void raise(dlx_status code, const std::string& msg);
 void set_last_error(const std::string& msg);  // dlx_last_error() of the calling thread
 // Runs f, mapping a thrown Error to its status code (and the message to dlx_last_error).
@@ -153,6 +158,7 @@ struct dlx_ctx {
   int device = 0;
   cudaStream_t internal = nullptr;
   dlx::Comm* comm = nullptr;  // dlx_comm_init (worker sync); null = single worker
+  cudaStream_t capture = nullptr;  // private stream for CUDA-graph captures (cold-start redo)
   // grow-only scratch arenas
   std::map<std::string, std::pair<void*, size_t>> arenas;
   void* scratch(const std::string& name, size_t bytes, bool zero = false);
@@ -168,6 +174,9 @@ struct dlx_layout {
   int64_t slab = 0;
   std::map<std::pair<int, int>, std::unique_ptr<dlx::Plan>> plans;
   void* d_spans = nullptr;  // staging-kernel tensor table (device), freed with the layout
+  // rank-independent derived tables (work lists that every plan of this layout shares, so a
+  // rank change under the adaptive schedule does not rebuild them)
+  std::map<std::string, std::unique_ptr<dlx::PlanExt>> ext;
   dlx::Plan& plan(int rank, int qbits);
   ~dlx_layout() {
     if (d_spans) cudaFree(d_spans);
@@ -177,14 +186,10 @@ struct dlx_layout {
 
 namespace dlx {
 
-// Derived per-plan state (tile tables, tensor-map caches) owned by the Plan; its device
-// buffers come from Plan::dev_alloc and are freed with the plan (no address-keyed caches).
-struct PlanExt {
-  virtual ~PlanExt() = default;
-};
 
 // Host + device description of (layout, rank, qbits).
 struct Plan {
+  const dlx_layout* layout = nullptr;  // the owning layout (layout_ext tables)
   int rank = 0, qbits = 0;
   std::vector<DevT2> t2;
   std::vector<DevT1> t1;
@@ -216,10 +221,6 @@ struct Plan {
   std::vector<int4> k1_rest, k2_rest;  // SIMT tiles of tensors outside the tcgen05 path
   int4* d_k1_rest = nullptr;
   int4* d_k2_rest = nullptr;
-  std::vector<int4> k5_tiles;   // (t2 slot, m0, n0, -): register kernel (b % 4 != 0)
-  int4* d_k5_tiles = nullptr;
-  std::vector<int4> k5s_tiles;  // streamed persistent kernel, column-block-major order
-  int4* d_k5s_tiles = nullptr;
   // speculative cold-start draw bases per 2-D slot, [0] stochastic (assumes no all-zero
   // chunk), [1] nearest (exact: quantisation draws nothing)
   std::vector<int64_t> cold_base_spec[2];
@@ -230,6 +231,15 @@ struct Plan {
   void* dev_alloc(size_t bytes) const;  // cudaMalloc, freed in ~Plan
   ~Plan();
 };
+
+// Typed layout-level ext slot (see dlx_layout::ext).
+template <class T>
+T& layout_ext(const dlx_layout& L, const std::string& key, bool* fresh = nullptr) {
+  auto& e = const_cast<dlx_layout&>(L).ext[key];
+  if (fresh) *fresh = !e;
+  if (!e) e.reset(new T());
+  return *static_cast<T*>(e.get());
+}
 
 // Typed ext slot: created empty (default-constructed) on first use; *fresh tells the caller.
 template <class T>
@@ -308,8 +318,9 @@ T* plan_upload(const Plan& P, const std::vector<T>& v, size_t min_elems = 0) {
 // Kernel launchers (csrc/*.cu)
 void launch_fill_gaussian(const dlx_layout& L, float* out, const float* base, float scale,
                           uint64_t seed, uint64_t tag, uint64_t worker, cudaStream_t s);
+// s0p (nullable): read the stream state from device memory instead of s0 (graph replays)
 void launch_cold_init(const Plan& P, float* q, const int64_t* d_cold_base, uint64_t s0,
-                      cudaStream_t s);
+                      cudaStream_t s, const uint64_t* s0p = nullptr);
 void launch_k1(const Plan& P, const float* slab, const float* q, float* y, cudaStream_t s);
 bool tc_supported(const Plan& P);
 bool tc_eligible(const DevT2& t);
@@ -336,7 +347,8 @@ void orthonormalize_batched(dlx_ctx* ctx, const Plan& P, int side, float* buf, f
 void quantize_all(dlx_ctx* ctx, const Plan& P, const float* pbuf, const float* qbuf,
                   const float* slab, int rounding, uint64_t s0, int cold,
                   const int64_t* d_cold_base_used, uint8_t* payload, uint64_t* d_draws,
-                  int* d_mismatch, int64_t* d_cold_base_actual, cudaStream_t s);
+                  int* d_mismatch, int64_t* d_cold_base_actual, cudaStream_t s,
+                  const uint64_t* s0p = nullptr);
 void dequant_factors(const Plan& P, int D, const uint8_t* gathered, int64_t pay_bytes,
                      float* phat, float* qhat, int64_t lda_tot, cudaStream_t s);
 // Slot ranges of one outer-update call: 2-D slots [s0, s1), 1-D slots [u0, u1) (the tensors

@@ -512,7 +512,9 @@ SlotRange slot_range(const Plan& P, int t_begin, int t_end) {
   return R;
 }
 
-// SIMT K5 tiles of a slot range (the plan's full lists when the range is the whole layout)
+// SIMT K5 tiles of a slot range, built on first use of the SIMT outer update (the tcgen05
+// path never needs them): (t2 slot, m0, n0, -); the streamed kernel's list is
+// column-block-major, the register kernel's (b % 4 != 0) row-block-major.
 struct K5RangeTiles : PlanExt {
   std::vector<int4> k5s, k5;
   int4* d_k5s = nullptr;
@@ -551,26 +553,28 @@ void launch_outer_2d_impl(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gat
                        gamma, beta, classical, stats, R, s);
     return;
   }
-  const std::vector<int4>* k5s_tiles = &P.k5s_tiles;
-  const std::vector<int4>* k5_tiles = &P.k5_tiles;
-  const int4* d_k5s_tiles = P.d_k5s_tiles;
-  const int4* d_k5_tiles = P.d_k5_tiles;
-  if (!R.full(P)) {
-    bool fresh = false;
-    K5RangeTiles& T = plan_ext<K5RangeTiles>(P, "k5_range:" + R.key(), &fresh);
-    if (fresh) {
-      for (const int4& t : P.k5s_tiles)
-        if (t.x >= R.s0 && t.x < R.s1) T.k5s.push_back(t);
-      for (const int4& t : P.k5_tiles)
-        if (t.x >= R.s0 && t.x < R.s1) T.k5.push_back(t);
-      T.d_k5s = plan_upload(P, T.k5s);
-      T.d_k5 = plan_upload(P, T.k5);
+  bool fresh = false;
+  K5RangeTiles& T = plan_ext<K5RangeTiles>(P, "k5_range:" + R.key(), &fresh);
+  if (fresh) {
+    for (int k = R.s0; k < R.s1; ++k) {
+      const DevT2& t = P.t2[k];
+      if (t.b % 4 == 0) {
+        for (int64_t n0 = 0; n0 < t.b; n0 += 128)
+          for (int64_t m0 = 0; m0 < t.a; m0 += 16)
+            T.k5s.push_back(make_int4(k, static_cast<int>(m0), static_cast<int>(n0), 0));
+      } else {
+        for (int64_t m0 = 0; m0 < t.a; m0 += 16)
+          for (int64_t n0 = 0; n0 < t.b; n0 += 128)
+            T.k5.push_back(make_int4(k, static_cast<int>(m0), static_cast<int>(n0), 0));
+      }
     }
-    k5s_tiles = &T.k5s;
-    k5_tiles = &T.k5;
-    d_k5s_tiles = T.d_k5s;
-    d_k5_tiles = T.d_k5;
+    T.d_k5s = plan_upload(P, T.k5s);
+    T.d_k5 = plan_upload(P, T.k5);
   }
+  const std::vector<int4>* k5s_tiles = &T.k5s;
+  const std::vector<int4>* k5_tiles = &T.k5;
+  const int4* d_k5s_tiles = T.d_k5s;
+  const int4* d_k5_tiles = T.d_k5;
   float* phat = static_cast<float*>(ctx->scratch("phat", sizeof(float) * P.pelems * D));
   float* qhat = static_cast<float*>(ctx->scratch("qhat", sizeof(float) * P.qelems * D));
   dequant_factors(P, D, gathered, P.payload_bytes, phat, qhat, 0, s);

@@ -757,14 +757,14 @@ struct O5State : PlanExt {
   int nbr = 0;             // B ring slots (bf16 path)
   int a_mode = 0;          // fp16 path: A-box issuer / early drain (see k_o5)
   size_t smem = 0;
-  std::vector<int4> rows;
-  int4* d_rows = nullptr;
+  int nrows = 0;
+  const int4* d_rows = nullptr;  // layout-owned (O5Tables)
   std::vector<int64_t> aoff, boff;  // per slot: element offsets of A [lda][KA], B [ldb][KA]
   int64_t a_elems = 0, b_elems = 0;
   int64_t params = 0;  // 2-D parameters covered
   int s0 = 0, s1 = 0;  // slot range
-  std::vector<int4> bands;  // (t2 slot, m0, first column, columns) in claim order
-  int4* d_bands = nullptr;
+  int nbands = 0;
+  const int4* d_bands = nullptr;  // (t2 slot, m0, first column, columns), claim order
   int* d_ctr = nullptr;
   int64_t* d_aoff = nullptr;
   int64_t* d_boff = nullptr;
@@ -782,6 +782,45 @@ bool o5_eligible(const Plan& P, int D, int self_index) {
     for (const DevT2& t : P.t2)
       if (t.r % ks != 0) return false;  // own-payload k steps must align with the MMA K
   return true;
+}
+
+// Rank-independent work lists of one slot range: row bands (128 rows x `chunk` columns, claimed
+// in band-major order) and the factor rows k_o5_prep converts. Owned by the layout.
+struct O5Tables : PlanExt {
+  std::vector<int4> bands, rows;
+  int4* d_bands = nullptr;
+  int4* d_rows = nullptr;
+  int64_t params = 0;
+  ~O5Tables() override {
+    if (d_bands) cudaFree(d_bands);
+    if (d_rows) cudaFree(d_rows);
+  }
+};
+
+static const O5Tables& o5_tables(const Plan& P, const SlotRange& R, int64_t chunk) {
+  bool fresh = false;
+  O5Tables& W = layout_ext<O5Tables>(*P.layout, "o5tab:" + R.key() + ":" + std::to_string(chunk),
+                                     &fresh);
+  if (!fresh) return W;
+  HostProf hp("o5_tables (new)");
+  for (int k = R.s0; k < R.s1; ++k) {
+    const DevT2& t = P.t2[k];
+    for (int64_t m0 = 0; m0 < t.a; m0 += 128)
+      for (int64_t n0 = 0; n0 < t.b; n0 += chunk)
+        W.bands.push_back(make_int4(k, static_cast<int>(m0), static_cast<int>(n0),
+                                    static_cast<int>(std::min(chunk, t.b - n0))));
+    for (int side = 0; side < 2; ++side) {
+      const int64_t ld = side == 0 ? t.lda : t.ldb;
+      for (int64_t r = 0; r < ld; ++r) W.rows.push_back(make_int4(k, side, static_cast<int>(r), 0));
+    }
+    W.params += t.a * t.b;
+  }
+  for (auto* v : {&W.bands, &W.rows}) {
+    int4*& d = v == &W.bands ? W.d_bands : W.d_rows;
+    DLX_CUDA(cudaMalloc(&d, sizeof(int4) * std::max<size_t>(v->size(), 1)));
+    upload_now(d, v->data(), sizeof(int4) * v->size());
+  }
+  return W;
 }
 
 static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
@@ -852,28 +891,21 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   const int64_t chunk = chunk_env ? chunk_env
                         : S.bf ? (nkc >= 4 ? 192 : 128)
                                : (S.nab == 2 ? 128 : 256);
+  // the band / row work lists do not depend on the rank: shared by every plan of the layout
+  const O5Tables& W = o5_tables(P, R, chunk);
+  S.nbands = static_cast<int>(W.bands.size());
+  S.nrows = static_cast<int>(W.rows.size());
+  S.d_bands = W.d_bands;
+  S.d_rows = W.d_rows;
+  S.params = W.params;
   for (size_t k = 0; k < P.t2.size(); ++k) {
     const DevT2& t = P.t2[k];
-    const bool in = static_cast<int>(k) >= R.s0 && static_cast<int>(k) < R.s1;
-    if (in) {
-      for (int64_t m0 = 0; m0 < t.a; m0 += 128)
-        for (int64_t n0 = 0; n0 < t.b; n0 += chunk)
-          S.bands.push_back(make_int4(static_cast<int>(k), static_cast<int>(m0),
-                                      static_cast<int>(n0), static_cast<int>(std::min(chunk, t.b - n0))));
-      for (int side = 0; side < 2; ++side) {
-        const int64_t ld = side == 0 ? t.lda : t.ldb;
-        for (int64_t r = 0; r < ld; ++r) S.rows.push_back(make_int4(static_cast<int>(k), side, static_cast<int>(r), 0));
-      }
-      S.params += t.a * t.b;
-    }
     S.aoff.push_back(S.a_elems);
     S.boff.push_back(S.b_elems);
     S.a_elems += t.lda * S.KA;
     S.b_elems += t.ldb * S.KA;
   }
-  S.d_bands = plan_upload(P, S.bands, 1);
   S.d_ctr = static_cast<int*>(P.dev_alloc(sizeof(int)));
-  S.d_rows = plan_upload(P, S.rows, 1);
   S.d_aoff = plan_upload(P, S.aoff, 1);
   S.d_boff = plan_upload(P, S.boff, 1);
   return S;
@@ -896,7 +928,7 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
                         int classical, dlx_round_stats* stats, const SlotRange& R,
                         cudaStream_t s) {
   O5State& S = o5_state(P, D, R);
-  if (S.bands.empty()) return;
+  if (S.nbands == 0) return;
   const int KA = S.KA;
   const size_t es = S.bf ? 2 : 4;
   void* A = ctx->scratch("o5_A", es * (S.a_elems + 1024));
@@ -912,12 +944,12 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
     DLX_LAUNCHED();
   }
   if (S.bf)
-    k_o5_prep<true><<<static_cast<unsigned>(ceil_div(S.rows.size(), prep_rows<true>())), 256, 0, s>>>(
-        P.d_t2, S.d_rows, static_cast<int>(S.rows.size()), S.d_aoff, S.d_boff, gathered,
+    k_o5_prep<true><<<static_cast<unsigned>(ceil_div(S.nrows, prep_rows<true>())), 256, 0, s>>>(
+        P.d_t2, S.d_rows, S.nrows, S.d_aoff, S.d_boff, gathered,
         P.payload_bytes, P.qbits, D, KA, pre, A, B[0], B[1]);
   else
-    k_o5_prep<false><<<static_cast<unsigned>(ceil_div(S.rows.size(), prep_rows<false>())), 256, 0, s>>>(
-        P.d_t2, S.d_rows, static_cast<int>(S.rows.size()), S.d_aoff, S.d_boff, gathered,
+    k_o5_prep<false><<<static_cast<unsigned>(ceil_div(S.nrows, prep_rows<false>())), 256, 0, s>>>(
+        P.d_t2, S.d_rows, S.nrows, S.d_aoff, S.d_boff, gathered,
         P.payload_bytes, P.qbits, D, KA, pre, A, B[0], B[1]);
   DLX_LAUNCHED();
   const void* key[8] = {pending, anchor, velocity, mode == DLX_MODE_OVERLAPPED ? local : nullptr,
@@ -943,7 +975,7 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   int dev = 0, sms = 0;
   DLX_CUDA(cudaGetDevice(&dev));
   DLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int nbands = static_cast<int>(S.bands.size());
+  const int nbands = S.nbands;
   const int grid = std::min(nbands, sms);
   DLX_CUDA(cudaMemsetAsync(S.d_ctr, 0, sizeof(int), s));
   // algorithmic bytes: read pending, anchor, velocity (+ local in overlapped mode), write

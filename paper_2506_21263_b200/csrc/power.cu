@@ -59,7 +59,9 @@ void launch_fill_gaussian(const dlx_layout& L, float* out, const float* base, fl
 // --------------------------------------------------------------- cold start (compress.cpp:64-69)
 // Q0 = uniform(-1, 1)^{b x r} row-major from the shared stream at the tensor's draw base,
 // stored column-major. Value = lo + (hi - lo) * u with separate roundings (rng.hpp:39).
-__global__ void k_cold_init(const DevT2* T, int nt2, float* q, const int64_t* bases, uint64_t s0) {
+__global__ void k_cold_init(const DevT2* T, int nt2, float* q, const int64_t* bases, uint64_t s0,
+                            const uint64_t* s0p) {
+  if (s0p) s0 = *s0p;
   const int k = blockIdx.y;
   const DevT2 t = T[k];
   const int64_t total = t.b * t.r;
@@ -73,12 +75,13 @@ __global__ void k_cold_init(const DevT2* T, int nt2, float* q, const int64_t* ba
 }
 
 void launch_cold_init(const Plan& P, float* q, const int64_t* d_bases, uint64_t s0,
-                      cudaStream_t s) {
+                      cudaStream_t s, const uint64_t* s0p) {
   if (P.t2.empty()) return;
   int64_t mx = 1;
   for (const DevT2& t : P.t2) mx = std::max(mx, t.b * t.r);
   const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 512));
-  k_cold_init<<<dim3(gx, P.t2.size()), 256, 0, s>>>(P.d_t2, (int)P.t2.size(), q, d_bases, s0);
+  k_cold_init<<<dim3(gx, P.t2.size()), 256, 0, s>>>(P.d_t2, (int)P.t2.size(), q, d_bases, s0,
+                                                   s0p);
   DLX_LAUNCHED();
 }
 

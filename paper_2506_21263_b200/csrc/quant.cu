@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(256) k_quant_pack(const DevStream* __restrict_
                                                     const float* __restrict__ q,
                                                     const float* __restrict__ slab, int qbits,
                                                     int stochastic, uint64_t s0,
+                                                    const uint64_t* __restrict__ s0p,
                                                     uint8_t* __restrict__ payload) {
+  if (s0p) s0 = *s0p;
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ngroups) return;
   int lo = 0, hi = nstreams - 1;  // last stream with group0 <= g
@@ -182,7 +184,8 @@ __global__ void __launch_bounds__(256) k_quant_pack(const DevStream* __restrict_
 void quantize_all(dlx_ctx* ctx, const Plan& P, const float* pbuf, const float* qbuf,
                   const float* slab, int rounding, uint64_t s0, int cold,
                   const int64_t* d_cold_base_used, uint8_t* payload, uint64_t* d_draws,
-                  int* d_mismatch, int64_t* d_cold_base_actual, cudaStream_t s) {
+                  int* d_mismatch, int64_t* d_cold_base_actual, cudaStream_t s,
+                  const uint64_t* s0p) {
   HostProf hp_("quantize_all");
   const int nc = static_cast<int>(P.chunks.size());
   if (nc == 0) {
@@ -202,7 +205,7 @@ void quantize_all(dlx_ctx* ctx, const Plan& P, const float* pbuf, const float* q
   const int64_t ng = P.ngroups;
   k_quant_pack<<<static_cast<unsigned>(ceil_div(ng, 256)), 256, 0, s>>>(
       P.d_streams, static_cast<int>(P.streams.size()), ng, base, inv, cmax, pbuf, qbuf, slab,
-      P.qbits, stochastic, s0, payload);
+      P.qbits, stochastic, s0, s0p, payload);
   DLX_LAUNCHED();
 }
 

@@ -38,7 +38,7 @@ def _run(exe, args, out):
 CASES = {
     # adaptive on: r' ~ 2 drives r_t from 8 down once the window fills (cold restarts)
     "overlap_q4_adaptive": dict(mode="dilocox", D=1, act="tanh", q=4, rounding="stochastic",
-                                adaptive=1, steps=60, H1=5),
+                                adaptive=1, window=3, steps=40, H1=5),
     "overlap_D2_threads_q8": dict(mode="dilocox", D=2, act="relu", q=8, rounding="nearest",
                                   adaptive=0, steps=40, H1=5, threads=2),
     "sync_D2_q8": dict(mode="dilocox-no-overlap", D=2, act="tanh", q=8, rounding="stochastic",

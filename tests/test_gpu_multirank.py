@@ -88,3 +88,67 @@ def test_two_ranks_nccl_identical_state(tmp_path, oracle, lib_nccl):
     assert rel_fro(a0 - anchor0, a - anchor0) <= 1e-2
     for k in range(2):
         assert rel_fro(np.array(res[k]["pend"], np.float32), pend[k]) <= 1e-2
+
+
+PY_WORKER = r'''
+import json, os, sys
+sys.path.insert(0, os.environ["DLX_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+from paper_2506_21263_b200 import api, layouts
+from paper_2506_21263_b200.engine import OuterConfig, OuterSync
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("nccl", device_id=torch.device(f"cuda:{rank}"))
+ctx = api.Context(rank)
+L = api.Layout(ctx, layouts.mini_opt())
+anchor = L.empty()
+api.fill_gaussian(L, anchor, 0.02, seed=7, tag=0xA7C4, worker=0)
+local = L.empty()
+api.fill_gaussian(L, local, -1e-3, seed=1, tag=0xDA7A, worker=rank, base=anchor)
+cfg = OuterConfig(rank1=8, qbits=4, power_iters=2, adaptive=True, window_c=5, H1=125, seed=1,
+                  overlap=True, hold_rank=False)
+eng = OuterSync(L, cfg, anchor, world=world, rank=rank)
+recs = [eng.step(local) for _ in range(4)]
+torch.cuda.synchronize()
+L.unpack(eng.anchor).tofile(os.path.join(os.environ["DLX_OUT"], f"py{rank}.bin"))
+json.dump([r.r_prime for r in recs], open(os.path.join(os.environ["DLX_OUT"], f"py{rank}.json"), "w"))
+dist.barrier()
+dist.destroy_process_group()
+'''
+
+
+def test_cpp_worker_processes_match_python_engine(tmp_path):
+    """A pure C++ host (cpp/worker_main: one process per GPU, NCCL bootstrapped from a file,
+    everything through the C-ABI — dlx_ctx_create_dist, dlx_compress, dlx_exchange,
+    dlx_effective_rank, dlx_outer_update, dlx_adapt_compression) on the SURVEY C1 layout:
+    both ranks end with bitwise-identical anchors, and the result is bitwise identical to the
+    Python engine (OuterSync over torchrun) on the same inputs — the same kernels in the
+    same order, whichever host drives them (the Python engine is checked against the
+    reference in test_gpu_engine / test_gpu_headline)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    exe = os.path.join(ROOT, "cpp", "_build", "worker_main")
+    if not os.path.exists(exe):
+        pytest.skip("cpp/_build/worker_main not built")
+    uid = tmp_path / "uid"
+    procs = [subprocess.Popen([exe, str(r), "2", str(r), str(uid), str(tmp_path / f"cpp{r}"),
+                               "4", "8", "4", "1"], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for r in range(2)]
+    for p in procs:
+        out, err = p.communicate(timeout=600)
+        assert p.returncode == 0, err[-3000:]
+    c0 = np.fromfile(tmp_path / "cpp0.bin", dtype=np.float32)
+    c1 = np.fromfile(tmp_path / "cpp1.bin", dtype=np.float32)
+    assert np.array_equal(c0, c1), "C++ workers disagree"
+    script = tmp_path / "pyworker.py"
+    script.write_text(PY_WORKER)
+    env = dict(os.environ, DLX_ROOT=ROOT, DLX_OUT=str(tmp_path))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    p0 = np.fromfile(tmp_path / "py0.bin", dtype=np.float32)
+    assert np.array_equal(p0, c0), "C++ host and Python host disagree"
+    rp_cpp = [int(line.split()[2]) for line in open(tmp_path / "cpp0.txt")]
+    assert rp_cpp == json.load(open(tmp_path / "py0.json"))

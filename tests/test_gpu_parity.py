@@ -560,3 +560,30 @@ def test_adamw_step_bitexact(ctx, oracle):
     g[5] = np.inf
     with pytest.raises(NumericError):
         api.adamw_step(ctx, st, dp, torch.from_numpy(g).cuda(), raise_nonfinite=True)
+
+
+@pytest.mark.parametrize("q", [2, 4, 8])
+def test_cold_start_zero_tensors_verified_on_device(ctx, oracle, q):
+    """Cold start under stochastic rounding with all-zero tensors interleaved (they draw
+    nothing, compress.cpp:28-30, so every later tensor's cold-init offset moves): the
+    speculative offsets are corrected by the device-side redo (CUDA-graph WHILE node) —
+    draws consumed and codes must equal the reference's; twice in a row (graph replay)."""
+    from paper_2506_21263_b200 import api
+    shapes = [(20, 16), (16,), (30, 24), (24,), (12, 40), (40, 10), (9,), (33, 17)]
+    zero = {0, 1, 4, 6}
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    parts = []
+    for i, s in enumerate(shapes):
+        n = int(np.prod(s))
+        parts.append(np.zeros(n, np.float32) if i in zero else
+                     oracle.gaussian(oracle.stream(i, 31), n)[0])
+    flat = np.concatenate(parts).astype(np.float32)
+    for rep in range(2):
+        st0 = oracle.stream(3, 100 + rep)
+        ref = oracle.compress(t, flat, 6, q, 0, 2, st0)
+        res = api.compress(L, L.pack(flat), 6, api.QuantSpec(q, 0), None, 0, 2, st0)
+        assert int(res.draws.item()) == draws_between(st0, ref["state"])
+        codes, scales = decode_payload(L, res.payload, 6, q)
+        assert (codes == ref["codes"]).mean() >= 0.999
+        assert np.allclose(scales, ref["scales"], rtol=1e-5, atol=0)
