@@ -29,9 +29,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "outer-sync ms/round & params/s (compress→allreduce→Nesterov), 1/2/4/8 GPU"
-# bounded CPU sample: a 512-row slab of an OPT-1.3B 2048x2048 attention-projection delta
-# plus its 2048 bias (1 050 624 params), full reference round with the adaptive SVD
-CPU_SAMPLE = [(512, 2048), (2048,)]
+# bounded CPU sample: one whole OPT-1.3B attention projection (2048 x 2048) plus its bias
+# (4 196 352 params), full reference round with the adaptive SVD. Every OPT-1.3B 2-D tensor
+# has a short side of 2048, which sets the reference's per-parameter SVD cost (Gram a^2 b,
+# Householder a^3); a narrower slab would overstate the CPU's throughput.
+CPU_SAMPLE = [(2048, 2048), (2048,)]
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 # dominant kernels timed with per-launch CUDA events (dlx_kernel_time)
 KERNELS = ("k_o5", "k_tc_sweep_k1", "k_tc_sweep_k2", "k_outer_raw")
 
@@ -51,6 +63,8 @@ def parse():
                          "rank1 (default: the controller's rank is applied from the next round "
                          "on, engine.cpp:476-487, 506-507 — configs[1]'s adaptive schedule)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-held-rank", action="store_true",
+                    help="skip the secondary rank-held (r1) measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compress", action="store_true",
                     help="dilocox-no-compress ablation: raw fp32 exchange (compress_raw)")
@@ -204,7 +218,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- reference arm
-def cpu_reference_round_time(D: int, rounds: int, threads: int):
+def cpu_reference_round_time(D: int, rounds: int, threads: int, warmup: int = 0):
     """Time the reference's own CPU round (oracle/_ref: compress per worker on
     min(D, threads) threads as parallel_over, allreduce_avg, measure_error, error feedback,
     staging, Nesterov, effective_rank) on the bounded sample. Returns (s/round, kind)."""
@@ -222,11 +236,14 @@ def cpu_reference_round_time(D: int, rounds: int, threads: int):
     wq = np.zeros(2048 * 32, np.float32)
     wr = 0
     times = []
-    for i in range(rounds):
+    for i in range(warmup + rounds):
+        # warm-up rounds (allocator / caches) skip the adaptive SVD: only the timed ones matter
+        adaptive = i >= warmup
         t0 = time.perf_counter()
-        out = R.outer_round(t, D, 1, 2 + i, 32, 4, 0, 2, True, 0.5, 32, 0.7, 0.9, False, threads,
-                            anchor, vel, pend, local, wr, wq)
-        times.append(time.perf_counter() - t0)
+        out = R.outer_round(t, D, 1, 2 + i, 32, 4, 0, 2, adaptive, 0.5, 32, 0.7, 0.9, False,
+                            threads, anchor, vel, pend, local, wr, wq)
+        if adaptive:
+            times.append(time.perf_counter() - t0)
         wr = out["warm_rank"]
     return times, kind, n
 
@@ -237,8 +254,8 @@ def run_reference(args, world, rank):
     nproc = os.cpu_count() or 1
     D = world
     cores = min(D, nproc)
-    times, kind, n = cpu_reference_round_time(D, args.warmup + args.steps, nproc)
-    timed = times[args.warmup:]
+    times, kind, n = cpu_reference_round_time(D, args.steps, nproc, warmup=args.warmup)
+    timed = times
     s = sum(timed) / len(timed)
     value = D * n / s
     line = {
@@ -247,9 +264,14 @@ def run_reference(args, world, rank):
         "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config} outer-sync round, D={D} workers, r=32, q=4, adaptive",
-                   "sample": f"{CPU_SAMPLE} per worker ({n} params)", "threads": cores},
+                   "sample": f"{CPU_SAMPLE} per worker ({n} params)", "threads": cores,
+                   "nproc": nproc, "cpu_model": cpu_model()},
         "cpu_baseline": {"value": value, "unit": "params/s", "cores": cores, "kind": kind,
-                         "sample": f"full reference round on {CPU_SAMPLE} x D={D} workers"},
+                         "sample": f"full reference round (compress r=32 q=4, allreduce_avg, "
+                                   f"measure_error, error feedback, staging, Nesterov, "
+                                   f"effective_rank) on {CPU_SAMPLE} x D={D} workers, "
+                                   f"{args.warmup} warm-up rounds without the adaptive SVD",
+                         "nproc": nproc, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -450,15 +472,44 @@ def main():
         ms_e2e = float(m.item())
     e2e_value = world * P / (ms_e2e / ke / 1e3)
 
+    # ---------------- the same rounds at the configured rank r1, controller evaluated but not
+    # applied (hold_rank): the per-round cost of the full-rank compress, for comparison
+    held = None
+    if not args.hold_rank and cfg.adaptive and not args.no_held_rank:
+        eng.cfg.hold_rank = True
+        eng.r_t = cfg.rank1
+        for _ in range(args.warmup):
+            eng.step(local)
+        barrier()
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(args.steps):
+            eng.step(local)
+        h1.record(stream)
+        barrier()
+        hms = h0.elapsed_time(h1)
+        if world > 1:
+            m = torch.tensor([hms], device=dev)
+            dist.all_reduce(m, op=dist.ReduceOp.MAX)
+            hms = float(m.item())
+        eng.flush()
+        held = {"rank": cfg.rank1, "ms_per_step": hms / args.steps,
+                "value": world * P / (hms / args.steps / 1e3), "unit": "params/s",
+                "note": "same rounds with the controller evaluated but the rank held at r1"}
+
     # ---------------- CPU baseline (rank 0, N=1 only): the reference round on a sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times, kind, n = cpu_reference_round_time(1, 6, 1)
+        times, kind, n = cpu_reference_round_time(1, 1, 1, warmup=1)
         s = sum(times) / len(times)
         cpu = {"value": n / s, "unit": "params/s", "cores": 1, "kind": kind,
-               "sample": f"{len(times)} full reference rounds (compress r=32 q=4, allreduce_avg, "
+               "sample": f"{len(times)} full reference round (compress r=32 q=4, allreduce_avg, "
                          f"measure_error, error feedback, staging, Nesterov, effective_rank) on "
-                         f"{CPU_SAMPLE} ({n} params), D=1, {sum(times):.1f} s total"}
+                         f"{CPU_SAMPLE} ({n} params: one OPT-1.3B attention projection + bias), "
+                         f"D=1, {sum(times):.1f} s; extrapolated to the whole model by parameter "
+                         f"count ({P / n:.0f}x: {P / (n / s) / 60:.0f} min per worker-round)",
+               "nproc": os.cpu_count(), "cpu_model": cpu_model(), "extrapolated": True}
 
     if rank == 0:
         rts = sorted({r.r_t for r in recs})
@@ -492,6 +543,7 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "comp_error": recs[-1].comp_error if recs else None,
+            **({"rank_held": held} if held else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

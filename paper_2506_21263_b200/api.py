@@ -88,6 +88,18 @@ class Context:
         check(lib().dlx_exchange_wait_warm(self.h, _stream(stream)))
 
 
+def ensure_comm(ctx: Context, rank: int, world: int, group=None) -> None:
+    """Give `ctx` the library's NCCL communicator for this D-worker group, bootstrapped
+    through torch.distributed (rank 0's unique id is broadcast as an object); no-op if it
+    already has one for `world` ranks or world == 1."""
+    if world <= 1 or getattr(ctx, "world", 1) == world:
+        return
+    import torch.distributed as dist
+    uid = [comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0, group=group)
+    ctx.init_comm(rank, world, uid[0])
+
+
 def comm_unique_id() -> bytes:
     """dlx_comm_unique_id: 128 opaque bytes rank 0 ships to every rank."""
     buf = C.create_string_buffer(128)

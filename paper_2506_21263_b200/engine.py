@@ -67,6 +67,9 @@ class OuterConfig:
     # benchmarking aid: run the adaptive measurement + controller every round but keep
     # operating at rank1 (the controller's choice is recorded in RoundRecord.r_next)
     hold_rank: bool = False
+    # build every rank's device plan up front (OuterSync.prepare) when the controller is
+    # applied, so a rank change does not stall the host between rounds
+    prepare_ranks: bool = True
 
     def resolved_H_min(self) -> int:
         return self.H_min if self.H_min > 0 else (self.H1 + 9) // 10
@@ -190,11 +193,8 @@ class OuterSync:
         # rank 0's unique id); DLX_LIB_NCCL=0 keeps the exchange in torch.distributed.
         self.lib_comm = (world > 1 and anchor.is_cuda and
                          os.environ.get("DLX_LIB_NCCL", "1") == "1")
-        if self.lib_comm and getattr(layout.ctx, "world", 1) != world:
-            import torch.distributed as dist
-            uid = [api.comm_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0, group=group)
-            layout.ctx.init_comm(rank, world, uid[0])
+        if self.lib_comm:
+            api.ensure_comm(layout.ctx, rank, world, group)
         # warm-start broadcast right after the all-gather, before the outer update: 57 MB at
         # OPT-1.3B r=32 (~0.1 ms over NVLink); issued asynchronously it ran beside the outer
         # update's persistent grid and was the other source of multi-ms rank stalls
@@ -224,6 +224,52 @@ class OuterSync:
         self._host_job = None        # per-step chunk schedule while step_host runs
         self.host_chunks = 8         # tensor groups of the chunked host pipeline
         self._groups = None
+        self._begun = None           # begin_round state awaiting finish_round
+        self.overlap_events = None   # optional: (before, after) of each finish_round join
+        if (cfg.prepare_ranks and cfg.adaptive and not cfg.hold_rank and cfg.compress and
+                anchor.is_cuda and self._n2):
+            self.prepare()
+
+    PREPARE_MAX_RANK = 64
+
+    def prepare(self, ranks=None) -> None:
+        """Build the device plans of every rank the adaptive schedule can reach (r1 down to 1,
+        capped at PREPARE_MAX_RANK): plan tables, tensor-core tile lists, Gram jobs, the
+        cold-start redo graph, effective-rank jobs and the outer update's shared-memory
+        plan. The controller only moves r_t at round boundaries (engine.cpp:476-487,
+        506-507) and each new rank would otherwise build all of that on the host between
+        two rounds. Dry runs on the engine's own buffers, before round 1: compress of a
+        noise-filled pending delta, the effective rank of an all-zero exchange, and a
+        sync-mode outer update with a zero Delta and zero velocity — an exact no-op on the
+        anchor and the pending delta (which is re-zeroed)."""
+        cfg, L = self.cfg, self.L
+        if self.round != 0:
+            raise api._lib.ValidationError("prepare: only before the first round")
+        if ranks is None:
+            top = min(cfg.rank1, self.PREPARE_MAX_RANK)
+            ranks = range(top, 0, -1)  # largest first: scratch buffers never grow afterwards
+        api.fill_gaussian(L, self.pending, 1e-3, seed=0x5EED, tag=0x9E9A, worker=self.rank)
+        nb = max(self._n2, 1)
+        for r in ranks:
+            pb = L.payload_bytes(r, cfg.qbits)
+            qel = L.q_factor_elems(r)
+            api.compress(L, self.pending, r, QuantSpec(cfg.qbits, cfg.rounding), None, 0,
+                         cfg.power_iters, 0x1234, payload=self.payload[:pb],
+                         q_out=self.warm_q[:max(qel, 1)])
+            g = self.gathered[:self.world * pb] if self.world > 1 else self.payload[:pb]
+            g.zero_()
+            sharded = self.side is not None and self.er_shards > 1
+            for shd in ((True, False) if sharded else (False,)):
+                api.effective_rank_device(L, g, self.world, r, cfg.qbits, cfg.tau,
+                                          shard=self.rank if shd else 0,
+                                          nshards=self.er_shards if shd else 1,
+                                          per=self.er_per, energy=self.er_dev[nb:])
+            api.outer_update(L, g, self.world, r, cfg.qbits, self.pending, self.anchor, None,
+                             self.velocity, cfg.outer_lr, cfg.outer_momentum,
+                             cfg.outer_classical, mode=SYNC,
+                             self_index=self.rank if cfg.measure_error else -1, stats=self.stats)
+        self.pending.zero_()
+        torch.cuda.synchronize(self.anchor.device)
 
     def _wait_pre_update(self):
         cur = torch.cuda.current_stream()
@@ -314,9 +360,18 @@ class OuterSync:
 
     def collective_average(self, local: torch.Tensor | None, mode: int) -> RoundRecord:
         """Compress (shared stream per round), exchange, measure, fused outer update."""
-        cfg, L = self.cfg, self.L
-        if not cfg.compress:
+        if not self.cfg.compress:
             return self._collective_average_raw(local, mode)
+        return self._sync_finish(self._sync_begin(early_rank=self.side is None), local, mode)
+
+    def _sync_begin(self, early_rank: bool) -> dict:
+        """First half of collective_average (engine.cpp:215-263), on the CURRENT stream:
+        compress of the pending delta (shared RNG stream per round, engine.cpp:226), the
+        exchange (all-gather of the payloads + worker-0 warm-Q broadcast) and — when
+        `early_rank` — the unsharded effective rank, queued for the host before the outer
+        update. Depends only on the pending delta and the warm Q, so it may run concurrently
+        with the round's inner steps (one-step-delay overlap)."""
+        cfg, L = self.cfg, self.L
         r, q = self.r_t, cfg.qbits
         pb = L.payload_bytes(r, q)
         qel = L.q_factor_elems(r)
@@ -334,26 +389,37 @@ class OuterSync:
         rec = RoundRecord(round=self.round, r_t=r, H_t=self.H_t, averaged=True,
                           payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
         measure = cfg.adaptive and self._n2 > 0
-        side = self.side if self.side is not None else None
-        if measure and side is None:
-            # Unsharded measurement on the main stream BEFORE the outer update: r' (and so the
-            # controller's next rank, engine.cpp:476-487) is on the host while the outer update
-            # still runs, so applying the controller costs no host round trip on the device
-            # timeline. (The persistent outer-update grid holds every SM, so a side stream
-            # would only serialise behind it.)
+        if measure and early_rank:
+            # Unsharded measurement BEFORE the outer update: r' (and so the controller's next
+            # rank, engine.cpp:476-487) reaches the host while the outer update still runs, so
+            # applying the controller costs no host round trip on the device timeline. (The
+            # persistent outer-update grid holds every SM, so a side stream would only
+            # serialise behind it.)
             self._ev("effective_rank")
-            self._effective_rank(gathered, r, q, cur)
+            self._effective_rank(gathered, r, q, cur, sharded=False)
             self._queue_er(rec, cur)
-        elif measure:
+        self.warm_rank = r
+        return dict(r=r, q=q, gathered=gathered, rec=rec, measure=measure,
+                    late_rank=measure and not early_rank)
+
+    def _sync_finish(self, st: dict, local: torch.Tensor | None, mode: int) -> RoundRecord:
+        """Second half: the fused outer update (error feedback, staging, Nesterov) on the
+        current stream, plus the sharded effective rank beside it at N > 1."""
+        cfg = self.cfg
+        r, q, gathered, rec = st["r"], st["q"], st["gathered"], st["rec"]
+        cur = torch.cuda.current_stream()
+        side = self.side
+        if st["late_rank"]:
             # sharded across the ranks, on a high-priority side stream beside the outer update
+            side = side or cur
             side.wait_stream(cur)
             with torch.cuda.stream(side):
-                self._effective_rank(gathered, r, q, side)
+                self._effective_rank(gathered, r, q, side, sharded=True)
         self._ev("outer_update")
         self._outer_update(gathered, r, q, local, mode, cur)
         self._ev("end")
         self.stats_host[self.round % self.STATS_SLOTS].copy_(self.stats, non_blocking=True)
-        if measure and side is not None:
+        if st["late_rank"]:
             # the shards' per-tensor (k, energy) are summed AFTER the outer update, on the main
             # stream: no collective runs beside its persistent grid (an NCCL all-reduce there,
             # or a per-round CPU/gloo one, measured 20-260 ms rank stalls)
@@ -372,11 +438,11 @@ class OuterSync:
             rec.r_prime = 1
             self._push_window(1)
             rec.r_next, rec.H_next = self._adapt()
-        self.warm_rank = r
         return rec
 
-    def _effective_rank(self, gathered, r: int, q: int, stream):
-        """Factor-space effective rank (dlx_effective_rank_shard) into er_dev."""
+    def _effective_rank(self, gathered, r: int, q: int, stream, sharded: bool):
+        """Factor-space effective rank (dlx_effective_rank_shard) into er_dev; sharded: this
+        rank measures only its 1/world of the tensors (the others read 0)."""
         cfg, L = self.cfg, self.L
         e0 = e1 = None
         if self.phase_events is not None:
@@ -384,8 +450,8 @@ class OuterSync:
             e0.record(stream)
         nb = max(self._n2, 1)
         api.effective_rank_device(L, gathered, self.world, r, q, cfg.tau, stream=stream,
-                                  shard=self.rank if self.er_shards > 1 else 0,
-                                  nshards=self.er_shards, per=self.er_per,
+                                  shard=self.rank if (sharded and self.er_shards > 1) else 0,
+                                  nshards=self.er_shards if sharded else 1, per=self.er_per,
                                   energy=self.er_dev[nb:])
         self.er_dev[:nb].copy_(self.er_per)
         if e0 is not None:
@@ -499,9 +565,56 @@ class OuterSync:
         """run_round_overlapped (engine.cpp:458-509) minus inner training: the sync of the
         previous round's delta, then staging of this round's delta against the pre-update
         anchor, then the one-step-delayed Nesterov step — all fused in one device pass."""
+        if self._begun is None:
+            self.begin_round()
+        return self.finish_round(local)
+
+    def begin_round(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Start round t's outer sync of delta^{t-1} — compress, exchange, effective rank —
+        on `stream` (default: the current stream). These read only the pending delta and the
+        warm Q, so with a separate stream they run concurrently with the round's inner steps
+        on the main stream: the one-step-delay overlap (engine.cpp:464-468), with the
+        exchange on a side stream. finish_round(local) joins it before the outer update."""
+        if self._begun is not None:
+            raise api._lib.ValidationError("begin_round: the previous round was not finished")
         self.round += 1
+        st = None
+        if self.has_pending and self.cfg.overlap and self.cfg.compress:
+            if stream is None:
+                st = self._sync_begin(early_rank=self.side is None)
+            else:
+                stream.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(stream):
+                    st = self._sync_begin(early_rank=True)
+                    done = torch.cuda.Event(enable_timing=True)
+                    done.record(stream)
+                st["joined"] = done
+        self._begun = {"sync": st}
+
+    def finish_round(self, local: torch.Tensor) -> RoundRecord:
+        """Complete the round begun by begin_round with this round's local parameters."""
+        if self._begun is None:
+            self.begin_round()
+        st = self._begun["sync"]
+        self._begun = None
+        if not self.cfg.overlap:
+            self.round -= 1
+            return self.round_sync(local)
         if self.has_pending:
-            rec = self.collective_average(local, OVERLAPPED)
+            if st is None:  # no-compress ablation
+                rec = self.collective_average(local, OVERLAPPED)
+            else:
+                if "joined" in st:
+                    cur = torch.cuda.current_stream()
+                    if self.overlap_events is not None:
+                        w0 = torch.cuda.Event(enable_timing=True)
+                        w0.record(cur)
+                    cur.wait_event(st["joined"])
+                    if self.overlap_events is not None:
+                        w1 = torch.cuda.Event(enable_timing=True)
+                        w1.record(cur)
+                        self.overlap_events.append((w0, w1))
+                rec = self._sync_finish(st, local, OVERLAPPED)
             # rank held: r' is not needed before the next round (read lazily); else wait
             self._drain_er(block=not self.cfg.hold_rank)
         else:

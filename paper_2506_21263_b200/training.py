@@ -155,18 +155,83 @@ def shard(features: np.ndarray, targets: np.ndarray, D: int, i: int):
 
 def train_overlapped(layout: api.Layout, mlp: MLP, anchor: torch.Tensor, replica: Replica,
                      cfg: OuterConfig, total_steps: int, batch: int, world: int = 1,
-                     rank: int = 0, group=None):
+                     rank: int = 0, group=None, side_sync: bool = True, engine=None):
     """reference_overlapped_run (test_support.hpp:114-218) for this process's replica (one
     process per replica / GPU; world = D). Returns (final anchor slab, per-round losses of
-    this replica, round records)."""
-    eng = OuterSync(layout, cfg, anchor, world=world, rank=rank, group=group)
+    this replica, round records).
+
+    side_sync: round t's sync of delta^{t-1} — compress, the NCCL exchange of the compressed
+    factors and the effective rank — runs on a side stream CONCURRENTLY with round t's inner
+    steps on the main stream (engine.begin_round), and is joined right before the fused
+    outer update (engine.finish_round): the one-step-delay overlap run_round_overlapped
+    simulates in virtual time (engine.cpp:464-468). The results are identical to the
+    serial order (same kernels, same inputs); only the schedule differs."""
+    eng = engine or OuterSync(layout, cfg, anchor, world=world, rank=rank, group=group)
+    sync_stream = torch.cuda.Stream(device=anchor.device) if side_sync else None
     local = torch.empty_like(anchor)
     steps, losses, recs = 0, [], []
     while steps < total_steps:
         h_used = min(eng.H_t, total_steps - steps)
         local.copy_(eng.anchor)  # continue_from_local = false
+        eng.begin_round(sync_stream)
         losses.append(replica.inner_steps(local, h_used, batch))
         steps += h_used
-        recs.append(eng.step(local))
+        recs.append(eng.finish_round(local))
     torch.cuda.synchronize()
     return eng.anchor, losses, recs
+
+
+def train_allreduce_per_step(layout: api.Layout, mlp: MLP, params: torch.Tensor,
+                             replica: Replica, total_steps: int, batch: int, record_every: int,
+                             world: int = 1, rank: int = 0, hyper: api.AdamWHyper | None = None,
+                             exact: bool = True, group=None):
+    """The per-step all-reduce baseline (run_allreduce_per_step, engine.cpp:517-591; mode
+    allreduce-per-step): every inner step each worker computes its
+    gradient on its own batch, the gradients are averaged across the D workers and ONE
+    AdamW step updates the shared parameters (one optimiser state, engine.cpp:521).
+
+    exact=True averages as the reference does — all-gather of the D gradient slabs through
+    the library's NCCL communicator (dlx_comm_allgather) and the worker-order fp64 mean
+    (dlx_mean_slabs, engine.cpp:559-570): bit-identical gradients on every rank and to the
+    reference's mean. exact=False uses an NCCL all-reduce (sum, then x 1/D) — the fast
+    collective a real DDP baseline uses (summation order differs from the reference's).
+
+    Returns (params, per-record mean train losses over workers and steps — RoundRecord
+    train_loss every `record_every` steps, engine.cpp:576-589)."""
+    ctx = layout.ctx
+    n = params.numel()
+    opt = api.AdamWState(params, hyper or replica.hyper)
+    grads = torch.zeros_like(params)
+    mean = torch.empty_like(params)
+    gathered = None
+    if world > 1 and exact:
+        api.ensure_comm(ctx, rank, world, group)
+        gathered = torch.empty(world * n, dtype=torch.float32, device=params.device)
+    losses, block, in_block, steps = [], 0.0, 0, 0
+    while steps < total_steps:
+        xb, yb = replica.next_batch(batch)
+        loss = mlp.forward_backward(params, xb, yb, grads)
+        if world > 1:
+            import torch.distributed as dist
+            if exact:
+                api.comm_allgather(ctx, grads, gathered)
+                api.mean_slabs(ctx, gathered, world, n, out=mean)
+            else:
+                mean.copy_(grads)
+                dist.all_reduce(mean, group=group)
+                mean.mul_(1.0 / world)
+            lt = torch.tensor([loss], dtype=torch.float64, device=params.device)
+            dist.all_reduce(lt, group=group)  # sum of the workers' losses (engine.cpp:575)
+            loss_sum = float(lt.item())
+        else:
+            api.mean_slabs(ctx, grads, 1, n, out=mean)
+            loss_sum = loss
+        api.adamw_step(ctx, opt, params, mean)
+        steps += 1
+        in_block += 1
+        block += loss_sum
+        if steps % record_every == 0 or steps == total_steps:
+            losses.append(block / (in_block * world))
+            block, in_block = 0.0, 0
+    torch.cuda.synchronize()
+    return params, losses
