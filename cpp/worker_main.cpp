@@ -166,7 +166,9 @@ int main(int argc, char** argv) {
   cu(cudaMalloc(&per, sizeof(int) * n2), "malloc");
   cu(cudaMalloc(&energy, sizeof(double) * n2), "malloc");
   cu(cudaMalloc(&draws, 8), "malloc");
-  for (float* p : {anchor, velocity, pending, local}) cu(cudaMemset(p, 0, 4 * slab), "memset");
+  // zeroed on the worker stream (a legacy-stream memset would race the non-blocking stream)
+  for (float* p : {anchor, velocity, pending, local})
+    cu(cudaMemsetAsync(p, 0, 4 * slab, s), "memset");
   ok(dlx_fill_gaussian(ctx, L, anchor, nullptr, 0.02f, 7, 0xA7C4, 0, s), "fill anchor");
   ok(dlx_fill_gaussian(ctx, L, local, anchor, -1e-3f, 1, 0xDA7A, rank, s), "fill local");
 

@@ -62,6 +62,13 @@ struct O5Maps {
 template <bool BF>
 constexpr int prep_rows() { return BF ? 32 : 64; }  // factor rows per k_o5_prep block
 
+// K columns per worker in the A / B operands: with D > 1 every worker's r columns start on
+// an MMA K-step boundary (zero-padded to a multiple of kpad), so the worker's own k-steps
+// (the measure_error accumulator) never straddle a neighbour's columns, whatever r is.
+__host__ __device__ __forceinline__ int o5_rpad(int r, int D, int kpad) {
+  return D > 1 ? (r + kpad - 1) / kpad * kpad : r;
+}
+
 // fp16 path: per-tensor power-of-two prescale of B = code_Q s_P s_Q / D, chosen so that
 // max |B| 2^e lies in [2^14, 2^15): both fp16 planes stay in range and the scaling is exact
 // (undone on the fp32 accumulator in the epilogue). pre = 2^e, post = 2^-e per 2-D slot.
@@ -101,7 +108,7 @@ template <bool BF>
 __global__ void __launch_bounds__(256) k_o5_prep(
     const DevT2* __restrict__ T, const int4* __restrict__ rows, int nrows,
     const int64_t* __restrict__ aoff, const int64_t* __restrict__ boff,
-    const uint8_t* __restrict__ gathered, int64_t pay_bytes, int qbits, int D, int KA,
+    const uint8_t* __restrict__ gathered, int64_t pay_bytes, int qbits, int D, int KA, int kpad,
     const float* __restrict__ pre, void* __restrict__ A_, void* __restrict__ B0_,
     void* __restrict__ B1_) {
   float* A = static_cast<float*>(A_);
@@ -137,9 +144,10 @@ __global__ void __launch_bounds__(256) k_o5_prep(
     const DevT2& t = T[rw.x];
     const int side = rw.y, row0 = rw.z;
     const int64_t n = side == 0 ? t.a : t.b;
-    const int w = k / t.r, j = k % t.r;
+    const int rp = o5_rpad(t.r, D, kpad);
+    const int w = k / rp, j = k % rp;
     float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (w < D && row0 < n) {
+    if (w < D && j < t.r && row0 < n) {
       const uint8_t* pay = gathered + w * pay_bytes;
       const int64_t bit = (w * pay_bytes + (side == 0 ? t.seg_pc : t.seg_qc)) * 8 +
                           ((int64_t)j * n + row0) * qbits;
@@ -473,8 +481,9 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
 #pragma unroll
       for (int pl = 0; pl < KD::NBP; ++pl) b0[pl] = sdesc(bbase + pl * nkc * kO5BBox, 16u, 1024u);
       const uint32_t dacc = tmem + 32u * c, sacc = dacc + 16u;
-      const int K = D * t.r;
-      const int s_lo = self_index * t.r, s_hi = s_lo + t.r;
+      const int rp = o5_rpad(t.r, D, KD::KS);
+      const int K = D * rp;
+      const int s_lo = self_index * rp, s_hi = s_lo + rp;
       const uint32_t a_t = a_tmem0 + ta * a_slot_cols;
       auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc, int kstep) {
         if (TA)
@@ -773,14 +782,12 @@ struct O5State : PlanExt {
 
 bool o5_eligible(const Plan& P, int D, int self_index) {
   if (P.t2.empty()) return false;
-  const int K = D * P.rmax;
+  const int ks = D * P.rmax > 32 ? 16 : 8;  // MMA K step of the operand kind
+  const int K = D * o5_rpad(P.rmax, D, ks);
   if (K > kO5MaxK) return false;  // A band (128 x K) + B stages must fit shared memory
   for (const DevT2& t : P.t2)
     if (t.b % 4 != 0) return false;
-  const int ks = K > 32 ? 16 : 8;  // MMA K step of the operand kind
-  if (self_index >= 0 && D > 1)
-    for (const DevT2& t : P.t2)
-      if (t.r % ks != 0) return false;  // own-payload k steps must align with the MMA K
+  (void)self_index;
   return true;
 }
 
@@ -829,8 +836,8 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   if (!fresh) return S;
   HostProf hp("o5_state (new)");
   S.D = D;
-  const int K = D * P.rmax;
-  S.bf = K > 32;
+  S.bf = D * P.rmax > 32;
+  const int K = D * o5_rpad(P.rmax, D, S.bf ? O5Kind<true>::KS : O5Kind<false>::KS);
   const int ak = S.bf ? O5Kind<true>::AK : O5Kind<false>::AK;
   const int nbp = S.bf ? 3 : 2;
   S.KA = static_cast<int>(round_up(K, ak));
@@ -946,11 +953,13 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   if (S.bf)
     k_o5_prep<true><<<static_cast<unsigned>(ceil_div(S.nrows, prep_rows<true>())), 256, 0, s>>>(
         P.d_t2, S.d_rows, S.nrows, S.d_aoff, S.d_boff, gathered,
-        P.payload_bytes, P.qbits, D, KA, pre, A, B[0], B[1]);
+        P.payload_bytes, P.qbits, D, KA, S.bf ? O5Kind<true>::KS : O5Kind<false>::KS, pre, A,
+        B[0], B[1]);
   else
     k_o5_prep<false><<<static_cast<unsigned>(ceil_div(S.nrows, prep_rows<false>())), 256, 0, s>>>(
         P.d_t2, S.d_rows, S.nrows, S.d_aoff, S.d_boff, gathered,
-        P.payload_bytes, P.qbits, D, KA, pre, A, B[0], B[1]);
+        P.payload_bytes, P.qbits, D, KA, S.bf ? O5Kind<true>::KS : O5Kind<false>::KS, pre, A,
+        B[0], B[1]);
   DLX_LAUNCHED();
   const void* key[8] = {pending, anchor, velocity, mode == DLX_MODE_OVERLAPPED ? local : nullptr,
                         A, B[0], B[1], nullptr};

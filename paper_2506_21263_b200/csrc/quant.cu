@@ -126,12 +126,22 @@ __global__ void __launch_bounds__(256) k_quant_pack(const DevStream* __restrict_
                                                     uint8_t* __restrict__ payload) {
   if (s0p) s0 = *s0p;
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= ngroups) return;
-  int lo = 0, hi = nstreams - 1;  // last stream with group0 <= g
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (streams[mid].group0 <= g) lo = mid; else hi = mid - 1;
+  // the stream of the block's first group: one binary search per block (not a chain of
+  // dependent global loads per thread), then a short forward walk per thread
+  __shared__ int s_first;
+  if (threadIdx.x == 0) {
+    const int64_t g0 = blockIdx.x * (int64_t)blockDim.x;
+    int lo = 0, hi = nstreams - 1;  // last stream with group0 <= g0
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (streams[mid].group0 <= g0) lo = mid; else hi = mid - 1;
+    }
+    s_first = lo;
   }
+  __syncthreads();
+  if (g >= ngroups) return;
+  int lo = s_first;
+  while (lo + 1 < nstreams && streams[lo + 1].group0 <= g) ++lo;
   const DevStream st = streams[lo];
   const int64_t lg = g - st.group0;
   const int64_t total = st.col_len * st.ncols;
@@ -144,6 +154,43 @@ __global__ void __launch_bounds__(256) k_quant_pack(const DevStream* __restrict_
   const uint32_t clen = static_cast<uint32_t>(st.col_len);
   const uint32_t idx0 = static_cast<uint32_t>(lg * 8);
   uint32_t colw = idx0 / clen, roww = idx0 - colw * clen;
+  const float* gsrc = src + static_cast<int64_t>(colw) * st.ld + roww;
+  if (roww + 8 <= clen && (reinterpret_cast<uintptr_t>(gsrc) & 15) == 0) {
+    // the whole group in one column, 16-B aligned: two vector loads, one chunk's constants
+    const int64_t c = st.chunk0 + colw;
+    const float mx = cmax[c];
+    if (mx != 0.f) {
+      const float iv = inv[c];
+      const float4 v0 = *reinterpret_cast<const float4*>(gsrc);
+      const float4 v1 = *reinterpret_cast<const float4*>(gsrc + 4);
+      const float xs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      const uint64_t b0 = static_cast<uint64_t>(base[c] + roww + 1);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float y = __fmul_rn(xs[t], iv);
+        int code;
+        if (!stochastic) {
+          code = __float2int_rn(y);
+        } else {
+          const float fl = floorf(y);
+          const float frac = __fsub_rn(y, fl);
+          const float u = unit_f(draw_at(s0, b0 + t));
+          code = static_cast<int>(fl) + (u < frac ? 1 : 0);
+        }
+        code = max(-L, min(L, code));
+        bits |= (static_cast<uint64_t>(static_cast<uint32_t>(code)) & mask) << (t * qbits);
+      }
+    }
+    uint8_t* dst = payload + st.code_dst + lg * qbits;
+    if (qbits == 4) {
+      *reinterpret_cast<uint32_t*>(dst) = static_cast<uint32_t>(bits);
+    } else if (qbits == 8) {
+      *reinterpret_cast<uint2*>(dst) = make_uint2(static_cast<uint32_t>(bits), static_cast<uint32_t>(bits >> 32));
+    } else {
+      for (int i = 0; i < qbits; ++i) dst[i] = static_cast<uint8_t>(bits >> (8 * i));
+    }
+    return;
+  }
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int64_t idx = lg * 8 + t;
@@ -232,12 +279,20 @@ __global__ void __launch_bounds__(256) k_dequant(const DevStream* __restrict__ s
                                                  float* __restrict__ qhat) {
   const int w = blockIdx.y;
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= ngroups) return;
-  int lo = 0, hi = nstreams - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (streams[mid].group0 <= g) lo = mid; else hi = mid - 1;
+  __shared__ int s_first;  // the block's first stream (see k_quant_pack)
+  if (threadIdx.x == 0) {
+    const int64_t g0 = blockIdx.x * (int64_t)blockDim.x;
+    int lo = 0, hi = nstreams - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (streams[mid].group0 <= g0) lo = mid; else hi = mid - 1;
+    }
+    s_first = lo;
   }
+  __syncthreads();
+  if (g >= ngroups) return;
+  int lo = s_first;
+  while (lo + 1 < nstreams && streams[lo + 1].group0 <= g) ++lo;
   const DevStream st = streams[lo];
   if (st.t2 < 0) return;  // 1-D tensors are reconstructed in place by the 1-D kernels
   const DevT2 t = T[st.t2];

@@ -364,13 +364,15 @@ class OuterSync:
             return self._collective_average_raw(local, mode)
         return self._sync_finish(self._sync_begin(early_rank=self.side is None), local, mode)
 
-    def _sync_begin(self, early_rank: bool) -> dict:
-        """First half of collective_average (engine.cpp:215-263), on the CURRENT stream:
-        compress of the pending delta (shared RNG stream per round, engine.cpp:226), the
+    def _sync_begin(self, early_rank: bool, xstream=None) -> dict:
+        """First half of collective_average (engine.cpp:215-263): compress of the pending
+        delta (shared RNG stream per round, engine.cpp:226) on the CURRENT stream, then the
         exchange (all-gather of the payloads + worker-0 warm-Q broadcast) and — when
         `early_rank` — the unsharded effective rank, queued for the host before the outer
-        update. Depends only on the pending delta and the warm Q, so it may run concurrently
-        with the round's inner steps (one-step-delay overlap)."""
+        update. With `xstream` the exchange and the measurement run on that stream (after the
+        compress), so they proceed concurrently with whatever the current stream does next —
+        the round's inner steps (one-step-delay overlap); the returned state carries the
+        event finish_round joins."""
         cfg, L = self.cfg, self.L
         r, q = self.r_t, cfg.qbits
         pb = L.payload_bytes(r, q)
@@ -383,24 +385,33 @@ class OuterSync:
         api.compress(L, self.pending, r, QuantSpec(q, cfg.rounding),
                      self.warm_q if self.warm_rank == r else None, self.warm_rank,
                      cfg.power_iters, s0, payload=self.payload[:pb], q_out=self.warm_q[:max(qel, 1)])
-        self._ev("exchange")
-        gathered = self._exchange(pb, qel)
-        cur = torch.cuda.current_stream()
         rec = RoundRecord(round=self.round, r_t=r, H_t=self.H_t, averaged=True,
                           payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
         measure = cfg.adaptive and self._n2 > 0
-        if measure and early_rank:
-            # Unsharded measurement BEFORE the outer update: r' (and so the controller's next
-            # rank, engine.cpp:476-487) reaches the host while the outer update still runs, so
-            # applying the controller costs no host round trip on the device timeline. (The
-            # persistent outer-update grid holds every SM, so a side stream would only
-            # serialise behind it.)
-            self._ev("effective_rank")
-            self._effective_rank(gathered, r, q, cur, sharded=False)
-            self._queue_er(rec, cur)
+        main = torch.cuda.current_stream()
+        st = dict(r=r, q=q, rec=rec, measure=measure, late_rank=measure and not early_rank)
+        if xstream is not None:
+            xstream.wait_stream(main)
+        with torch.cuda.stream(xstream if xstream is not None else main):
+            cur = torch.cuda.current_stream()
+            self._ev("exchange")
+            gathered = self._exchange(pb, qel)
+            if measure and early_rank:
+                # Unsharded measurement BEFORE the outer update: r' (and so the controller's
+                # next rank, engine.cpp:476-487) reaches the host while the outer update still
+                # runs, so applying the controller costs no host round trip on the device
+                # timeline. (The persistent outer-update grid holds every SM, so a side stream
+                # would only serialise behind it.)
+                self._ev("effective_rank")
+                self._effective_rank(gathered, r, q, cur, sharded=False)
+                self._queue_er(rec, cur)
+            if xstream is not None:
+                done = torch.cuda.Event(enable_timing=True)
+                done.record(xstream)
+                st["joined"] = done
         self.warm_rank = r
-        return dict(r=r, q=q, gathered=gathered, rec=rec, measure=measure,
-                    late_rank=measure and not early_rank)
+        st["gathered"] = gathered
+        return st
 
     def _sync_finish(self, st: dict, local: torch.Tensor | None, mode: int) -> RoundRecord:
         """Second half: the fused outer update (error feedback, staging, Nesterov) on the
@@ -570,11 +581,12 @@ class OuterSync:
         return self.finish_round(local)
 
     def begin_round(self, stream: torch.cuda.Stream | None = None) -> None:
-        """Start round t's outer sync of delta^{t-1} — compress, exchange, effective rank —
-        on `stream` (default: the current stream). These read only the pending delta and the
-        warm Q, so with a separate stream they run concurrently with the round's inner steps
-        on the main stream: the one-step-delay overlap (engine.cpp:464-468), with the
-        exchange on a side stream. finish_round(local) joins it before the outer update."""
+        """Start round t's outer sync of delta^{t-1}: compress on the current stream, then
+        the exchange of the compressed factors (NCCL) and the effective rank on `stream`
+        (default: the current stream too). These read only the pending delta and the warm Q,
+        so with a separate stream the exchange runs concurrently with the round's inner steps
+        on the main stream: the one-step-delay overlap (engine.cpp:464-468).
+        finish_round(local) joins it before the fused outer update."""
         if self._begun is not None:
             raise api._lib.ValidationError("begin_round: the previous round was not finished")
         self.round += 1
@@ -583,12 +595,10 @@ class OuterSync:
             if stream is None:
                 st = self._sync_begin(early_rank=self.side is None)
             else:
-                stream.wait_stream(torch.cuda.current_stream())
-                with torch.cuda.stream(stream):
-                    st = self._sync_begin(early_rank=True)
-                    done = torch.cuda.Event(enable_timing=True)
-                    done.record(stream)
-                st["joined"] = done
+                # compress stays on the main stream (HBM-bound like the inner steps: sharing
+                # the device with them measured slower than running it first); the exchange
+                # and the measurement move to `stream` and overlap the inner steps
+                st = self._sync_begin(early_rank=True, xstream=stream)
         self._begun = {"sync": st}
 
     def finish_round(self, local: torch.Tensor) -> RoundRecord:

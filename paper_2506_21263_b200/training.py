@@ -160,12 +160,12 @@ def train_overlapped(layout: api.Layout, mlp: MLP, anchor: torch.Tensor, replica
     process per replica / GPU; world = D). Returns (final anchor slab, per-round losses of
     this replica, round records).
 
-    side_sync: round t's sync of delta^{t-1} — compress, the NCCL exchange of the compressed
-    factors and the effective rank — runs on a side stream CONCURRENTLY with round t's inner
-    steps on the main stream (engine.begin_round), and is joined right before the fused
-    outer update (engine.finish_round): the one-step-delay overlap run_round_overlapped
-    simulates in virtual time (engine.cpp:464-468). The results are identical to the
-    serial order (same kernels, same inputs); only the schedule differs."""
+    side_sync: round t's sync of delta^{t-1} starts before round t's inner steps: compress on
+    the main stream, then the NCCL exchange of the compressed factors and the effective rank
+    on a side stream CONCURRENTLY with the inner steps (engine.begin_round), joined right
+    before the fused outer update (engine.finish_round) — the one-step-delay overlap
+    run_round_overlapped simulates in virtual time (engine.cpp:464-468). The results are
+    identical to the serial order (same kernels, same inputs); only the schedule differs."""
     eng = engine or OuterSync(layout, cfg, anchor, world=world, rank=rank, group=group)
     sync_stream = torch.cuda.Stream(device=anchor.device) if side_sync else None
     local = torch.empty_like(anchor)

@@ -1,9 +1,10 @@
 #!/usr/bin/env python
-"""One-step-delay overlap at OPT-1.3B scale: round t's outer sync of delta^{t-1} (compress,
-NCCL exchange of the compressed factors, effective rank — OuterSync.begin_round on a side
-stream) runs concurrently with round t's H inner AdamW steps on the main stream
-(dlx_adamw_step over the 1.316 G-parameter slab), joined before the fused outer update
-(finish_round). Reports per round, max over ranks (CUDA events):
+"""One-step-delay overlap at OPT-1.3B scale: round t's outer sync of delta^{t-1} starts
+before round t's H inner AdamW steps (dlx_adamw_step over the 1.316 G-parameter slab):
+compress on the main stream, then the NCCL exchange of the compressed factors and the
+effective rank on a side stream concurrently with the inner steps (OuterSync.begin_round),
+joined before the fused outer update (finish_round). Reports per round, max over ranks
+(CUDA events):
 
   inner      H inner steps alone
   sync       begin + finish alone (serial)
