@@ -387,6 +387,132 @@ __global__ void __launch_bounds__(256) k_chol(const DevMat* __restrict__ mats,
   }
 }
 
+// 32 < r <= 128: the whole factorisation in shared memory (r x (r + 1) doubles <= 132 KB):
+// fold, right-looking Cholesky with the trailing update spread over 4 row groups x r
+// columns, then R^-1 IN PLACE (upper triangular inversion column by column, the dot
+// products of column j split over 4 lanes each) — no global round trips inside the O(r^3)
+// loops. Same pivot test / flags / need2 as k_chol.
+constexpr int kChol128Threads = 512;
+
+__global__ void __launch_bounds__(kChol128Threads) k_chol128(const DevMat* __restrict__ mats,
+                                                           const int* __restrict__ part0,
+                                                           const int* __restrict__ nparts,
+                                                           int rr,
+                                                           const double* __restrict__ partial,
+                                                           double* __restrict__ rinv,
+                                                           int* __restrict__ flags,
+                                                           int* __restrict__ need2,
+                                                           const int* __restrict__ only) {
+  extern __shared__ __align__(16) double Wc[];  // [r][r + 1], upper triangle used
+  __shared__ double tmp[128];
+  __shared__ double red[2][kChol128Threads / 32];
+  const int e = blockIdx.x, tid = threadIdx.x;
+  if (only && !only[e]) {
+    if (tid == 0) {
+      flags[e] = 0;
+      if (need2) need2[e] = 0;
+    }
+    return;
+  }
+  const DevMat m = mats[e];
+  const int r = m.r, ld = r + 1;
+  const double* src = partial + (int64_t)part0[e] * rr * rr;
+  const int np = nparts[e];
+  const int64_t st = (int64_t)rr * rr;
+  for (int idx = tid; idx < r * r; idx += kChol128Threads) {
+    const int j = idx / r, k = idx % r;
+    if (k < j) continue;
+    const double* sp = src + j * rr + k;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    int p = 0;
+    for (; p + 4 <= np; p += 4)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] += sp[(p + u) * st];
+    for (; p < np; ++p) a[p & 3] += sp[p * st];
+    Wc[j * ld + k] = (a[0] + a[1]) + (a[2] + a[3]);
+  }
+  __syncthreads();
+  double mx = 0.0;
+  for (int j = 0; j < r; ++j) mx = fmax(mx, Wc[j * ld + j]);
+  const double tol = 1e-7 * fmax(1.0, sqrt(mx));
+  const double thr = (10.0 * tol) * (10.0 * tol);
+  const int g = tid / 128, c = tid % 128;  // trailing update: row group g, column c
+  int flag = 0;
+  for (int j = 0; j < r; ++j) {
+    const double d = Wc[j * ld + j];
+    if (!(d > thr)) {  // every thread read the same pivot: uniform exit
+      flag = 1;
+      break;
+    }
+    const double rjj = sqrt(d), inv = 1.0 / rjj;
+    __syncthreads();  // the pivot has been read everywhere
+    for (int k = j + 1 + tid; k < r; k += kChol128Threads) Wc[j * ld + k] *= inv;
+    if (tid == 0) Wc[j * ld + j] = rjj;
+    __syncthreads();
+    const int k = j + 1 + c;
+    if (k < r) {
+      const double rjk = Wc[j * ld + k];
+      for (int i = j + 1 + g; i <= k; i += 4) Wc[i * ld + k] = fma(-Wc[j * ld + i], rjk, Wc[i * ld + k]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) flags[e] = flag;
+  if (flag) {
+    if (need2 && tid == 0) need2[e] = 0;
+    return;
+  }
+  // ||R||_F^2 before the inversion overwrites R
+  double rf = 0.0;
+  for (int idx = tid; idx < r * r; idx += kChol128Threads) {
+    const int i = idx / r, k = idx % r;
+    if (k >= i) rf += Wc[i * ld + k] * Wc[i * ld + k];
+  }
+  __syncthreads();
+  // R^-1 in place (upper): column j = -(inv(R[0:j,0:j]) R[0:j, j]) / R[j][j]
+  for (int j = 0; j < r; ++j) {
+    const double djj = 1.0 / Wc[j * ld + j];
+    const int i = tid >> 2, q = tid & 3;  // row i, lane q of its 4-lane dot product
+    double s = 0.0;
+    if (i < j)
+      for (int k = i + q; k < j; k += 4) s = fma(Wc[i * ld + k], Wc[k * ld + j], s);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (i < j && q == 0) tmp[i] = s;
+    __syncthreads();
+    for (int ii = tid; ii < j; ii += kChol128Threads) Wc[ii * ld + j] = -tmp[ii] * djj;
+    if (tid == 0) Wc[j * ld + j] = djj;
+    __syncthreads();
+  }
+  double xf = 0.0;
+  double* X = rinv + (int64_t)e * rr * rr;
+  for (int idx = tid; idx < r * r; idx += kChol128Threads) {
+    const int i = idx / r, k = idx % r;
+    const double v = k >= i ? Wc[i * ld + k] : 0.0;
+    xf += v * v;
+    X[i * rr + k] = v;
+  }
+  if (need2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      xf += __shfl_xor_sync(0xffffffffu, xf, o);
+      rf += __shfl_xor_sync(0xffffffffu, rf, o);
+    }
+    if ((tid & 31) == 0) {
+      red[0][tid / 32] = xf;
+      red[1][tid / 32] = rf;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double xs = 0.0, rs = 0.0;
+      for (int w = 0; w < kChol128Threads / 32; ++w) {
+        xs += red[0][w];
+        rs += red[1][w];
+      }
+      need2[e] = (sqrt(xs) * sqrt(rs) > 2e3) ? 1 : 0;
+    }
+  }
+}
+
 // r <= 32 fast path: the partial Grams are folded by the whole CTA, then one warp factors
 // in registers — lane c holds column c of the (upper) matrix, the pivot row is broadcast
 // with shuffles, so a step costs no block barrier — and inverts R from shared memory (lane
@@ -723,10 +849,15 @@ static void launch_chol(const GramJob& J, int rr, const double* partial, double*
                         double* rinv, int* flags, int* need2, const int* only, size_t csm,
                         cudaStream_t s) {
   const int ne = static_cast<int>(J.mats.size());
-  if (rr <= 32)
+  if (rr <= 32) {
     k_chol32<<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, rinv, flags, need2,
                                 only);
-  else
+  } else if (rr <= 128) {
+    const int smem = static_cast<int>(sizeof(double) * rr * (rr + 1));
+    smem_optin(reinterpret_cast<const void*>(k_chol128), smem);
+    k_chol128<<<ne, kChol128Threads, smem, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial,
+                                                rinv, flags, need2, only);
+  } else
     k_chol<<<ne, 256, csm, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, work, rinv, flags,
                                 need2, only);
   DLX_LAUNCHED();
