@@ -380,6 +380,7 @@ def main():
     phases = {}
     ev = eng.phase_events
     exch = []  # per-round exchange time (all-gather incl. waiting for the other ranks)
+    per_round = {}  # phase -> per-round device ms (DLX_BENCH_DETAIL=1 prints them)
     gaps = []  # device idle between one round's end and the next round's compress
     for (n0, e0), (n1, e1) in zip(ev, ev[1:]):
         if n0 == "end":
@@ -388,9 +389,13 @@ def main():
             continue
         t = e0.elapsed_time(e1)
         phases[n0] = phases.get(n0, 0.0) + t
+        per_round.setdefault(n0, []).append(round(t, 3))
         if n0 == "exchange":
             exch.append(t)
     phases = {k: v / args.steps for k, v in phases.items()}
+    if os.environ.get("DLX_BENCH_DETAIL") == "1":
+        print(json.dumps({"rank": rank, "per_round_ms": per_round,
+                          "r_t": [r.r_t for r in recs]}), file=sys.stderr, flush=True)
     if exch:
         phases["exchange_max"] = max(exch)
     if gaps:

@@ -66,11 +66,14 @@ __global__ void k_cold_init(const DevT2* T, int nt2, float* q, const int64_t* ba
   const DevT2 t = T[k];
   const int64_t total = t.b * t.r;
   const uint64_t base = static_cast<uint64_t>(bases[k]);
+  // walk the column-major destination (coalesced stores); element (i, j) is row-major draw
+  // i * r + j of the tensor's init (Tensor::uniform, tensor.cpp:43-47)
+  const uint32_t b = static_cast<uint32_t>(t.b);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / t.r, j = e % t.r;
-    const float u = unit_f(draw_at(s0, base + e + 1));
-    q[t.qoff + j * t.ldb + i] = __fadd_rn(-1.0f, __fmul_rn(2.0f, u));
+    const uint32_t j = static_cast<uint32_t>(e) / b, i = static_cast<uint32_t>(e) - j * b;
+    const float u = unit_f(draw_at(s0, base + static_cast<uint64_t>(i) * t.r + j + 1));
+    q[t.qoff + static_cast<int64_t>(j) * t.ldb + i] = __fadd_rn(-1.0f, __fmul_rn(2.0f, u));
   }
 }
 
