@@ -517,6 +517,7 @@ __global__ void __launch_bounds__(kChol128Threads) k_chol128(const DevMat* __res
 // in registers — lane c holds column c of the (upper) matrix, the pivot row is broadcast
 // with shuffles, so a step costs no block barrier — and inverts R from shared memory (lane
 // c back-substitutes column c of R^-1). Same pivot test / flags / need2 as k_chol.
+template <int RR>
 __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
                                                 const int* __restrict__ part0,
                                                 const int* __restrict__ nparts, int rr,
@@ -525,8 +526,8 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
                                                 int* __restrict__ flags,
                                                 int* __restrict__ need2,
                                                 const int* __restrict__ only) {
-  __shared__ double G[32][33];
-  __shared__ double dinv[32];
+  __shared__ double G[RR][RR + 1];
+  __shared__ double dinv[RR];
   const int e = blockIdx.x;
   if (only && !only[e]) {
     if (threadIdx.x == 0) {
@@ -539,12 +540,12 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
   const int r = m.r;
   const double* src = partial + (int64_t)part0[e] * rr * rr;
   const int np = nparts[e];
-  // fold; columns >= r are padded with the identity so the factorisation below runs all 32
-  // steps without data-dependent branches
+  // fold; columns >= r are padded with the identity so the factorisation below runs all RR
+  // (8 / 16 / 32, the rank rounded up) steps without data-dependent branches
   // (8 independent partial sums per element: the row-split partials are L2 reads, and a
   // single dependent chain over ~100 of them made this fold the kernel's whole cost)
-  for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
-    const int j = idx / 32, k = idx % 32;
+  for (int idx = threadIdx.x; idx < RR * RR; idx += blockDim.x) {
+    const int j = idx / RR, k = idx % RR;
     double g = (j == k && j >= r) ? 1.0 : 0.0;
     if (j < r && k < r && k >= j) {
       const double* sp = src + j * rr + k;
@@ -561,17 +562,17 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
-  const int c = threadIdx.x;
-  double w[32];
+  const int c = threadIdx.x;  // lanes >= RR idle along (their columns stay zero)
+  double w[RR];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) w[i] = (i <= c) ? G[i][c] : 0.0;  // column c, upper part
+  for (int i = 0; i < RR; ++i) w[i] = (i <= c && c < RR) ? G[i][c] : 0.0;  // column c, upper
   double mx = 0.0;
   for (int j = 0; j < r; ++j) mx = fmax(mx, G[j][j]);
   const double tol = 1e-7 * fmax(1.0, sqrt(mx));
   const double thr = (10.0 * tol) * (10.0 * tol);
   bool bad = false;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < RR; ++j) {
     const double d = __shfl_sync(0xffffffffu, w[j], j);  // W[j][j] from lane j
     bad |= !(d > thr);
     const double rjj = sqrt(d);
@@ -582,7 +583,7 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
     }
     if (c > j) w[j] *= inv;  // R[j][c]
 #pragma unroll
-    for (int i = j + 1; i < 32; ++i) {  // W[i][c] -= R[j][i] R[j][c], j < i <= c
+    for (int i = j + 1; i < RR; ++i) {  // W[i][c] -= R[j][i] R[j][c], j < i <= c
       const double rji = __shfl_sync(0xffffffffu, w[j], i);
       if (i <= c) w[i] = fma(-rji, w[j], w[i]);
     }
@@ -594,31 +595,34 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
     return;
   }
   __syncwarp();
+  if (c < RR) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) G[i][c] = (i <= c) ? w[i] : 0.0;  // R, upper
+    for (int i = 0; i < RR; ++i) G[i][c] = (i <= c) ? w[i] : 0.0;  // R, upper
+  }
   __syncwarp();
   // X = R^-1: lane c solves R x = e_c by back substitution (rolled over i)
-  double x[32];
+  double x[RR];
+  const int cc = c < RR ? c : RR - 1;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) x[i] = (i == c) ? dinv[c] : 0.0;
+  for (int i = 0; i < RR; ++i) x[i] = (i == c) ? dinv[cc] : 0.0;
 #pragma unroll
-  for (int i = 30; i >= 0; --i) {
+  for (int i = RR - 2; i >= 0; --i) {
     double sum = 0.0;
 #pragma unroll
-    for (int k = i + 1; k < 32; ++k) sum = fma(G[i][k], x[k], sum);
+    for (int k = i + 1; k < RR; ++k) sum = fma(G[i][k], x[k], sum);
     if (i < c) x[i] = -sum * dinv[i];
   }
   double xf = 0.0, rf = 0.0;
   if (c < r) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < RR; ++i) {
       xf = fma(x[i], x[i], xf);
       rf = fma(G[i][c], G[i][c], rf);
     }
   }
   double* X = rinv + (int64_t)e * rr * rr;
 #pragma unroll
-  for (int i = 0; i < 32; ++i)
+  for (int i = 0; i < RR; ++i)
     if (i < r && c < r) X[i * rr + c] = x[i];
   if (need2) {
 #pragma unroll
@@ -850,8 +854,17 @@ static void launch_chol(const GramJob& J, int rr, const double* partial, double*
                         cudaStream_t s) {
   const int ne = static_cast<int>(J.mats.size());
   if (rr <= 32) {
-    k_chol32<<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, rinv, flags, need2,
-                                only);
+    // the fixed-size factorisation shrinks with the rank (the adaptive schedule drives r_t
+    // to a few columns): 8 / 16 / 32 steps
+    if (rr <= 8)
+      k_chol32<8><<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, rinv, flags,
+                                     need2, only);
+    else if (rr <= 16)
+      k_chol32<16><<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, rinv, flags,
+                                      need2, only);
+    else
+      k_chol32<32><<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, rinv, flags,
+                                      need2, only);
   } else if (rr <= 128) {
     const int smem = static_cast<int>(sizeof(double) * rr * (rr + 1));
     smem_optin(reinterpret_cast<const void*>(k_chol128), smem);

@@ -403,7 +403,12 @@ class OuterSync:
                 # timeline. (The persistent outer-update grid holds every SM, so a side stream
                 # would only serialise behind it.)
                 self._ev("effective_rank")
-                self._effective_rank(gathered, r, q, cur, sharded=False)
+                # beside the inner steps (xstream) the ranks split the eigenproblems and sum
+                # the per-tensor results right away (exact: one nonzero term per entry)
+                sharded = xstream is not None and self.er_shards > 1
+                self._effective_rank(gathered, r, q, cur, sharded=sharded)
+                if sharded:
+                    self._sum_er_shards()
                 self._queue_er(rec, cur)
             if xstream is not None:
                 done = torch.cuda.Event(enable_timing=True)
@@ -436,12 +441,7 @@ class OuterSync:
             # or a per-round CPU/gloo one, measured 20-260 ms rank stalls)
             cur.wait_stream(side)
             if self.er_shards > 1:
-                # one nonzero term per entry: the sum is exact and identical on every rank
-                if self.lib_comm:
-                    api.comm_allreduce_sum_f64(self.L.ctx, self.er_dev)
-                else:
-                    import torch.distributed as dist
-                    dist.all_reduce(self.er_dev, group=self.group)
+                self._sum_er_shards()
             self._queue_er(rec, cur)
         elif cfg.adaptive and cfg.compress and self._n2 == 0:
             # no 2-D tensor: effective_rank's aggregate is 1 (compress.cpp:333-339), pushed
@@ -450,6 +450,15 @@ class OuterSync:
             self._push_window(1)
             rec.r_next, rec.H_next = self._adapt()
         return rec
+
+    def _sum_er_shards(self):
+        """Sum the ranks' per-tensor (k, energy) shards on the current stream: one nonzero
+        term per entry, so the sum is exact and identical on every rank."""
+        if self.lib_comm:
+            api.comm_allreduce_sum_f64(self.L.ctx, self.er_dev)
+        else:
+            import torch.distributed as dist
+            dist.all_reduce(self.er_dev, group=self.group)
 
     def _effective_rank(self, gathered, r: int, q: int, stream, sharded: bool):
         """Factor-space effective rank (dlx_effective_rank_shard) into er_dev; sharded: this
