@@ -247,6 +247,86 @@ __global__ void __launch_bounds__(320) k_gram_dmma(const DevMat* __restrict__ ma
   }
 }
 
+// 32 < r <= 128 on DMMA: 32-row slabs of Y staged as fp64 ([col][row]); warp w owns the 8x8
+// blocks w, w + 8, w + 16, ... of the upper block triangle of G = Y^T Y (up to 17 blocks at
+// r = 128), one accumulator pair each — independent chains, so the DMMA pipe stays busy.
+constexpr int kGbRows = 32;
+constexpr int kGbLd = kGbRows + 4;
+
+template <int NB>
+__global__ void __launch_bounds__(256) k_gram_dmma_big(const DevMat* __restrict__ mats,
+                                                       const int4* __restrict__ splits,
+                                                       const float* __restrict__ buf, int rr,
+                                                       double* __restrict__ partial,
+                                                       const int* __restrict__ only) {
+  constexpr int kMaxB = (NB * (NB + 1) / 2 + 7) / 8;  // blocks per warp
+  constexpr int kPer = NB * 8 * kGbRows / 256;         // staged elements per thread
+  __shared__ double Ys[NB * 8 * kGbLd];
+  const int4 sp = splits[blockIdx.x];
+  if (only && !only[sp.x]) return;
+  const DevMat m = mats[sp.x];
+  const int nb = (m.r + 7) / 8, nblk = nb * (nb + 1) / 2;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int ci[kMaxB], cj[kMaxB];
+#pragma unroll
+  for (int q = 0; q < kMaxB; ++q) {
+    int rem = warp + 8 * q, a = 0;
+    while (a < nb && rem >= nb - a) {
+      rem -= nb - a;
+      ++a;
+    }
+    ci[q] = a;
+    cj[q] = a + rem;
+  }
+  double acc[kMaxB][2];
+#pragma unroll
+  for (int q = 0; q < kMaxB; ++q) acc[q][0] = acc[q][1] = 0.0;
+  const float* Y = buf + m.off;
+  float pre[kPer];
+  auto fetch = [&](int r0) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int c = e / kGbRows, rl = e % kGbRows;
+      const int row = r0 + rl;
+      pre[u] = (c < m.r && row < sp.z) ? __ldg(&Y[(int64_t)c * m.ld + row]) : 0.f;
+    }
+  };
+  fetch(sp.y);
+  for (int r0 = sp.y; r0 < sp.z; r0 += kGbRows) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      Ys[(e / kGbRows) * kGbLd + e % kGbRows] = (double)pre[u];
+    }
+    __syncthreads();
+    if (r0 + kGbRows < sp.z) fetch(r0 + kGbRows);
+#pragma unroll
+    for (int k = 0; k < kGbRows; k += 4) {
+#pragma unroll
+      for (int q = 0; q < kMaxB; ++q) {
+        if (warp + 8 * q < nblk) {
+          const double a = Ys[(ci[q] * 8 + lane / 4) * kGbLd + lane % 4 + k];
+          const double b = Ys[(cj[q] * 8 + lane / 4) * kGbLd + lane % 4 + k];
+          dmma_8x8x4(acc[q], a, b);
+        }
+      }
+    }
+  }
+  double* out = partial + (int64_t)sp.w * rr * rr;
+#pragma unroll
+  for (int q = 0; q < kMaxB; ++q) {
+    if (warp + 8 * q >= nblk) continue;
+    const int gj = ci[q] * 8 + lane / 4;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gk = cj[q] * 8 + 2 * (lane % 4) + h;
+      if (gj < m.r && gk < m.r && gj <= gk) out[gj * rr + gk] = acc[q][h];
+    }
+  }
+}
+
 static size_t gram_smem(int rmax) {
   const int rpad = (rmax + 3) / 4 * 4;
   return std::max<size_t>(sizeof(float) * rpad * (kGramRows + 1), sizeof(double) * 16 * 256);
@@ -259,6 +339,13 @@ static void launch_gram(const GramJob& J, const float* buf, double* partial, cud
     DLX_LAUNCHED();
     return;
   }
+  if (J.rmax <= 64) {
+    k_gram_dmma_big<8><<<J.splits.size(), 256, 0, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial,
+                                                       only);
+    DLX_LAUNCHED();
+    return;
+  }
+
   const int nb = (J.rmax + 3) / 4, nblk = nb * (nb + 1) / 2;
   const int gy = nblk >= 256 ? (nblk + 255) / 256 : 1;
   const size_t sm = gram_smem(J.rmax);
@@ -387,6 +474,9 @@ __global__ void __launch_bounds__(256) k_chol(const DevMat* __restrict__ mats,
   }
 }
 
+// (A register-tiled variant — 4 x 8 tiles per thread, pivot rows broadcast through shared
+// memory — measured slower on the Llama-7B layer: r = 64 120 vs 70 us, r = 128 258 vs 219 us
+// per call.)
 // 32 < r <= 128: the whole factorisation in shared memory (r x (r + 1) doubles <= 132 KB):
 // fold, right-looking Cholesky with the trailing update spread over 4 row groups x r
 // columns, then R^-1 IN PLACE (upper triangular inversion column by column, the dot
@@ -777,6 +867,78 @@ __global__ void __launch_bounds__(128) k_apply_dmma(const DevMat* __restrict__ m
   }
 }
 
+// 32 < r <= 128 on DMMA: Y <- Y R^-1 for one 128-row job in two 64-row halves. R^-1 (upper,
+// zero-padded) is staged once per factor in shared memory; warp w owns the 8-row block w of
+// the half and every 8-column block of the output (NB independent accumulator pairs), and
+// column block cj only takes the k steps k < 8 (cj + 1) (triangular).
+template <int NB>
+__global__ void __launch_bounds__(256) k_apply_dmma_big(const DevMat* __restrict__ mats,
+                                                        const int4* __restrict__ jobs, int njobs,
+                                                        int per_cta, int rr,
+                                                        const double* __restrict__ rinv,
+                                                        const int* __restrict__ skip,
+                                                        const int* __restrict__ only,
+                                                        float* __restrict__ buf) {
+  constexpr int C = NB * 8;       // padded columns
+  constexpr int LY = C + 4;       // [row][k] stride
+  constexpr int LR = C + 8;       // [k][col] stride
+  extern __shared__ __align__(16) double ad_smem[];
+  double* Ys = ad_smem;           // [64][LY]
+  double* Rs = Ys + 64 * LY;      // [C][LR]
+  const int j0 = blockIdx.x * per_cta, j1 = min(njobs, j0 + per_cta);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int cur = -1;
+  for (int j = j0; j < j1; ++j) {
+    const int4 jb = jobs[j];
+    const int e = jb.x;
+    if (skip[e] || (only && !only[e])) continue;
+    const DevMat m = mats[e];
+    const int r = m.r, nb = (r + 7) / 8;
+    float* Y = buf + m.off;
+    if (e != cur) {
+      __syncthreads();
+      const double* X = rinv + (int64_t)e * rr * rr;
+      for (int idx = threadIdx.x; idx < C * C; idx += 256) {
+        const int k = idx / C, c = idx % C;
+        Rs[k * LR + c] = (k < r && c < r && k <= c) ? X[k * rr + c] : 0.0;
+      }
+      cur = e;
+    }
+    for (int h = 0; h < 2; ++h) {
+      const int64_t row0 = jb.y + 64 * h;
+      __syncthreads();  // Rs staged / the previous half's Ys consumed
+      for (int idx = threadIdx.x; idx < 64 * C; idx += 256) {
+        const int k = idx / 64, rl = idx % 64;  // coalesced over rows of a column
+        const int64_t row = row0 + rl;
+        Ys[rl * LY + k] = (k < r && row < m.n) ? (double)Y[(int64_t)k * m.ld + row] : 0.0;
+      }
+      __syncthreads();
+      double acc[NB][2];
+#pragma unroll
+      for (int cj = 0; cj < NB; ++cj) acc[cj][0] = acc[cj][1] = 0.0;
+      const double* pa = Ys + (warp * 8 + lane / 4) * LY + lane % 4;
+      const double* pb = Rs + (lane % 4) * LR + lane / 4;
+      for (int k = 0; k < 8 * nb; k += 4) {
+        const double a = pa[k];
+#pragma unroll
+        for (int cj = 0; cj < NB; ++cj)
+          if (cj < nb && k < 8 * (cj + 1)) dmma_8x8x4(acc[cj], a, pb[k * LR + cj * 8]);
+      }
+      __syncthreads();  // every warp read its Ys rows before the in-place stores below
+      const int64_t row = row0 + warp * 8 + lane / 4;
+      if (row < m.n) {
+#pragma unroll
+        for (int cj = 0; cj < NB; ++cj)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int col = cj * 8 + 2 * (lane % 4) + q;
+            if (cj < nb && col < r) Y[(int64_t)col * m.ld + row] = (float)acc[cj][q];
+          }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ exact MGS2 fallback
 __global__ void __launch_bounds__(1024) k_mgs_fallback(const DevMat* __restrict__ mats,
                                                        const int* __restrict__ flags,
@@ -836,6 +998,16 @@ __global__ void __launch_bounds__(1024) k_mgs_fallback(const DevMat* __restrict_
 // ------------------------------------------------------------------ driver
 static size_t apply_smem(int rmax) { return 32 * 33 * sizeof(double) + sizeof(float) * rmax * 129; }
 
+// k_apply_dmma_big measured slower than the SIMT k_apply on the Llama-7B layer (r = 64: 212
+// vs 165 us, r = 128: 492 vs 408 us per call); kept for experiments (DLX_APPLY_DMMA=1)
+static bool apply_dmma_big_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DLX_APPLY_DMMA");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 static void launch_apply(const GramJob& J, int rr, const double* rinv, const int* skip,
                          const int* only, float* buf, size_t asm_, cudaStream_t s) {
   if (rr <= 32) {
@@ -844,8 +1016,23 @@ static void launch_apply(const GramJob& J, int rr, const double* rinv, const int
     k_apply_dmma<<<(nj + per - 1) / per, 128, 0, s>>>(J.d_mats, J.d_apply, nj, per, rr, rinv, skip,
                                                       only, buf);
   }
-  else
+  else if (rr <= 128 && apply_dmma_big_enabled()) {
+    const int nj = static_cast<int>(J.apply.size());
+    const int per = std::max(1, (nj + 148 - 1) / 148);
+    if (rr <= 64) {
+      const int sm = static_cast<int>(sizeof(double) * (64 * 68 + 64 * 72));
+      smem_optin(reinterpret_cast<const void*>(k_apply_dmma_big<8>), sm);
+      k_apply_dmma_big<8><<<(nj + per - 1) / per, 256, sm, s>>>(J.d_mats, J.d_apply, nj, per, rr,
+                                                               rinv, skip, only, buf);
+    } else {
+      const int sm = static_cast<int>(sizeof(double) * (64 * 132 + 128 * 136));
+      smem_optin(reinterpret_cast<const void*>(k_apply_dmma_big<16>), sm);
+      k_apply_dmma_big<16><<<(nj + per - 1) / per, 256, sm, s>>>(J.d_mats, J.d_apply, nj, per, rr,
+                                                                rinv, skip, only, buf);
+    }
+  } else {
     k_apply<<<J.apply.size(), 128, asm_, s>>>(J.d_mats, J.d_apply, rr, rinv, skip, only, buf);
+  }
   DLX_LAUNCHED();
 }
 

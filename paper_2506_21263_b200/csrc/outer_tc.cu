@@ -68,6 +68,9 @@ constexpr int prep_rows() { return BF ? 32 : 64; }  // factor rows per k_o5_prep
 __host__ __device__ __forceinline__ int o5_rpad(int r, int D, int kpad) {
   return D > 1 ? (r + kpad - 1) / kpad * kpad : r;
 }
+// operand kind: tf32 (A band in shared memory) while the padded K fits one 32-wide band,
+// fp16 with A in TMEM above
+inline bool o5_bf(int rmax, int D) { return D * o5_rpad(rmax, D, 8) > 32; }
 
 // fp16 path: per-tensor power-of-two prescale of B = code_Q s_P s_Q / D, chosen so that
 // max |B| 2^e lies in [2^14, 2^15): both fp16 planes stay in range and the scaling is exact
@@ -782,7 +785,7 @@ struct O5State : PlanExt {
 
 bool o5_eligible(const Plan& P, int D, int self_index) {
   if (P.t2.empty()) return false;
-  const int ks = D * P.rmax > 32 ? 16 : 8;  // MMA K step of the operand kind
+  const int ks = o5_bf(P.rmax, D) ? 16 : 8;  // MMA K step of the operand kind
   const int K = D * o5_rpad(P.rmax, D, ks);
   if (K > kO5MaxK) return false;  // A band (128 x K) + B stages must fit shared memory
   for (const DevT2& t : P.t2)
@@ -836,7 +839,7 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
   if (!fresh) return S;
   HostProf hp("o5_state (new)");
   S.D = D;
-  S.bf = D * P.rmax > 32;
+  S.bf = o5_bf(P.rmax, D);
   const int K = D * o5_rpad(P.rmax, D, S.bf ? O5Kind<true>::KS : O5Kind<false>::KS);
   const int ak = S.bf ? O5Kind<true>::AK : O5Kind<false>::AK;
   const int nbp = S.bf ? 3 : 2;

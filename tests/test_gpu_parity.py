@@ -266,9 +266,10 @@ def test_compress_larger_shapes(ctx, oracle):
 
 
 @pytest.mark.parametrize("rank,q,D", [(6, 8, 3), (16, 2, 1), (32, 4, 2), (30, 4, 3)])
-def test_effective_rank_factor_space(ctx, oracle, rank, q, D):
+def test_effective_rank_factor_space(ctx, oracle, reference, rank, q, D):
     """Factor-space r' (integer code Grams for D*r <= 64, fp64 dequantised Grams above) vs
-    the reference's dense SVD of the averaged Delta; energy = ||Delta||_F^2."""
+    the compiled reference's dense SVD (Gram -> Householder -> implicit QL, tensor.cpp:229-361)
+    of the averaged Delta; energy = ||Delta||_F^2."""
     from paper_2506_21263_b200 import api
     import torch
     shapes = [(48, 40), (40,), (30, 64), (20, 20), (70, 36)]
@@ -284,7 +285,7 @@ def test_effective_rank_factor_space(ctx, oracle, rank, q, D):
     avg = oracle.allreduce_avg(t, ranks, codes, scales)
     dense = [x for x, s in zip(split_dense(shapes, avg), shapes) if len(s) == 2]
     for tau in (0.3, 0.5, 0.9):
-        per, agg, allz = oracle.effective_rank(t, avg, tau, rank)
+        per, agg, allz = reference.effective_rank(t, avg, tau, rank)
         er = api.effective_rank(L, torch.cat(pays), D, rank, q, tau, rank)
         assert [k for _, k in er.per_tensor] == per.tolist()
         assert er.aggregate == agg and er.all_zero == allz
@@ -306,10 +307,10 @@ def test_effective_rank_factor_space(ctx, oracle, rank, q, D):
 
 @pytest.mark.parametrize("D,rank,big_from", [(8, 32, 128), (5, 32, 128), (3, 32, 0), (2, 8, 0),
                                            (1, 8, 0)])
-def test_effective_rank_large_k(ctx, oracle, D, rank, big_from):
+def test_effective_rank_large_k(ctx, oracle, reference, D, rank, big_from):
     """The large-K eigen kernel (blocked Cholesky, tiled DMMA products, packed fused
-    Householder, certified multisection; K = D r up to 256) vs the reference's dense SVD of
-    the averaged Delta, per tensor; big_from = 0 forces it on small K too."""
+    Householder, certified multisection; K = D r up to 256) vs the compiled reference's dense
+    SVD of the averaged Delta, per tensor; big_from = 0 forces it on small K too."""
     from paper_2506_21263_b200 import api
     import torch
     shapes = [(300, 280), (280,), (260, 400), (40, 300)]
@@ -327,7 +328,7 @@ def test_effective_rank_large_k(ctx, oracle, D, rank, big_from):
     api.set_option("effrank_big_from", big_from)
     try:
         for tau in (0.3, 0.5, 0.9):
-            per, agg, allz = oracle.effective_rank(t, avg, tau, rank)
+            per, agg, allz = reference.effective_rank(t, avg, tau, rank)
             er = api.effective_rank(L, torch.cat(pays), D, rank, 4, tau, rank)
             assert [k for _, k in er.per_tensor] == per.tolist()
             assert er.aggregate == agg and er.all_zero == allz
