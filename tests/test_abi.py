@@ -84,3 +84,16 @@ def test_payload_formula_matches_oracle(oracle):
     assert oracle.payload_bits(t, t.ranks(32), 4) / 8 == pytest.approx(15.418e6, rel=1e-4)
     t = Table([s for _, s in layouts.mini_opt()])
     assert oracle.payload_bits(t, t.ranks(8), 8) / 8 == pytest.approx(240_616, abs=1)
+
+
+def test_worker_sync_entry_points_on_cpu():
+    """dlx_comm_unique_id needs only NCCL (dlopen'ed at run time), not a GPU; the other
+    worker-sync calls reject a null context with a typed error instead of crashing."""
+    from paper_2506_21263_b200 import _lib, api
+    uid = api.comm_unique_id()
+    assert len(uid) == 128 and any(uid)
+    L = _lib.lib()
+    assert L.dlx_comm_check(None) == 1
+    assert L.dlx_exchange(None, None, 0, None, None, 0, 0, None) == 1
+    assert L.dlx_comm_allgather(None, None, 0, None, None) == 1
+    assert L.dlx_exchange_wait_warm(None, None) == 1
