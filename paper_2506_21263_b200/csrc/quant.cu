@@ -164,9 +164,11 @@ __global__ void __launch_bounds__(256) k_quant_pack(const DevStream* __restrict_
       const float4 v0 = *reinterpret_cast<const float4*>(gsrc);
       const float4 v1 = *reinterpret_cast<const float4*>(gsrc + 4);
       const float xs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      const uint64_t b0 = static_cast<uint64_t>(base[c] + roww + 1);
+      // counter of the group's first draw; the next ones are +gamma each (no 64-bit multiply
+      // per element: the integer pipe, not HBM, bounds this kernel)
+      uint64_t z = s0 + static_cast<uint64_t>(base[c] + roww + 1) * kGolden;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+      for (int t = 0; t < 8; ++t, z += kGolden) {
         const float y = __fmul_rn(xs[t], iv);
         int code;
         if (!stochastic) {
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(256) k_quant_pack(const DevStream* __restrict_
         } else {
           const float fl = floorf(y);
           const float frac = __fsub_rn(y, fl);
-          const float u = unit_f(draw_at(s0, b0 + t));
+          const float u = unit_f(fmix64(z));
           code = static_cast<int>(fl) + (u < frac ? 1 : 0);
         }
         code = max(-L, min(L, code));
