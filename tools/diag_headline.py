@@ -1,5 +1,9 @@
+"""Per-column diagnosis of the headline compress parity (tests/test_gpu_headline.py): the
+scales, codes and Q factors of dlx_compress vs the compiled reference on the OPT-1.3B
+embedding + position table + decoder layer, worst offenders first
+(profiles/r02_headline_compress_diag.log)."""
 import sys, numpy as np
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import torch
 from oracle.oracle import Oracle, Table
 from tests.test_gpu_headline import _head_table, _lowrank_noise, RANK, Q
