@@ -10,6 +10,8 @@
 #include <tuple>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "dlx_internal.cuh"
 
 namespace dlx {
@@ -24,6 +26,9 @@ void check_cuda(cudaError_t e, const char* what) {
 }
 
 void count_launch(int n) { g_launches += static_cast<uint64_t>(n); }
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 namespace {
 struct ProfEntry {
@@ -734,6 +739,7 @@ static void run_compress(dlx_ctx* ctx, dlx_layout* L, const float* d_delta, int 
                          int warm_rank, uint8_t* d_payload, float* d_q_out, uint64_t* d_draws,
                          cudaStream_t s) {
   HostProf hp("compress");
+  NvtxRange nv("dlx_compress");
   validate_quant(rank, qbits);
   if (iters < 1) raise(DLX_ERR_VALIDATION, "lowrank_approx: iters must be >= 1");
   if (rounding != 0 && rounding != 1) raise(DLX_ERR_VALIDATION, "unknown rounding mode");
@@ -843,6 +849,7 @@ dlx_status dlx_outer_update_range(dlx_ctx* ctx, const dlx_layout* layout, int ra
     if (t_begin < 0 || t_end > layout->nt || t_begin > t_end)
       raise(DLX_ERR_VALIDATION, "outer_update: tensor range out of bounds");
     const SlotRange R = slot_range(P, t_begin, t_end);
+    NvtxRange nv("dlx_outer_update");
     if (d_stats && t_begin == 0) DLX_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(dlx_round_stats), s));
     launch_outer_2d(ctx, P, D, d_gathered, self_index, mode, d_pending, d_anchor, d_local,
                     d_velocity, gamma, beta, classical, d_stats, R, s);
@@ -961,6 +968,7 @@ dlx_status dlx_effective_rank_shard(dlx_ctx* ctx, const dlx_layout* layout, int 
     if (!(tau > 0.0) || !(tau < 1.0)) raise(DLX_ERR_VALIDATION, "effective_rank: need 0 < tau < 1");
     if (D < 1) raise(DLX_ERR_VALIDATION, "effective_rank: no payloads");
     Plan& P = const_cast<dlx_layout*>(layout)->plan(rank, qbits);
+    NvtxRange nv("dlx_effective_rank");
     effective_rank_factors(ctx, P, D, d_gathered, tau, d_per_tensor, d_energy, shard, nshards,
                            as_stream(stream));
   });

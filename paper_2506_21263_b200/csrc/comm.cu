@@ -186,6 +186,7 @@ dlx_status dlx_exchange(dlx_ctx* ctx, const uint8_t* d_payload, int64_t payload_
     }
     Comm& c = comm_of(ctx);
     const NcclApi& n = nccl();
+    NvtxRange nv("dlx_exchange");
     join_in(c, s);
     if (payload_bytes > 0) {
       // worker w's bytes land at [w * payload_bytes, (w + 1) * payload_bytes): worker order =

@@ -50,6 +50,14 @@ void count_launch(int n = 1);
 // attribute is per device, so the opt-in is cached per (device, kernel, bytes): a second
 // context on another device in the same process gets its own.
 void smem_optin(const void* func, int bytes);
+// NVTX range over one C-ABI stage (compress, exchange, outer update, effective rank): free
+// unless a tool (nsys / ncu --nvtx) is attached — NVTX v3 is header-only and loads the
+// injection library only then.
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+};
+
 // Host-side wall time per scope, reported at exit when DLX_HOST_PROF=1 (where the host
 // spends its time between launches: plan / state builds on a rank change, waits).
 struct HostProf {

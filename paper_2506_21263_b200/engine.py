@@ -278,6 +278,8 @@ class OuterSync:
         self._pre_update = []
 
     def _ev(self, name: str):
+        # NVTX marks of the round's phases on the host timeline (free without a tool)
+        torch.cuda.nvtx.mark(f"dlx round {self.round}: {name}")
         if self.phase_events is None:
             return None
         e = torch.cuda.Event(enable_timing=True)
