@@ -306,14 +306,16 @@ def fill_gaussian(layout: Layout, out: torch.Tensor, scale: float, seed: int, ta
 def compress(layout: Layout, delta: torch.Tensor, rank: int, spec: QuantSpec,
              warm_q: torch.Tensor | None, warm_rank: int, power_iters: int, rng_state: int,
              payload: torch.Tensor | None = None, q_out: torch.Tensor | None = None,
-             stream=None) -> CompressResult:
-    """compress (compress.cpp:146-183). q_out may alias warm_q (in-place warm refresh)."""
+             stream=None, draws: torch.Tensor | None = None) -> CompressResult:
+    """compress (compress.cpp:146-183). q_out may alias warm_q (in-place warm refresh).
+    draws (device int64[1], optional) receives the number of RNG draws consumed."""
     dev = delta.device
     if payload is None:
         payload = torch.empty(layout.payload_bytes(rank, spec.qbits), dtype=torch.uint8, device=dev)
     if q_out is None:
         q_out = torch.zeros(max(layout.q_factor_elems(rank), 1), dtype=torch.float32, device=dev)
-    draws = torch.zeros(1, dtype=torch.int64, device=dev)
+    if draws is None:
+        draws = torch.zeros(1, dtype=torch.int64, device=dev)
     check(lib().dlx_compress(layout.ctx.h, layout.h, _ptr(delta), rank, spec.qbits, spec.rounding,
                              power_iters, rng_state & M64, _ptr(warm_q), warm_rank, _ptr(payload),
                              _ptr(q_out), _ptr(draws), _stream(stream)))

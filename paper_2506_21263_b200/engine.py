@@ -174,6 +174,7 @@ class OuterSync:
         self.payload = torch.zeros(pb, dtype=torch.uint8, device=dev)
         self.gathered = torch.zeros(world * pb, dtype=torch.uint8, device=dev)
         self.stats = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.draws = torch.zeros(1, dtype=torch.int64, device=dev)  # RNG draws of the last compress
         # Side stream for the effective-rank measurement. Default off at world == 1: the fused
         # outer update is a persistent grid with ~215 KB of shared memory per SM, so side
         # kernels cannot co-reside and only serialise behind it (measured 0.1-0.2 ms slower).
@@ -386,7 +387,8 @@ class OuterSync:
         # then rank 0's copy is broadcast (engine.cpp:498-501)
         api.compress(L, self.pending, r, QuantSpec(q, cfg.rounding),
                      self.warm_q if self.warm_rank == r else None, self.warm_rank,
-                     cfg.power_iters, s0, payload=self.payload[:pb], q_out=self.warm_q[:max(qel, 1)])
+                     cfg.power_iters, s0, payload=self.payload[:pb], q_out=self.warm_q[:max(qel, 1)],
+                     draws=self.draws)
         rec = RoundRecord(round=self.round, r_t=r, H_t=self.H_t, averaged=True,
                           payload_bytes=L.payload_bits(r, q) / 8.0, omega_sq=self._omega_sq(r))
         measure = cfg.adaptive and self._n2 > 0

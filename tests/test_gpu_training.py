@@ -184,3 +184,66 @@ def test_allreduce_per_step_baseline_matches_reference(ctx, tmp_path):
     rel = np.linalg.norm(got - p_ref) / np.linalg.norm(p_ref - p0)
     print(f"allreduce-per-step final params rel diff {rel:.2e}")
     assert rel <= 1e-2, rel
+
+
+AR_WORKER = r'''
+import json, os, sys
+sys.path.insert(0, os.environ["DLX_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+from oracle.oracle import ref_mlp_overlapped_run
+from paper_2506_21263_b200 import api
+from paper_2506_21263_b200.training import MLP, Replica, mlp_table, shard, train_allreduce_per_step
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("nccl", device_id=torch.device(f"cuda:{rank}"))
+widths, seed, H1, steps, batch = [16, 64, 64, 8], 5, 5, 30, 8
+data = ref_mlp_overlapped_run(widths, "tanh", 2000, 32, seed, world, H1, 5, batch, 8, 8, 0, 2, False)
+ctx = api.Context(rank)
+L = api.Layout(ctx, mlp_table(widths))
+mlp = MLP(L, widths, "tanh")
+xs, ys = shard(data["train_x"], data["train_y"], world, rank)
+rep = Replica(mlp, torch.from_numpy(np.ascontiguousarray(xs)).cuda(),
+              torch.from_numpy(np.ascontiguousarray(ys)).cuda(), seed, rank)
+params, losses = train_allreduce_per_step(L, mlp, L.pack(data["anchor0"]), rep, steps, batch, H1,
+                                          world=world, rank=rank)
+L.unpack(params).tofile(os.path.join(os.environ["DLX_OUT"], f"ar{rank}.bin"))
+json.dump({"losses": losses, "anchor0": data["anchor0"].tolist()},
+          open(os.path.join(os.environ["DLX_OUT"], f"ar{rank}.json"), "w"))
+dist.barrier()
+dist.destroy_process_group()
+'''
+
+
+def test_two_rank_allreduce_per_step_matches_reference(tmp_path):
+    """The per-step all-reduce baseline over two NCCL ranks (exact gradient mean through the
+    library's communicator: all-gather + worker-order fp64 mean): both ranks end with
+    bitwise-identical parameters, and the run tracks the reference's D = 2
+    run_allreduce_per_step (engine.cpp:517-591)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    import torch
+    from oracle.oracle import available
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    if not available("reference"):
+        pytest.skip("reference library (oracle/_ref) not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "arworker.py"
+    script.write_text(AR_WORKER)
+    env = dict(os.environ, DLX_ROOT=root, DLX_OUT=str(tmp_path))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29547", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    p0 = np.fromfile(tmp_path / "ar0.bin", np.float32)
+    p1 = np.fromfile(tmp_path / "ar1.bin", np.float32)
+    assert np.array_equal(p0, p1), "ranks disagree"
+    recs, p_ref, init = _ref_run(dict(mode="allreduce-per-step", D=2, widths="16,64,64,8",
+                                      act="tanh", samples=2000, teacher=32, seed=5, H1=5,
+                                      steps=30, batch=8), tmp_path / "ref")
+    got = json.load(open(tmp_path / "ar0.json"))
+    np.testing.assert_allclose(got["losses"], [x["train_loss"] for x in recs], rtol=2e-3)
+    rel = np.linalg.norm(p0 - p_ref) / np.linalg.norm(p_ref - init)
+    assert rel <= 1e-2, rel
