@@ -260,26 +260,24 @@ T& plan_ext(const Plan& P, const std::string& key, bool* fresh = nullptr) {
 
 // Device copies of per-tensor TMA descriptor tables, keyed by the buffer addresses they were
 // encoded for. A caller that alternates buffers (ping-pong local / anchor slabs) hits the
-// cache instead of re-encoding. Each entry's host side is pinned and never rewritten while
-// the entry lives, so the upload is a plain stream-ordered copy with no host
-// synchronisation; only evicting an entry (more than kEntries distinct keys) waits for the
-// device, since in-flight kernels may still read the evicted table.
+// cache instead of re-encoding. A new entry is encoded on the host and uploaded with
+// upload_now (a private non-blocking stream: no wait for the compute streams, no pinned
+// allocation — cudaMallocHost measured multi-ms stalls with several processes per node);
+// only evicting an entry (more than kEntries distinct keys) waits for the device, since
+// in-flight kernels may still read the evicted table.
 template <class T, int NK>
 struct MapTableCache : PlanExt {
   static constexpr int kEntries = 4;
   struct Entry {
     const void* key[NK];
-    T* host = nullptr;  // pinned
     T* dev = nullptr;
     uint64_t used = 0;
   };
   std::vector<Entry> entries;
   uint64_t tick = 0;
   ~MapTableCache() override {
-    for (Entry& e : entries) {
-      if (e.host) cudaFreeHost(e.host);
+    for (Entry& e : entries)
       if (e.dev) cudaFree(e.dev);
-    }
   }
   // Returns the device table for `key`; `encode(T* host)` fills a new table of n entries.
   template <class F>
@@ -294,7 +292,6 @@ struct MapTableCache : PlanExt {
       auto victim = std::min_element(entries.begin(), entries.end(),
                                      [](const Entry& x, const Entry& y) { return x.used < y.used; });
       DLX_CUDA(cudaDeviceSynchronize());
-      cudaFreeHost(victim->host);
       cudaFree(victim->dev);
       entries.erase(victim);
     }
@@ -302,11 +299,12 @@ struct MapTableCache : PlanExt {
     Entry e{};
     std::copy(key, key + NK, e.key);
     const size_t bytes = sizeof(T) * std::max<size_t>(n, 1);
-    DLX_CUDA(cudaMallocHost(&e.host, bytes));
+    std::vector<T> host(std::max<size_t>(n, 1));
+    std::memset(static_cast<void*>(host.data()), 0, bytes);
+    encode(host.data());
     DLX_CUDA(cudaMalloc(&e.dev, bytes));
-    std::memset(static_cast<void*>(e.host), 0, bytes);
-    encode(e.host);
-    DLX_CUDA(cudaMemcpyAsync(e.dev, e.host, bytes, cudaMemcpyHostToDevice, s));
+    upload_now(e.dev, host.data(), bytes);
+    (void)s;
     e.used = tick;
     entries.push_back(e);
     return entries.back().dev;

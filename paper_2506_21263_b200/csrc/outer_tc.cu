@@ -52,8 +52,13 @@ struct O5Kind {
   static constexpr int NBP = 2;            // B planes (hi + lo)
 };
 
-struct O5Maps {
+// Per-tensor TMA descriptors, split by what they depend on: the four parameter streams
+// depend only on the state buffers (shared by every rank's plan of a layout), the operand
+// maps on the rank (K) and the staging buffers.
+struct O5StreamMaps {
   CUtensorMap s[4];  // pending, anchor, velocity, local: dims {b, a}, box {16, 128}, SW64
+};
+struct O5OpMaps {
   CUtensorMap a;     // A (codes of P): dims {KA, lda}, box {AK, 128}, SW128
   CUtensorMap b[2];  // B planes: dims {KA, ldb}, box {AK, 16}, SW128
 };
@@ -248,7 +253,8 @@ __global__ void __launch_bounds__(256) k_o5_prep(
 // ahead) and the MMA of a tile no longer waits for that tile's stream data.
 template <bool SELF, bool BF>
 __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
-    k_o5(const DevT2* __restrict__ T, const O5Maps* __restrict__ maps,
+    k_o5(const DevT2* __restrict__ T, const O5StreamMaps* __restrict__ smaps,
+         const O5OpMaps* __restrict__ omaps,
          const int4* __restrict__ bands, int nbands, int* __restrict__ band_ctr, int D, int KA,
          int nst, int nab, int nbr, int a_mode, int self_index, int mode, float gamma,
          float beta, int classical, const float* __restrict__ post, dlx_round_stats* stats) {
@@ -338,7 +344,8 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       band = __shfl_sync(0xffffffffu, band, 0);
       if (band >= nbands) break;
       const int4 bd = bands[band];  // (slot, m0, first column, columns)
-      const O5Maps* mp = maps + bd.x;
+      const O5StreamMaps* ms = smaps + bd.x;
+      const O5OpMaps* mo = omaps + bd.x;
       const int ntile = (bd.w + kO5TileN - 1) / kO5TileN;
       auto push_tile = [&](int n) {  // TA: stream boxes only (B: warp 10)
         mbar_wait(&sempty[s], sph ^ 1);
@@ -349,7 +356,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
           uint8_t* st = smem + s * stage_bytes;
           mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox);
           for (int q = 0; q < nstreams; ++q)
-            tma_load_2d(st + q * kO5StreamBox, &mp->s[q], &sfull[s], n0, bd.y);
+            tma_load_2d(st + q * kO5StreamBox, &ms->s[q], &sfull[s], n0, bd.y);
         }
         __syncwarp();
         if (++s == nst) {
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
           mbar_wait(&aempty[ar], arph ^ 1);
           if (elect_one()) {
             mbar_expect_tx(&afull[ar], kO5ABox);
-            tma_load_2d(abuf + ar * kO5ABox, &mp->a, &afull[ar], KD::AK * kc, bd.y);
+            tma_load_2d(abuf + ar * kO5ABox, &mo->a, &afull[ar], KD::AK * kc, bd.y);
           }
           __syncwarp();
           if (++ar == nab) {
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       if (elect_one()) {
         mbar_expect_tx(&afull[a], aband_bytes);
         for (int kc = 0; kc < nkc; ++kc)
-          tma_load_2d(abuf + a * aband_bytes + kc * kO5ABox, &mp->a, &afull[a], KD::AK * kc, bd.y);
+          tma_load_2d(abuf + a * aband_bytes + kc * kO5ABox, &mo->a, &afull[a], KD::AK * kc, bd.y);
       }
       __syncwarp();
       for (int n = 0; n < ntile; ++n) {
@@ -394,11 +401,11 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
           uint8_t* st = smem + s * stage_bytes;
           mbar_expect_tx(&sfull[s], nstreams * kO5StreamBox + KD::NBP * nkc * kO5BBox);
           for (int q = 0; q < nstreams; ++q)
-            tma_load_2d(st + q * kO5StreamBox, &mp->s[q], &sfull[s], n0, bd.y);
+            tma_load_2d(st + q * kO5StreamBox, &ms->s[q], &sfull[s], n0, bd.y);
           uint8_t* bb = st + 4 * kO5StreamBox;
           for (int pl = 0; pl < KD::NBP; ++pl)
             for (int kc = 0; kc < nkc; ++kc)
-              tma_load_2d(bb + (pl * nkc + kc) * kO5BBox, &mp->b[pl], &sfull[s], KD::AK * kc, n0);
+              tma_load_2d(bb + (pl * nkc + kc) * kO5BBox, &mo->b[pl], &sfull[s], KD::AK * kc, n0);
         }
         __syncwarp();
         if (++s == nst) {
@@ -551,14 +558,15 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       mbar_wait(&tinfo[s], sph);
       const int4 tl = sinfo[s];
       if (tl.x < 0) break;
-      const O5Maps* mp = maps + tl.x;
+      const O5StreamMaps* ms = smaps + tl.x;
+      const O5OpMaps* mo = omaps + tl.x;
       if (a_src == 1 && (tl.w & 2)) {
         // the whole A band fits the box ring: issue it as soon as the chunk is scheduled
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait(&aempty[ar], arph ^ 1);
           if (elect_one()) {
             mbar_expect_tx(&afull[ar], kO5ABox);
-            tma_load_2d(abuf + ar * kO5ABox, &mp->a, &afull[ar], KD::AK * kc, tl.y);
+            tma_load_2d(abuf + ar * kO5ABox, &mo->a, &afull[ar], KD::AK * kc, tl.y);
           }
           __syncwarp();
           if (++ar == nab) {
@@ -573,7 +581,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
         mbar_expect_tx(&bfull[bs], bslot_bytes);
         for (int pl = 0; pl < KD::NBP; ++pl)
           for (int kc = 0; kc < nkc; ++kc)
-            tma_load_2d(bb + (pl * nkc + kc) * kO5BBox, &mp->b[pl], &bfull[bs], KD::AK * kc, tl.z);
+            tma_load_2d(bb + (pl * nkc + kc) * kO5BBox, &mo->b[pl], &bfull[bs], KD::AK * kc, tl.z);
       }
       __syncwarp();
       if (++s == nst) {
@@ -594,12 +602,13 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       const int4 tl = sinfo[s];
       if (tl.x < 0) break;
       if (tl.w & 2) {
-        const O5Maps* mp = maps + tl.x;
+        const O5StreamMaps* ms = smaps + tl.x;
+      const O5OpMaps* mo = omaps + tl.x;
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait(&aempty[ar], arph ^ 1);
           if (elect_one()) {
             mbar_expect_tx(&afull[ar], kO5ABox);
-            tma_load_2d(abuf + ar * kO5ABox, &mp->a, &afull[ar], KD::AK * kc, tl.y);
+            tma_load_2d(abuf + ar * kO5ABox, &mo->a, &afull[ar], KD::AK * kc, tl.y);
           }
           __syncwarp();
           if (++ar == nab) {
@@ -693,8 +702,9 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       fence_async_smem();
       named_bar(1, 256);
       if (et == 0) {
-        const O5Maps* mp = maps + tl.x;
-        for (int q = 0; q < 3; ++q) tma_store_2d(&mp->s[q], st + q * kO5StreamBox, tl.z, tl.y);
+        const O5StreamMaps* ms = smaps + tl.x;
+      const O5OpMaps* mo = omaps + tl.x;
+        for (int q = 0; q < 3; ++q) tma_store_2d(&ms->s[q], st + q * kO5StreamBox, tl.z, tl.y);
         bulk_commit();
         // a stage may be refilled once its stores have read it: release the previous tile's
         // stage (its store group is the older one), keeping the store latency off this path
@@ -780,7 +790,7 @@ struct O5State : PlanExt {
   int* d_ctr = nullptr;
   int64_t* d_aoff = nullptr;
   int64_t* d_boff = nullptr;
-  MapTableCache<O5Maps, 8> maps;  // descriptor tables keyed by the state / operand buffers
+  MapTableCache<O5OpMaps, 3> maps;  // operand descriptors keyed by the staging buffers
 };
 
 bool o5_eligible(const Plan& P, int D, int self_index) {
@@ -922,13 +932,14 @@ static O5State& o5_state(const Plan& P, int D, const SlotRange& R) {
 }
 
 template <bool SELF, bool BF>
-static void launch_o5(const Plan& P, const O5State& S, const O5Maps* maps, int grid, int nbands,
+static void launch_o5(const Plan& P, const O5State& S, const O5StreamMaps* smaps,
+                      const O5OpMaps* maps, int grid, int nbands,
                       int D, int self_index,
                       int mode, float gamma, float beta, int classical, const float* post,
                       dlx_round_stats* stats, cudaStream_t s) {
   smem_optin(reinterpret_cast<const void*>(k_o5<SELF, BF>), 227 * 1024);
   k_o5<SELF, BF><<<grid, BF ? kO5ThreadsTA : kO5Threads, S.smem, s>>>(
-      P.d_t2, maps, S.d_bands, nbands, S.d_ctr, D, S.KA, S.nst, S.nab, S.nbr, S.a_mode,
+      P.d_t2, smaps, maps, S.d_bands, nbands, S.d_ctr, D, S.KA, S.nst, S.nab, S.nbr, S.a_mode,
       self_index, mode, gamma, beta, classical, post, stats);
 }
 
@@ -964,19 +975,28 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
         P.payload_bytes, P.qbits, D, KA, S.bf ? O5Kind<true>::KS : O5Kind<false>::KS, pre, A,
         B[0], B[1]);
   DLX_LAUNCHED();
-  const void* key[8] = {pending, anchor, velocity, mode == DLX_MODE_OVERLAPPED ? local : nullptr,
-                        A, B[0], B[1], nullptr};
-  const O5Maps* maps = S.maps.get(key, P.t2.size(), s, [&](O5Maps* h) {
+  // parameter-stream descriptors: per layout (every rank's plan shares them), all tensors
+  const float* srcs[4] = {pending, anchor, velocity,
+                          mode == DLX_MODE_OVERLAPPED ? local : nullptr};
+  const void* skey[4] = {srcs[0], srcs[1], srcs[2], srcs[3]};
+  auto& scache = layout_ext<MapTableCache<O5StreamMaps, 4>>(*P.layout, "o5_stream_maps");
+  const O5StreamMaps* smaps = scache.get(skey, P.t2.size(), s, [&](O5StreamMaps* h) {
+    for (size_t k = 0; k < P.t2.size(); ++k) {
+      const DevT2& t = P.t2[k];
+      for (int q = 0; q < 4; ++q)
+        if (srcs[q])
+          o5_encode_map(&h[k].s[q], srcs[q] + t.off, t.b, t.a, t.b * 4, kO5TileN, 128,
+                        CU_TENSOR_MAP_SWIZZLE_64B);
+    }
+  });
+  // operand descriptors: per plan state (K), keyed by the staging buffers
+  const void* key[3] = {A, B[0], B[1]};
+  const O5OpMaps* maps = S.maps.get(key, P.t2.size(), s, [&](O5OpMaps* h) {
     const CUtensorMapDataType dt = S.bf ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const uint32_t ak = S.bf ? O5Kind<true>::AK : O5Kind<false>::AK;
     for (size_t k = S.s0; k < static_cast<size_t>(S.s1); ++k) {
       const DevT2& t = P.t2[k];
-      O5Maps& m = h[k];
-      const float* srcs[4] = {pending, anchor, velocity, local};
-      for (int q = 0; q < 4; ++q)
-        if (srcs[q] && (q < 3 || mode == DLX_MODE_OVERLAPPED))
-          o5_encode_map(&m.s[q], srcs[q] + t.off, t.b, t.a, t.b * 4, kO5TileN, 128,
-                        CU_TENSOR_MAP_SWIZZLE_64B);
+      O5OpMaps& m = h[k];
       o5_encode_map(&m.a, static_cast<uint8_t*>(A) + es * S.aoff[k], KA, t.lda, KA * es, ak, 128,
                     CU_TENSOR_MAP_SWIZZLE_128B, dt);
       for (int pl = 0; pl < 2; ++pl)
@@ -995,14 +1015,14 @@ void launch_outer_2d_tc(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* gathe
   KernelTimer timer("k_o5", (mode == DLX_MODE_OVERLAPPED ? 28.0 : 24.0) * S.params, s);
   if (self_index >= 0) {
     if (S.bf)
-      launch_o5<true, true>(P, S, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
+      launch_o5<true, true>(P, S, smaps, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
     else
-      launch_o5<true, false>(P, S, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
+      launch_o5<true, false>(P, S, smaps, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
   } else {
     if (S.bf)
-      launch_o5<false, true>(P, S, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
+      launch_o5<false, true>(P, S, smaps, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
     else
-      launch_o5<false, false>(P, S, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
+      launch_o5<false, false>(P, S, smaps, maps, grid, nbands, D, self_index, mode, gamma, beta, classical, post, stats, s);
   }
   DLX_LAUNCHED();
 }
