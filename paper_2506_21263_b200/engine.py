@@ -365,7 +365,15 @@ class OuterSync:
         """Compress (shared stream per round), exchange, measure, fused outer update."""
         if not self.cfg.compress:
             return self._collective_average_raw(local, mode)
-        return self._sync_finish(self._sync_begin(early_rank=self.side is None), local, mode)
+        return self._sync_finish(self._sync_begin(early_rank=self._early_rank()), local, mode)
+
+    def _early_rank(self) -> bool:
+        """Measure r' before the outer update (the host then has r_{t+1} while the outer
+        update runs): always at N = 1; at N > 1 whenever the controller is applied — the
+        ranks' shards and their sum then run ahead of the outer update instead of beside it
+        (measured: the host-side wait for r' after the outer update cost more than the
+        shard)."""
+        return self.side is None or not self.cfg.hold_rank
 
     def _sync_begin(self, early_rank: bool, xstream=None) -> dict:
         """First half of collective_average (engine.cpp:215-263): compress of the pending
@@ -407,9 +415,9 @@ class OuterSync:
                 # timeline. (The persistent outer-update grid holds every SM, so a side stream
                 # would only serialise behind it.)
                 self._ev("effective_rank")
-                # beside the inner steps (xstream) the ranks split the eigenproblems and sum
-                # the per-tensor results right away (exact: one nonzero term per entry)
-                sharded = xstream is not None and self.er_shards > 1
+                # at N > 1 the ranks split the eigenproblems and sum the per-tensor results
+                # right away (exact: one nonzero term per entry)
+                sharded = self.er_shards > 1
                 self._effective_rank(gathered, r, q, cur, sharded=sharded)
                 if sharded:
                     self._sum_er_shards()
@@ -606,7 +614,7 @@ class OuterSync:
         st = None
         if self.has_pending and self.cfg.overlap and self.cfg.compress:
             if stream is None:
-                st = self._sync_begin(early_rank=self.side is None)
+                st = self._sync_begin(early_rank=self._early_rank())
             else:
                 # compress stays on the main stream (HBM-bound like the inner steps: sharing
                 # the device with them measured slower than running it first); the exchange
