@@ -189,6 +189,7 @@ class OuterSync:
             shard_effective_rank = False
         self.er_shards = world if (shard_effective_rank and world > 1) else 1
         self._bcast_work = None  # in-flight warm-start broadcast (waited before next compress)
+        self._warm_elems = 0     # worker-0 Q elements gathered-but-not-yet-broadcast
         # worker sync through the library's own NCCL communicator (dlx_exchange: all-gather +
         # warm-Q broadcast on its side stream). torch.distributed only bootstraps it (ships
         # rank 0's unique id); DLX_LIB_NCCL=0 keeps the exchange in torch.distributed.
@@ -308,9 +309,11 @@ class OuterSync:
         if self.world == 1:
             return self.payload[:pb]
         if self.lib_comm:
-            return api.exchange(self.L.ctx, self.payload[:pb], self.gathered,
-                                self.warm_q[:qel] if qel else None,
-                                defer_warm=not self.bcast_sync)
+            # worker 0's Q is only needed if the next round is warm (same rank): its broadcast
+            # waits until the controller has decided (_broadcast_warm, before the next
+            # compress) — a rank change skips it
+            self._warm_elems = qel
+            return api.exchange(self.L.ctx, self.payload[:pb], self.gathered, None)
         if self.bcast_sync:
             return exchange(self.payload[:pb], self.gathered, self.warm_q[:qel] if qel else None,
                             self.world, self.group)
@@ -320,6 +323,13 @@ class OuterSync:
             self._bcast_work = dist.broadcast(self.warm_q[:qel], src=0, group=self.group,
                                               async_op=True)
         return g
+
+    def _broadcast_warm(self, r: int):
+        """Broadcast worker 0's float Q as everyone's warm start (engine.cpp:498-501) if this
+        round uses it (warm_rank == r_t, compress.cpp:161); dropped on a rank change."""
+        qel, self._warm_elems = self._warm_elems, 0
+        if qel and self.warm_rank == r:
+            api.exchange(self.L.ctx, self.payload[:0], self.gathered, self.warm_q[:qel])
 
     def _wait_bcast(self):
         if self.lib_comm:
@@ -389,6 +399,8 @@ class OuterSync:
         pb = L.payload_bytes(r, q)
         qel = L.q_factor_elems(r)
         s0 = api.rng_stream(cfg.seed, api.stream_key(0xC09C, self.round))  # engine.cpp:226
+        if self.lib_comm:
+            self._broadcast_warm(r)
         self._wait_bcast()
         self._ev("compress")
         # compress in place over the warm buffer: each rank overwrites it with its own Q,
