@@ -377,13 +377,18 @@ class OuterSync:
             return self._collective_average_raw(local, mode)
         return self._sync_finish(self._sync_begin(early_rank=self._early_rank()), local, mode)
 
+    EARLY_RANK_MAX_K = 64
+
     def _early_rank(self) -> bool:
         """Measure r' before the outer update (the host then has r_{t+1} while the outer
-        update runs): always at N = 1; at N > 1 whenever the controller is applied — the
-        ranks' shards and their sum then run ahead of the outer update instead of beside it
-        (measured: the host-side wait for r' after the outer update cost more than the
-        shard)."""
-        return self.side is None or not self.cfg.hold_rank
+        update runs): always at N = 1; at N > 1 when the controller is applied and the
+        eigenproblems are small (K = N r_t <= 64: a shard takes ~0.2-0.4 ms, less than the
+        host-side wait for r' after the outer update it saves). Larger K (one CTA per tensor:
+        ~1 ms at K = 128, ~3 ms at K = 256 whatever the shard size) stays beside the outer
+        update on the side stream."""
+        if self.side is None:
+            return True
+        return not self.cfg.hold_rank and self.world * self.r_t <= self.EARLY_RANK_MAX_K
 
     def _sync_begin(self, early_rank: bool, xstream=None) -> dict:
         """First half of collective_average (engine.cpp:215-263): compress of the pending
