@@ -377,13 +377,13 @@ class OuterSync:
             return self._collective_average_raw(local, mode)
         return self._sync_finish(self._sync_begin(early_rank=self._early_rank()), local, mode)
 
-    EARLY_RANK_MAX_K = 64
+    EARLY_RANK_MAX_K = 128
 
     def _early_rank(self) -> bool:
         """Measure r' before the outer update (the host then has r_{t+1} while the outer
         update runs): always at N = 1; at N > 1 when the controller is applied and the
-        eigenproblems are small (K = N r_t <= 64: a shard takes ~0.2-0.4 ms, less than the
-        host-side wait for r' after the outer update it saves). Larger K (one CTA per tensor:
+        eigenproblems are small (K = N r_t <= 128: measured faster at N = 2 and 4 than the
+        host-side wait for r' after the outer update). Larger K (one CTA per tensor:
         ~1 ms at K = 128, ~3 ms at K = 256 whatever the shard size) stays beside the outer
         update on the side stream."""
         if self.side is None:
