@@ -64,16 +64,26 @@ __global__ void k_cold_init(const DevT2* T, int nt2, float* q, const int64_t* ba
   if (s0p) s0 = *s0p;
   const int k = blockIdx.y;
   const DevT2 t = T[k];
-  const int64_t total = t.b * t.r;
   const uint64_t base = static_cast<uint64_t>(bases[k]);
-  // walk the column-major destination (coalesced stores); element (i, j) is row-major draw
-  // i * r + j of the tensor's init (Tensor::uniform, tensor.cpp:43-47)
-  const uint32_t b = static_cast<uint32_t>(t.b);
+  // walk the column-major destination in runs of 8 rows (coalesced stores); element (i, j)
+  // is row-major draw i * r + j of the tensor's init (Tensor::uniform, tensor.cpp:43-47), so
+  // down a run the draw counter steps by r * gamma (one 64-bit multiply per run, not per
+  // element: the integer pipe bounds this kernel)
+  const uint32_t runs = static_cast<uint32_t>((t.b + 7) / 8);
+  const int64_t total = static_cast<int64_t>(runs) * t.r;
+  const uint64_t step = static_cast<uint64_t>(t.r) * kGolden;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t j = static_cast<uint32_t>(e) / b, i = static_cast<uint32_t>(e) - j * b;
-    const float u = unit_f(draw_at(s0, base + static_cast<uint64_t>(i) * t.r + j + 1));
-    q[t.qoff + static_cast<int64_t>(j) * t.ldb + i] = __fadd_rn(-1.0f, __fmul_rn(2.0f, u));
+    const uint32_t j = static_cast<uint32_t>(e) / runs;
+    const uint32_t i0 = 8 * (static_cast<uint32_t>(e) - j * runs);
+    uint64_t z = s0 + (base + static_cast<uint64_t>(i0) * t.r + j + 1) * kGolden;
+    float* dst = q + t.qoff + static_cast<int64_t>(j) * t.ldb + i0;
+#pragma unroll
+    for (int u8 = 0; u8 < 8; ++u8, z += step) {
+      if (i0 + u8 >= t.b) break;
+      const float u = unit_f(fmix64(z));
+      dst[u8] = __fadd_rn(-1.0f, __fmul_rn(2.0f, u));
+    }
   }
 }
 
@@ -81,7 +91,7 @@ void launch_cold_init(const Plan& P, float* q, const int64_t* d_bases, uint64_t 
                       cudaStream_t s, const uint64_t* s0p) {
   if (P.t2.empty()) return;
   int64_t mx = 1;
-  for (const DevT2& t : P.t2) mx = std::max(mx, t.b * t.r);
+  for (const DevT2& t : P.t2) mx = std::max(mx, ceil_div(t.b, 8) * t.r);
   const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 512));
   k_cold_init<<<dim3(gx, P.t2.size()), 256, 0, s>>>(P.d_t2, (int)P.t2.size(), q, d_bases, s0,
                                                    s0p);
