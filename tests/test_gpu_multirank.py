@@ -152,3 +152,53 @@ def test_cpp_worker_processes_match_python_engine(tmp_path):
     assert np.array_equal(p0, c0), "C++ host and Python host disagree"
     rp_cpp = [int(line.split()[2]) for line in open(tmp_path / "cpp0.txt")]
     assert rp_cpp == json.load(open(tmp_path / "py0.json"))
+
+
+XCHG_WORKER = r'''
+import os, sys
+sys.path.insert(0, os.environ["DLX_ROOT"])
+import torch, torch.distributed as dist
+from paper_2506_21263_b200 import api
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("nccl", device_id=torch.device(f"cuda:{rank}"))
+ctx = api.Context(rank)
+api.ensure_comm(ctx, rank, world)
+pb = 1000003
+pay = torch.full((pb,), rank + 1, dtype=torch.uint8, device="cuda")
+gat = torch.zeros(world * pb, dtype=torch.uint8, device="cuda")
+wq = torch.full((77777,), float(rank + 10), device="cuda")
+side = torch.cuda.Stream()
+with torch.cuda.stream(side):
+    api.exchange(ctx, pay, gat, wq, defer_warm=True)   # broadcast joined later
+    ctx.wait_warm()
+    out = torch.zeros(1, dtype=torch.int32, device="cuda")
+torch.cuda.current_stream().wait_stream(side)
+ok = all(bool((gat[w * pb:(w + 1) * pb] == w + 1).all()) for w in range(world))
+ok = ok and bool((wq == 10.0).all())
+# the all-gather helper and the exact f64 sum used by the effective-rank shards
+x = torch.full((5,), float(rank + 1), dtype=torch.float64, device="cuda")
+api.comm_allreduce_sum_f64(ctx, x)
+ok = ok and bool((x == world * (world + 1) / 2).all())
+ctx.comm_check()
+torch.cuda.synchronize()
+open(os.path.join(os.environ["DLX_OUT"], f"x{rank}"), "w").write("ok" if ok else "bad")
+dist.barrier()
+dist.destroy_process_group()
+'''
+
+
+def test_library_exchange_primitives(tmp_path):
+    """dlx_exchange (all-gather in worker order + worker-0 broadcast, deferred and joined with
+    dlx_exchange_wait_warm), dlx_comm_allreduce_sum_f64 and dlx_comm_check over two ranks."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    script = tmp_path / "xworker.py"
+    script.write_text(XCHG_WORKER)
+    env = dict(os.environ, DLX_ROOT=ROOT, DLX_OUT=str(tmp_path))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29551", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert [open(tmp_path / f"x{k}").read() for k in range(2)] == ["ok", "ok"]
