@@ -165,10 +165,11 @@ dlx_status dlx_comm_init(dlx_ctx* ctx, int rank, int world, const void* uid) {
 }
 
 dlx_status dlx_comm_info(const dlx_ctx* ctx, int* rank, int* world) {
-  if (!ctx) return DLX_ERR_VALIDATION;
-  if (rank) *rank = ctx->comm ? ctx->comm->rank : 0;
-  if (world) *world = ctx->comm ? ctx->comm->world : 1;
-  return DLX_OK;
+  return guard([&] {
+    if (!ctx) raise(DLX_ERR_VALIDATION, "null context");
+    if (rank) *rank = ctx->comm ? ctx->comm->rank : 0;
+    if (world) *world = ctx->comm ? ctx->comm->world : 1;
+  });
 }
 
 dlx_status dlx_exchange(dlx_ctx* ctx, const uint8_t* d_payload, int64_t payload_bytes,
@@ -267,14 +268,15 @@ dlx_status dlx_comm_check(dlx_ctx* ctx) {
 }
 
 dlx_status dlx_comm_destroy(dlx_ctx* ctx) {
-  if (!ctx) return DLX_ERR_VALIDATION;
-  if (ctx->comm) {
-    cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->comm->side);
-    delete ctx->comm;
-    ctx->comm = nullptr;
-  }
-  return DLX_OK;
+  return guard([&] {
+    if (!ctx) raise(DLX_ERR_VALIDATION, "null context");
+    if (ctx->comm) {
+      DLX_CUDA(cudaSetDevice(ctx->device));
+      DLX_CUDA(cudaStreamSynchronize(ctx->comm->side));
+      delete ctx->comm;
+      ctx->comm = nullptr;
+    }
+  });
 }
 
 }  // extern "C"
