@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compress", action="store_true",
                     help="dilocox-no-compress ablation: raw fp32 exchange (compress_raw)")
+    ap.add_argument("--option", action="append", default=[], metavar="KEY=VALUE",
+                    help="dlx_set_option before the run (A/B: e.g. cholqr_blocked=0)")
     ap.add_argument("--side-stream", type=int, default=None,
                     help="1/0: run the effective-rank measurement on a side stream (default: "
                          "on when N > 1, where the ranks split the eigenproblems)")
@@ -299,6 +301,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     dev = f"cuda:{local_rank}"
     ctx = api.Context(local_rank)
+    for kv in args.option:
+        k, v = kv.split("=", 1)
+        api.set_option(k, int(v))
     table = layouts.CONFIGS[args.config]()
     L = api.Layout(ctx, table)
     P = L.total_params
@@ -537,6 +542,7 @@ def main():
                        "mode": "overlapped (one-step delay)", "parallelism": f"dp{world}",
                        "payload_bytes": recs[-1].payload_bytes if recs else None,
                        "l2": "inputs (>=5 GB slabs) larger than L2; no flush",
+                       **({"options": args.option} if args.option else {}),
                        "phase_ms": phases,
                        **({"phase_ms_per_rank": phases_per_rank} if phases_per_rank else {})},
             "roofline": roofline,

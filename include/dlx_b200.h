@@ -283,8 +283,10 @@ dlx_status dlx_parse(const dlx_layout* layout, int rank, int qbits, const uint8_
  * "outer_tensor_cores" (default 1): 0 runs the fused outer update with the SIMT factor GEMM
  * instead of the tcgen05/TMA kernel (env DLX_OUTER_TC=0). "kernel_events" (default 0): 1
  * brackets each launch of the dominant kernels (k_o5, k_tc_sweep K1/K2) with CUDA events on
- * the launching stream, for dlx_kernel_time. "effrank_big_from" (default 128): effective-rank
- * eigenproblems with K = D * r above this size run the blocked large-K kernel. */
+ * the launching stream, for dlx_kernel_time. "effrank_big_from" (default 96): effective-rank
+ * eigenproblems with K = D * r above this size run the blocked large-K kernel.
+ * "cholqr_blocked" (default 1): 0 factors 32 < r <= 128 CholQR Grams with the unblocked
+ * shared-memory kernel instead of the blocked DMMA one. */
 dlx_status dlx_set_option(const char* key, int value);
 
 /* Device time (ms, from the CUDA events), algorithmic HBM bytes and launch count of every

@@ -396,6 +396,8 @@ dlx_status dlx_set_option(const char* key, int value) {
       option_outer_tc() = value != 0;
     } else if (k == "effrank_big_from") {
       option_effrank_big_from() = value;
+    } else if (k == "cholqr_blocked") {
+      option_cholblk() = value != 0;
     } else if (k == "kernel_events") {
       g_kernel_events = value != 0;
     } else {

@@ -336,6 +336,7 @@ void launch_k2_tc(const Plan& P, const float* slab, const float* p, float* z, fl
 bool& option_tensor_cores();
 bool& option_outer_tc();
 int& option_effrank_big_from();
+bool& option_cholblk();
 
 // Optional CUDA-event timing of the dominant kernels (dlx_set_option("kernel_events", 1)):
 // events recorded on the launching stream around one launch, with the launch's algorithmic

@@ -320,8 +320,11 @@ __global__ void __launch_bounds__(256) k_code_gram_mma(const DevT2* __restrict__
 // Grams come either as fp64 matrices (GA, GB; row stride rr) or as integer code Grams (GI,
 // upper triangle, stride rr) scaled by the payload's column scales.
 __device__ long long g_er_prof[16];
-int& option_effrank_big_from() {  // K above which k_effrank_big runs (dlx_set_option)
-  static int v = 128;
+// K above which k_effrank_big runs (dlx_set_option). 96: tools/er_bigfrom.py on B200 —
+// K = 128: blocked 0.82 vs 1.11 ms (Llama-7B layer, r = 128), 1.08 vs 1.12 ms (OPT-1.3B,
+// D = 4); K = 96 on OPT-1.3B (D = 3): 0.76 vs 0.71 ms, so the unblocked kernel keeps K <= 96
+int& option_effrank_big_from() {
+  static int v = 96;
   return v;
 }  // experiments (DLX_ER_PROF): phase cycles of block 0
 constexpr int kErAllSmem = 64;   // n <= 64: L, G_A L, M staged in shared memory
@@ -642,7 +645,11 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
       if (L > 0) blo = s_lo;
       if (L < G) bhi = s_hi;
     }
-    if (l == 0 && idx < n && tid < lanes) ev[n - 1 - idx] = fmax(0.5 * (blo + bhi), 0.0);
+    // (an all-zero M — an all-zero exchange — has exactly zero eigenvalues: without the
+    // guard the bisection midpoint of the [-1e-300, 1e-300] bracket leaves a denormal-size
+    // energy and the reduce would not flag the round all-zero)
+    if (l == 0 && idx < n && tid < lanes)
+      ev[n - 1 - idx] = amax > 0.0 ? fmax(0.5 * (blo + bhi), 0.0) : 0.0;
   }
   __syncthreads();
   ER_MARK(4);

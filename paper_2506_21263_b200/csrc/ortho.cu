@@ -42,7 +42,11 @@ static void make_job(const Plan& P, GramJob* J, const std::vector<DevMat>& mats)
       const char* e = getenv("DLX_GRAM_SPLIT");
       return static_cast<int64_t>(e ? atoi(e) : 512);
     }();
-    const int64_t ns = std::max<int64_t>(1, ceil_div(m.n, split_rows));
+    // at most kMaxParts row splits per factor: the Cholesky kernels fold an entry's partials
+    // in one CTA, so the longest factor (the 50272-row embedding: ~100 splits of 512 rows)
+    // set the whole launch's duration
+    constexpr int64_t kMaxParts = 32;
+    const int64_t ns = std::max<int64_t>(1, std::min(kMaxParts, ceil_div(m.n, split_rows)));
     const int64_t rows = round_up(ceil_div(m.n, ns), 32);
     J->part0.push_back(J->total_parts);
     int cnt = 0;
@@ -603,10 +607,106 @@ __global__ void __launch_bounds__(kChol128Threads) k_chol128(const DevMat* __res
   }
 }
 
+// Branch-free fp64 1/sqrt: MUFU seed + three Newton steps. (The library rsqrt carries a
+// special-case branch, which splits the basic block and keeps the scheduler from overlapping
+// the next pivot's square root with the current trailing update.)
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double h = 0.5 * d;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+// Shared-memory scratch of one warp_chol_inv<RR>: the current pivot row of R (double-
+// buffered, zeros in front) and R^T with RR zeros in front of every row.
+template <int RR>
+struct CholScratch {
+  static constexpr int LT = 2 * RR + 2;  // R^T row stride (doubles; rows 16-B aligned)
+  double row[2][64];
+  double rt[RR * LT];
+};
+
+// One warp factors the RR x RR (RR <= 32) symmetric block whose upper triangle sits in
+// shared memory at G (row stride ldg) as G = R^T R and inverts R. Lane c owns column c; the
+// step loops are ROLLED with a register window that shifts by one row per step (position
+// i = row j + i), so every register index stays static (fully unrolled, the factorisation +
+// inversion was ~10k instructions run by ONE warp per SM: instruction-cache misses were
+// half of its time). tools/micro/chol_micro.cu measures the variants (B200, one 32 x 32
+// factor + inverse per SM): unrolled shuffles 33 us, rolled shuffles 16.9 us, this 12.1 us.
+//   factor: row j of R goes through shared memory (broadcast loads instead of shuffles);
+//           the next pivot is updated first and its rsqrt issued before the rest of the
+//           trailing update (lookahead: the two dependent chains overlap);
+//   invert: right-looking back substitution from the bottom — once x_k = R^-1[k][c] is known
+//           every partial sum of the rows above takes its fma, column k of R read as one
+//           contiguous clamp-free run of R^T, so the dependent chain is two ops per step;
+//           put(k, x_k) receives row k of column c.
+// rf / xf: this lane's ||R[:,c]||^2 / ||R^-1[:,c]||^2 for columns c < r; dinv[j] = 1/R[j][j].
+// Returns the (warp-uniform) pivot failure (some pivot <= thr).
+template <int RR, typename Put>
+__device__ __forceinline__ bool warp_chol_inv(const double* G, int ldg, int r, double thr,
+                                              double* dinv, CholScratch<RR>& sc, Put put,
+                                              double& rf, double& xf) {
+  constexpr int LT = CholScratch<RR>::LT;
+  const int c = threadIdx.x & 31;
+  const bool own = c < RR;
+  double w[RR];  // w[i] = W[j + i][c]
+#pragma unroll
+  for (int i = 0; i < RR; ++i) w[i] = (i <= c && own) ? G[i * ldg + c] : 0.0;
+  for (int i = c; i < RR * LT; i += 32) sc.rt[i] = 0.0;
+  sc.row[0][c] = sc.row[1][c] = 0.0;
+  bool bad = false;
+  rf = 0.0;
+  double d = __shfl_sync(0xffffffffu, w[0], 0);
+  double inv = rsqrt_nr(d);
+#pragma unroll 1
+  for (int j = 0; j < RR; ++j) {
+    bad |= !(d > thr);
+    const double rj = c == j ? d * inv : w[0] * inv;  // R[j][c] (0 for c < j)
+    if (c == j) dinv[j] = inv;
+    if (own) {
+      sc.row[j & 1][32 + c] = rj;
+      sc.rt[c * LT + RR + j] = rj;
+    }
+    if (c < r) rf = fma(rj, rj, rf);
+    __syncwarp();
+    const double* rr = &sc.row[j & 1][32 + j];  // rr[i] = R[j][j + i]
+    const double r1 = (j + 1 < RR) ? rr[1] : 0.0;
+    w[0] = (j + 1 <= c) ? fma(-r1, rj, w[1]) : w[1];
+    const double dn = __shfl_sync(0xffffffffu, w[0], (j + 1) & 31);
+    const double invn = rsqrt_nr(dn);
+#pragma unroll
+    for (int i = 2; i < RR; ++i) {  // W[j+i][c] -= R[j][j+i] R[j][c]  (j + i <= c), shifted
+      const double rji = (j + i < RR) ? rr[i] : 0.0;
+      w[i - 1] = (j + i <= c) ? fma(-rji, rj, w[i]) : w[i];
+    }
+    w[RR - 1] = 0.0;
+    d = dn;
+    inv = invn;
+  }
+  if (__any_sync(0xffffffffu, bad)) return true;
+  __syncwarp();  // R^T and dinv visible to the whole warp
+  double sacc[RR];  // sacc[i] = partial sum of row k - i
+#pragma unroll
+  for (int i = 0; i < RR; ++i) sacc[i] = 0.0;
+  xf = 0.0;
+#pragma unroll 1
+  for (int k = RR - 1; k >= 0; --k) {
+    const double xk = ((k == c ? 1.0 : 0.0) - sacc[0]) * dinv[k];
+    put(k, xk);
+    if (c < r) xf = fma(xk, xk, xf);
+    const double* col = sc.rt + k * LT + RR + k;  // col[-i] = R[k - i][k] (0 above row 0)
+#pragma unroll
+    for (int i = 1; i < RR; ++i) sacc[i - 1] = fma(col[-i], xk, sacc[i]);
+    sacc[RR - 1] = 0.0;
+  }
+  return false;
+}
+
 // r <= 32 fast path: the partial Grams are folded by the whole CTA, then one warp factors
-// in registers — lane c holds column c of the (upper) matrix, the pivot row is broadcast
-// with shuffles, so a step costs no block barrier — and inverts R from shared memory (lane
-// c back-substitutes column c of R^-1). Same pivot test / flags / need2 as k_chol.
+// and inverts (warp_chol_inv). Same pivot test / flags / need2 as k_chol.
 template <int RR>
 __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
                                                 const int* __restrict__ part0,
@@ -618,6 +718,7 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
                                                 const int* __restrict__ only) {
   __shared__ double G[RR][RR + 1];
   __shared__ double dinv[RR];
+  __shared__ __align__(16) CholScratch<RR> scr;
   const int e = blockIdx.x;
   if (only && !only[e]) {
     if (threadIdx.x == 0) {
@@ -631,89 +732,67 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
   const double* src = partial + (int64_t)part0[e] * rr * rr;
   const int np = nparts[e];
   // fold; columns >= r are padded with the identity so the factorisation below runs all RR
-  // (8 / 16 / 32, the rank rounded up) steps without data-dependent branches
-  // (8 independent partial sums per element: the row-split partials are L2 reads, and a
-  // single dependent chain over ~100 of them made this fold the kernel's whole cost)
-  for (int idx = threadIdx.x; idx < RR * RR; idx += blockDim.x) {
-    const int j = idx / RR, k = idx % RR;
-    double g = (j == k && j >= r) ? 1.0 : 0.0;
-    if (j < r && k < r && k >= j) {
-      const double* sp = src + j * rr + k;
-      const int64_t st = (int64_t)rr * rr;
-      double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      int p = 0;
-      for (; p + 8 <= np; p += 8)
+  // (8 / 16 / 32, the rank rounded up) steps without data-dependent branches. The kernel
+  // lasts as long as its slowest entry — the one with the most row-split partials (~100 for
+  // the 50272-row embedding) — so every thread keeps kU elements x 8 partials of loads in
+  // flight per step (unconditional loads at clamped addresses, masked in the fma).
+  constexpr int kU = (RR * RR + 255) / 256;
+  {
+    const int64_t st = (int64_t)rr * rr;
+    int off[kU];
+    double msk[kU], acc[kU][2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] += sp[(p + u) * st];
-      for (; p < np; ++p) a[p & 7] += sp[p * st];
-      g += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    for (int u = 0; u < kU; ++u) {
+      const int idx = threadIdx.x + 256 * u;
+      const int j = idx / RR, k = idx % RR;
+      const bool live = idx < RR * RR && j < r && k < r && k >= j;
+      off[u] = live ? j * rr + k : 0;
+      msk[u] = live ? 1.0 : 0.0;
+      acc[u][0] = acc[u][1] = 0.0;
     }
-    G[j][k] = g;
+    int p = 0;
+    for (; p + 8 <= np; p += 8) {
+      double v[kU][8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u][q] = __ldg(src + (p + q) * st + off[u]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[u][q & 1] = fma(msk[u], v[u][q], acc[u][q & 1]);
+    }
+    for (; p < np; ++p)
+#pragma unroll
+      for (int u = 0; u < kU; ++u) acc[u][0] = fma(msk[u], __ldg(src + p * st + off[u]), acc[u][0]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = threadIdx.x + 256 * u;
+      const int j = idx / RR, k = idx % RR;
+      if (idx < RR * RR) G[j][k] = (j == k && j >= r) ? 1.0 : acc[u][0] + acc[u][1];
+    }
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int c = threadIdx.x;  // lanes >= RR idle along (their columns stay zero)
-  double w[RR];
-#pragma unroll
-  for (int i = 0; i < RR; ++i) w[i] = (i <= c && c < RR) ? G[i][c] : 0.0;  // column c, upper
   double mx = 0.0;
   for (int j = 0; j < r; ++j) mx = fmax(mx, G[j][j]);
   const double tol = 1e-7 * fmax(1.0, sqrt(mx));
   const double thr = (10.0 * tol) * (10.0 * tol);
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < RR; ++j) {
-    const double d = __shfl_sync(0xffffffffu, w[j], j);  // W[j][j] from lane j
-    bad |= !(d > thr);
-    const double rjj = sqrt(d);
-    const double inv = 1.0 / rjj;
-    if (c == j) {
-      w[j] = rjj;
-      dinv[j] = inv;
-    }
-    if (c > j) w[j] *= inv;  // R[j][c]
-#pragma unroll
-    for (int i = j + 1; i < RR; ++i) {  // W[i][c] -= R[j][i] R[j][c], j < i <= c
-      const double rji = __shfl_sync(0xffffffffu, w[j], i);
-      if (i <= c) w[i] = fma(-rji, w[j], w[i]);
-    }
-  }
-  const int flag = __any_sync(0xffffffffu, bad) ? 1 : 0;
+  double rf = 0.0, xf = 0.0;
+  double* X = rinv + (int64_t)e * rr * rr;
+  const int flag = warp_chol_inv<RR>(&G[0][0], RR + 1, r, thr, dinv, scr,
+                                     [&](int k, double v) {
+                                       if (k < r && c < r) X[k * rr + c] = v;
+                                     },
+                                     rf, xf)
+                       ? 1
+                       : 0;
   if (c == 0) flags[e] = flag;
   if (flag) {
     if (need2 && c == 0) need2[e] = 0;
     return;
   }
-  __syncwarp();
-  if (c < RR) {
-#pragma unroll
-    for (int i = 0; i < RR; ++i) G[i][c] = (i <= c) ? w[i] : 0.0;  // R, upper
-  }
-  __syncwarp();
-  // X = R^-1: lane c solves R x = e_c by back substitution (rolled over i)
-  double x[RR];
-  const int cc = c < RR ? c : RR - 1;
-#pragma unroll
-  for (int i = 0; i < RR; ++i) x[i] = (i == c) ? dinv[cc] : 0.0;
-#pragma unroll
-  for (int i = RR - 2; i >= 0; --i) {
-    double sum = 0.0;
-#pragma unroll
-    for (int k = i + 1; k < RR; ++k) sum = fma(G[i][k], x[k], sum);
-    if (i < c) x[i] = -sum * dinv[i];
-  }
-  double xf = 0.0, rf = 0.0;
-  if (c < r) {
-#pragma unroll
-    for (int i = 0; i < RR; ++i) {
-      xf = fma(x[i], x[i], xf);
-      rf = fma(G[i][c], G[i][c], rf);
-    }
-  }
-  double* X = rinv + (int64_t)e * rr * rr;
-#pragma unroll
-  for (int i = 0; i < RR; ++i)
-    if (i < r && c < r) X[i * rr + c] = x[i];
   if (need2) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -721,6 +800,252 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
       rf += __shfl_xor_sync(0xffffffffu, rf, o);
     }
     if (c == 0) need2[e] = (sqrt(xf) * sqrt(rf) > 2e3) ? 1 : 0;
+  }
+}
+
+// 32 < r <= 128, blocked (RR = 32 NB, the rank padded with the identity): the whole
+// factorisation in shared memory, 32-wide panels. Per panel p: one warp factors and inverts
+// the diagonal block (warp_chol_inv), the CTA forms the panel row R_pq = R_pp^-T W_pq and
+// the trailing update W_qq' -= R_pq^T R_pq' on the fp64 tensor cores (DMMA m8n8k4); then
+// R^-1 block row by block row from the bottom, X_ij = -R_ii^-1 sum_{k=i+1..j} R_ik X_kj
+// (DMMA). The serial part is NB warp factorisations instead of r barrier-separated steps.
+constexpr int kCholBlkThreads = 256;
+
+__host__ __device__ constexpr size_t cholblk_smem(int NB) {
+  return sizeof(double) * (static_cast<size_t>(32 * NB) * (32 * NB + 1) + 2 * NB * 32 * 33) +
+         sizeof(CholScratch<32>);
+}
+
+// D (8x8 tile at row m0, col n0 of a 32-row block product) = sum over k < kn of A[m][k] B[k][n]
+// for A, B given as element accessors; fragments of dmma_8x8x4.
+template <typename FA, typename FB>
+__device__ __forceinline__ void dmma_tile(double (&d)[2], int kn, FA fa, FB fb) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < kn; k += 4) dmma_8x8x4(d, fa(lane >> 2, k + (lane & 3)), fb(k + (lane & 3), lane >> 2));
+}
+
+// warp 0's share of a panel: factor + invert the diagonal block, R_pp^-1 into Xo. (Kept out of
+// line: inlined into the panel loop, the register arrays of warp_chol_inv were demoted to
+// local memory.)
+template <int LD, int XL>
+__device__ __noinline__ double diag_block(const double* G, int r, double thr, double* dinv,
+                                         CholScratch<32>& sc, double* Xo, int* flag) {
+  const int lane = threadIdx.x & 31;
+  double rfp = 0.0, xfp = 0.0;
+  const bool bad = warp_chol_inv<32>(G, LD, r, thr, dinv, sc,
+                                     [&](int k, double v) { Xo[k * XL + lane] = v; }, rfp, xfp);
+  if (lane == 0) *flag = bad ? 1 : 0;
+  return bad ? 0.0 : rfp;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kCholBlkThreads, 1) k_cholblk(const DevMat* __restrict__ mats,
+                                                             const int* __restrict__ part0,
+                                                             const int* __restrict__ nparts,
+                                                             int rr,
+                                                             const double* __restrict__ partial,
+                                                             double* __restrict__ rinv,
+                                                             int* __restrict__ flags,
+                                                             int* __restrict__ need2,
+                                                             const int* __restrict__ only) {
+  constexpr int RR = 32 * NB, LD = RR + 1, XL = 33;
+  constexpr int NW = kCholBlkThreads / 32;
+  extern __shared__ __align__(16) double cb_smem[];
+  double* W = cb_smem;              // [RR][LD]: G, then R (upper), then R^-1 off the diagonal
+  double* Xd = W + RR * LD;         // [NB][32][XL]: R_pp^-1
+  double* Tb = Xd + NB * 32 * XL;   // [NB][32][XL]: block-row temporaries
+  auto* scr = reinterpret_cast<CholScratch<32>*>(Tb + NB * 32 * XL);  // warp 0's scratch
+  __shared__ double dinv[32];
+  __shared__ double red[2][NW];
+  __shared__ int s_flag;
+  const int e = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (only && !only[e]) {
+    if (tid == 0) {
+      flags[e] = 0;
+      if (need2) need2[e] = 0;
+    }
+    return;
+  }
+  const DevMat m = mats[e];
+  const int r = m.r;
+  const double* src = partial + (int64_t)part0[e] * rr * rr;
+  const int np = nparts[e];
+  const int64_t st = (int64_t)rr * rr;
+  // fold: 16 elements per thread per pass, the partials outermost (16 independent loads in
+  // flight per step); identity padding past r
+  constexpr int kU = 16;
+  for (int base = 0; base < RR * RR; base += kU * kCholBlkThreads) {
+    double acc[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc[u] = 0.0;
+    // element offsets (clamped to a valid address where the element is not folded) and
+    // masks computed once: the loads are unconditional, so all kU of a step issue together
+    int off[kU];
+    double msk[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = base + u * kCholBlkThreads + tid;
+      const int j = idx / RR, k = idx % RR;
+      const bool live = idx < RR * RR && j < r && k < r && k >= j;
+      off[u] = live ? j * rr + k : 0;
+      msk[u] = live ? 1.0 : 0.0;
+    }
+    for (int p = 0; p < np; ++p) {
+      const double* sp = src + p * st;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) acc[u] = fma(msk[u], __ldg(sp + off[u]), acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = base + u * kCholBlkThreads + tid;
+      const int j = idx / RR, k = idx % RR;
+      if (idx < RR * RR) W[j * LD + k] = (j == k && j >= r) ? 1.0 : acc[u];
+    }
+  }
+  __syncthreads();
+  double mx = 0.0;
+  for (int j = 0; j < r; ++j) mx = fmax(mx, W[j * LD + j]);
+  const double tol = 1e-7 * fmax(1.0, sqrt(mx));
+  const double thr = (10.0 * tol) * (10.0 * tol);
+  double rf = 0.0;  // ||R||_F^2 (columns < r), lane-partial
+#pragma unroll 1
+  for (int p = 0; p < NB; ++p) {
+    const int o = 32 * p;
+    if (warp == 0) {
+      const double rfp = diag_block<LD, XL>(W + o * LD + o, r - o, thr, dinv, *scr,
+                                            Xd + p * 32 * XL, &s_flag);
+      rf += rfp;
+    }
+    __syncthreads();
+    if (s_flag) {
+      if (tid == 0) {
+        flags[e] = 1;
+        if (need2) need2[e] = 0;
+      }
+      return;
+    }
+    if (p == NB - 1) break;
+    const int q0 = o + 32, nq = RR - q0;  // trailing columns
+    // panel row: R[o+i][q0+n] = sum_k Xd[p][k][i] W[o+k][q0+n]   (k <= i); its squares
+    // (columns < r) join ||R||_F^2 here, before the inversion overwrites these blocks
+    {
+      constexpr int kSlots = 2 * (NB - 1);  // >= ceil(16 (NB - 1) / NW) tiles per warp
+      const int ntn = nq / 8, ntiles = 4 * ntn;
+      double dres[kSlots][2];
+#pragma unroll
+      for (int it = 0; it < kSlots; ++it) {
+        const int t = warp + it * NW;
+        dres[it][0] = dres[it][1] = 0.0;
+        if (t < ntiles) {
+          const int ti = t / ntn, tj = t % ntn;
+          const double* xa = Xd + p * 32 * XL;
+          dmma_tile(dres[it], 8 * ti + 8,
+                    [&](int mm, int k) { return xa[k * XL + 8 * ti + mm]; },
+                    [&](int k, int n) { return W[(o + k) * LD + q0 + 8 * tj + n]; });
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int it = 0; it < kSlots; ++it) {
+        const int t = warp + it * NW;
+        if (t < ntiles) {
+          const int ti = t / ntn, tj = t % ntn;
+          const int col = q0 + 8 * tj + 2 * (lane & 3);
+          double* dst = W + (o + 8 * ti + (lane >> 2)) * LD + col;
+          dst[0] = dres[it][0];
+          dst[1] = dres[it][1];
+          if (col < r) rf = fma(dres[it][0], dres[it][0], rf);
+          if (col + 1 < r) rf = fma(dres[it][1], dres[it][1], rf);
+        }
+      }
+      __syncthreads();
+    }
+    // trailing update (upper tile triangle): W[a][b] -= sum_k R[o+k][a] R[o+k][b]
+    {
+      const int mt = nq / 8, ntiles = mt * (mt + 1) / 2;
+      for (int t = warp; t < ntiles; t += NW) {
+        int ti = 0, rem = t;
+        while (rem >= mt - ti) {
+          rem -= mt - ti;
+          ++ti;
+        }
+        const int tj = ti + rem;
+        double* dst = W + (q0 + 8 * ti + (lane >> 2)) * LD + q0 + 8 * tj + 2 * (lane & 3);
+        double d[2] = {0.0, 0.0};
+        dmma_tile(d, 32,
+                  [&](int mm, int k) { return W[(o + k) * LD + q0 + 8 * ti + mm]; },
+                  [&](int k, int n) { return W[(o + k) * LD + q0 + 8 * tj + n]; });
+        dst[0] -= d[0];
+        dst[1] -= d[1];
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) flags[e] = 0;
+  // R^-1 off the diagonal, block rows from the bottom; X_kj (k > i) already sits in W
+#pragma unroll 1
+  for (int i = NB - 2; i >= 0; --i) {
+    const int nj = NB - 1 - i;  // blocks j = i+1 .. NB-1
+    // T_j = sum_{k=i+1..j} R_ik X_kj
+    for (int t = warp; t < nj * 16; t += NW) {
+      const int jb = i + 1 + t / 16, ti = (t % 16) / 4, tj = t % 4;
+      double d[2] = {0.0, 0.0};
+      for (int kb = i + 1; kb <= jb; ++kb) {
+        const double* xb = kb == jb ? Xd + jb * 32 * XL : nullptr;
+        dmma_tile(d, 32,
+                  [&](int mm, int k) { return W[(32 * i + 8 * ti + mm) * LD + 32 * kb + k]; },
+                  [&](int k, int n) {
+                    return xb ? xb[k * XL + 8 * tj + n] : W[(32 * kb + k) * LD + 32 * jb + 8 * tj + n];
+                  });
+      }
+      double* dst = Tb + (jb * 32 + 8 * ti + (lane >> 2)) * XL + 8 * tj + 2 * (lane & 3);
+      dst[0] = d[0];
+      dst[1] = d[1];
+    }
+    __syncthreads();
+    // X_ij = -R_ii^-1 T_j  (R_ii^-1 upper: k >= row)
+    for (int t = warp; t < nj * 16; t += NW) {
+      const int jb = i + 1 + t / 16, ti = (t % 16) / 4, tj = t % 4;
+      double d[2] = {0.0, 0.0};
+      const double* xa = Xd + i * 32 * XL;
+      const double* tb = Tb + jb * 32 * XL;
+      dmma_tile(d, 32,
+                [&](int mm, int k) { return xa[(8 * ti + mm) * XL + k]; },
+                [&](int k, int n) { return tb[k * XL + 8 * tj + n]; });
+      double* dst = W + (32 * i + 8 * ti + (lane >> 2)) * LD + 32 * jb + 8 * tj + 2 * (lane & 3);
+      dst[0] = -d[0];
+      dst[1] = -d[1];
+    }
+    __syncthreads();
+  }
+  double xf = 0.0;
+  double* X = rinv + (int64_t)e * rr * rr;
+  for (int idx = tid; idx < r * r; idx += kCholBlkThreads) {
+    const int i = idx / r, k = idx % r;
+    double v = 0.0;
+    if (k >= i) v = (i >> 5) == (k >> 5) ? Xd[((i >> 5) * 32 + (i & 31)) * XL + (k & 31)] : W[i * LD + k];
+    xf = fma(v, v, xf);
+    X[i * rr + k] = v;
+  }
+  if (need2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      xf += __shfl_xor_sync(0xffffffffu, xf, o);
+      rf += __shfl_xor_sync(0xffffffffu, rf, o);
+    }
+    if (lane == 0) {
+      red[0][warp] = xf;
+      red[1][warp] = rf;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double xs = 0.0, rs = 0.0;
+      for (int w = 0; w < NW; ++w) {
+        xs += red[0][w];
+        rs += red[1][w];
+      }
+      need2[e] = (sqrt(xs) * sqrt(rs) > 2e3) ? 1 : 0;
+    }
   }
 }
 
@@ -1036,6 +1361,13 @@ static void launch_apply(const GramJob& J, int rr, const double* rinv, const int
   DLX_LAUNCHED();
 }
 
+// dlx_set_option("cholqr_blocked", 0) selects the unblocked shared-memory k_chol128 for
+// 32 < r <= 128 (A/B measurements and cross-checks)
+bool& option_cholblk() {
+  static bool on = true;
+  return on;
+}
+
 static void launch_chol(const GramJob& J, int rr, const double* partial, double* work,
                         double* rinv, int* flags, int* need2, const int* only, size_t csm,
                         cudaStream_t s) {
@@ -1052,6 +1384,19 @@ static void launch_chol(const GramJob& J, int rr, const double* partial, double*
     else
       k_chol32<32><<<ne, 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, rinv, flags,
                                       need2, only);
+  } else if (rr <= 128 && option_cholblk()) {
+    auto go = [&](auto kern, int nb) {
+      const int smem = static_cast<int>(cholblk_smem(nb));
+      smem_optin(reinterpret_cast<const void*>(kern), smem);
+      kern<<<ne, kCholBlkThreads, smem, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, rinv,
+                                             flags, need2, only);
+    };
+    if (rr <= 64)
+      go(k_cholblk<2>, 2);
+    else if (rr <= 96)
+      go(k_cholblk<3>, 3);
+    else
+      go(k_cholblk<4>, 4);
   } else if (rr <= 128) {
     const int smem = static_cast<int>(sizeof(double) * rr * (rr + 1));
     smem_optin(reinterpret_cast<const void*>(k_chol128), smem);

@@ -227,17 +227,17 @@ def test_compress_against_oracle(ctx, oracle, golden, tname, q, rnd):
     _check_compress(L, t, oracle, ref_w, res_w, rank, q, st0)
 
 
-def _check_compress(L, t, oracle, ref, res, rank, q, st0):
+def _check_compress(L, t, oracle, ref, res, rank, q, st0, scale_rtol=1e-5, q_tols=None):
     codes, scales = decode_payload(L, res.payload, rank, q)
     assert int(res.draws.item()) == draws_between(st0, ref["state"])
     assert (codes == ref["codes"]).mean() >= 0.999
     qs = L.factors_from_device(res.q_factors, rank, 1)
-    for got, want in zip(qs, split_q(t.shapes, rank, ref["q"])):
-        assert np.abs(got - want).max() <= TOL_Q
+    for i, (got, want) in enumerate(zip(qs, split_q(t.shapes, rank, ref["q"]))):
+        assert np.abs(got - want).max() <= (q_tols[i] if q_tols else TOL_Q), i
     d_gpu = oracle.decompress(t, ref["ranks"], codes, scales)
     d_ref = oracle.decompress(t, ref["ranks"], ref["codes"], ref["scales"])
     assert rel_fro(d_gpu, d_ref) <= TOL_COMPRESS
-    assert np.allclose(scales, ref["scales"], rtol=1e-5, atol=0)
+    assert np.allclose(scales, ref["scales"], rtol=scale_rtol, atol=0)
 
 
 def test_compress_larger_shapes(ctx, oracle):
@@ -263,6 +263,54 @@ def test_compress_larger_shapes(ctx, oracle):
         ref = oracle.compress(t, flat, rank, 8, 0, 2, st)
         res = api.compress(L, L.pack(flat), rank, api.QuantSpec(8, 0), None, 0, 2, st)
         _check_compress(L, t, oracle, ref, res, rank, 8, st)
+
+
+@pytest.mark.parametrize("rank", [33, 64, 96, 128])
+@pytest.mark.parametrize("blocked", [1, 0])
+def test_compress_high_rank_cholqr(ctx, oracle, rank, blocked):
+    """32 < r <= 128 (SURVEY C3's rank sweep): the blocked DMMA CholQR (k_cholblk, 32-wide
+    panels) and the unblocked one (k_chol128) against the reference compress, on rank-r +
+    noise data (a well-defined subspace), an all-zero tensor (every pivot fails -> exact MGS2
+    replacement fallback) and an exact rank-r tensor with a 1e3 singular-value spread (the
+    conditioning test sends it through the second CholQR pass)."""
+    from paper_2506_21263_b200 import api
+    shapes = [(700, 300), (300,), (260, 520), (200, 150), (160, 140)]
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    st = oracle.stream(11, rank)
+    data = []
+    for i, s in enumerate(shapes):
+        if len(s) == 1:
+            data.append(oracle.gaussian(oracle.stream(i, 4), s[0])[0])
+            continue
+        a, b = s
+        if i == 3:
+            data.append(np.zeros(a * b, np.float32))
+            continue
+        k = min(rank, a, b)
+        u = oracle.gaussian(oracle.stream(i, 1), a * k)[0].reshape(a, k)
+        v = oracle.gaussian(oracle.stream(i, 2), b * k)[0].reshape(b, k)
+        if i == 4:
+            u = (u * np.float32(10.0) ** (-3.0 * np.arange(k) / max(k - 1, 1))).astype(np.float32)
+        m = oracle.matmul_nt(u, v)
+        if i != 4:
+            m = m + np.float32(0.05) * oracle.gaussian(oracle.stream(i, 3), a * b)[0].reshape(a, b)
+        data.append(m.reshape(-1))
+    flat = np.concatenate(data).astype(np.float32)
+    ref = oracle.compress(t, flat, rank, 8, 0, 2, st)
+    api.set_option("cholqr_blocked", blocked)
+    try:
+        res = api.compress(L, L.pack(flat), rank, api.QuantSpec(8, 0), None, 0, 2, st)
+    finally:
+        api.set_option("cholqr_blocked", 1)
+    # the 1e3-spread tensor (last in the table) amplifies the fp32 sweeps' rounding in its
+    # weak directions (~cond x 6e-8): its Q entries are held to 1e-3 and its scales (max
+    # |column|) to 1e-2 relative; every other scale to 1e-4
+    k4 = min(rank, *shapes[4])
+    rt = np.full(len(ref["scales"]), 1e-4)
+    rt[-2 * k4:] = 1e-2
+    _check_compress(L, t, oracle, ref, res, rank, 8, st, scale_rtol=rt,
+                    q_tols=[TOL_Q, TOL_Q, TOL_Q, 1e-3])
 
 
 @pytest.mark.parametrize("rank,q,D", [(6, 8, 3), (16, 2, 1), (32, 4, 2), (30, 4, 3)])
@@ -306,7 +354,7 @@ def test_effective_rank_factor_space(ctx, oracle, reference, rank, q, D):
 
 
 @pytest.mark.parametrize("D,rank,big_from", [(8, 32, 128), (5, 32, 128), (3, 32, 0), (2, 8, 0),
-                                           (1, 8, 0)])
+                                           (1, 8, 0), (3, 32, 96), (4, 32, 96)])
 def test_effective_rank_large_k(ctx, oracle, reference, D, rank, big_from):
     """The large-K eigen kernel (blocked Cholesky, tiled DMMA products, packed fused
     Householder, certified multisection; K = D r up to 256) vs the compiled reference's dense
@@ -341,7 +389,7 @@ def test_effective_rank_large_k(ctx, oracle, reference, D, rank, big_from):
         er = api.effective_rank(L, z, D, rank, 4, 0.5, rank)
         assert er.all_zero and er.aggregate == 1 and all(k == 1 for _, k in er.per_tensor)
     finally:
-        api.set_option("effrank_big_from", 128)
+        api.set_option("effrank_big_from", 96)
 
 
 def test_errors_are_typed(ctx):
