@@ -607,26 +607,27 @@ __global__ void __launch_bounds__(kChol128Threads) k_chol128(const DevMat* __res
   }
 }
 
-// Branch-free fp64 1/sqrt: MUFU seed + three Newton steps. (The library rsqrt carries a
+// Branch-free fp64 1/sqrt: MUFU seed + two Newton steps (same result as the library rsqrt
+// to 1 ulp on tools/micro/chol_micro.cu; one step leaves 1e-13). The library rsqrt carries a
 // special-case branch, which splits the basic block and keeps the scheduler from overlapping
-// the next pivot's square root with the current trailing update.)
+// the next pivot's square root with the current trailing update.
 __device__ __forceinline__ double rsqrt_nr(double d) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
   const double h = 0.5 * d;
   y = y * fma(-h * y, y, 1.5);
   y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
   return y;
 }
 
 // Shared-memory scratch of one warp_chol_inv<RR>: the current pivot row of R (double-
-// buffered, zeros in front) and R^T with RR zeros in front of every row.
+// buffered; lane c stores R[j][c] at 32 + c - j - 1, so R[j][j+1 ..] starts on an aligned
+// index) and the columns of R reversed (ct[k][d + 1] = R[k - d][k], zeros for k - d < 0).
 template <int RR>
 struct CholScratch {
-  static constexpr int LT = 2 * RR + 2;  // R^T row stride (doubles; rows 16-B aligned)
-  double row[2][64];
-  double rt[RR * LT];
+  static constexpr int LC = 2 * RR + 2;  // ct row stride (doubles; rows 16-B aligned)
+  double row[2][128];
+  double ct[RR * LC];
 };
 
 // One warp factors the RR x RR (RR <= 32) symmetric block whose upper triangle sits in
@@ -634,14 +635,16 @@ struct CholScratch {
 // step loops are ROLLED with a register window that shifts by one row per step (position
 // i = row j + i), so every register index stays static (fully unrolled, the factorisation +
 // inversion was ~10k instructions run by ONE warp per SM: instruction-cache misses were
-// half of its time). tools/micro/chol_micro.cu measures the variants (B200, one 32 x 32
-// factor + inverse per SM): unrolled shuffles 33 us, rolled shuffles 16.9 us, this 12.1 us.
-//   factor: row j of R goes through shared memory (broadcast loads instead of shuffles);
-//           the next pivot is updated first and its rsqrt issued before the rest of the
-//           trailing update (lookahead: the two dependent chains overlap);
+// half of its time). tools/micro/chol_micro.cu (B200, one 32 x 32 factor + inverse per SM):
+// unrolled with shuffles 33 us, rolled with shuffles 16.9 us, this 7.4 us.
+//   factor: row j of R goes through shared memory and is read back with 16-B broadcast
+//           loads; the next pivot is updated first and its rsqrt issued before the rest of
+//           the trailing update (lookahead: the two dependent chains overlap); the updates
+//           are unconditional — the strictly-lower entries (and rows past RR) they also touch
+//           are never read;
 //   invert: right-looking back substitution from the bottom — once x_k = R^-1[k][c] is known
-//           every partial sum of the rows above takes its fma, column k of R read as one
-//           contiguous clamp-free run of R^T, so the dependent chain is two ops per step;
+//           every partial sum of the rows above takes its fma, column k of R read with 16-B
+//           loads from ct, so the dependent chain is two ops per step;
 //           put(k, x_k) receives row k of column c.
 // rf / xf: this lane's ||R[:,c]||^2 / ||R^-1[:,c]||^2 for columns c < r; dinv[j] = 1/R[j][j].
 // Returns the (warp-uniform) pivot failure (some pivot <= thr).
@@ -649,45 +652,50 @@ template <int RR, typename Put>
 __device__ __forceinline__ bool warp_chol_inv(const double* G, int ldg, int r, double thr,
                                               double* dinv, CholScratch<RR>& sc, Put put,
                                               double& rf, double& xf) {
-  constexpr int LT = CholScratch<RR>::LT;
+  constexpr int LC = CholScratch<RR>::LC;
   const int c = threadIdx.x & 31;
   const bool own = c < RR;
   double w[RR];  // w[i] = W[j + i][c]
 #pragma unroll
   for (int i = 0; i < RR; ++i) w[i] = (i <= c && own) ? G[i * ldg + c] : 0.0;
-  for (int i = c; i < RR * LT; i += 32) sc.rt[i] = 0.0;
-  sc.row[0][c] = sc.row[1][c] = 0.0;
+  for (int i = c; i < RR * LC; i += 32) sc.ct[i] = 0.0;
+  for (int i = c; i < 256; i += 32) sc.row[0][i] = 0.0;
   bool bad = false;
   rf = 0.0;
+  __syncwarp();
   double d = __shfl_sync(0xffffffffu, w[0], 0);
   double inv = rsqrt_nr(d);
 #pragma unroll 1
   for (int j = 0; j < RR; ++j) {
     bad |= !(d > thr);
-    const double rj = c == j ? d * inv : w[0] * inv;  // R[j][c] (0 for c < j)
+    const double rj = c == j ? d * inv : w[0] * inv;  // R[j][c] for c >= j
     if (c == j) dinv[j] = inv;
-    if (own) {
-      sc.row[j & 1][32 + c] = rj;
-      sc.rt[c * LT + RR + j] = rj;
+    double* row = sc.row[j & 1];
+    if (own) row[32 + c - j - 1] = rj;  // row[32 + i - 1] = R[j][j + i]
+    if (own && c >= j) {
+      sc.ct[c * LC + (c - j) + 1] = rj;
+      if (c < r) rf = fma(rj, rj, rf);
     }
-    if (c < r) rf = fma(rj, rj, rf);
     __syncwarp();
-    const double* rr = &sc.row[j & 1][32 + j];  // rr[i] = R[j][j + i]
-    const double r1 = (j + 1 < RR) ? rr[1] : 0.0;
-    w[0] = (j + 1 <= c) ? fma(-r1, rj, w[1]) : w[1];
+    double rv[RR];
+    const double2* rp = reinterpret_cast<const double2*>(row + 32);
+#pragma unroll
+    for (int i = 0; i < RR / 2; ++i) {
+      const double2 t = rp[i];
+      rv[2 * i] = t.x;
+      rv[2 * i + 1] = t.y;
+    }
+    w[0] = fma(-rv[0], rj, w[1]);
     const double dn = __shfl_sync(0xffffffffu, w[0], (j + 1) & 31);
     const double invn = rsqrt_nr(dn);
 #pragma unroll
-    for (int i = 2; i < RR; ++i) {  // W[j+i][c] -= R[j][j+i] R[j][c]  (j + i <= c), shifted
-      const double rji = (j + i < RR) ? rr[i] : 0.0;
-      w[i - 1] = (j + i <= c) ? fma(-rji, rj, w[i]) : w[i];
-    }
+    for (int i = 2; i < RR; ++i) w[i - 1] = fma(-rv[i - 1], rj, w[i]);  // W[j+i][c] -= R[j][j+i] R[j][c]
     w[RR - 1] = 0.0;
     d = dn;
     inv = invn;
   }
   if (__any_sync(0xffffffffu, bad)) return true;
-  __syncwarp();  // R^T and dinv visible to the whole warp
+  __syncwarp();  // ct and dinv visible to the whole warp
   double sacc[RR];  // sacc[i] = partial sum of row k - i
 #pragma unroll
   for (int i = 0; i < RR; ++i) sacc[i] = 0.0;
@@ -697,9 +705,16 @@ __device__ __forceinline__ bool warp_chol_inv(const double* G, int ldg, int r, d
     const double xk = ((k == c ? 1.0 : 0.0) - sacc[0]) * dinv[k];
     put(k, xk);
     if (c < r) xf = fma(xk, xk, xf);
-    const double* col = sc.rt + k * LT + RR + k;  // col[-i] = R[k - i][k] (0 above row 0)
+    double cv[RR];  // cv[i - 1] = R[k - i][k]
+    const double2* cp = reinterpret_cast<const double2*>(sc.ct + k * LC + 2);
 #pragma unroll
-    for (int i = 1; i < RR; ++i) sacc[i - 1] = fma(col[-i], xk, sacc[i]);
+    for (int i = 0; i < RR / 2; ++i) {
+      const double2 t = cp[i];
+      cv[2 * i] = t.x;
+      cv[2 * i + 1] = t.y;
+    }
+#pragma unroll
+    for (int i = 1; i < RR; ++i) sacc[i - 1] = fma(cv[i - 1], xk, sacc[i]);
     sacc[RR - 1] = 0.0;
   }
   return false;

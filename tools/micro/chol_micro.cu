@@ -127,13 +127,13 @@ __device__ void v2(double* G, double* dinv, double* X) {
 
 // branch-free fp64 rsqrt: MUFU seed + three Newton steps (no special-case paths, so the
 // scheduler can interleave it with independent work of the same basic block)
+template <int NR = 3>
 __device__ __forceinline__ double rsqrt_nr(double d) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
   const double h = 0.5 * d;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
+#pragma unroll
+  for (int i = 0; i < NR; ++i) y = y * fma(-h * y, y, 1.5);
   return y;
 }
 
@@ -222,12 +222,120 @@ __device__ void v4(double* G, double* dinv, double* X, double* Rrow, double* Rt)
   }
 }
 
+
+// V5: V4 with unconditional loads (row buffer zero past the block) and unconditional
+// trailing fmas (the strictly-lower entries they touch are never read)
+__device__ void v5(double* G, double* dinv, double* X, double* Rrow, double* Rt) {
+  const int c = threadIdx.x & 31;
+  double w[RR];
+#pragma unroll
+  for (int i = 0; i < RR; ++i) w[i] = (i <= c) ? G[i * LDG + c] : 0.0;
+  for (int i = c; i < RR * LT; i += 32) Rt[i] = 0.0;
+  for (int i = c; i < 256; i += 32) Rrow[i] = 0.0;
+  __syncwarp();
+  double d = __shfl_sync(0xffffffffu, w[0], 0);
+  double inv = rsqrt_nr(d);
+#pragma unroll 1
+  for (int j = 0; j < RR; ++j) {
+    const double rj = c == j ? d * inv : w[0] * inv;
+    if (c == j) dinv[j] = inv;
+    Rrow[(j & 1) * 128 + 32 + c] = rj;
+    Rt[c * LT + RR + j] = rj;
+    __syncwarp();
+    const double* rr = Rrow + (j & 1) * 128 + 32 + j;
+    w[0] = fma(-rr[1], rj, w[1]);
+    const double dn = __shfl_sync(0xffffffffu, w[0], (j + 1) & 31);
+    const double invn = rsqrt_nr(dn);
+#pragma unroll
+    for (int i = 2; i < RR; ++i) w[i - 1] = fma(-rr[i], rj, w[i]);
+    w[RR - 1] = 0.0;
+    d = dn;
+    inv = invn;
+  }
+  __syncwarp();
+  double s[RR];
+#pragma unroll
+  for (int i = 0; i < RR; ++i) s[i] = 0.0;
+#pragma unroll 1
+  for (int k = RR - 1; k >= 0; --k) {
+    const double xk = ((k == c ? 1.0 : 0.0) - s[0]) * dinv[k];
+    X[k * RR + c] = xk;
+    const double* col = Rt + k * LT + RR + k;
+#pragma unroll
+    for (int i = 1; i < RR; ++i) s[i - 1] = fma(col[-i], xk, s[i]);
+    s[RR - 1] = 0.0;
+  }
+}
+
+
+// V6: V5 with 16-B vector loads: the pivot row is written shifted by the step (lane c stores
+// R[j][c] at 32 + c - j - 1, so R[j][j+1..j+31] starts on an aligned index), and column k of
+// R is kept reversed per row of Ct (Ct[k][d + 1] = R[k - d][k]) so the back substitution reads
+// it from an aligned index too
+constexpr int LC = 2 * RR + 2;
+template <int NR>
+__device__ void v6(double* G, double* dinv, double* X, double* Rrow, double* Ct) {
+  const int c = threadIdx.x & 31;
+  double w[RR];
+#pragma unroll
+  for (int i = 0; i < RR; ++i) w[i] = (i <= c) ? G[i * LDG + c] : 0.0;
+  for (int i = c; i < RR * LC; i += 32) Ct[i] = 0.0;
+  __syncwarp();
+  double d = __shfl_sync(0xffffffffu, w[0], 0);
+  double inv = rsqrt_nr<NR>(d);
+#pragma unroll 1
+  for (int j = 0; j < RR; ++j) {
+    const double rj = c == j ? d * inv : w[0] * inv;
+    if (c == j) dinv[j] = inv;
+    double* row = Rrow + (j & 1) * 128;
+    row[32 + c - j - 1] = rj;                 // row[32 + i - 1] = R[j][j + i]
+    if (c >= j) Ct[c * LC + (c - j) + 1] = rj;  // Ct[c][d + 1] = R[c - d][c]
+    __syncwarp();
+    const double2* rv = reinterpret_cast<const double2*>(row + 32);
+    double rrv[RR];
+#pragma unroll
+    for (int i = 0; i < RR / 2; ++i) {
+      const double2 t = rv[i];
+      rrv[2 * i] = t.x;
+      rrv[2 * i + 1] = t.y;
+    }
+    w[0] = fma(-rrv[0], rj, w[1]);
+    const double dn = __shfl_sync(0xffffffffu, w[0], (j + 1) & 31);
+    const double invn = rsqrt_nr<NR>(dn);
+#pragma unroll
+    for (int i = 2; i < RR; ++i) w[i - 1] = fma(-rrv[i - 1], rj, w[i]);
+    w[RR - 1] = 0.0;
+    d = dn;
+    inv = invn;
+  }
+  __syncwarp();
+  double s[RR];
+#pragma unroll
+  for (int i = 0; i < RR; ++i) s[i] = 0.0;
+#pragma unroll 1
+  for (int k = RR - 1; k >= 0; --k) {
+    const double xk = ((k == c ? 1.0 : 0.0) - s[0]) * dinv[k];
+    X[k * RR + c] = xk;
+    const double2* cv = reinterpret_cast<const double2*>(Ct + k * LC + 2);  // d = 1, 2, ...
+    double cc[RR];
+#pragma unroll
+    for (int i = 0; i < RR / 2; ++i) {
+      const double2 t = cv[i];
+      cc[2 * i] = t.x;
+      cc[2 * i + 1] = t.y;
+    }
+#pragma unroll
+    for (int i = 1; i < RR; ++i) s[i - 1] = fma(cc[i - 1], xk, s[i]);
+    s[RR - 1] = 0.0;
+  }
+}
+
 template <int V>
 __global__ void __launch_bounds__(32) kern(const double* A, double* out, int reps) {
   __shared__ double G[RR * LDG];
   __shared__ double dinv[RR];
-  __shared__ __align__(16) double Rrow[128];
-  __shared__ __align__(16) double Rt[RR * LT];
+  __shared__ __align__(16) double Rrow[256];
+  __shared__ __align__(16) double Rt[RR * LC];
   const int c = threadIdx.x;
   for (int rep = 0; rep < reps; ++rep) {
     for (int i = 0; i < RR; ++i) G[i * LDG + c] = A[i * RR + c];
@@ -238,6 +346,10 @@ __global__ void __launch_bounds__(32) kern(const double* A, double* out, int rep
     if (V == 2) v2(G, dinv, X);
     if (V == 3) v3(G, dinv, X, Rrow, Rt);
     if (V == 4) v4(G, dinv, X, Rrow, Rt);
+    if (V == 5) v5(G, dinv, X, Rrow, Rt);
+    if (V == 6) v6<3>(G, dinv, X, Rrow, Rt);
+    if (V == 7) v6<2>(G, dinv, X, Rrow, Rt);
+    if (V == 8) v6<1>(G, dinv, X, Rrow, Rt);
     __syncwarp();
   }
 }
@@ -254,17 +366,21 @@ int main() {
     }
   double *dA, *dO;
   cudaMalloc(&dA, sizeof(double) * RR * RR);
-  cudaMalloc(&dO, sizeof(double) * RR * RR * 148 * 5);
+  cudaMalloc(&dO, sizeof(double) * RR * RR * 148 * 9);
   cudaMemcpy(dA, g.data(), sizeof(double) * RR * RR, cudaMemcpyHostToDevice);
-  std::vector<double> res[5];
+  std::vector<double> res[9];
   const int reps = 10;
-  for (int v = 0; v < 5; ++v) {
+  for (int v = 0; v < 9; ++v) {
     auto launch = [&] {
       if (v == 0) kern<0><<<148, 32>>>(dA, dO + v * RR * RR * 148, reps);
       if (v == 1) kern<1><<<148, 32>>>(dA, dO + v * RR * RR * 148, reps);
       if (v == 2) kern<2><<<148, 32>>>(dA, dO + v * RR * RR * 148, reps);
       if (v == 3) kern<3><<<148, 32>>>(dA, dO + v * RR * RR * 148, reps);
       if (v == 4) kern<4><<<148, 32>>>(dA, dO + v * RR * RR * 148, reps);
+      if (v == 5) kern<5><<<148, 32>>>(dA, dO + v * RR * RR * 148, reps);
+      if (v == 6) kern<6><<<148, 32>>>(dA, dO + v * RR * RR * 148, reps);
+      if (v == 7) kern<7><<<148, 32>>>(dA, dO + v * RR * RR * 148, reps);
+      if (v == 8) kern<8><<<148, 32>>>(dA, dO + v * RR * RR * 148, reps);
     };
     launch();
     cudaDeviceSynchronize();
