@@ -607,6 +607,16 @@ __global__ void __launch_bounds__(kChol128Threads) k_chol128(const DevMat* __res
   }
 }
 
+// max of the first r diagonal entries of a shared-memory matrix, lane-parallel + warp
+// reduction (every lane of the calling warp gets it)
+__device__ __forceinline__ double warp_diag_max(const double* A, int ld, int r) {
+  double mx = 0.0;
+  for (int j = threadIdx.x & 31; j < r; j += 32) mx = fmax(mx, A[j * ld + j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  return mx;
+}
+
 // Branch-free fp64 1/sqrt: MUFU seed + two Newton steps (same result as the library rsqrt
 // to 1 ulp on tools/micro/chol_micro.cu; one step leaves 1e-13). The library rsqrt carries a
 // special-case branch, which splits the basic block and keeps the scheduler from overlapping
@@ -790,8 +800,7 @@ __global__ void __launch_bounds__(256) k_chol32(const DevMat* __restrict__ mats,
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int c = threadIdx.x;  // lanes >= RR idle along (their columns stay zero)
-  double mx = 0.0;
-  for (int j = 0; j < r; ++j) mx = fmax(mx, G[j][j]);
+  const double mx = warp_diag_max(&G[0][0], RR + 1, r);
   const double tol = 1e-7 * fmax(1.0, sqrt(mx));
   const double thr = (10.0 * tol) * (10.0 * tol);
   double rf = 0.0, xf = 0.0;
@@ -837,6 +846,19 @@ template <typename FA, typename FB>
 __device__ __forceinline__ void dmma_tile(double (&d)[2], int kn, FA fa, FB fb) {
   const int lane = threadIdx.x & 31;
   for (int k = 0; k < kn; k += 4) dmma_8x8x4(d, fa(lane >> 2, k + (lane & 3)), fb(k + (lane & 3), lane >> 2));
+}
+
+// two independent tiles interleaved (two DMMA chains in flight per warp); `two` is
+// warp-uniform
+template <typename FA0, typename FB0, typename FA1, typename FB1>
+__device__ __forceinline__ void dmma_tile2(double (&d0)[2], double (&d1)[2], int kn, bool two,
+                                           FA0 fa0, FB0 fb0, FA1 fa1, FB1 fb1) {
+  const int lane = threadIdx.x & 31, m = lane >> 2;
+  for (int k = 0; k < kn; k += 4) {
+    const int ka = k + (lane & 3);
+    dmma_8x8x4(d0, fa0(m, ka), fb0(ka, m));
+    if (two) dmma_8x8x4(d1, fa1(m, ka), fb1(ka, m));
+  }
 }
 
 // warp 0's share of a panel: factor + invert the diagonal block, R_pp^-1 into Xo. (Kept out of
@@ -918,8 +940,7 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) k_cholblk(const DevMat* __
     }
   }
   __syncthreads();
-  double mx = 0.0;
-  for (int j = 0; j < r; ++j) mx = fmax(mx, W[j * LD + j]);
+  const double mx = warp_diag_max(W, LD, r);
   const double tol = 1e-7 * fmax(1.0, sqrt(mx));
   const double thr = (10.0 * tol) * (10.0 * tol);
   double rf = 0.0;  // ||R||_F^2 (columns < r), lane-partial
@@ -978,20 +999,35 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) k_cholblk(const DevMat* __
     // trailing update (upper tile triangle): W[a][b] -= sum_k R[o+k][a] R[o+k][b]
     {
       const int mt = nq / 8, ntiles = mt * (mt + 1) / 2;
-      for (int t = warp; t < ntiles; t += NW) {
-        int ti = 0, rem = t;
+      auto unrank = [&](int t, int& ti, int& tj) {
+        int rem = t;
+        ti = 0;
         while (rem >= mt - ti) {
           rem -= mt - ti;
           ++ti;
         }
-        const int tj = ti + rem;
+        tj = ti + rem;
+      };
+      for (int t = warp; t < ntiles; t += 2 * NW) {
+        const int t2 = t + NW;
+        const bool two = t2 < ntiles;
+        int ti, tj, ti2 = 0, tj2 = 0;
+        unrank(t, ti, tj);
+        if (two) unrank(t2, ti2, tj2);
+        double d[2] = {0.0, 0.0}, d2[2] = {0.0, 0.0};
+        dmma_tile2(d, d2, 32, two,
+                   [&](int mm, int k) { return W[(o + k) * LD + q0 + 8 * ti + mm]; },
+                   [&](int k, int n) { return W[(o + k) * LD + q0 + 8 * tj + n]; },
+                   [&](int mm, int k) { return W[(o + k) * LD + q0 + 8 * ti2 + mm]; },
+                   [&](int k, int n) { return W[(o + k) * LD + q0 + 8 * tj2 + n]; });
         double* dst = W + (q0 + 8 * ti + (lane >> 2)) * LD + q0 + 8 * tj + 2 * (lane & 3);
-        double d[2] = {0.0, 0.0};
-        dmma_tile(d, 32,
-                  [&](int mm, int k) { return W[(o + k) * LD + q0 + 8 * ti + mm]; },
-                  [&](int k, int n) { return W[(o + k) * LD + q0 + 8 * tj + n]; });
         dst[0] -= d[0];
         dst[1] -= d[1];
+        if (two) {
+          double* dst2 = W + (q0 + 8 * ti2 + (lane >> 2)) * LD + q0 + 8 * tj2 + 2 * (lane & 3);
+          dst2[0] -= d2[0];
+          dst2[1] -= d2[1];
+        }
       }
       __syncthreads();
     }
@@ -1019,29 +1055,40 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) k_cholblk(const DevMat* __
     }
     __syncthreads();
     // X_ij = -R_ii^-1 T_j  (R_ii^-1 upper: k >= row)
-    for (int t = warp; t < nj * 16; t += NW) {
+    const double* xa = Xd + i * 32 * XL;
+    for (int t = warp; t < nj * 16; t += 2 * NW) {
+      const int t2 = t + NW;
+      const bool two = t2 < nj * 16;
       const int jb = i + 1 + t / 16, ti = (t % 16) / 4, tj = t % 4;
-      double d[2] = {0.0, 0.0};
-      const double* xa = Xd + i * 32 * XL;
+      const int jb2 = two ? i + 1 + t2 / 16 : jb, ti2 = (t2 % 16) / 4, tj2 = t2 % 4;
       const double* tb = Tb + jb * 32 * XL;
-      dmma_tile(d, 32,
-                [&](int mm, int k) { return xa[(8 * ti + mm) * XL + k]; },
-                [&](int k, int n) { return tb[k * XL + 8 * tj + n]; });
+      const double* tb2 = Tb + jb2 * 32 * XL;
+      double d[2] = {0.0, 0.0}, d2[2] = {0.0, 0.0};
+      dmma_tile2(d, d2, 32, two,
+                 [&](int mm, int k) { return xa[(8 * ti + mm) * XL + k]; },
+                 [&](int k, int n) { return tb[k * XL + 8 * tj + n]; },
+                 [&](int mm, int k) { return xa[(8 * ti2 + mm) * XL + k]; },
+                 [&](int k, int n) { return tb2[k * XL + 8 * tj2 + n]; });
       double* dst = W + (32 * i + 8 * ti + (lane >> 2)) * LD + 32 * jb + 8 * tj + 2 * (lane & 3);
       dst[0] = -d[0];
       dst[1] = -d[1];
+      if (two) {
+        double* dst2 = W + (32 * i + 8 * ti2 + (lane >> 2)) * LD + 32 * jb2 + 8 * tj2 + 2 * (lane & 3);
+        dst2[0] = -d2[0];
+        dst2[1] = -d2[1];
+      }
     }
     __syncthreads();
   }
   double xf = 0.0;
   double* X = rinv + (int64_t)e * rr * rr;
-  for (int idx = tid; idx < r * r; idx += kCholBlkThreads) {
-    const int i = idx / r, k = idx % r;
-    double v = 0.0;
-    if (k >= i) v = (i >> 5) == (k >> 5) ? Xd[((i >> 5) * 32 + (i & 31)) * XL + (k & 31)] : W[i * LD + k];
-    xf = fma(v, v, xf);
-    X[i * rr + k] = v;
-  }
+  for (int i = warp; i < r; i += NW)  // row i, lanes over columns (no runtime divisions)
+    for (int k = lane; k < r; k += 32) {
+      double v = 0.0;
+      if (k >= i) v = (i >> 5) == (k >> 5) ? Xd[((i >> 5) * 32 + (i & 31)) * XL + (k & 31)] : W[i * LD + k];
+      xf = fma(v, v, xf);
+      X[i * rr + k] = v;
+    }
   if (need2) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
