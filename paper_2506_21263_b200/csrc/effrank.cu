@@ -413,9 +413,8 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
                                                  double* __restrict__ energy, int shard,
                                                  int nshards) {
   extern __shared__ double er_sm[];
-  __shared__ double red[32];
   __shared__ double tri[4 * kErMaxN];  // V | A v / H | diagonal | squared off-diagonal
-  __shared__ double s_H, s_alpha, s_K, s_tot;
+  __shared__ double s_tot;
   __shared__ int s_k;
   const int e = shard + blockIdx.x * nshards;  // this shard's tensors: e % nshards == shard
   const DevT2& t = T[e];
@@ -597,7 +596,6 @@ __global__ void __launch_bounds__(512) k_effrank(const DevT2* __restrict__ T, in
   }
   hi += 1e-14 * amax + 1e-300;
   lo -= 1e-14 * amax + 1e-300;
-  const double pivmin = 1e-290 + 1e-30 * amax * amax;
   double* ev = V;  // eigenvalues, descending (V is free now)
   int G = 1;
   while (G * 2 <= 32 && G * 2 * n <= nt) G *= 2;

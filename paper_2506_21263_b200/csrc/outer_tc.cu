@@ -558,7 +558,6 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       mbar_wait(&tinfo[s], sph);
       const int4 tl = sinfo[s];
       if (tl.x < 0) break;
-      const O5StreamMaps* ms = smaps + tl.x;
       const O5OpMaps* mo = omaps + tl.x;
       if (a_src == 1 && (tl.w & 2)) {
         // the whole A band fits the box ring: issue it as soon as the chunk is scheduled
@@ -602,8 +601,7 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       const int4 tl = sinfo[s];
       if (tl.x < 0) break;
       if (tl.w & 2) {
-        const O5StreamMaps* ms = smaps + tl.x;
-      const O5OpMaps* mo = omaps + tl.x;
+        const O5OpMaps* mo = omaps + tl.x;
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait(&aempty[ar], arph ^ 1);
           if (elect_one()) {
@@ -703,7 +701,6 @@ __global__ void __launch_bounds__(BF ? kO5ThreadsTA : kO5Threads, 1)
       named_bar(1, 256);
       if (et == 0) {
         const O5StreamMaps* ms = smaps + tl.x;
-      const O5OpMaps* mo = omaps + tl.x;
         for (int q = 0; q < 3; ++q) tma_store_2d(&ms->s[q], st + q * kO5StreamBox, tl.z, tl.y);
         bulk_commit();
         // a stage may be refilled once its stores have read it: release the previous tile's
