@@ -226,19 +226,21 @@ __global__ void __launch_bounds__(256) k_o5_prep(
         *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(Bp[1]) + o) = pl;
       }
     }
-  } else {  // tf32: A exact, B = hi + lo
-    for (int e = threadIdx.x; e < kPrepRows * KA; e += 256) {
-      const int rl = e / KA, k = e - rl * KA;
+  } else {  // tf32: A exact, B = hi + lo; 4 consecutive k per thread -> 16-B stores (row
+            // starts are 16-B aligned: KA is a multiple of 32 floats)
+    const int kq_n = KA / 4;
+    for (int e = threadIdx.x; e < kPrepRows * kq_n; e += 256) {
+      const int rl = e / kq_n, k = 4 * (e - rl * kq_n);
       const int64_t dof = dst_off[rl];
       if (dof < 0) break;
-      const float v = tile[rl][k];
+      const float4 v = make_float4(tile[rl][k], tile[rl][k + 1], tile[rl][k + 2], tile[rl][k + 3]);
       if (!(dof >> 62)) {
-        A[dof + k] = v;
+        *reinterpret_cast<float4*>(A + dof + k) = v;
       } else {
         const int64_t o = (dof & ((int64_t(1) << 62) - 1)) + k;
-        const float h = tf32_hi(v);
-        Bp[0][o] = h;
-        Bp[1][o] = v - h;
+        const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+        *reinterpret_cast<float4*>(Bp[0] + o) = h;
+        *reinterpret_cast<float4*>(Bp[1] + o) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
       }
     }
   }
