@@ -297,6 +297,8 @@ def main():
     from paper_2506_21263_b200.engine import OuterConfig, OuterSync
 
     torch.cuda.set_device(local_rank)
+    # host-resident e2e leg: this rank's pinned buffers on its GPU's NUMA node
+    numa_cpus = api.bind_host_to_device(local_rank) if os.environ.get("DLX_NUMA_BIND", "1") == "1" else []
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     dev = f"cuda:{local_rank}"
@@ -550,7 +552,9 @@ def main():
             "e2e": {"value": e2e_value, "unit": "params/s", "steps": ke,
                     "h2d_bytes_per_step": int(L.slab_elems * 4),
                     "d2h_bytes_per_step": int(L.slab_elems * 4),
-                    "ms_per_step": ms_e2e / ke},
+                    "ms_per_step": ms_e2e / ke,
+                    "host_cpus": (f"{len(numa_cpus)} CPUs local to the GPU (NVML affinity)"
+                                  if numa_cpus else "unbound")},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "comp_error": recs[-1].comp_error if recs else None,

@@ -529,6 +529,27 @@ def omega_bound(r: int, d: int, q: int) -> float:
     return v
 
 
+def bind_host_to_device(device: int) -> list[int]:
+    """Pin the calling process to the CPUs NVML reports as local to `device` (its NUMA node)
+    and return them. Call before allocating the pinned host buffers a host-resident caller
+    hands to OuterSync.step_host: pinned pages land on the node of the allocating CPU, and
+    with one process per GPU the 2 x 5.26 GB of copies per round otherwise cross the socket
+    link for the GPUs on the other node. No-op (returns []) when NVML is unavailable."""
+    import os
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = [64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1]
+        cpus = [c for c in cpus if c < os.cpu_count()]
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return cpus
+    except Exception:
+        return []
+
+
 def take_launch_count() -> int:
     return int(lib().dlx_take_launch_count())
 
