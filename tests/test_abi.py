@@ -97,3 +97,20 @@ def test_worker_sync_entry_points_on_cpu():
     assert L.dlx_exchange(None, None, 0, None, None, 0, 0, None) == 1
     assert L.dlx_comm_allgather(None, None, 0, None, None) == 1
     assert L.dlx_exchange_wait_warm(None, None) == 1
+
+
+def test_bind_host_to_device_is_safe_without_nvml():
+    """api.bind_host_to_device: without a GPU / NVML it is a no-op returning []; with one it
+    returns a non-empty CPU list that the process is then pinned to."""
+    import os
+    from paper_2506_21263_b200 import api
+    before = os.sched_getaffinity(0)
+    try:
+        cpus = api.bind_host_to_device(0)
+        assert isinstance(cpus, list)
+        if cpus:
+            assert os.sched_getaffinity(0) == set(cpus)
+        else:
+            assert os.sched_getaffinity(0) == before
+    finally:
+        os.sched_setaffinity(0, before)
