@@ -1163,6 +1163,57 @@ __global__ void __launch_bounds__(128) k_apply(const DevMat* __restrict__ mats,
   }
 }
 
+// r <= 16: SIMT fp64, lane = row. One CTA per 128-row job: the job's rows load their r
+// columns (coalesced: 128 B per column per warp), out[j] = sum_{k <= j} y[k] X[k][j] with X
+// broadcast from shared memory (16-B loads), each output column stored coalesced. At these
+// ranks the DMMA tile (fixed 32-wide staging, 2 of 4 column blocks live) was half idle:
+// tools/micro/apply_micro.cu on the OPT-1.3B P side at r = 16, 45 us (DMMA) vs 23 us.
+template <int RR>
+__global__ void __launch_bounds__(128) k_apply_simt(const DevMat* __restrict__ mats,
+                                                    const int4* __restrict__ jobs, int rr,
+                                                    const double* __restrict__ rinv,
+                                                    const int* __restrict__ skip,
+                                                    const int* __restrict__ only,
+                                                    float* __restrict__ buf) {
+  __shared__ __align__(16) double Xs[RR * RR];  // [k][j], upper, zeros elsewhere
+  const int4 jb = jobs[blockIdx.x];
+  if (skip[jb.x] || (only && !only[jb.x])) return;
+  const DevMat m = mats[jb.x];
+  const int r = m.r;
+  const double* X = rinv + (int64_t)jb.x * rr * rr;
+  for (int idx = threadIdx.x; idx < RR * RR; idx += 128) {
+    const int k = idx / RR, c = idx % RR;
+    Xs[idx] = (k < r && c < r && k <= c) ? X[k * rr + c] : 0.0;
+  }
+  const int64_t row = jb.y + threadIdx.x;
+  const bool live = row < m.n;
+  float* Y = buf + m.off;
+  float v[RR];
+#pragma unroll
+  for (int k = 0; k < RR; ++k) v[k] = (k < r && live) ? Y[(int64_t)k * m.ld + row] : 0.f;
+  __syncthreads();
+  double o[RR];
+#pragma unroll
+  for (int j = 0; j < RR; ++j) o[j] = 0.0;
+#pragma unroll
+  for (int k = 0; k < RR; ++k) {
+    const double y = (double)v[k];
+    const double2* xr = reinterpret_cast<const double2*>(Xs + k * RR);
+#pragma unroll
+    for (int j2 = 0; j2 < RR / 2; ++j2) {
+      if (2 * j2 + 1 < k) continue;  // X[k][j] = 0 for j < k
+      const double2 x = xr[j2];
+      o[2 * j2] = fma(y, x.x, o[2 * j2]);
+      o[2 * j2 + 1] = fma(y, x.y, o[2 * j2 + 1]);
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int j = 0; j < RR; ++j)
+      if (j < r) Y[(int64_t)j * m.ld + row] = (float)o[j];
+  }
+}
+
 // r <= 32 fast path on DMMA: Y <- Y R^-1 for one 128-row tile. The tile (fp64, [row][k])
 // and R^-1 (upper, zero-padded) are staged in shared memory; warp w owns rows
 // [32 w, 32 w + 32) = four 8-row blocks, and column block cj only needs the k steps
@@ -1397,7 +1448,13 @@ static bool apply_dmma_big_enabled() {
 
 static void launch_apply(const GramJob& J, int rr, const double* rinv, const int* skip,
                          const int* only, float* buf, size_t asm_, cudaStream_t s) {
-  if (rr <= 32) {
+  if (rr <= 16) {
+    const int nj = static_cast<int>(J.apply.size());
+    if (rr <= 8)
+      k_apply_simt<8><<<nj, 128, 0, s>>>(J.d_mats, J.d_apply, rr, rinv, skip, only, buf);
+    else
+      k_apply_simt<16><<<nj, 128, 0, s>>>(J.d_mats, J.d_apply, rr, rinv, skip, only, buf);
+  } else if (rr <= 32) {
     const int nj = static_cast<int>(J.apply.size());
     const int per = std::max(1, (nj + 4 * 148 - 1) / (4 * 148));
     k_apply_dmma<<<(nj + per - 1) / per, 128, 0, s>>>(J.d_mats, J.d_apply, nj, per, rr, rinv, skip,
