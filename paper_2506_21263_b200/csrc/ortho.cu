@@ -183,6 +183,7 @@ constexpr int kGdRows = 64;
 constexpr int kGdLd = kGdRows + 4;  // [col][row] stride: conflict-free fragment loads
 
 
+template <int TSH>  // tile rows 64 << TSH: 2 for r <= 8, 1 for r <= 16, 0 above
 __global__ void __launch_bounds__(320) k_gram_dmma(const DevMat* __restrict__ mats,
                                                    const int4* __restrict__ splits,
                                                    const float* __restrict__ buf, int rr,
@@ -194,53 +195,85 @@ __global__ void __launch_bounds__(320) k_gram_dmma(const DevMat* __restrict__ ma
   const DevMat m = mats[sp.x];
   const int nb = (m.r + 7) / 8, nblk = nb * (nb + 1) / 2;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // fewer columns -> taller tiles in the same shared memory (8 cols x 256 rows, 16 x 128,
+  // 32 x 64), and the 10 warps split each tile's k steps between `nsl` slices of every 8x8
+  // block (summed in a fixed order at the end): at the low ranks the adaptive schedule
+  // reaches, one to three blocks otherwise left most warps idle behind two barriers per
+  // 64 rows
+  constexpr int TR = kGdRows << TSH, LD = TR + 4;
+  const int nsl = TSH == 0 ? 1 : 10 / nblk;
+  const int blk = warp % nblk, slice = warp / nblk;
   int ci = 0, cj = 0;
   {
-    int rem = warp;
+    int rem = blk;
     while (ci < nb && rem >= nb - ci) {
       rem -= nb - ci;
       ++ci;
     }
     cj = ci + rem;
   }
-  const bool active = warp < nblk;
+  const bool active = slice < nsl;
   double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};  // two independent DMMA chains
   const float* Y = buf + m.off;
   const int cols = nb * 8;
-  const int per = (cols * kGdRows + 319) / 320;  // staged elements per thread (<= 7)
+  const int per = (cols * TR + 319) / 320;  // staged elements per thread (<= 7)
   float pre[7];
   auto fetch = [&](int r0) {
 #pragma unroll
     for (int i = 0; i < 7; ++i) {
       const int e = threadIdx.x + 320 * i;
-      const int c = e / kGdRows, rl = e % kGdRows;
+      const int c = e >> (6 + TSH), rl = e & (TR - 1);
       const int row = r0 + rl;
       pre[i] = (i < per && c < m.r && row < sp.z) ? __ldg(&Y[(int64_t)c * m.ld + row]) : 0.f;
     }
   };
   fetch(sp.y);
-  for (int r0 = sp.y; r0 < sp.z; r0 += kGdRows) {
+  for (int r0 = sp.y; r0 < sp.z; r0 += TR) {
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 7; ++i) {
       const int e = threadIdx.x + 320 * i;
-      if (i < per && e < cols * kGdRows) Ys[(e / kGdRows) * kGdLd + e % kGdRows] = (double)pre[i];
+      if (i < per && e < cols * TR) Ys[(e >> (6 + TSH)) * LD + (e & (TR - 1))] = (double)pre[i];
     }
     __syncthreads();
-    if (r0 + kGdRows < sp.z) fetch(r0 + kGdRows);
+    if (r0 + TR < sp.z) fetch(r0 + TR);
     if (active) {
-      const double* pa = Ys + (ci * 8 + lane / 4) * kGdLd + lane % 4;
-      const double* pb = Ys + (cj * 8 + lane / 4) * kGdLd + lane % 4;
+      const double* pa = Ys + (ci * 8 + lane / 4) * LD + lane % 4;
+      const double* pb = Ys + (cj * 8 + lane / 4) * LD + lane % 4;
+      if (TSH == 0) {  // nb >= 3: 64-row tiles, one slice, constant offsets
 #pragma unroll 4
-      for (int k = 0; k < kGdRows; k += 8) {
-        dmma_8x8x4(acc, pa[k], pb[k]);
-        dmma_8x8x4(acc2, pa[k + 4], pb[k + 4]);
+        for (int k = 0; k < kGdRows; k += 8) {
+          dmma_8x8x4(acc, pa[k], pb[k]);
+          dmma_8x8x4(acc2, pa[k + 4], pb[k + 4]);
+        }
+      } else {
+        const int step = 4 * nsl;
+        int k = 4 * slice;
+        for (; k + step < TR; k += 2 * step) {
+          dmma_8x8x4(acc, pa[k], pb[k]);
+          dmma_8x8x4(acc2, pa[k + step], pb[k + step]);
+        }
+        if (k < TR) dmma_8x8x4(acc, pa[k], pb[k]);
       }
     }
   }
-  if (active) {
+  // slices of a block summed in slice order (deterministic)
+  double* red = Ys;  // [slice][blk][lane][2]
+  if (TSH > 0) {
+    __syncthreads();
+    if (active && slice > 0) {
+      red[((slice * nblk + blk) * 32 + lane) * 2] = acc[0] + acc2[0];
+      red[((slice * nblk + blk) * 32 + lane) * 2 + 1] = acc[1] + acc2[1];
+    }
+    __syncthreads();
+  }
+  if (active && slice == 0) {
     acc[0] += acc2[0];
     acc[1] += acc2[1];
+    for (int sl = 1; sl < nsl; ++sl) {
+      acc[0] += red[((sl * nblk + blk) * 32 + lane) * 2];
+      acc[1] += red[((sl * nblk + blk) * 32 + lane) * 2 + 1];
+    }
     double* out = partial + (int64_t)sp.w * rr * rr;
     const int gj = ci * 8 + lane / 4;
 #pragma unroll
@@ -339,7 +372,12 @@ static size_t gram_smem(int rmax) {
 static void launch_gram(const GramJob& J, const float* buf, double* partial, cudaStream_t s,
                         const int* only = nullptr) {
   if (J.rmax <= 32) {
-    k_gram_dmma<<<J.splits.size(), 320, 0, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial, only);
+    if (J.rmax <= 8)
+      k_gram_dmma<2><<<J.splits.size(), 320, 0, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial, only);
+    else if (J.rmax <= 16)
+      k_gram_dmma<1><<<J.splits.size(), 320, 0, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial, only);
+    else
+      k_gram_dmma<0><<<J.splits.size(), 320, 0, s>>>(J.d_mats, J.d_splits, buf, J.rmax, partial, only);
     DLX_LAUNCHED();
     return;
   }
