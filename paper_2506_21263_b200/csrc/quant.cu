@@ -28,7 +28,29 @@ __global__ void __launch_bounds__(256) k_chunk_max(const DevChunk* __restrict__ 
   const DevChunk c = chunks[blockIdx.x];
   const float* src = buf_ptr(c.buf, p, q, slab) + c.src;
   float m = 0.f;
-  for (int64_t i = threadIdx.x; i < c.len; i += blockDim.x) m = fmaxf(m, fabsf(src[i]));
+  // 16-B loads where the chunk start is 16-B aligned (factor columns start on 32-float rows,
+  // tensors on 256-B offsets), 4 in flight per thread: the long pole is the embedding's
+  // 50272-row columns, one CTA each
+  int64_t head = 0;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const int64_t nv = c.len / 4;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    int64_t i = threadIdx.x;
+    for (; i + 3 * 256 < nv; i += 4 * 256) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(s4 + i + u * 256);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+    }
+    for (; i < nv; i += 256) {
+      const float4 v = __ldg(s4 + i);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    head = 4 * nv;
+  }
+  for (int64_t i = head + threadIdx.x; i < c.len; i += blockDim.x) m = fmaxf(m, fabsf(src[i]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = m;
@@ -59,14 +81,24 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(const DevChunk* __restrict_
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // the next 1024 chunks are loaded while the current ones are scanned (one exposed load
+  // latency per launch instead of one per 1024 chunks)
+  DevChunk nch{};
+  float nmx = 0.f;
+  if (threadIdx.x < n) {
+    nch = chunks[threadIdx.x];
+    nmx = cmax[threadIdx.x];
+  }
   for (int t0 = 0; t0 < n; t0 += 1024) {
     const int c = t0 + threadIdx.x;
+    const DevChunk ch = nch;
+    const float mx = nmx;
+    if (c + 1024 < n) {
+      nch = chunks[c + 1024];
+      nmx = cmax[c + 1024];
+    }
     int64_t extra = 0, own = 0;
-    float mx = 0.f;
-    DevChunk ch{};
     if (c < n) {
-      ch = chunks[c];
-      mx = cmax[c];
       extra = cold ? ch.extra : 0;
       own = (stochastic && mx != 0.f) ? ch.len : 0;
     }
