@@ -33,138 +33,20 @@ __device__ double er_block_sum(double v, double* red) {
 }
 
 // ------------------------------------------------------------------ code Grams
-// For K = D r <= 64 the factor Grams come straight from the packed codes: C^T C over the
-// gathered codes of one side of one tensor is an integer matrix (|c| <= 2^(q-1)), formed on
-// the fp64 tensor cores (DMMA) from exactly converted codes — every partial sum is an
-// integer below 2^53, so the chunk sums added with fp64 atomics are exact and independent of
-// their order. G = diag(s) C^T C diag(s) with the column scales is formed inside k_effrank.
-// No dequantised factor copies, no fp32 Gram sweep; the kernel's footprint (320 threads,
-// 35 KB) lets it share an SM with the fused outer update it overlaps.
-constexpr int kCgChunk = 1024;  // rows per k_code_gram block
-constexpr int kCgTile = 64;     // rows staged in shared memory per pass
-constexpr int kCgLd = kCgTile + 4;
-constexpr int kCgMaxK = 64;
+// The factor Grams come straight from the packed codes: C^T C over the gathered codes of one
+// side of one tensor is an integer matrix (|c| <= 2^(q-1)), so it can be formed exactly on
+// tensor cores from the codes themselves — no dequantised factor copies, no fp32 Gram sweep.
+// G = diag(s) C^T C diag(s) with the column scales is formed inside k_effrank. (An fp64 DMMA
+// variant for K <= 64 from round 1 was no longer launched — every K goes through the bf16
+// kernel below, equally exact — and has been removed.)
+constexpr int kCgChunk = 1024;  // rows per code-Gram block
 
 struct CodeGramJob : PlanExt {
   std::vector<int4> chunks;  // (t2 slot, side, row0, row1)
   int4* d = nullptr;
 };
 
-// Decode task = 8 consecutive rows of one column: their 8 q-bit codes are one <= 64-bit field
-// read with three aligned 32-bit loads (prefetched one pass ahead).
-struct CgTask {
-  uint32_t w0, w1, w2;
-};
-
-__global__ void __launch_bounds__(320) k_code_gram(const DevT2* __restrict__ T,
-                                                   const int4* __restrict__ chunks,
-                                                   const uint8_t* __restrict__ gathered,
-                                                   int64_t pay_bytes, int qbits, int D, int kst,
-                                                   double* __restrict__ G) {
-  __shared__ double tile[kCgMaxK * kCgLd];  // [k][row]
-  const int4 ch = chunks[blockIdx.x];
-  const DevT2& t = T[ch.x];
-  const int side = ch.y, r = t.r, K = D * r;
-  const int64_t n = side == 0 ? t.a : t.b;
-  const int nb = (K + 7) / 8, nblk = nb * (nb + 1) / 2;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t* words = reinterpret_cast<const uint32_t*>(gathered);
-  const int64_t nwords = D * pay_bytes / 4;
-  // tasks: (column k, 8-row group g) for k < 8 nb, g < 8; two per thread at most
-  const int ntask = 8 * nb * 8;
-  int tk[2], tg[2];
-  int64_t tbit[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int id = threadIdx.x + 320 * u;
-    tk[u] = id < ntask ? id / 8 : -1;
-    tg[u] = id % 8;
-    tbit[u] = -1;
-    if (tk[u] >= 0 && tk[u] < K) {
-      const int w = tk[u] / r, j = tk[u] % r;
-      tbit[u] = (w * pay_bytes + (side == 0 ? t.seg_pc : t.seg_qc)) * 8 + (int64_t)j * n * qbits;
-    }
-  }
-  const int64_t rend = min((int64_t)ch.w, n);
-  CgTask pre[2];
-  auto fetch = [&](int64_t row0) {
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      pre[u] = {0u, 0u, 0u};
-      const int64_t row = row0 + 8 * tg[u];
-      if (tbit[u] >= 0 && row < rend) {
-        const int64_t bit = tbit[u] + row * qbits;
-        const int64_t wi = bit >> 5;
-        pre[u].w0 = words[wi];
-        pre[u].w1 = wi + 1 < nwords ? words[wi + 1] : 0u;
-        pre[u].w2 = wi + 2 < nwords ? words[wi + 2] : 0u;
-      }
-    }
-  };
-  double acc[4][2];
-#pragma unroll
-  for (int b = 0; b < 4; ++b) acc[b][0] = acc[b][1] = 0.0;
-  const uint32_t mask = (1u << qbits) - 1u;
-  const int sh = 32 - qbits;
-  fetch(ch.z);
-  for (int64_t row0 = ch.z; row0 < ch.w; row0 += kCgTile) {
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      if (tk[u] < 0) continue;
-      const int64_t rowg = row0 + 8 * tg[u];
-      const int s = tbit[u] >= 0 ? static_cast<int>((tbit[u] + rowg * qbits) & 31) : 0;
-      const uint64_t lo = static_cast<uint64_t>(pre[u].w0) | (static_cast<uint64_t>(pre[u].w1) << 32);
-      const uint64_t v = (lo >> s) | (s ? (static_cast<uint64_t>(pre[u].w2) << (64 - s)) : 0ull);
-      double* dst = tile + tk[u] * kCgLd + 8 * tg[u];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        int c = static_cast<int>((static_cast<uint32_t>(v >> (i * qbits)) & mask) << sh) >> sh;
-        if (tbit[u] < 0 || rowg + i >= rend) c = 0;
-        dst[i] = static_cast<double>(c);
-      }
-    }
-    __syncthreads();
-    if (row0 + kCgTile < ch.w) fetch(row0 + kCgTile);
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int blk = warp + 10 * b;
-      if (blk < nblk) {
-        int bi = 0, rem = blk;
-        while (rem >= nb - bi) {
-          rem -= nb - bi;
-          ++bi;
-        }
-        const int bj = bi + rem;
-        const double* pa = tile + (bi * 8 + lane / 4) * kCgLd + lane % 4;
-        const double* pb = tile + (bj * 8 + lane / 4) * kCgLd + lane % 4;
-#pragma unroll 4
-        for (int k = 0; k < kCgTile; k += 4) dmma_8x8x4(acc[b], pa[k], pb[k]);
-      }
-    }
-  }
-  double* g = G + ((int64_t)ch.x * 2 + side) * kst * kst;
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const int blk = warp + 10 * b;
-    if (blk < nblk) {
-      int bi = 0, rem = blk;
-      while (rem >= nb - bi) {
-        rem -= nb - bi;
-        ++bi;
-      }
-      const int bj = bi + rem;
-      const int i = bi * 8 + lane / 4;
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int j = bj * 8 + 2 * (lane % 4) + q;
-        if (i < K && j < K && i <= j && acc[b][q] != 0.0) atomicAdd(&g[i * kst + j], acc[b][q]);
-      }
-    }
-  }
-}
-
-// K up to 256: the same integer Gram on the bf16 tensor cores (mma.sync m16n8k16, fp32
+// K up to 256: the integer Gram on the bf16 tensor cores (mma.sync m16n8k16, fp32
 // accumulate). Codes are exact in bf16 and every per-chunk partial sum is an integer below
 // 1024 * 127^2 < 2^24, so the fp32 accumulation is exact; chunk sums are added as fp64 (exact,
 // order-independent). Block = (1024-row chunk of one factor side, group of 32x32 output
