@@ -17,21 +17,6 @@
 
 namespace dlx {
 
-void gram_batched(dlx_ctx* ctx, const Plan& P, const std::string& key,
-                  const std::vector<DevMat>& mats, const float* buf, double* out,
-                  cudaStream_t s);
-
-__device__ double er_block_sum(double v, double* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double s = 0.0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-  return s;
-}
-
 // ------------------------------------------------------------------ code Grams
 // The factor Grams come straight from the packed codes: C^T C over the gathered codes of one
 // side of one tensor is an integer matrix (|c| <= 2^(q-1)), so it can be formed exactly on
@@ -1150,51 +1135,33 @@ void effective_rank_factors(dlx_ctx* ctx, const Plan& P, int D, const uint8_t* g
   const int nown = (static_cast<int>(ne) - shard + nshards - 1) / nshards;
   if (nown <= 0) return;
   auto* W = static_cast<double*>(ctx->scratch("er_W", sizeof(double) * mat * nown * 3));
-  if (K <= kErMaxN) {
-    // integer code Grams straight from the gathered payloads
-    bool fresh = false;
-    CodeGramJob& J = plan_ext<CodeGramJob>(
-        P, "code_gram/" + std::to_string(shard) + "/" + std::to_string(nshards), &fresh);
-    if (fresh) {
-      for (size_t k = shard; k < ne; k += static_cast<size_t>(nshards))
-        for (int side = 0; side < 2; ++side) {
-          const int64_t n = side == 0 ? P.t2[k].a : P.t2[k].b;
-          for (int64_t r0 = 0; r0 < n; r0 += kCgChunk)
-            J.chunks.push_back(make_int4(static_cast<int>(k), side, static_cast<int>(r0),
-                                         static_cast<int>(std::min(n, r0 + kCgChunk))));
-        }
-      J.d = plan_upload(P, J.chunks);
-    }
-    auto* GI = static_cast<double*>(ctx->scratch("er_GI", sizeof(double) * mat * ne * 2));
-    DLX_CUDA(cudaMemsetAsync(GI, 0, sizeof(double) * mat * ne * 2, s));
-    if (J.chunks.empty()) return;
-    {
-      const int nt32 = (K + 31) / 32;
-      const int gy = (nt32 * (nt32 + 1) / 2 + kCgmWarps * kCgmTilesPerWarp - 1) /
-                     (kCgmWarps * kCgmTilesPerWarp);
-      k_code_gram_mma<<<dim3(J.chunks.size(), gy), 256, 0, s>>>(P.d_t2, J.d, gathered,
-                                                                P.payload_bytes, P.qbits, D, K, GI);
-      DLX_LAUNCHED();
-    }
-    launch_effrank(P, D, K, nullptr, nullptr, GI, gathered,
-                   W, tau, d_per, d_energy, shard, nshards, s);
-    return;
+  // integer code Grams straight from the gathered payloads
+  bool fresh = false;
+  CodeGramJob& J = plan_ext<CodeGramJob>(
+      P, "code_gram/" + std::to_string(shard) + "/" + std::to_string(nshards), &fresh);
+  if (fresh) {
+    for (size_t k = shard; k < ne; k += static_cast<size_t>(nshards))
+      for (int side = 0; side < 2; ++side) {
+        const int64_t n = side == 0 ? P.t2[k].a : P.t2[k].b;
+        for (int64_t r0 = 0; r0 < n; r0 += kCgChunk)
+          J.chunks.push_back(make_int4(static_cast<int>(k), side, static_cast<int>(r0),
+                                       static_cast<int>(std::min(n, r0 + kCgChunk))));
+      }
+    J.d = plan_upload(P, J.chunks);
   }
-  float* phat = static_cast<float*>(ctx->scratch("er_phat", sizeof(float) * P.pelems * D));
-  float* qhat = static_cast<float*>(ctx->scratch("er_qhat", sizeof(float) * P.qelems * D));
-  dequant_factors(P, D, gathered, P.payload_bytes, phat, qhat, 0, s);
-  std::vector<DevMat> A, B;
-  for (size_t k = 0; k < P.t2.size(); ++k) {
-    const DevT2& t = P.t2[k];
-    A.push_back(DevMat{D * t.poff, t.a, t.lda, D * t.r, static_cast<int>(k)});
-    B.push_back(DevMat{D * t.qoff, t.b, t.ldb, D * t.r, static_cast<int>(k)});
+  auto* GI = static_cast<double*>(ctx->scratch("er_GI", sizeof(double) * mat * ne * 2));
+  DLX_CUDA(cudaMemsetAsync(GI, 0, sizeof(double) * mat * ne * 2, s));
+  if (J.chunks.empty()) return;
+  {
+    const int nt32 = (K + 31) / 32;
+    const int gy = (nt32 * (nt32 + 1) / 2 + kCgmWarps * kCgmTilesPerWarp - 1) /
+                   (kCgmWarps * kCgmTilesPerWarp);
+    k_code_gram_mma<<<dim3(J.chunks.size(), gy), 256, 0, s>>>(P.d_t2, J.d, gathered,
+                                                              P.payload_bytes, P.qbits, D, K, GI);
+    DLX_LAUNCHED();
   }
-  auto* GA = static_cast<double*>(ctx->scratch("er_GA", sizeof(double) * mat * ne));
-  auto* GB = static_cast<double*>(ctx->scratch("er_GB", sizeof(double) * mat * ne));
-  const std::string tag = std::to_string(D);
-  gram_batched(ctx, P, "erA" + tag, A, phat, GA, s);
-  gram_batched(ctx, P, "erB" + tag, B, qhat, GB, s);
-  launch_effrank(P, D, K, GA, GB, nullptr, nullptr, W, tau, d_per, d_energy, shard, nshards, s);
+  launch_effrank(P, D, K, nullptr, nullptr, GI, gathered,
+                 W, tau, d_per, d_energy, shard, nshards, s);
 }
 
 }  // namespace dlx

@@ -1601,39 +1601,4 @@ void orthonormalize_batched(dlx_ctx* ctx, const Plan& P, int side, float* buf, f
   cholqr2(ctx, J, buf, tmp, side == 0 ? "P" : "Q", side == 0 ? P.pelems : P.qelems, s);
 }
 
-__global__ void k_gram_fold(const DevMat* __restrict__ mats, const int* __restrict__ part0,
-                            const int* __restrict__ nparts, int rr,
-                            const double* __restrict__ partial, double* __restrict__ out) {
-  const int e = blockIdx.x;
-  const int r = mats[e].r;
-  const double* src = partial + (int64_t)part0[e] * rr * rr;
-  double* dst = out + (int64_t)e * rr * rr;
-  for (int idx = threadIdx.x; idx < rr * rr; idx += blockDim.x) {
-    const int j = idx / rr, k = idx % rr;
-    double g = 0.0;
-    if (j < r && k < r) {
-      const int a = min(j, k), b = max(j, k);
-      for (int p = 0; p < nparts[e]; ++p) g += src[(int64_t)p * rr * rr + a * rr + b];
-    }
-    dst[idx] = g;  // full symmetric
-  }
-}
-
-// Batched fp64 Gram of arbitrary column-major matrices: out[e] = M_e^T M_e (rr x rr full,
-// rr = max columns). Used by the factor-space effective rank.
-void gram_batched(dlx_ctx* ctx, const Plan& P, const std::string& key,
-                  const std::vector<DevMat>& mats, const float* buf, double* out,
-                  cudaStream_t s) {
-  GramJob& J = job_for(P, key, mats);
-  const int rr = J.rmax;
-  auto* partial = static_cast<double*>(ctx->scratch("gram_part_er", sizeof(double) * J.total_parts * rr * rr));
-  launch_gram(J, buf, partial, s);
-  k_gram_fold<<<J.mats.size(), 256, 0, s>>>(J.d_mats, J.d_part0, J.d_nparts, rr, partial, out);
-  DLX_LAUNCHED();
-}
-
-int gram_rr(const Plan& P, const std::string& key, const std::vector<DevMat>& mats) {
-  return job_for(P, key, mats).rmax;
-}
-
 }  // namespace dlx
