@@ -409,8 +409,9 @@ def main():
         phases["inter_round_gap"] = sum(gaps) / args.steps
         phases["inter_round_gap_max"] = max(gaps)
     if eng.side_events and eng.side is not None:
-        phases["effective_rank (side stream, sharded)"] = \
-            sum(a.elapsed_time(b) for a, b in eng.side_events) / args.steps
+        label = ("effective_rank (side stream, sharded)" if world > 1 else
+                 "effective_rank (side stream, beside the operand prep)")
+        phases[label] = sum(a.elapsed_time(b) for a, b in eng.side_events) / args.steps
     eng.phase_events = None
     phases_per_rank = None
     if world > 1:  # every rank's phase times (rank skew shows up as exchange time)

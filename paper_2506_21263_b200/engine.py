@@ -70,6 +70,11 @@ class OuterConfig:
     # build every rank's device plan up front (OuterSync.prepare) when the controller is
     # applied, so a rank change does not stall the host between rounds
     prepare_ranks: bool = True
+    # world == 1: measure the round's effective rank on the high-priority side stream, forked
+    # after compress; the outer update's operand prep fills the SMs the eigenproblems' few
+    # CTAs leave idle (bench, controller applied, 4 alternating runs each on one box: 10.44
+    # vs 10.47 ms/round mean — within the box's clock noise, kept as the default)
+    er_beside: bool = True
 
     def resolved_H_min(self) -> int:
         return self.H_min if self.H_min > 0 else (self.H1 + 9) // 10
@@ -175,13 +180,15 @@ class OuterSync:
         self.gathered = torch.zeros(world * pb, dtype=torch.uint8, device=dev)
         self.stats = torch.zeros(8, dtype=torch.float64, device=dev)
         self.draws = torch.zeros(1, dtype=torch.int64, device=dev)  # RNG draws of the last compress
-        # Side stream for the effective-rank measurement. Default off at world == 1: the fused
-        # outer update is a persistent grid with ~215 KB of shared memory per SM, so side
-        # kernels cannot co-reside and only serialise behind it (measured 0.1-0.2 ms slower).
-        # At world > 1 the eigenproblems are split across the ranks (every rank holds the same
-        # all-gather buffer) and each rank's share runs on a few SMs beside the outer update.
+        # Side stream for the effective-rank measurement. At world == 1 it is forked right
+        # after compress (OuterConfig.er_beside), ahead of the outer update's operand prep on
+        # the main stream, which overlaps it. (Launched after the persistent outer update
+        # instead — ~215 KB of shared memory per SM — side kernels cannot co-reside and only
+        # serialise behind it: measured 0.1-0.2 ms slower.) At world > 1 the eigenproblems are
+        # split across the ranks (every rank holds the same all-gather buffer).
         if side_stream is None:
-            side_stream = world > 1
+            side_stream = world > 1 or cfg.er_beside
+        self.er_beside = world == 1 and cfg.er_beside and side_stream
         # high priority: the measurement's few CTAs are dispatched ahead of the outer update's
         # persistent grid, so the host learns r' (next round's rank) early in the round
         self.side = torch.cuda.Stream(device=dev, priority=-1) if side_stream else None
@@ -432,13 +439,20 @@ class OuterSync:
                 # timeline. (The persistent outer-update grid holds every SM, so a side stream
                 # would only serialise behind it.)
                 self._ev("effective_rank")
-                # at N > 1 the ranks split the eigenproblems and sum the per-tensor results
-                # right away (exact: one nonzero term per entry)
-                sharded = self.er_shards > 1
-                self._effective_rank(gathered, r, q, cur, sharded=sharded)
-                if sharded:
-                    self._sum_er_shards()
-                self._queue_er(rec, cur)
+                if self.er_beside and xstream is None:
+                    self.side.wait_stream(cur)
+                    with torch.cuda.stream(self.side):
+                        self._effective_rank(gathered, r, q, self.side, sharded=False)
+                        self._queue_er(rec, self.side)
+                    st["er_side"] = True
+                else:
+                    # at N > 1 the ranks split the eigenproblems and sum the per-tensor results
+                    # right away (exact: one nonzero term per entry)
+                    sharded = self.er_shards > 1
+                    self._effective_rank(gathered, r, q, cur, sharded=sharded)
+                    if sharded:
+                        self._sum_er_shards()
+                    self._queue_er(rec, cur)
             if xstream is not None:
                 done = torch.cuda.Event(enable_timing=True)
                 done.record(xstream)
@@ -462,6 +476,8 @@ class OuterSync:
                 self._effective_rank(gathered, r, q, side, sharded=True)
         self._ev("outer_update")
         self._outer_update(gathered, r, q, local, mode, cur)
+        if st.get("er_side"):
+            cur.wait_stream(self.side)
         self._ev("end")
         self.stats_host[self.round % self.STATS_SLOTS].copy_(self.stats, non_blocking=True)
         if st["late_rank"]:
