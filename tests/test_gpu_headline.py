@@ -305,7 +305,8 @@ def test_headline_effective_rank_vs_reference(ctx, reference):
         assert er.aggregate == agg and er.all_zero == allz
 
 
-def test_engine_controller_applied_vs_reference(ctx, reference):
+@pytest.mark.parametrize("side", [None, False])
+def test_engine_controller_applied_vs_reference(ctx, reference, side):
     """OuterSync with the adaptive controller APPLIED (hold_rank=False) for 9 rounds against
     the reference's round (orc_outer_round = collective_average + stage_deltas + Nesterov +
     warm refresh, engine.cpp:215-276, 494-501) and the reference's own controller
@@ -313,7 +314,9 @@ def test_engine_controller_applied_vs_reference(ctx, reference):
     r_t from r1 = 12 once the window fills, which forces a stochastic cold restart
     (compress.cpp:161-164) with the speculative draw bases verified on the device. Each round
     the reference starts from the engine's own state (anchor, velocity, pending delta, warm Q),
-    so the per-round map is compared at the tight bar and the schedule must match exactly."""
+    so the per-round map is compared at the tight bar and the schedule must match exactly.
+    side=None: the default N = 1 ordering (effective rank on the side stream forked after
+    compress); side=False: everything on the main stream."""
     from paper_2506_21263_b200 import api
     from paper_2506_21263_b200.engine import OuterConfig, OuterSync
     shapes = [(96, 80), (80,), (128, 64), (64, 40), (40,), (48, 96)]
@@ -326,7 +329,8 @@ def test_engine_controller_applied_vs_reference(ctx, reference):
     L = api.Layout(ctx, [(f"t{i}", s) for i, s in enumerate(shapes)])
     cfg = OuterConfig(rank1=r1, qbits=Q, power_iters=2, adaptive=True, window_c=c, tau=0.5,
                       H1=H1, seed=1, overlap=True, hold_rank=False)
-    eng = OuterSync(L, cfg, L.pack(anchor0))
+    eng = OuterSync(L, cfg, L.pack(anchor0), side_stream=side)
+    assert eng.er_beside == (side is None)
     dlocal = L.pack(local)
     rec = eng.step(dlocal)  # round 1: staging only (engine.cpp:473)
     assert rec.r_t == r1
