@@ -1,10 +1,13 @@
 // ortho.cu — batched orthonormalisation of the power-iteration factors
-// (orthonormalize tensor.cpp:174-227) and the batched fp64 Gram used by the effective rank.
+// (orthonormalize tensor.cpp:174-227).
 //
 // B200 design: all factors of one side (every P, or every Q) are orthonormalised in one
 // pass of four launches instead of a column-serial MGS per tensor:
 //   Gram (fp64, row-split, deterministic) -> Cholesky + R^-1 (one CTA per factor)
 //   -> apply Y R^-1 (fp64 accumulate)  — twice (CholQR2, equal to MGS2 up to rounding).
+// Cholesky + R^-1: r <= 32 one warp in registers (warp_chol_inv); 32 < r <= 128 blocked,
+// 32-wide panels (k_cholblk: warp_chol_inv on the diagonal blocks, DMMA for the panel rows,
+// trailing updates and the off-diagonal blocks of R^-1); above, k_chol in global memory.
 // A factor whose Cholesky pivot falls within 10x of the reference's dependence tolerance
 // (1e-7 * max(1, largest column norm)) is left untouched by CholQR2 and re-done by an exact
 // MGS2 kernel with the reference's seeded column replacement (RngStream(0x5eedc01,
