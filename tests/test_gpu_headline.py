@@ -361,3 +361,42 @@ def test_engine_controller_applied_vs_reference(ctx, reference, side):
         assert rel_fro(L.unpack(eng.velocity), v) <= 1e-2, rnd
         assert rel_fro(L.unpack(eng.pending), pend[0]) <= 1e-2, rnd
     assert ranks_seen[0] == r1 and ranks_seen[-1] < r1, ranks_seen  # a rank change happened
+
+
+@pytest.mark.parametrize("rank", [64, 128])
+def test_llama_layer_high_rank_compress_vs_reference(ctx, reference, rank):
+    """SURVEY C3 at its top ranks on real shapes: the Llama-7B down projection (11008 x 4096,
+    K2 split over 11008 rows) plus one attention projection and a norm vector, through the
+    blocked CholQR (k_cholblk), the SIMT Gram / apply at r > 64 and the 3xTF32 sweeps at
+    N = 64 / 128, against the reference's compress (cold start, stochastic rounding, q = 4:
+    a stochastic code flips with probability ~ (2^(q-1) - 1) x the factor's relative error,
+    and the fp32-accumulated sweeps over K = 4096-11008 carry ~1e-5 — at q = 8 that is
+    ~0.15 % flipped codes, at q = 4 below the 0.1 % bar).
+    Exact rank-r data (singular values decaying 0.97 per index, cond 50 at r = 128) over a
+    1e-8 noise floor: the r-dimensional subspace is determined after one sweep, so no small
+    gap at its edge amplifies the fp32-vs-fp64 difference."""
+    import torch
+    from paper_2506_21263_b200 import api
+    tbl = [("self_attn.o_proj.weight", (4096, 4096)), ("mlp.down_proj.weight", (11008, 4096)),
+           ("input_layernorm.weight", (4096,))]
+    shapes = [s for _, s in tbl]
+    t = Table(shapes)
+    L = api.Layout(ctx, tbl)
+    flat = _lowrank_noise(shapes, 7 + rank, k=rank, decay=0.97, noise=1e-8)
+    st0 = reference.stream(2, reference.stream_key(0xC09C, rank))
+    q = 4
+    ref = reference.compress(t, flat, rank, q, 0, 2, st0)
+    res = api.compress(L, L.pack(flat), rank, api.QuantSpec(q, api.STOCHASTIC), None, 0, 2, st0)
+    assert int(res.draws.item()) == draws_between(st0, ref["state"])
+    codes, scales = decode_payload(L, res.payload, rank, q)
+    same = (codes == ref["codes"]).mean()
+    assert same >= 0.999, same
+    assert np.allclose(scales, ref["scales"], rtol=TOL_SCALE, atol=0)
+    for got, want in zip(L.factors_from_device(res.q_factors, rank, 1),
+                         split_q(shapes, rank, ref["q"])):
+        assert np.abs(got - want).max() <= TOL_Q
+    d_gpu = api.decompress(L, res.payload, rank, q)
+    d_ref = api.decompress(L, L.parse(reference.serialize(t, ref["ranks"], rank, q, ref["codes"],
+                                                          ref["scales"]), rank, q), rank, q)
+    num = float(torch.linalg.vector_norm((d_gpu - d_ref).double()))
+    assert num <= TOL_COMPRESS * float(torch.linalg.vector_norm(d_ref.double()))
