@@ -452,6 +452,10 @@ def main():
     achieved = per_kernel[dom]["GBps"] if dom else 0.0
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
                 "unit": "GB/s", "frac": achieved / hbm_peak, "peak_source": peak_src,
+                "peak_note": ("the peak is a torch copy_ (one read + one write stream); the "
+                              "TMA-streamed kernels can sit at or slightly above it (k_o5: 4 "
+                              "reads + 3 writes); a pure TMA read stream tops out at 6.9-7.3 "
+                              "TB/s (profiles/r02b_tma_read_bw.log)"),
                 "traffic": traffic,
                 "algorithmic_bytes_per_launch": per_kernel[dom]["bytes_per_launch"] if dom else None,
                 "kernels": per_kernel,
