@@ -59,10 +59,20 @@ void launch_fill_gaussian(const dlx_layout& L, float* out, const float* base, fl
 // --------------------------------------------------------------- cold start (compress.cpp:64-69)
 // Q0 = uniform(-1, 1)^{b x r} row-major from the shared stream at the tensor's draw base,
 // stored column-major. Value = lo + (hi - lo) * u with separate roundings (rng.hpp:39).
-__global__ void k_cold_init(const DevT2* T, int nt2, float* q, const int64_t* bases, uint64_t s0,
-                            const uint64_t* s0p) {
+// One block per 256 runs of one tensor: blk0[k] = first block of tensor k (prefix over the
+// tensors' run counts), found by binary search (a max-work x tensors grid launched 74752
+// mostly empty blocks for OPT-1.3B; same time — the 64-bit integer hash is the cost)
+__global__ void __launch_bounds__(256) k_cold_init(const DevT2* T, int nt2,
+                                                   const int* __restrict__ blk0, float* q,
+                                                   const int64_t* bases, uint64_t s0,
+                                                   const uint64_t* s0p) {
   if (s0p) s0 = *s0p;
-  const int k = blockIdx.y;
+  int lo = 0, hi = nt2 - 1;  // last k with blk0[k] <= blockIdx.x
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (blk0[mid] <= static_cast<int>(blockIdx.x)) lo = mid; else hi = mid - 1;
+  }
+  const int k = lo;
   const DevT2 t = T[k];
   const uint64_t base = static_cast<uint64_t>(bases[k]);
   // walk the column-major destination in runs of 8 rows (coalesced stores); element (i, j)
@@ -72,29 +82,41 @@ __global__ void k_cold_init(const DevT2* T, int nt2, float* q, const int64_t* ba
   const uint32_t runs = static_cast<uint32_t>((t.b + 7) / 8);
   const int64_t total = static_cast<int64_t>(runs) * t.r;
   const uint64_t step = static_cast<uint64_t>(t.r) * kGolden;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t j = static_cast<uint32_t>(e) / runs;
-    const uint32_t i0 = 8 * (static_cast<uint32_t>(e) - j * runs);
-    uint64_t z = s0 + (base + static_cast<uint64_t>(i0) * t.r + j + 1) * kGolden;
-    float* dst = q + t.qoff + static_cast<int64_t>(j) * t.ldb + i0;
+  const int64_t e = static_cast<int64_t>(blockIdx.x - blk0[k]) * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const uint32_t j = static_cast<uint32_t>(e) / runs;
+  const uint32_t i0 = 8 * (static_cast<uint32_t>(e) - j * runs);
+  uint64_t z = s0 + (base + static_cast<uint64_t>(i0) * t.r + j + 1) * kGolden;
+  float* dst = q + t.qoff + static_cast<int64_t>(j) * t.ldb + i0;
 #pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8, z += step) {
-      if (i0 + u8 >= t.b) break;
-      const float u = unit_f(fmix64(z));
-      dst[u8] = __fadd_rn(-1.0f, __fmul_rn(2.0f, u));
-    }
+  for (int u8 = 0; u8 < 8; ++u8, z += step) {
+    if (i0 + u8 >= t.b) break;
+    const float u = unit_f(fmix64(z));
+    dst[u8] = __fadd_rn(-1.0f, __fmul_rn(2.0f, u));
   }
 }
 
 void launch_cold_init(const Plan& P, float* q, const int64_t* d_bases, uint64_t s0,
                       cudaStream_t s, const uint64_t* s0p) {
   if (P.t2.empty()) return;
-  int64_t mx = 1;
-  for (const DevT2& t : P.t2) mx = std::max(mx, ceil_div(t.b, 8) * t.r);
-  const int gx = static_cast<int>(std::min<int64_t>(ceil_div(mx, 256), 512));
-  k_cold_init<<<dim3(gx, P.t2.size()), 256, 0, s>>>(P.d_t2, (int)P.t2.size(), q, d_bases, s0,
-                                                   s0p);
+  struct ColdBlocks : PlanExt {
+    int* d = nullptr;
+    int total = 0;
+  };
+  bool fresh = false;
+  ColdBlocks& cb = plan_ext<ColdBlocks>(P, "cold_init_blocks", &fresh);
+  if (fresh) {
+    std::vector<int> blk0;
+    int acc = 0;
+    for (const DevT2& t : P.t2) {
+      blk0.push_back(acc);
+      acc += static_cast<int>(ceil_div(ceil_div(t.b, 8) * t.r, 256));
+    }
+    cb.d = plan_upload(P, blk0);
+    cb.total = acc;
+  }
+  if (cb.total == 0) return;
+  k_cold_init<<<cb.total, 256, 0, s>>>(P.d_t2, (int)P.t2.size(), cb.d, q, d_bases, s0, s0p);
   DLX_LAUNCHED();
 }
 
