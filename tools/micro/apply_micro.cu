@@ -207,10 +207,15 @@ int main() {
     cudaMalloc(&dY0, sizeof(float) * total); cudaMemcpy(dY0, h.data(), sizeof(float) * total, cudaMemcpyHostToDevice);
     cudaMalloc(&dY, sizeof(float) * total);
     std::vector<float> ref;
-    for (int v = 0; v < 3; ++v) {
+    for (int v = 0; v < 7; ++v) {
       auto launch = [&] {
-        if (v == 0) {
-          const int nj = jobs128.size(), per = std::max(1, (nj + 4 * 148 - 1) / (4 * 148));
+        if (v == 0 || v >= 3) {
+          const int nj = jobs128.size();
+          int per = std::max(1, (nj + 4 * 148 - 1) / (4 * 148));
+          if (v == 3) per = 1;
+          if (v == 4) per = 2;
+          if (v == 5) per = 4;
+          if (v == 6) per = 12;
           v0<<<(nj + per - 1) / per, 128>>>(dm, dj128, nj, per, 32, dX, dY);
         } else if (v == 2) {
           v2<<<jobs256.size(), 512>>>(dm, dj256, jobs256.size(), 32, dX, dY);
