@@ -177,6 +177,126 @@ __global__ void __launch_bounds__(512) v2(const DevMat* mats, const int4* jobs, 
   }
 }
 
+
+// ---- V3 (r <= 32): DMMA with the A fragments loaded straight from global memory (fp32 ->
+// fp64 in registers), no shared-memory staging of Y and no block barriers per tile: each warp
+// owns 32-row slices; R^-1 staged once per CTA (one factor per CTA-run of jobs as V0).
+__global__ void __launch_bounds__(128) v3(const DevMat* mats, const int4* jobs, int njobs, int per_cta,
+                                         int rr, const double* rinv, float* buf) {
+  __shared__ double Rs[32 * kAdLdR];
+  const int j0 = blockIdx.x * per_cta, j1 = min(njobs, j0 + per_cta);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int cur = -1;
+  for (int j = j0; j < j1; ++j) {
+    const int4 jb = jobs[j];
+    const DevMat m = mats[jb.x];
+    const int r = m.r, nb = (r + 7) / 8;
+    if (jb.x != cur) {
+      __syncthreads();
+      const double* X = rinv + (long long)jb.x * rr * rr;
+      for (int idx = threadIdx.x; idx < 32 * 32; idx += 128) {
+        const int k = idx / 32, c = idx % 32;
+        Rs[k * kAdLdR + c] = (k < r && c < r && k <= c) ? X[k * rr + c] : 0.0;
+      }
+      __syncthreads();
+      cur = jb.x;
+    }
+    float* Y = buf + m.off;
+    const double* pb = Rs + (lane % 4) * kAdLdR + lane / 4;
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) {
+      const long long row = jb.y + warp * 32 + rb * 8 + lane / 4;
+      const bool live = row < m.n;
+      // this lane's A elements: Y[row][k + lane%4] for the 8 k-steps
+      float a[8];
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int col = 4 * ks + lane % 4;
+        a[ks] = (live && col < r) ? Y[(long long)col * m.ld + row] : 0.f;
+      }
+      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int k = 4 * ks;
+        const double ad = (double)a[ks];
+#pragma unroll
+        for (int cj = 0; cj < 4; ++cj)
+          if (cj < nb && k < 8 * (cj + 1)) dmma_8x8x4(acc[cj], ad, pb[k * kAdLdR + cj * 8]);
+      }
+      __syncwarp();  // every lane has read its rows before the in-place stores (same warp)
+      if (live) {
+#pragma unroll
+        for (int cj = 0; cj < 4; ++cj)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int col = cj * 8 + 2 * (lane % 4) + q;
+            if (cj < nb && col < r) Y[(long long)col * m.ld + row] = (float)acc[cj][q];
+          }
+      }
+    }
+  }
+}
+
+
+__global__ void __launch_bounds__(128) v4(const DevMat* mats, const int4* jobs, int njobs, int per_cta,
+                                         int rr, const double* rinv, float* buf) {
+  __shared__ double Rs[32 * kAdLdR];
+  const int j0 = blockIdx.x * per_cta, j1 = min(njobs, j0 + per_cta);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int cur = -1;
+  for (int j = j0; j < j1; ++j) {
+    const int4 jb = jobs[j];
+    const DevMat m = mats[jb.x];
+    const int r = m.r, nb = (r + 7) / 8;
+    if (jb.x != cur) {
+      __syncthreads();
+      const double* X = rinv + (long long)jb.x * rr * rr;
+      for (int idx = threadIdx.x; idx < 32 * 32; idx += 128) {
+        const int k = idx / 32, c = idx % 32;
+        Rs[k * kAdLdR + c] = (k < r && c < r && k <= c) ? X[k * rr + c] : 0.0;
+      }
+      __syncthreads();
+      cur = jb.x;
+    }
+    float* Y = buf + m.off;
+    const double* pb = Rs + (lane % 4) * kAdLdR + lane / 4;
+    float a[4][8];
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) {
+      const long long row = jb.y + warp * 32 + rb * 8 + lane / 4;
+      const bool live = row < m.n;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int col = 4 * ks + lane % 4;
+        a[rb][ks] = (live && col < r) ? Y[(long long)col * m.ld + row] : 0.f;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) {
+      const long long row = jb.y + warp * 32 + rb * 8 + lane / 4;
+      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int k = 4 * ks;
+        const double ad = (double)a[rb][ks];
+#pragma unroll
+        for (int cj = 0; cj < 4; ++cj)
+          if (cj < nb && k < 8 * (cj + 1)) dmma_8x8x4(acc[cj], ad, pb[k * kAdLdR + cj * 8]);
+      }
+      if (row < m.n) {
+#pragma unroll
+        for (int cj = 0; cj < 4; ++cj)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int col = cj * 8 + 2 * (lane % 4) + q;
+            if (cj < nb && col < r) Y[(long long)col * m.ld + row] = (float)acc[cj][q];
+          }
+      }
+    }
+  }
+}
+
 int main() {
   // OPT-1.3B P side: embed 50272, pos 2050, 24 x (q,k,v,o 2048; fc1 8192; fc2 2048)
   std::vector<long long> ns = {50272, 2050};
@@ -207,9 +327,9 @@ int main() {
     cudaMalloc(&dY0, sizeof(float) * total); cudaMemcpy(dY0, h.data(), sizeof(float) * total, cudaMemcpyHostToDevice);
     cudaMalloc(&dY, sizeof(float) * total);
     std::vector<float> ref;
-    for (int v = 0; v < 7; ++v) {
+    for (int v = 0; v < 12; ++v) {
       auto launch = [&] {
-        if (v == 0 || v >= 3) {
+        if (v == 0 || (v >= 3 && v <= 6)) {
           const int nj = jobs128.size();
           int per = std::max(1, (nj + 4 * 148 - 1) / (4 * 148));
           if (v == 3) per = 1;
@@ -217,6 +337,14 @@ int main() {
           if (v == 5) per = 4;
           if (v == 6) per = 12;
           v0<<<(nj + per - 1) / per, 128>>>(dm, dj128, nj, per, 32, dX, dY);
+        } else if (v >= 7 && v <= 9) {
+          const int nj = jobs128.size();
+          const int per = v == 7 ? std::max(1, (nj + 4 * 148 - 1) / (4 * 148)) : (v == 8 ? 2 : 1);
+          v3<<<(nj + per - 1) / per, 128>>>(dm, dj128, nj, per, 32, dX, dY);
+        } else if (v >= 10) {
+          const int nj = jobs128.size();
+          const int per = v == 10 ? 1 : 2;
+          v4<<<(nj + per - 1) / per, 128>>>(dm, dj128, nj, per, 32, dX, dY);
         } else if (v == 2) {
           v2<<<jobs256.size(), 512>>>(dm, dj256, jobs256.size(), 32, dX, dY);
         } else if (R == 32) {
