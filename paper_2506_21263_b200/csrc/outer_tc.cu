@@ -160,10 +160,12 @@ __global__ void __launch_bounds__(256) k_o5_prep(
       const int64_t bit = (w * pay_bytes + (side == 0 ? t.seg_pc : t.seg_qc)) * 8 +
                           ((int64_t)j * n + row0) * qbits;
       const int64_t wi = bit >> 5;
-      const uint32_t w0 = words[wi];
-      const uint32_t w1 = wi + 1 < nwords ? words[wi + 1] : 0u;
-      const uint32_t w2 = wi + 2 < nwords ? words[wi + 2] : 0u;
       const int s = static_cast<int>(bit & 31);
+      // only the words the 8 codes touch (q = 4 groups are one aligned word)
+      const int span = s + 8 * qbits;
+      const uint32_t w0 = words[wi];
+      const uint32_t w1 = (span > 32 && wi + 1 < nwords) ? words[wi + 1] : 0u;
+      const uint32_t w2 = (span > 64 && wi + 2 < nwords) ? words[wi + 2] : 0u;
       const uint64_t lo = static_cast<uint64_t>(w0) | (static_cast<uint64_t>(w1) << 32);
       const uint64_t f = (lo >> s) | (s ? (static_cast<uint64_t>(w2) << (64 - s)) : 0ull);
       float scale = 1.f, ps = 1.f;
