@@ -313,6 +313,42 @@ def test_compress_high_rank_cholqr(ctx, oracle, rank, blocked):
                     q_tols=[TOL_Q, TOL_Q, TOL_Q, 1e-3])
 
 
+@pytest.mark.parametrize("blocked", [1, 0])
+def test_compress_mixed_rank_clamp_cholqr(ctx, oracle, blocked):
+    """Rank 128 on tensors whose short side clamps the rank (r_eff = 128, 90, 70, 40): one
+    blocked factorisation size (RR = 128) serves every factor, the smaller ones padded with
+    the identity past their r_eff (k_cholblk), and the effective-rank and quantiser tables
+    follow the per-tensor ranks."""
+    from paper_2506_21263_b200 import api
+    shapes = [(700, 300), (300,), (90, 400), (300, 70), (40, 40)]
+    t = Table(shapes)
+    L = mk(ctx, shapes)
+    rank = 128
+    st = oracle.stream(13, 5)
+    data = []
+    for i, s in enumerate(shapes):
+        if len(s) == 1:
+            data.append(oracle.gaussian(oracle.stream(i, 4), s[0])[0])
+            continue
+        a, b = s
+        k = min(rank, a, b)
+        u = oracle.gaussian(oracle.stream(i, 1), a * k)[0].reshape(a, k)
+        v = oracle.gaussian(oracle.stream(i, 2), b * k)[0].reshape(b, k)
+        u = (u * np.float32(0.97) ** np.arange(k, dtype=np.float32)).astype(np.float32)
+        data.append(oracle.matmul_nt(u, v).reshape(-1))
+    flat = np.concatenate(data).astype(np.float32)
+    ref = oracle.compress(t, flat, rank, 4, 0, 2, st)
+    assert list(ref["ranks"]) == [128, 0, 90, 70, 40]
+    api.set_option("cholqr_blocked", blocked)
+    try:
+        res = api.compress(L, L.pack(flat), rank, api.QuantSpec(4, 0), None, 0, 2, st)
+    finally:
+        api.set_option("cholqr_blocked", 1)
+    # (full-rank clamped tensors keep their weakest directions: their column maxima carry
+    # the fp32-vs-fp64 sweep difference at up to ~1e-3; codes and Q hold the usual bars)
+    _check_compress(L, t, oracle, ref, res, rank, 4, st, scale_rtol=1e-2)
+
+
 @pytest.mark.parametrize("rank,q,D", [(6, 8, 3), (16, 2, 1), (32, 4, 2), (30, 4, 3)])
 def test_effective_rank_factor_space(ctx, oracle, reference, rank, q, D):
     """Factor-space r' (integer code Grams for D*r <= 64, fp64 dequantised Grams above) vs
